@@ -1,0 +1,119 @@
+/*
+ * gpubpe.h -- C ABI of the B200 GPT-2 byte-level BPE encoder.
+ *
+ * This is the drop-in boundary for the reference's encode path
+ * (/root/reference/pkg, package `lanebpe`).  The reference is pure Python, so
+ * its "FFI" is its Python call surface; each entry point below names the
+ * reference interface it replaces.  A maintainer binds it with ctypes (see
+ * INTEGRATION.md); paper_2603_02597_b200/_native.py is exactly that binding.
+ *
+ * Conventions: plain pointers and sizes, no torch types.  Pointers prefixed
+ * d_ are device (HBM) pointers on the context's device; h_ are host pointers.
+ * Every function returns 0 on success or a GPUBPE_E* code; the message of the
+ * last failure is available from gpubpe_last_error().  A context is not
+ * thread-safe: callers serialise use of one context (the Python layer holds a
+ * lock), or create one context per thread.
+ */
+#ifndef GPUBPE_H
+#define GPUBPE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPUBPE_OK 0
+#define GPUBPE_EINVAL 1     /* bad argument (maps to ValueError / InvalidBudget) */
+#define GPUBPE_ECUDA 2      /* CUDA runtime / launch failure (DeviceError) */
+#define GPUBPE_ENOMEM 3     /* device or host allocation failed (DeviceError) */
+#define GPUBPE_ETABLE 4     /* merge table rejected: duplicate pair / reserved key */
+
+#define GPUBPE_API_VERSION 1
+
+typedef struct gpubpe_ctx gpubpe_ctx;
+
+/* Counters of the last encode (lanebpe PassCounters, engines.py:77-97, plus
+ * device-side evidence).  passes == n_bytes - n_ids always
+ * (test_acceptance.py:363-376). */
+typedef struct gpubpe_stats {
+    uint64_t n_bytes;          /* base tokens in (one per byte) */
+    uint64_t n_ids;            /* ids out */
+    uint64_t passes;           /* merges applied = n_bytes - n_ids */
+    uint64_t n_segments;       /* junction segments (incl. chunk / doc cuts) */
+    uint64_t memo_hits;        /* segments resolved by one memo probe */
+    uint64_t short_merges;     /* segments merged by the per-thread greedy loop */
+    uint64_t medium_segments;  /* segments merged by the CTA engine in smem */
+    uint64_t giant_segments;   /* segments merged by the giant (multi-window) engine */
+    uint64_t giant_bytes;      /* bytes inside giant segments */
+    uint64_t engine_passes;    /* multi-merge passes run by CTA/giant engines */
+    uint64_t tiles;            /* encode tiles launched */
+    uint64_t overflow;         /* 1 if the giant arena overflowed (call re-run) */
+    uint64_t well_formed;      /* 1 if the table admits exact multi-merge passes */
+} gpubpe_stats;
+
+/* Context flags */
+#define GPUBPE_F_NO_MEMO 1u      /* disable the vocab-string memo (evidence runs) */
+#define GPUBPE_F_STRICT 2u       /* force one-merge-per-pass even if well-formed */
+
+/*
+ * Build a device context (replaces Tokenizer.__init__ / Tokenizer.from_files,
+ * chunker.py:74-93, and build_table, merge_table.py:246-278, as the place the
+ * tables are materialised).
+ *   base_ids[256]        byte -> token id (byte_codec.py:97-111)
+ *   left/right/rank/new  n_rules merge rules (merge_table.py:80-116)
+ *   vocab_ids/bytes/offs n_vocab tokens with their byte strings (symbols
+ *                        containing non-byte characters omitted); used for the
+ *                        vocab-string memo, which is verified on the device at
+ *                        creation time (only strings whose BPE is themselves)
+ *   flags                GPUBPE_F_*
+ * Errors: GPUBPE_ETABLE for a duplicate (left,right) pair (DuplicatePair).
+ */
+int gpubpe_ctx_create(int device, const uint32_t *base_ids, const uint32_t *left,
+                      const uint32_t *right, const uint32_t *rank, const uint32_t *new_tok,
+                      uint64_t n_rules, const uint32_t *vocab_ids, const uint8_t *vocab_bytes,
+                      const uint64_t *vocab_offs, uint64_t n_vocab, uint32_t flags,
+                      gpubpe_ctx **out);
+
+/*
+ * Encode a packed batch (replaces tokenize_batch, chunker.py:110-187, with
+ * the sequential engine's output, engines.py:269-335).
+ *   d_bytes[n_bytes]          all documents back to back (uint8)
+ *   d_doc_offs[n_docs+1]      int64 CSR offsets, d_doc_offs[0] == 0,
+ *                             d_doc_offs[n_docs] == n_bytes
+ *   max_seq_len, chunk_budget BlockConfig (engines.py:40-65): a document longer
+ *                             than max_seq_len is cut at multiples of
+ *                             chunk_budget (chunker.py:42-53,139-144)
+ *   d_out_ids                 capacity n_bytes uint32 ids
+ *   d_out_offs[n_docs+1]      int64 CSR offsets of the ids
+ *   stream                    cudaStream_t (NULL = legacy default stream)
+ * Asynchronous: returns once the kernels are enqueued, except when the input
+ * is large enough that the giant-segment arena might overflow, in which case
+ * it synchronises the stream and re-runs with a larger arena.
+ */
+int gpubpe_encode(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes,
+                  const int64_t *d_doc_offs, uint64_t n_docs, uint64_t max_seq_len,
+                  uint64_t chunk_budget, uint32_t *d_out_ids, int64_t *d_out_offs,
+                  void *stream);
+
+/* Synchronise `stream` and read the counters of the last encode on it
+ * (BatchResult.counters, chunker.py:56-64). */
+int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out);
+
+/* Number of encode kernels one gpubpe_encode enqueues (launch accounting). */
+int gpubpe_launches_per_encode(void);
+
+/* Device-side probe of the packed pair table: for i < n, (d_left[i],
+ * d_right[i]) -> d_new[i], d_rank[i] (0xFFFFFFFF rank on miss).  Replaces
+ * PackedPairTable.lookup_pairs (merge_table.py:232-243); used by the table
+ * conformance tests. */
+int gpubpe_lookup_pairs(gpubpe_ctx *ctx, const uint32_t *d_left, const uint32_t *d_right,
+                        uint64_t n, uint32_t *d_new, uint32_t *d_rank, void *stream);
+
+const char *gpubpe_last_error(gpubpe_ctx *ctx);
+void gpubpe_ctx_destroy(gpubpe_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPUBPE_H */

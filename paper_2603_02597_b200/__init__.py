@@ -1,0 +1,35 @@
+"""B200-native GPT-2 byte-level BPE encoder.
+
+Drop-in for the encode path of the reference package `lanebpe`
+(/root/reference/pkg): same construction API (Vocab / parse_merges /
+build_table / Tokenizer / BlockConfig), same batch API (tokenize_batch ->
+BatchResult, TokenizerHandle.tokenize_batch), same exceptions -- with the
+merge loop running as hand-written sm_100a CUDA kernels behind the C ABI in
+include/gpubpe.h (libgpubpe.so, built in-tree).  No CPU fallback.
+"""
+
+from . import errors
+from .bindings import TokenizerHandle
+from .byte_codec import ByteEncoder, Vocab, base_id_table, build_byte_encoder, decode_tokens, encode_bytes
+from .chunker import ENGINE_NAMES, BatchResult, Chunk, Tokenizer, chunk_tokens, pack_texts, tokenize_batch
+from .engine import BlockConfig, PassCounters
+from .merge_table import (
+    MergeRule,
+    PackedPairTable,
+    build_table,
+    pack_key,
+    pack_value,
+    parse_merges,
+    rule_arrays,
+    unpack_value,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BatchResult", "BlockConfig", "ByteEncoder", "Chunk", "ENGINE_NAMES", "MergeRule",
+    "PackedPairTable", "PassCounters", "Tokenizer", "TokenizerHandle", "Vocab", "base_id_table",
+    "build_byte_encoder", "build_table", "chunk_tokens", "decode_tokens", "encode_bytes", "errors",
+    "pack_key", "pack_texts", "pack_value", "parse_merges", "rule_arrays", "tokenize_batch",
+    "unpack_value", "__version__",
+]

@@ -1,0 +1,86 @@
+// common.cuh -- device tables, hashes and probes shared by all encode kernels.
+//
+// Layout in HBM (built once per context by ctx.cu, L2-resident afterwards):
+//   pair table   uint4 slots {left, right, rank, new}, power-of-two capacity at
+//                <= 50% load, fmix64 hash of (left<<32)|right, linear probing.
+//                Same hash family as the reference (merge_table.py:49-57) but a
+//                single 16-byte slot per probe instead of two 8-byte arrays.
+//   rl / rr      per internal id: min rank of any rule with the id as LEFT /
+//                RIGHT operand (INF if none) -- the blocking test of the exact
+//                multi-merge pass.
+//   jbits        65536-bit junction bitmap: bit (x<<8|y) set iff some reachable
+//                rule joins a token ending in byte x to one starting with byte
+//                y.  A byte pair outside J can never be merged across, so it
+//                is an exact segment boundary.
+//   base         byte -> internal id (byte_codec.py:97-111)
+//   memo         uint4 slots {bytes0-3, bytes4-7, id, len | blob_off<<8} keyed
+//                by the byte string of a vocab token whose BPE is itself;
+//                blob holds the full strings (for tokens longer than 8 bytes).
+//   ext_id       internal -> external id (NULL when ids are used as-is).
+#pragma once
+#include <cstdint>
+
+#define GPUBPE_INF 0xFFFFFFFFu
+
+struct DevTables {
+    const uint4 *pairs;
+    uint32_t pair_mask;
+    const uint32_t *rl;
+    const uint32_t *rr;
+    const uint32_t *jbits;
+    const uint32_t *base;
+    const uint4 *memo;
+    uint32_t memo_mask;  // 0 with memo == nullptr disables the memo
+    const uint8_t *blob;
+    const uint32_t *ext_id;
+    int well_formed;  // exact multi-merge allowed (else one global-min merge per pass)
+};
+
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xFF51AFD7ED558CCDull;
+    x ^= x >> 33;
+    x *= 0xC4CEB9FE1A85EC53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+__host__ __device__ __forceinline__ uint32_t pair_home(uint32_t l, uint32_t r, uint32_t mask) {
+    return (uint32_t)(fmix64(((uint64_t)l << 32) | r) & mask);
+}
+
+// Memo hash over a byte string given as 8-byte little-endian chunks.
+__host__ __device__ __forceinline__ uint64_t memo_hash_step(uint64_t h, uint64_t chunk) {
+    return fmix64(h ^ chunk);
+}
+__host__ __device__ __forceinline__ uint64_t memo_hash_init(uint32_t len) {
+    return 0x9E3779B97F4A7C15ull * (uint64_t)(len + 1);
+}
+
+#ifdef __CUDACC__
+
+struct PairHit {
+    uint32_t rank;  // GPUBPE_INF on miss
+    uint32_t nw;
+};
+
+__device__ __forceinline__ PairHit probe_pair(const DevTables &T, uint32_t l, uint32_t r) {
+    uint32_t i = pair_home(l, r, T.pair_mask);
+    for (;;) {
+        uint4 s = __ldg(&T.pairs[i]);
+        if (s.x == l && s.y == r) return PairHit{s.z, s.w};
+        if (s.x == GPUBPE_INF && s.y == GPUBPE_INF) return PairHit{GPUBPE_INF, 0};
+        i = (i + 1) & T.pair_mask;
+    }
+}
+
+__device__ __forceinline__ bool is_junction(const uint32_t *jb, uint32_t x, uint32_t y) {
+    uint32_t k = (x << 8) | y;
+    return (__ldg(&jb[k >> 5]) >> (k & 31)) & 1u;
+}
+
+__device__ __forceinline__ uint32_t out_id(const DevTables &T, uint32_t v) {
+    return T.ext_id ? __ldg(&T.ext_id[v]) : v;
+}
+
+#endif

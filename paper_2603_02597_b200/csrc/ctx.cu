@@ -1,0 +1,485 @@
+// ctx.cu -- host side of the C ABI (include/gpubpe.h): table construction,
+// workspace management, launch and counters.
+//
+// Construction restates what the reference derives from its inputs
+// (byte_codec.py:97-111 base ids, merge_table.py:246-278 the pair table with
+// DuplicatePair detection) and adds the device-only structures described in
+// common.cuh (rl/rr, junction bitmap, well-formedness, verified memo).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/gpubpe.h"
+#include "kernels.cuh"
+
+size_t tile_smem_bytes();
+cudaError_t launch_encode(const EncodeParams &P, int grid_tile, int grid_giant, cudaStream_t s);
+cudaError_t setup_kernels();
+cudaError_t tile_occupancy(int *blocks);
+cudaError_t launch_lookup(const DevTables &T, const uint32_t *l, const uint32_t *r,
+                          unsigned long long n, uint32_t *nw, uint32_t *rank, cudaStream_t s);
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct gpubpe_ctx {
+    int device = 0;
+    int num_sms = 0;
+    int tile_blocks_per_sm = 1;
+    uint32_t flags = 0;
+    DevTables T{};
+    // owned table buffers
+    std::vector<void *> owned;
+    // workspace
+    DevBuf ws_state, ws_wdoc, ws_wclear, ws_gat, ws_recs, ws_status, ws_med, ws_arena;
+    unsigned int epoch = 0;
+    EncodeState *h_state = nullptr;  // pinned
+    std::string err;
+    uint64_t n_ids_identity = 0;
+};
+
+static int fail(gpubpe_ctx *c, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? GPUBPE_ENOMEM : GPUBPE_ECUDA, \
+                        "%s: %s", #call, cudaGetErrorString(e_));                         \
+    } while (0)
+
+template <typename V>
+static int upload(gpubpe_ctx *ctx, const std::vector<V> &h, const V **out) {
+    void *d = nullptr;
+    size_t bytes = std::max<size_t>(h.size() * sizeof(V), 16);
+    CK(cudaMalloc(&d, bytes));
+    ctx->owned.push_back(d);
+    if (!h.empty()) CK(cudaMemcpy(d, h.data(), h.size() * sizeof(V), cudaMemcpyHostToDevice));
+    *out = static_cast<const V *>(d);
+    return GPUBPE_OK;
+}
+
+static int ensure(gpubpe_ctx *ctx, DevBuf &b, size_t bytes, bool zero) {
+    if (b.bytes >= bytes && b.p) return GPUBPE_OK;
+    CK(cudaDeviceSynchronize());
+    if (b.p) CK(cudaFree(b.p));
+    b.p = nullptr;
+    b.bytes = 0;
+    size_t nb = std::max<size_t>(bytes + bytes / 4, 256);
+    CK(cudaMalloc(&b.p, nb));
+    if (zero) CK(cudaMemset(b.p, 0, nb));
+    b.bytes = nb;
+    return GPUBPE_OK;
+}
+
+static uint64_t memo_hash_bytes(const uint8_t *s, uint32_t len) {
+    uint64_t h = memo_hash_init(len);
+    for (uint32_t c = 0; c < len || c == 0; c += 8) {
+        uint64_t ch = 0;
+        for (uint32_t j = c; j < len && j < c + 8; ++j) ch |= (uint64_t)s[j] << (8 * (j - c));
+        h = memo_hash_step(h, ch);
+        if (len <= 8) break;
+    }
+    return h;
+}
+
+static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes,
+                       const int64_t *d_doc_offs, uint64_t n_docs, uint64_t max_seq_len,
+                       uint64_t chunk_budget, uint32_t *d_out_ids, int64_t *d_out_offs,
+                       cudaStream_t s, bool *checked);
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int device, const uint32_t *base_ids, const uint32_t *left,
+                                 const uint32_t *right, const uint32_t *rank,
+                                 const uint32_t *new_tok, uint64_t n_rules,
+                                 const uint32_t *vocab_ids, const uint8_t *vocab_bytes,
+                                 const uint64_t *vocab_offs, uint64_t n_vocab, uint32_t flags,
+                                 gpubpe_ctx **out) {
+    if (!out) return GPUBPE_EINVAL;
+    *out = nullptr;
+    gpubpe_ctx *ctx = new gpubpe_ctx();
+    ctx->device = device;
+    ctx->flags = flags;
+    int rc = GPUBPE_OK;
+    auto bail = [&](int code) {
+        *out = ctx;  // keep the message readable; caller destroys
+        return code;
+    };
+    if (!base_ids || (n_rules && (!left || !right || !rank || !new_tok)))
+        return bail(fail(ctx, GPUBPE_EINVAL, "null table pointer"));
+    {
+        cudaError_t e = cudaSetDevice(device);
+        if (e != cudaSuccess) return bail(fail(ctx, GPUBPE_ECUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e)));
+        cudaDeviceProp prop;
+        cudaGetDeviceProperties(&prop, device);
+        ctx->num_sms = prop.multiProcessorCount;
+        if ((e = setup_kernels()) != cudaSuccess)
+            return bail(fail(ctx, GPUBPE_ECUDA, "kernel setup: %s", cudaGetErrorString(e)));
+        int blocks = 1;
+        tile_occupancy(&blocks);
+        ctx->tile_blocks_per_sm = std::max(1, blocks);
+    }
+
+    // ---- internal ids: used as-is when every id < 2^24, else densely remapped
+    uint64_t max_id = 0;
+    for (int b = 0; b < 256; ++b) max_id = std::max<uint64_t>(max_id, base_ids[b]);
+    for (uint64_t i = 0; i < n_rules; ++i) {
+        max_id = std::max<uint64_t>(max_id, left[i]);
+        max_id = std::max<uint64_t>(max_id, right[i]);
+        max_id = std::max<uint64_t>(max_id, new_tok[i]);
+        if (rank[i] == GPUBPE_INF)
+            return bail(fail(ctx, GPUBPE_EINVAL, "rule %llu: rank 0xFFFFFFFF is reserved", (unsigned long long)i));
+    }
+    const bool identity = max_id < (1ull << 24);
+    std::unordered_map<uint32_t, uint32_t> remap;
+    std::vector<uint32_t> ext;  // internal -> external
+    auto intern = [&](uint32_t x) -> uint32_t {
+        if (identity) return x;
+        auto it = remap.find(x);
+        if (it != remap.end()) return it->second;
+        uint32_t v = (uint32_t)ext.size();
+        remap.emplace(x, v);
+        ext.push_back(x);
+        return v;
+    };
+    std::vector<uint32_t> base(256), L(n_rules), R(n_rules), NW(n_rules);
+    for (int b = 0; b < 256; ++b) base[b] = intern(base_ids[b]);
+    for (uint64_t i = 0; i < n_rules; ++i) {
+        L[i] = intern(left[i]);
+        R[i] = intern(right[i]);
+        NW[i] = intern(new_tok[i]);
+    }
+    const uint64_t n_ids = identity ? max_id + 1 : ext.size();
+
+    // ---- pair table
+    uint64_t cap = 2;
+    while (cap < 2 * n_rules) cap <<= 1;
+    std::vector<uint4> slots(cap, make_uint4(GPUBPE_INF, GPUBPE_INF, 0, 0));
+    for (uint64_t i = 0; i < n_rules; ++i) {
+        uint32_t h = pair_home(L[i], R[i], (uint32_t)(cap - 1));
+        for (;;) {
+            uint4 &sl = slots[h];
+            if (sl.x == GPUBPE_INF && sl.y == GPUBPE_INF) {
+                sl = make_uint4(L[i], R[i], rank[i], NW[i]);
+                break;
+            }
+            if (sl.x == L[i] && sl.y == R[i])
+                return bail(fail(ctx, GPUBPE_ETABLE, "pair (%u, %u) duplicated at rank %u",
+                                 left[i], right[i], rank[i]));
+            h = (h + 1) & (uint32_t)(cap - 1);
+        }
+    }
+    // ---- rl / rr and well-formedness
+    std::vector<uint32_t> rl(n_ids, GPUBPE_INF), rr(n_ids, GPUBPE_INF);
+    std::vector<int64_t> maxprod(n_ids, -1);
+    for (uint64_t i = 0; i < n_rules; ++i) {
+        rl[L[i]] = std::min(rl[L[i]], rank[i]);
+        rr[R[i]] = std::min(rr[R[i]], rank[i]);
+        maxprod[NW[i]] = std::max<int64_t>(maxprod[NW[i]], rank[i]);
+    }
+    bool wf = !(flags & GPUBPE_F_STRICT);
+    for (uint64_t i = 0; i < n_rules && wf; ++i)
+        if ((int64_t)rank[i] <= maxprod[L[i]] || (int64_t)rank[i] <= maxprod[R[i]]) wf = false;
+    // ---- junction bitmap: first/last covered byte sets to a fixpoint
+    std::vector<uint64_t> F(n_ids * 4, 0), B(n_ids * 4, 0);
+    for (int b = 0; b < 256; ++b) {
+        F[base[b] * 4 + (b >> 6)] |= 1ull << (b & 63);
+        B[base[b] * 4 + (b >> 6)] |= 1ull << (b & 63);
+    }
+    std::vector<uint64_t> order(n_rules);
+    for (uint64_t i = 0; i < n_rules; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](uint64_t x, uint64_t y) { return rank[x] < rank[y]; });
+    for (bool changed = true; changed;) {
+        changed = false;
+        for (uint64_t oi : order) {
+            for (int w = 0; w < 4; ++w) {
+                uint64_t f = F[NW[oi] * 4 + w] | F[L[oi] * 4 + w];
+                uint64_t l = B[NW[oi] * 4 + w] | B[R[oi] * 4 + w];
+                if (f != F[NW[oi] * 4 + w] || l != B[NW[oi] * 4 + w]) changed = true;
+                F[NW[oi] * 4 + w] = f;
+                B[NW[oi] * 4 + w] = l;
+            }
+        }
+    }
+    std::vector<uint64_t> J(65536 / 64, 0);  // row x: 256 bits of y
+    for (uint64_t i = 0; i < n_rules; ++i) {
+        for (int x = 0; x < 256; ++x) {
+            if (!((B[L[i] * 4 + (x >> 6)] >> (x & 63)) & 1)) continue;
+            for (int w = 0; w < 4; ++w) J[x * 4 + w] |= F[R[i] * 4 + w];
+        }
+    }
+    std::vector<uint32_t> jbits(2048);
+    for (int k = 0; k < 2048; ++k) jbits[k] = (uint32_t)(J[k >> 1] >> (32 * (k & 1)));
+
+    const uint32_t *d_rl, *d_rr, *d_j, *d_base;
+    const uint4 *d_pairs;
+    if ((rc = upload(ctx, slots, &d_pairs))) return bail(rc);
+    if ((rc = upload(ctx, rl, &d_rl))) return bail(rc);
+    if ((rc = upload(ctx, rr, &d_rr))) return bail(rc);
+    if ((rc = upload(ctx, jbits, &d_j))) return bail(rc);
+    if ((rc = upload(ctx, base, &d_base))) return bail(rc);
+    ctx->T.pairs = d_pairs;
+    ctx->T.pair_mask = (uint32_t)(cap - 1);
+    ctx->T.rl = d_rl;
+    ctx->T.rr = d_rr;
+    ctx->T.jbits = d_j;
+    ctx->T.base = d_base;
+    ctx->T.memo = nullptr;
+    ctx->T.memo_mask = 0;
+    ctx->T.blob = nullptr;
+    ctx->T.well_formed = wf ? 1 : 0;
+    ctx->T.ext_id = nullptr;
+    if (!identity) {
+        const uint32_t *d_ext;
+        if ((rc = upload(ctx, ext, &d_ext))) return bail(rc);
+        ctx->T.ext_id = d_ext;
+    }
+    ctx->h_state = nullptr;
+    {
+        cudaError_t e = cudaMallocHost(&ctx->h_state, sizeof(EncodeState));
+        if (e != cudaSuccess) return bail(fail(ctx, GPUBPE_ENOMEM, "pinned state: %s", cudaGetErrorString(e)));
+        memset(ctx->h_state, 0, sizeof(EncodeState));
+    }
+
+    // ---- memo: vocab strings whose BPE (computed by this engine) is themselves
+    if (!(flags & GPUBPE_F_NO_MEMO) && n_vocab && vocab_ids && vocab_bytes && vocab_offs) {
+        std::vector<uint64_t> cand;
+        std::vector<uint32_t> cand_int;
+        for (uint64_t v = 0; v < n_vocab; ++v) {
+            uint64_t len = vocab_offs[v + 1] - vocab_offs[v];
+            if (len < 2 || len > SHORT_MAX) continue;
+            uint32_t id = vocab_ids[v];
+            uint32_t iid;
+            if (identity) {
+                if (id >= n_ids) continue;
+                iid = id;
+            } else {
+                auto it = remap.find(id);
+                if (it == remap.end()) continue;
+                iid = it->second;
+            }
+            cand.push_back(v);
+            cand_int.push_back(iid);
+        }
+        if (!cand.empty()) {
+            std::vector<uint8_t> hb;
+            std::vector<int64_t> ho(cand.size() + 1, 0);
+            for (size_t k = 0; k < cand.size(); ++k) {
+                uint64_t v = cand[k];
+                hb.insert(hb.end(), vocab_bytes + vocab_offs[v], vocab_bytes + vocab_offs[v + 1]);
+                ho[k + 1] = (int64_t)hb.size();
+            }
+            uint8_t *db = nullptr;
+            int64_t *dof = nullptr, *doo = nullptr;
+            uint32_t *dids = nullptr;
+            CK(cudaMalloc(&db, hb.size()));
+            CK(cudaMalloc(&dof, ho.size() * 8));
+            CK(cudaMalloc(&doo, ho.size() * 8));
+            CK(cudaMalloc(&dids, hb.size() * 4));
+            CK(cudaMemcpy(db, hb.data(), hb.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dof, ho.data(), ho.size() * 8, cudaMemcpyHostToDevice));
+            DevTables saved = ctx->T;
+            ctx->T.ext_id = nullptr;  // verify in internal ids
+            bool checked = false;
+            rc = encode_impl(ctx, db, hb.size(), dof, cand.size(), ~0ull >> 2, ~0ull >> 2, dids,
+                             doo, 0, &checked);
+            ctx->T = saved;
+            if (rc) return bail(rc);
+            CK(cudaDeviceSynchronize());
+            std::vector<int64_t> oo(ho.size());
+            std::vector<uint32_t> oids(hb.size());
+            CK(cudaMemcpy(oo.data(), doo, oo.size() * 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(oids.data(), dids, hb.size() * 4, cudaMemcpyDeviceToHost));
+            cudaFree(db); cudaFree(dof); cudaFree(doo); cudaFree(dids);
+            std::vector<size_t> keep;
+            for (size_t k = 0; k < cand.size(); ++k)
+                if (oo[k + 1] - oo[k] == 1 && oids[oo[k]] == cand_int[k]) keep.push_back(k);
+            uint64_t mcap = 2;
+            while (mcap < 2 * keep.size()) mcap <<= 1;
+            std::vector<uint4> memo(mcap, make_uint4(0, 0, 0, 0));
+            std::vector<uint8_t> blob;
+            for (size_t k : keep) {
+                const uint8_t *sv = hb.data() + ho[k];
+                uint32_t len = (uint32_t)(ho[k + 1] - ho[k]);
+                uint64_t lo = 0;
+                for (uint32_t j = 0; j < len && j < 8; ++j) lo |= (uint64_t)sv[j] << (8 * j);
+                uint32_t boff = (uint32_t)blob.size();
+                if (len > 8) {
+                    if (boff >= (1u << 24)) continue;  // blob offset field is 24 bits
+                    blob.insert(blob.end(), sv, sv + len);
+                }
+                uint32_t h = (uint32_t)memo_hash_bytes(sv, len) & (uint32_t)(mcap - 1);
+                while (memo[h].w != 0) h = (h + 1) & (uint32_t)(mcap - 1);
+                memo[h] = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), cand_int[k],
+                                     len | (len > 8 ? boff << 8 : 0u));
+            }
+            const uint4 *d_memo;
+            const uint8_t *d_blob;
+            if ((rc = upload(ctx, memo, &d_memo))) return bail(rc);
+            if ((rc = upload(ctx, blob, &d_blob))) return bail(rc);
+            ctx->T.memo = d_memo;
+            ctx->T.memo_mask = (uint32_t)(mcap - 1);
+            ctx->T.blob = d_blob;
+        }
+    }
+    *out = ctx;
+    return GPUBPE_OK;
+}
+
+static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes,
+                       const int64_t *d_doc_offs, uint64_t n_docs, uint64_t max_seq_len,
+                       uint64_t chunk_budget, uint32_t *d_out_ids, int64_t *d_out_offs,
+                       cudaStream_t s, bool *checked) {
+    *checked = false;
+    const uint64_t n_win = (n_bytes + WIN - 1) / WIN;
+    const uint64_t n_tiles = (n_bytes + TILE - 1) / TILE;
+    int grid_tile = (int)std::min<uint64_t>(n_tiles, (uint64_t)ctx->num_sms * ctx->tile_blocks_per_sm);
+    int grid_giant = std::max(1, (int)std::min<uint64_t>((n_win + NT - 1) / NT, (uint64_t)ctx->num_sms * 2));
+    int rc;
+    if ((rc = ensure(ctx, ctx->ws_state, sizeof(EncodeState), true))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_wdoc, n_win * 8, false))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_wclear, n_win, false))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_gat, n_win * 4, false))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_recs, n_win * sizeof(GiantRec), false))) return rc;
+    if (ctx->ws_status.bytes < n_tiles * 8) ctx->epoch = 0;
+    if ((rc = ensure(ctx, ctx->ws_status, n_tiles * 8, true))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_med, (size_t)std::max(grid_tile, 1) * MED_BYTES, false))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_arena, 64ull << 20, false))) return rc;
+    if (++ctx->epoch >= (1u << 20)) {
+        CK(cudaMemsetAsync(ctx->ws_status.p, 0, ctx->ws_status.bytes, s));
+        ctx->epoch = 1;
+    }
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        EncodeParams P{};
+        P.T = ctx->T;
+        P.bytes = d_bytes;
+        P.n_bytes = n_bytes;
+        P.doc_offs = reinterpret_cast<const long long *>(d_doc_offs);
+        P.n_docs = n_docs;
+        P.max_seq_len = max_seq_len;
+        P.chunk_budget = chunk_budget;
+        P.out_ids = d_out_ids;
+        P.out_offs = reinterpret_cast<long long *>(d_out_offs);
+        P.st = static_cast<EncodeState *>(ctx->ws_state.p);
+        P.window_doc = static_cast<long long *>(ctx->ws_wdoc.p);
+        P.wclear = static_cast<uint8_t *>(ctx->ws_wclear.p);
+        P.giant_at = static_cast<int *>(ctx->ws_gat.p);
+        P.recs = static_cast<GiantRec *>(ctx->ws_recs.p);
+        P.status = static_cast<unsigned long long *>(ctx->ws_status.p);
+        P.med_scratch = static_cast<uint8_t *>(ctx->ws_med.p);
+        P.arena = static_cast<uint8_t *>(ctx->ws_arena.p);
+        P.arena_cap = ctx->ws_arena.bytes;
+        P.n_win = n_win;
+        P.n_tiles = n_tiles;
+        P.epoch = ctx->epoch;
+        P.strict = (ctx->flags & GPUBPE_F_STRICT) ? 1 : 0;
+        cudaError_t e = launch_encode(P, grid_tile, grid_giant, s);
+        if (e != cudaSuccess) return fail(ctx, GPUBPE_ECUDA, "encode launch: %s", cudaGetErrorString(e));
+        // The arena can only overflow if giant segments exceed its capacity;
+        // 25 bytes of arena per input byte always suffice.
+        if (n_bytes * 25 <= ctx->ws_arena.bytes) return GPUBPE_OK;
+        *checked = true;
+        CK(cudaMemcpyAsync(ctx->h_state, ctx->ws_state.p, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (!ctx->h_state->overflow) return GPUBPE_OK;
+        size_t need = (size_t)ctx->h_state->arena_used * 4;
+        if ((rc = ensure(ctx, ctx->ws_arena, need, false))) return rc;
+        if (++ctx->epoch >= (1u << 20)) {
+            CK(cudaMemsetAsync(ctx->ws_status.p, 0, ctx->ws_status.bytes, s));
+            ctx->epoch = 1;
+        }
+    }
+    return fail(ctx, GPUBPE_ENOMEM, "giant-segment arena kept overflowing");
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes,
+                             const int64_t *d_doc_offs, uint64_t n_docs, uint64_t max_seq_len,
+                             uint64_t chunk_budget, uint32_t *d_out_ids, int64_t *d_out_offs,
+                             void *stream) {
+    if (!ctx) return GPUBPE_EINVAL;
+    if (chunk_budget < 2 || chunk_budget > max_seq_len)
+        return fail(ctx, GPUBPE_EINVAL, "chunk_budget must be in [2, max_seq_len]");
+    if (n_docs && (!d_doc_offs || !d_out_offs)) return fail(ctx, GPUBPE_EINVAL, "null offsets");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device));
+    if (n_bytes == 0 || n_docs == 0) {
+        if (n_docs) CK(cudaMemsetAsync(d_out_offs, 0, (n_docs + 1) * 8, s));
+        int rc = ensure(ctx, ctx->ws_state, sizeof(EncodeState), true);
+        if (rc) return rc;
+        CK(cudaMemsetAsync(ctx->ws_state.p, 0, sizeof(EncodeState), s));
+        return GPUBPE_OK;
+    }
+    if (!d_bytes || !d_out_ids) return fail(ctx, GPUBPE_EINVAL, "null data pointer");
+    bool checked;
+    return encode_impl(ctx, d_bytes, n_bytes, d_doc_offs, n_docs, max_seq_len, chunk_budget,
+                       d_out_ids, d_out_offs, s, &checked);
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out) {
+    if (!ctx || !out) return GPUBPE_EINVAL;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    memset(out, 0, sizeof *out);
+    if (ctx->ws_state.p) {
+        CK(cudaMemcpyAsync(ctx->h_state, ctx->ws_state.p, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    const EncodeState &st = *ctx->h_state;
+    if (st.error) return fail(ctx, GPUBPE_ECUDA, "device reported an internal error (segment bound)");
+    out->n_ids = st.n_ids;
+    out->n_segments = st.n_segments;
+    out->memo_hits = st.memo_hits;
+    out->short_merges = st.short_merges;
+    out->medium_segments = st.medium_segments;
+    out->giant_segments = st.giant_segments;
+    out->giant_bytes = st.giant_bytes;
+    out->engine_passes = st.engine_passes;
+    out->tiles = st.tile_counter;
+    out->overflow = st.overflow;
+    out->well_formed = (uint64_t)ctx->T.well_formed;
+    return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_launches_per_encode(void) { return 3; }
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_lookup_pairs(gpubpe_ctx *ctx, const uint32_t *d_left, const uint32_t *d_right,
+                                   uint64_t n, uint32_t *d_new, uint32_t *d_rank, void *stream) {
+    if (!ctx) return GPUBPE_EINVAL;
+    if (ctx->T.ext_id) return fail(ctx, GPUBPE_EINVAL, "lookup_pairs needs ids < 2^24");
+    CK(cudaSetDevice(ctx->device));
+    CK(launch_lookup(ctx->T, d_left, d_right, n, d_new, d_rank, static_cast<cudaStream_t>(stream)));
+    return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) const char *gpubpe_last_error(gpubpe_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (void *p : ctx->owned) cudaFree(p);
+    for (DevBuf *b : {&ctx->ws_state, &ctx->ws_wdoc, &ctx->ws_wclear, &ctx->ws_gat, &ctx->ws_recs,
+                      &ctx->ws_status, &ctx->ws_med, &ctx->ws_arena})
+        if (b->p) cudaFree(b->p);
+    if (ctx->h_state) cudaFreeHost(ctx->h_state);
+    delete ctx;
+}

@@ -1,0 +1,239 @@
+// engine.cuh -- CTA-cooperative exact multi-merge BPE engine (K3 / K4 core).
+//
+// Runs greedy lowest-rank / leftmost BPE (reference: engines.py:269-335) on one
+// token sequence with the whole CTA, in passes.  Each pass
+//   1. reduces the minimum pair rank r_min (and its leftmost position),
+//   2. selects pairs to merge this pass,
+//   3. applies them with a double-buffered stream compaction and re-probes
+//      only the pairs next to a merge.
+// Selection rule:
+//   * strict mode (table not well-formed, or forced): the single leftmost
+//     global-min pair -- one merge per pass, exactly the reference's order;
+//   * well-formed tables (every rule using token T ranks above every rule
+//     producing T; GPT-2 is): all pairs p with even offset inside their run of
+//     equal-rank pairs and either rank == r_min, or a bounded "blocking walk"
+//     proves no lower-rank merge can reach p before its turn:
+//       left walk  from the run start j: stop OK at j==0 or rr[tok[j]] > r;
+//                  fail if rank(j-1) < r; else j -= 1
+//       right walk from j = p+1: stop OK at the last token or rl[tok[j]] > r;
+//                  fail if rank(j) < r; else j += 1
+//     (rl/rr = min rank of any rule with the token as left/right operand).
+//     Merges in a well-formed table happen in non-decreasing rank order, the
+//     walks show tokens p, p+1 are untouched until time r, and run parity is
+//     the reference's leftmost-first pairing inside a run; the global-min run
+//     starts are always selected, so every pass makes progress.  A truncated
+//     walk only defers a merge.  DESIGN.md "Exactness" has the argument; the
+//     fuzz tests check it against the oracle on random well-formed and
+//     non-well-formed tables.
+// Storage is generic (shared or global memory) so the same code serves the
+// in-tile medium path (per-CTA scratch) and giant segments (arena).
+#pragma once
+#include "common.cuh"
+
+#define ENGINE_WALK 64
+
+struct EngineMem {
+    uint32_t *tok, *tok2;  // tokens, double buffered
+    uint2 *pr, *pr2;       // pair i: {rank, new token}, double buffered
+    uint8_t *sel;          // pair i merged this pass
+};
+
+struct EngineShared {
+    unsigned long long red[32];
+    uint32_t scan[32];
+    unsigned long long kmin;
+    uint32_t carry;
+};
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
+
+// Block-wide min of a u64 (all threads get the result).
+__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, EngineShared &sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_min_u64(v);
+    __syncthreads();
+    if (lane == 0) sh.red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned long long x = lane < nw ? sh.red[lane] : ~0ull;
+        x = warp_min_u64(x);
+        if (lane == 0) sh.kmin = x;
+    }
+    __syncthreads();
+    return sh.kmin;
+}
+
+// Block exclusive prefix sum of v; *total gets the block sum.
+__device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, EngineShared &sh, uint32_t *total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) sh.scan[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t s = lane < nw ? sh.scan[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) sh.scan[lane] = s;  // inclusive warp totals
+    }
+    __syncthreads();
+    uint32_t before = wid ? sh.scan[wid - 1] : 0;
+    *total = sh.scan[nw - 1];
+    return before + x - v;
+}
+
+// Block inclusive max-scan of v (values >= 0).
+__device__ __forceinline__ uint32_t block_incl_max(uint32_t v, EngineShared &sh, uint32_t *total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = max(x, y);
+    }
+    __syncthreads();
+    if (lane == 31) sh.scan[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t s = lane < nw ? sh.scan[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s = max(s, y);
+        }
+        if (lane < nw) sh.scan[lane] = s;
+    }
+    __syncthreads();
+    uint32_t before = wid ? sh.scan[wid - 1] : 0;
+    *total = sh.scan[nw - 1];
+    return max(before, x);
+}
+
+__device__ __forceinline__ bool walk_left(const DevTables &T, const uint32_t *tok, const uint2 *pr,
+                                          uint32_t j, uint32_t r) {
+    for (int step = 0; step < ENGINE_WALK; ++step) {
+        if (j == 0) return true;
+        if (__ldg(&T.rr[tok[j]]) > r) return true;
+        if (pr[j - 1].x < r) return false;
+        --j;
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool walk_right(const DevTables &T, const uint32_t *tok, const uint2 *pr,
+                                           uint32_t j, uint32_t n, uint32_t r) {
+    for (int step = 0; step < ENGINE_WALK; ++step) {
+        if (j + 1 >= n) return true;
+        if (__ldg(&T.rl[tok[j]]) > r) return true;
+        if (pr[j].x < r) return false;
+        ++j;
+    }
+    return false;
+}
+
+// Runs the engine on M.tok[0..n).  Returns the output length; *out points at
+// the buffer holding the result.  Must be called by every thread of the CTA.
+static __device__ uint32_t engine_run(const DevTables &T, EngineMem M, uint32_t n, bool strict,
+                               EngineShared &sh, uint32_t *passes_out, const uint32_t **out) {
+    const uint32_t nt = blockDim.x;
+    uint32_t passes = 0;
+    for (uint32_t b = 0; b < n; b += nt) {
+        uint32_t i = b + threadIdx.x;
+        if (i + 1 < n) {
+            PairHit h = probe_pair(T, M.tok[i], M.tok[i + 1]);
+            M.pr[i] = make_uint2(h.rank, h.nw);
+        }
+    }
+    __syncthreads();
+    while (n >= 2) {
+        // 1. min (rank, position)
+        unsigned long long mine = ~0ull;
+        for (uint32_t b = 0; b < n - 1; b += nt) {
+            uint32_t i = b + threadIdx.x;
+            if (i < n - 1) {
+                uint32_t r = M.pr[i].x;
+                if (r != GPUBPE_INF) {
+                    unsigned long long k = ((unsigned long long)r << 32) | i;
+                    mine = k < mine ? k : mine;
+                }
+            }
+        }
+        unsigned long long kmin = block_min_u64(mine, sh);
+        if (kmin == ~0ull) break;
+        const uint32_t rmin = (uint32_t)(kmin >> 32);
+        const uint32_t pmin = (uint32_t)kmin;
+        // 2. selection
+        if (strict) {
+            for (uint32_t b = 0; b < n; b += nt) {
+                uint32_t i = b + threadIdx.x;
+                if (i < n) M.sel[i] = (i == pmin);
+            }
+        } else {
+            uint32_t carry = 0;
+            for (uint32_t b = 0; b < n; b += nt) {
+                uint32_t i = b + threadIdx.x;
+                bool pair = i + 1 < n;
+                uint32_t r = pair ? M.pr[i].x : GPUBPE_INF;
+                bool start = pair && (i == 0 || M.pr[i - 1].x != r);
+                uint32_t chunk_max;
+                uint32_t s = block_incl_max(start ? i : 0u, sh, &chunk_max);
+                s = max(s, carry);
+                carry = max(carry, chunk_max);
+                bool ok = pair && r != GPUBPE_INF && ((i - s) & 1u) == 0;
+                if (ok && r != rmin)
+                    ok = walk_left(T, M.tok, M.pr, s, r) && walk_right(T, M.tok, M.pr, i + 1, n, r);
+                if (i < n) M.sel[i] = ok;
+            }
+        }
+        __syncthreads();
+        // 3. apply + compact
+        uint32_t carry = 0;
+        for (uint32_t b = 0; b < n; b += nt) {
+            uint32_t j = b + threadIdx.x;
+            bool keep = j < n && !(j > 0 && M.sel[j - 1]);
+            uint32_t total;
+            uint32_t pos = carry + block_excl_sum(keep ? 1u : 0u, sh, &total);
+            carry += total;
+            if (keep) {
+                bool sj = M.sel[j];
+                uint2 pj = (j + 1 < n) ? M.pr[j] : make_uint2(GPUBPE_INF, 0);
+                uint32_t t = sj ? pj.y : M.tok[j];
+                M.tok2[pos] = t;
+                uint32_t jn = sj ? j + 2 : j + 1;
+                if (jn < n) {
+                    bool sn = M.sel[jn];
+                    uint32_t tn = sn ? M.pr[jn].y : M.tok[jn];
+                    if (sj || sn) {
+                        PairHit h = probe_pair(T, t, tn);
+                        M.pr2[pos] = make_uint2(h.rank, h.nw);
+                    } else {
+                        M.pr2[pos] = pj;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        n = carry;
+        uint32_t *tt = M.tok; M.tok = M.tok2; M.tok2 = tt;
+        uint2 *pp = M.pr; M.pr = M.pr2; M.pr2 = pp;
+        ++passes;
+    }
+    *passes_out = passes;
+    *out = M.tok;
+    return n;
+}

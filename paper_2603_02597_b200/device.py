@@ -1,0 +1,176 @@
+"""Device context: one per (tokenizer, GPU).  Wraps the C ABI of libgpubpe.so.
+
+`DeviceEncoder` owns the device tables (pair table, rl/rr, junction bitmap,
+memo) and the encode workspace.  Inputs and outputs are torch tensors only at
+this boundary; the kernels see raw pointers.  There is no CPU path: every
+method raises DeviceError when CUDA or the extension is unavailable.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _native
+from .errors import DeviceError, DuplicatePair
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+
+def _require_cuda():
+    if torch is None or not torch.cuda.is_available():
+        raise DeviceError("the GPT-2 BPE engine needs a CUDA device (no CPU fallback)")
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data) if a.size else None
+
+
+class DeviceEncoder:
+    """Device-resident tables for one merge table on one GPU."""
+
+    def __init__(self, base_ids, left, right, rank, new, vocab_ids=None, vocab_blob=None,
+                 vocab_offs=None, device: int | None = None, memo: bool = True,
+                 strict: bool = False):
+        _require_cuda()
+        lib = _native.load()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        arrs = [np.ascontiguousarray(x, dtype=np.uint32) for x in (left, right, rank, new)]
+        base = np.ascontiguousarray(base_ids, dtype=np.uint32)
+        if vocab_ids is None:
+            vocab_ids = np.empty(0, np.uint32)
+            vocab_blob = np.empty(0, np.uint8)
+            vocab_offs = np.zeros(1, np.uint64)
+        vids = np.ascontiguousarray(vocab_ids, dtype=np.uint32)
+        vblob = np.ascontiguousarray(vocab_blob, dtype=np.uint8)
+        voffs = np.ascontiguousarray(vocab_offs, dtype=np.uint64)
+        flags = (0 if memo else _native.F_NO_MEMO) | (_native.F_STRICT if strict else 0)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            rc = lib.gpubpe_ctx_create(self.device, _ptr(base), *[_ptr(a) for a in arrs],
+                                       len(arrs[0]), _ptr(vids), _ptr(vblob), _ptr(voffs),
+                                       len(vids), flags, ctypes.byref(h))
+        if rc != _native.OK:
+            msg = lib.gpubpe_last_error(h).decode() if h.value else ""
+            if h.value:
+                lib.gpubpe_ctx_destroy(h)
+            if rc == _native.ETABLE:
+                raise DuplicatePair(msg)
+            _native.check(rc, None, f"gpubpe_ctx_create: {msg}")
+        self._h = h
+        self._lib = lib
+        self._lock = threading.Lock()
+        self._pinned: dict[str, torch.Tensor] = {}
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.gpubpe_ctx_destroy(h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ device API
+
+    def encode_into(self, data: "torch.Tensor", doc_offs: "torch.Tensor", out_ids: "torch.Tensor",
+                    out_offs: "torch.Tensor", max_seq_len: int, chunk_budget: int,
+                    stream=None) -> None:
+        """Enqueue one encode on `stream` (default: current).  All tensors on
+        this device: data uint8[n], doc_offs int64[n_docs+1], out_ids
+        int32[>= n], out_offs int64[n_docs+1].  Asynchronous."""
+        n = data.numel()
+        n_docs = doc_offs.numel() - 1
+        if n_docs < 0:
+            raise ValueError("doc_offs must hold n_docs + 1 entries")
+        if out_ids.numel() < n or out_offs.numel() != n_docs + 1:
+            raise ValueError("output tensors too small")
+        for t, dt in ((data, torch.uint8), (doc_offs, torch.int64), (out_ids, torch.int32),
+                      (out_offs, torch.int64)):
+            if t.dtype != dt or not t.is_cuda or not t.is_contiguous() or t.device.index != self.device:
+                raise ValueError(f"expected contiguous {dt} on cuda:{self.device}, got {t.dtype} {t.device}")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self._lib.gpubpe_encode(self._h, data.data_ptr(), n, doc_offs.data_ptr(), n_docs,
+                                     int(max_seq_len), int(chunk_budget), out_ids.data_ptr(),
+                                     out_offs.data_ptr(), s.cuda_stream)
+        _native.check(rc, self._h, "gpubpe_encode")
+
+    def query(self, stream=None) -> dict:
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        st = _native.Stats()
+        rc = self._lib.gpubpe_query(self._h, s.cuda_stream, ctypes.byref(st))
+        _native.check(rc, self._h, "gpubpe_query")
+        return st.as_dict()
+
+    def encode_tensors(self, data, doc_offs, max_seq_len: int, chunk_budget: int):
+        """Device CSR in -> device CSR out: (ids int32[total], offsets int64[n_docs+1]).
+        Synchronises once (to learn the total)."""
+        with self._lock, torch.cuda.device(self.device):
+            n_docs = doc_offs.numel() - 1
+            out_ids = torch.empty(max(data.numel(), 1), dtype=torch.int32, device=data.device)
+            out_offs = torch.empty(n_docs + 1, dtype=torch.int64, device=data.device)
+            self.encode_into(data, doc_offs, out_ids, out_offs, max_seq_len, chunk_budget)
+            st = self.query()
+            total = int(out_offs[-1].item()) if n_docs >= 0 and data.numel() else 0
+            return out_ids[:total], out_offs, st
+
+    def lookup_pairs(self, left: np.ndarray, right: np.ndarray):
+        """(new uint32[], rank uint32[]) from the device table; rank 2**32-1 = miss."""
+        with self._lock, torch.cuda.device(self.device):
+            l = torch.from_numpy(np.ascontiguousarray(left, np.uint32).view(np.int32)).cuda()
+            r = torch.from_numpy(np.ascontiguousarray(right, np.uint32).view(np.int32)).cuda()
+            nw = torch.empty_like(l)
+            rk = torch.empty_like(l)
+            s = torch.cuda.current_stream()
+            rc = self._lib.gpubpe_lookup_pairs(self._h, l.data_ptr(), r.data_ptr(), l.numel(),
+                                               nw.data_ptr(), rk.data_ptr(), s.cuda_stream)
+            _native.check(rc, self._h, "gpubpe_lookup_pairs")
+            return nw.cpu().numpy().view(np.uint32), rk.cpu().numpy().view(np.uint32)
+
+    # ------------------------------------------------------------ host API
+
+    def _staging(self, key: str, n: int, dtype):
+        t = self._pinned.get(key)
+        if t is None or t.numel() < n:
+            t = torch.empty(max(n, 1 << 16), dtype=dtype, pin_memory=True)
+            self._pinned[key] = t
+        return t
+
+    def encode_packed_host(self, data: np.ndarray, offs: np.ndarray, max_seq_len: int,
+                           chunk_budget: int):
+        """Host CSR in -> host CSR out, timed.  Returns (ids uint32[], offs int64[],
+        stats, engine_ms)."""
+        with self._lock, torch.cuda.device(self.device):
+            n = int(data.size)
+            n_docs = int(offs.size) - 1
+            hb = self._staging("bytes", n, torch.uint8)
+            ho = self._staging("offs", n_docs + 1, torch.int64)
+            hb.numpy()[:n] = data
+            ho.numpy()[: n_docs + 1] = offs
+            dev = torch.device("cuda", self.device)
+            d_data = hb[: max(n, 1)].to(dev, non_blocking=True)[:n]
+            d_offs = ho[: n_docs + 1].to(dev, non_blocking=True)
+            out_ids = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            out_offs = torch.empty(n_docs + 1, dtype=torch.int64, device=dev)
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            self.encode_into(d_data, d_offs, out_ids, out_offs, max_seq_len, chunk_budget)
+            ev1.record()
+            h_offs = out_offs.cpu().numpy()
+            st = self.query()
+            total = int(h_offs[-1]) if n_docs >= 0 and n else 0
+            hi = self._staging("ids", total, torch.int32)
+            hi[:total].copy_(out_ids[:total])
+            ids = hi.numpy()[:total].view(np.uint32).copy()
+            if n == 0:
+                h_offs = np.zeros(n_docs + 1, dtype=np.int64)
+            return ids, h_offs, st, ev0.elapsed_time(ev1)

@@ -1,0 +1,168 @@
+"""Merge rules and the packed pair table (host side, construction time).
+
+Mirrors /root/reference/pkg/src/lanebpe/merge_table.py:
+  * `parse_merges` (:88-116): rank = 0-based rule line, an initial '#' line is a
+    header, new_token = vocab[left_sym + right_sym], MalformedLine/UnknownSymbol;
+  * `PackedPairTable` / `build_table` (:140-278): key (left<<32)|right, value
+    (new<<32)|rank, murmur3 fmix64, power-of-two linear probing at <= 50% load,
+    empty key 2**64-1, DuplicatePair / ReservedKey.  Slots are laid out exactly
+    as the reference lays them out (same hash, same insertion order), so a
+    table built by either package can be handed to the other.
+
+The device never probes this table: the context (device.py) re-packs the rules
+into its own L2-resident layout (csrc/tables.cu).  `rule_arrays()` recovers the
+rules from any object with the reference's `keys` / `values` / `count` fields.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .byte_codec import Vocab
+from .errors import DuplicatePair, MalformedLine, ReservedKey, UnknownSymbol
+
+U32_MASK = 0xFFFF_FFFF
+U64_MASK = 0xFFFF_FFFF_FFFF_FFFF
+EMPTY_KEY = U64_MASK
+_M1 = 0xFF51_AFD7_ED55_8CCD
+_M2 = 0xC4CE_B9FE_1A85_EC53
+
+
+def pack_key(left: int, right: int) -> int:
+    return (left << 32) | right
+
+
+def pack_value(new_token: int, rank: int) -> int:
+    return (new_token << 32) | rank
+
+
+def unpack_value(value: int) -> tuple[int, int]:
+    return value >> 32, value & U32_MASK
+
+
+def fmix64(x: int) -> int:
+    x &= U64_MASK
+    x = ((x ^ (x >> 33)) * _M1) & U64_MASK
+    x = ((x ^ (x >> 33)) * _M2) & U64_MASK
+    return x ^ (x >> 33)
+
+
+def fmix64_array(x: np.ndarray) -> np.ndarray:
+    x = np.asarray(x, dtype=np.uint64).copy()
+    with np.errstate(over="ignore"):
+        x ^= x >> np.uint64(33)
+        x *= np.uint64(_M1)
+        x ^= x >> np.uint64(33)
+        x *= np.uint64(_M2)
+        x ^= x >> np.uint64(33)
+    return x
+
+
+@dataclass(frozen=True)
+class MergeRule:
+    left: int
+    right: int
+    rank: int
+    new_token: int
+
+
+def parse_merges(merges_text, vocab: Vocab) -> list[MergeRule]:
+    if isinstance(merges_text, (bytes, bytearray)):
+        merges_text = merges_text.decode("utf-8")
+    lines = merges_text.splitlines()
+    skip = 1 if lines and lines[0].startswith("#") else 0
+    ids = vocab.symbol_to_id
+    rules = []
+    for rank, line in enumerate(lines[skip:]):
+        lineno = rank + skip + 1
+        parts = line.split(" ")
+        if len(parts) != 2 or not all(parts):
+            raise MalformedLine(f"line {lineno}: expected two symbols, got {line!r}")
+        a, b = parts
+        missing = next((s for s in (a, b, a + b) if s not in ids), None)
+        if missing is not None:
+            raise UnknownSymbol(f"line {lineno}: symbol {missing!r} not in vocabulary")
+        rules.append(MergeRule(ids[a], ids[b], rank, ids[a + b]))
+    return rules
+
+
+class PackedPairTable:
+    """Open-addressing pair table with the reference's exact slot layout."""
+
+    __slots__ = ("keys", "values", "capacity", "count", "_mask")
+
+    def __init__(self, keys: np.ndarray, values: np.ndarray, count: int):
+        self.keys = keys
+        self.values = values
+        self.capacity = len(keys)
+        self.count = count
+        self._mask = self.capacity - 1
+
+    def lookup(self, left: int, right: int):
+        key = pack_key(left, right)
+        if key == EMPTY_KEY:
+            return None
+        i = fmix64(key) & self._mask
+        while True:
+            k = int(self.keys[i])
+            if k == key:
+                return unpack_value(int(self.values[i]))
+            if k == EMPTY_KEY:
+                return None
+            i = (i + 1) & self._mask
+
+    def lookup_pairs(self, left: np.ndarray, right: np.ndarray):
+        """Vectorised probe: (found bool[], new_tokens u64[], ranks u64[])."""
+        key = (np.asarray(left, np.uint64) << np.uint64(32)) | np.asarray(right, np.uint64)
+        n = len(key)
+        found = np.zeros(n, dtype=bool)
+        vals = np.zeros(n, dtype=np.uint64)
+        idx = fmix64_array(key) & np.uint64(self._mask)
+        live = np.nonzero(key != np.uint64(EMPTY_KEY))[0]
+        while len(live):
+            slot = self.keys[idx[live]]
+            hit = slot == key[live]
+            found[live[hit]] = True
+            vals[live[hit]] = self.values[idx[live[hit]]]
+            live = live[~hit & (slot != np.uint64(EMPTY_KEY))]
+            idx[live] = (idx[live] + np.uint64(1)) & np.uint64(self._mask)
+        return found, vals >> np.uint64(32), vals & np.uint64(U32_MASK)
+
+
+def build_table(rules) -> PackedPairTable:
+    count = len(rules)
+    cap = 1
+    while cap < 2 * count:
+        cap <<= 1
+    mask = cap - 1
+    keys = [EMPTY_KEY] * cap
+    vals = [0] * cap
+    packed = [pack_key(r.left, r.right) for r in rules]
+    homes = (fmix64_array(np.array(packed, dtype=np.uint64)) & np.uint64(mask)).tolist() if rules else []
+    for rule, key, i in zip(rules, packed, homes):
+        if key == EMPTY_KEY:
+            raise ReservedKey(f"pair ({rule.left}, {rule.right}) packs to the empty-slot sentinel")
+        while keys[i] != EMPTY_KEY:
+            if keys[i] == key:
+                raise DuplicatePair(
+                    f"pair ({rule.left}, {rule.right}) already inserted at rank "
+                    f"{vals[i] & U32_MASK}, duplicated at rank {rule.rank}")
+            i = (i + 1) & mask
+        keys[i] = key
+        vals[i] = pack_value(rule.new_token, rule.rank)
+    return PackedPairTable(np.array(keys, dtype=np.uint64), np.array(vals, dtype=np.uint64), count)
+
+
+def rule_arrays(table) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
+    """(left, right, rank, new) uint32 arrays recovered from a packed table,
+    ordered by rank.  Works for this package's and the reference's tables."""
+    keys = np.asarray(table.keys, dtype=np.uint64)
+    vals = np.asarray(table.values, dtype=np.uint64)
+    used = keys != np.uint64(EMPTY_KEY)
+    k, v = keys[used], vals[used]
+    order = np.argsort(v & np.uint64(U32_MASK), kind="stable")
+    k, v = k[order], v[order]
+    return ((k >> np.uint64(32)).astype(np.uint32), (k & np.uint64(U32_MASK)).astype(np.uint32),
+            (v & np.uint64(U32_MASK)).astype(np.uint32), (v >> np.uint64(32)).astype(np.uint32))

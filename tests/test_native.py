@@ -1,0 +1,56 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol that
+include/gpubpe.h declares (no compute calls here)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "gpubpe.h"
+
+
+def declared_symbols() -> set[str]:
+    text = HEADER.read_text()
+    return set(re.findall(r"\b(gpubpe_[a-z_]+)\s*\(", text))
+
+
+def test_header_declares_the_api():
+    syms = declared_symbols()
+    assert {"gpubpe_ctx_create", "gpubpe_encode", "gpubpe_query", "gpubpe_last_error",
+            "gpubpe_ctx_destroy", "gpubpe_lookup_pairs", "gpubpe_launches_per_encode"} <= syms
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2603_02597_b200 import _native
+
+    if not _native.LIB_PATH.exists():
+        pytest.skip("libgpubpe.so not built (run __graft_entry__.build())")
+    lib = ctypes.CDLL(str(_native.LIB_PATH))
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing
+    assert set(_native.SIGNATURES) == declared_symbols()
+    _native.load()
+    assert lib.gpubpe_launches_per_encode() == 3
+
+
+def test_stats_struct_matches_header():
+    from paper_2603_02597_b200 import _native
+
+    text = HEADER.read_text()
+    body = text[text.index("typedef struct gpubpe_stats"): text.index("} gpubpe_stats;")]
+    fields = re.findall(r"uint64_t\s+(\w+);", body)
+    assert fields == [f for f, _ in _native.Stats._fields_]
+
+
+def test_device_api_refuses_without_cuda(tokenizer):
+    import torch
+
+    from paper_2603_02597_b200.errors import DeviceError
+    import paper_2603_02597_b200 as bpe
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    with pytest.raises(DeviceError):
+        bpe.tokenize_batch([b"hello"], tokenizer)

@@ -1,0 +1,181 @@
+"""Deterministic synthetic English-like text for parity fixtures and the bench.
+
+WikiText-103 is not available offline, so the benchmark text is generated:
+Zipf-weighted GPT-2 word tokens (the vocab symbols "Ġ[a-z]+" that are
+dictionary words, ranked by id, which tracks merge rank and therefore corpus
+frequency),
+capitalised sentence starts, commas, numbers, sentence punctuation and
+paragraph breaks ("\\n\\n").  Generation is vectorised numpy, deterministic for
+a given (seed, numpy version).
+
+`SIZES` pins, for each named workload, the byte length that BPE-encodes to the
+named number of output tokens under whole-sequence semantics (P-whole).  The
+lengths were calibrated with the CPU oracle (oracle/, pinned to the reference)
+by tests/golden/make_golden.py; the bench re-checks the count on the device.
+"""
+
+from __future__ import annotations
+
+import gzip
+import json
+from functools import lru_cache
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent.parent
+GPT2_DIR = REPO / "tests" / "golden" / "gpt2"
+VOCAB_GZ = GPT2_DIR / "vocab.json.gz"
+MERGES_GZ = GPT2_DIR / "merges.txt.gz"
+
+# name -> (seed, n_bytes, expected P-whole tokens); filled by make_golden.py
+SIZES_FILE = REPO / "tests" / "golden" / "synth_sizes.json"
+
+
+WORDS_GZ = REPO / "tests" / "golden" / "synth_words.txt.gz"
+
+
+@lru_cache(maxsize=1)
+def _word_table():
+    """Returns (blob uint8, offs int64, lens int64, probs, n) for the word pool.
+
+    synth_words.txt.gz lists the GPT-2 "Ġ[a-z]+" symbols that are dictionary
+    words, in GPT-2 id order (made once by tests/golden/make_golden.py).
+    """
+    words = gzip.decompress(WORDS_GZ.read_bytes()).decode("ascii").split()
+    lower = [(" " + w).encode("ascii") for w in words]
+    n = len(lower)
+    ranks = np.arange(n, dtype=np.float64)
+    probs = 1.0 / np.power(ranks + 2.7, 1.07)
+    probs /= probs.sum()
+    variants = []  # [lower, capitalised with space, capitalised no space]
+    for w in lower:
+        variants.append(w)
+    for w in lower:
+        variants.append(b" " + w[1:2].upper() + w[2:])
+    for w in lower:
+        variants.append(w[1:2].upper() + w[2:])
+    lens = np.array([len(v) for v in variants], dtype=np.int64)
+    offs = np.zeros(len(variants) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(lens)
+    blob = np.frombuffer(b"".join(variants), dtype=np.uint8)
+    return blob, offs, lens, probs, n
+
+
+def _numbers(rng: np.random.Generator, k: int) -> list[bytes]:
+    out = []
+    kinds = rng.integers(0, 4, size=k)
+    vals = rng.integers(0, 100000, size=k)
+    for kind, v in zip(kinds, vals):
+        if kind == 0:
+            out.append(b" %d" % (1800 + v % 225))
+        elif kind == 1:
+            out.append(b" %d" % (v % 100))
+        elif kind == 2:
+            out.append(b" %d.%d" % (v % 50, v % 10))
+        else:
+            out.append((" " + format(int(v) * 10, ",")).encode())
+    return out
+
+
+BLOCK_WORDS = 1 << 16
+
+
+def _block(seed: int, i: int) -> bytes:
+    """Block i of the stream for `seed` (~380 KB); blocks are independent."""
+    blob, offs, lens, probs, n = _word_table()
+    rng = np.random.default_rng([seed, i])
+    k = BLOCK_WORDS
+    idx = rng.choice(n, size=k, p=probs)
+    # sentence structure: 6..20 words, paragraph break after ~1 in 5 sentences
+    sent_len = rng.integers(6, 21, size=k // 6 + 2)
+    ends = np.cumsum(sent_len)
+    ends = ends[ends < k]
+    starts = np.concatenate(([0], ends))
+    para = rng.random(len(starts)) < 0.2
+    variant = np.zeros(k, dtype=np.int64)
+    variant[starts] = 1
+    variant[starts[para]] = 2
+    if i == 0:
+        variant[0] = 2
+    wid = idx + variant * n
+    wl = lens[wid]
+    pos = np.repeat(offs[wid] - np.concatenate(([0], np.cumsum(wl)[:-1])), wl)
+    text = blob[pos + np.arange(int(wl.sum()))].tobytes()
+    # splice punctuation / numbers at word boundaries
+    bounds = np.concatenate(([0], np.cumsum(wl)))
+    marks: dict[int, bytes] = {}
+    punct = rng.random(len(ends))
+    for e, p, brk in zip(ends, punct, para[1 : len(ends) + 1]):
+        mark = b"." if p < 0.9 else (b"?" if p < 0.95 else b"!")
+        marks[int(bounds[e])] = mark + (b"\n\n" if brk else b"")
+    for c in np.nonzero(rng.random(k) < 0.06)[0]:
+        marks.setdefault(int(bounds[c + 1]), b",")
+    nums = np.nonzero(rng.random(k) < 0.02)[0]
+    for c, t in zip(nums, _numbers(rng, len(nums))):
+        b = int(bounds[c + 1])
+        marks[b] = marks.get(b, b"") + t
+    pieces = []
+    last = 0
+    for b in sorted(marks):
+        pieces.append(text[last:b])
+        pieces.append(marks[b])
+        last = b
+    pieces.append(text[last:])
+    return b"".join(pieces) + b"."
+
+
+def english_bytes(n_bytes: int, seed: int = 0) -> bytes:
+    """The first n_bytes of the synthetic prose stream for `seed`.
+
+    The stream is a concatenation of independently seeded blocks, so a
+    shorter request is always a prefix of a longer one.
+    """
+    parts = []
+    total = 0
+    i = 0
+    while total < n_bytes:
+        blk = _block(seed, i)
+        parts.append(blk)
+        total += len(blk)
+        i += 1
+    return b"".join(parts)[: max(n_bytes, 0)]
+
+
+def load_sizes() -> dict:
+    if SIZES_FILE.exists():
+        return json.loads(SIZES_FILE.read_text())
+    return {}
+
+
+def workload_doc(name: str) -> tuple[bytes, int]:
+    """(bytes, expected P-whole token count) for a calibrated named workload."""
+    spec = load_sizes()[name]
+    return english_bytes(spec["n_bytes"], spec["seed"]), spec["tokens_whole"]
+
+
+def corpus_docs(total_bytes: int, seed: int = 0, min_doc: int = 1024, max_doc: int = 65536,
+                pool_bytes: int = 64 << 20) -> tuple[np.ndarray, np.ndarray]:
+    """Packed corpus of documents with log-uniform sizes in [min_doc, max_doc].
+
+    Documents are slices of a pool of generated prose (so 10 GB does not need
+    10 GB of generation).  Returns (uint8 data, int64 offsets).
+    """
+    rng = np.random.default_rng(seed + 7919)
+    pool = np.frombuffer(english_bytes(min(pool_bytes, max(total_bytes, max_doc) + max_doc), seed),
+                         dtype=np.uint8)
+    sizes = []
+    acc = 0
+    while acc < total_bytes:
+        s = int(np.exp(rng.uniform(np.log(min_doc), np.log(max_doc))))
+        s = min(s, total_bytes - acc)
+        sizes.append(s)
+        acc += s
+    sizes = np.array(sizes, dtype=np.int64)
+    offs = np.zeros(len(sizes) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(sizes)
+    starts = rng.integers(0, len(pool) - max_doc, size=len(sizes))
+    data = np.empty(int(offs[-1]), dtype=np.uint8)
+    for i, (s, st) in enumerate(zip(sizes, starts)):
+        data[offs[i] : offs[i + 1]] = pool[st : st + s]
+    return data, offs
