@@ -1,0 +1,333 @@
+#!/usr/bin/env python3
+"""Benchmark: GPT-2 BPE encode tokens/sec on a 131k-token sequence (B200).
+
+Contract:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+One step = one encode of one synthetic 131,072-token English-like sequence
+(configs[1] of BASELINE.json, the metric's workload), whole-sequence semantics
+(P-whole: no fixed-offset chunking), input resident in HBM.  L2 is flushed
+(256 MiB write) before every timed step, outside the step's events.  With
+N > 1 (torchrun), every rank encodes its own sequence (replicas; weak scaling,
+no collective on the data path); value = all ranks' tokens / max-over-ranks time.
+
+The line also carries: e2e (same metric through the public API,
+tokenize_batch, with host bytes in and host ids out), roofline (k_encode,
+the only kernel, HBM-bound), cpu_baseline (the CPU oracle port of the
+reference's sequential engine on this host), clocks (NVML during the timed
+region) and gpu_launches.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tools"))
+
+WORKLOAD = "c1_131k"
+METRIC = "GPT-2 BPE encode tokens/sec at 131k-token seqs; p50 latency per sequence"
+UNIT = "tokens/s"
+WHOLE = 1 << 40  # max_seq_len = chunk_budget beyond any input: P-whole
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default=WORKLOAD)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def load_workload(name: str):
+    import fixtures
+    import synth_corpus
+
+    spec = fixtures.synth_sizes()[name]
+    doc = synth_corpus.english_bytes(spec["n_bytes"], spec["seed"])
+    return doc, spec
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as exc:  # pragma: no cover - NVML is in the image
+            self._nv = None
+            self.error = str(exc)
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                get = getattr(self._nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    self._nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                mask = get(self._h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self._nv:
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self) -> dict:
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ reference arm
+
+
+def run_reference(args, rank, world):
+    """The reference's CPU path on this host: the oracle port (oracle/) of
+    sequential_bpe + tokenize_batch (the reference is pure Python and cannot
+    travel to this box; the port is pinned to its goldens)."""
+    if rank != 0:
+        return
+    from oracle.oracle import OracleEncoder, default_threads, load_tables
+    import fixtures
+    import numpy as np
+
+    doc, spec = load_workload(args.workload)
+    orc = OracleEncoder.from_tables(load_tables(*fixtures.gpt2_paths()))
+    threads = default_threads()
+    data = np.frombuffer(doc, dtype=np.uint8)
+    # size each step so the whole run stays within ~150 s
+    t0 = time.perf_counter()
+    ids, _, _ = orc.encode_packed(data, np.array([0, len(doc)]), WHOLE, WHOLE, threads)
+    est = time.perf_counter() - t0
+    n = len(doc)
+    frac = min(1.0, 150.0 / max(1e-9, est * (args.steps + args.warmup)))
+    cut = max(1024, int(n * frac))
+    sample = data[:cut]
+    offs = np.array([0, cut], dtype=np.int64)
+    for _ in range(args.warmup):
+        orc.encode_packed(sample, offs, WHOLE, WHOLE, threads)
+    times, toks = [], 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        out, _, _ = orc.encode_packed(sample, offs, WHOLE, WHOLE, threads)
+        times.append(time.perf_counter() - t0)
+        toks = len(out)
+    total = sum(times)
+    value = toks * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / len(times),
+        "p50_ms": 1000 * statistics.median(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8->u32", "data": "synthetic",
+        "config": {"workload": args.workload, "bytes": int(cut), "semantics": "P-whole",
+                   "tokens_per_step": int(toks)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"first {cut} of {n} bytes of {args.workload} per step; oracle port "
+                                   "of engines.py:269-335 sequential_bpe (one P-whole sequence is one "
+                                   f"chunk, so 1 of {threads} threads works)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(doc, seconds: float) -> dict:
+    from oracle.oracle import OracleEncoder, load_tables
+    import fixtures
+    import numpy as np
+
+    orc = OracleEncoder.from_tables(load_tables(*fixtures.gpt2_paths()))
+    data = np.frombuffer(doc, dtype=np.uint8)
+    offs = np.array([0, len(doc)], dtype=np.int64)
+    times, toks = [], 0
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or not times:
+        t0 = time.perf_counter()
+        out, _, _ = orc.encode_packed(data, offs, WHOLE, WHOLE, 1)
+        times.append(time.perf_counter() - t0)
+        toks = len(out)
+    return {"value": toks / statistics.median(times), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{len(times)} x whole {WORKLOAD} sequence ({len(doc)} B -> {toks} ids), P-whole, "
+                      "oracle port of the reference sequential engine (engines.py:269-335), 1 thread, "
+                      "median run"}
+
+
+# ------------------------------------------------------------------ our arm
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import numpy as np
+    import torch
+
+    import paper_2603_02597_b200 as bpe
+    import fixtures
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    doc, spec = load_workload(args.workload)
+    tok = bpe.Tokenizer.from_files(*fixtures.gpt2_paths(),
+                                   bpe.BlockConfig(max_seq_len=WHOLE, chunk_budget=WHOLE))
+    enc = tok.device_encoder(local)
+    dev = torch.device("cuda", local)
+    n = len(doc)
+    d_data = torch.frombuffer(bytearray(doc), dtype=torch.uint8).to(dev)
+    d_offs = torch.tensor([0, n], dtype=torch.int64, device=dev)
+    out_ids = torch.empty(n, dtype=torch.int32, device=dev)
+    out_offs = torch.empty(2, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        enc.encode_into(d_data, d_offs, out_ids, out_offs, WHOLE, WHOLE, stream)
+
+    # correctness of the measured configuration
+    step()
+    st = enc.query()
+    n_ids = int(out_offs[1].item())
+    assert n_ids == spec["tokens_whole"], (n_ids, spec["tokens_whole"])
+    import hashlib
+
+    digest = hashlib.sha256(out_ids[:n_ids].cpu().numpy().astype("<u4").tobytes()).hexdigest()
+    assert digest == spec["sha_whole"], "device ids differ from the reference digest"
+
+    enc.set_profiling(True)
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kern = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev0[i].record(stream)
+            step()
+            ev1[i].record(stream)
+            kern.append(enc.kernel_ms())  # syncs on this step only
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * n_ids * args.steps / (total_ms / 1000.0)
+    ms_per_step = total_ms / args.steps
+    k_tile = kern
+    t_tile = statistics.mean(k_tile) / 1000.0
+    b_alg = n + 4 * n_ids + 16 * 2  # bytes in + ids out + offsets in/out
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = b_alg / t_tile / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get(args.workload, {}).get("k_tile_dram_bytes")
+
+    # e2e through the public API: host bytes in, host ids out
+    e2e = None
+    if rank == 0 or True:
+        for _ in range(3):
+            bpe.tokenize_batch([doc], tok)
+        e2e_t = []
+        for _ in range(min(args.steps, 100)):
+            t0 = time.perf_counter()
+            r = bpe.tokenize_batch([doc], tok)
+            e2e_t.append(time.perf_counter() - t0)
+        assert len(r.token_ids[0]) == n_ids
+        e2e = {"value": world * n_ids / statistics.median(e2e_t), "unit": UNIT,
+               "h2d_bytes_per_step": n + 16, "d2h_bytes_per_step": 4 * n_ids + 16,
+               "p50_ms": 1000 * statistics.median(e2e_t), "api": "tokenize_batch"}
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    cpu = cpu_baseline(doc, args.cpu_seconds) if world == 1 else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "p50_ms": statistics.median(step_ms), "p90_ms": sorted(step_ms)[int(0.9 * (len(step_ms) - 1))],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8->u32",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "bytes": n, "tokens": n_ids, "semantics": "P-whole",
+                   "docs_per_gpu": 1, "l2": "flushed (256 MiB write) before every step",
+                   "parallelism": f"replicas x{world}"},
+        "e2e": e2e,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "k_encode",
+                     "alg_bytes_per_launch": b_alg, "kernel_ms": statistics.mean(k_tile),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)" if peaks else "fallback"},
+        "kernel_ms": {"k_encode": statistics.mean(k_tile), "k_encode_p50": statistics.median(k_tile)},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+        "gpu_launches": args.steps,
+        "device_stats": st,
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

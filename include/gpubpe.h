@@ -87,7 +87,7 @@ int gpubpe_ctx_create(int device, const uint32_t *base_ids, const uint32_t *left
  *   d_out_ids                 capacity n_bytes uint32 ids
  *   d_out_offs[n_docs+1]      int64 CSR offsets of the ids
  *   stream                    cudaStream_t (NULL = legacy default stream)
- * Asynchronous: returns once the kernels are enqueued, except when the input
+ * Asynchronous: returns once the kernel is enqueued, except when the input
  * is large enough that the giant-segment arena might overflow, in which case
  * it synchronises the stream and re-runs with a larger arena.
  */
@@ -100,7 +100,8 @@ int gpubpe_encode(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes,
  * (BatchResult.counters, chunker.py:56-64). */
 int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out);
 
-/* Number of encode kernels one gpubpe_encode enqueues (launch accounting). */
+/* Number of kernels one gpubpe_encode enqueues (launch accounting): 1, the
+ * fused persistent k_encode. */
 int gpubpe_launches_per_encode(void);
 
 /* Device-side probe of the packed pair table: for i < n, (d_left[i],
@@ -109,6 +110,13 @@ int gpubpe_launches_per_encode(void);
  * conformance tests. */
 int gpubpe_lookup_pairs(gpubpe_ctx *ctx, const uint32_t *d_left, const uint32_t *d_right,
                         uint64_t n, uint32_t *d_new, uint32_t *d_rank, void *stream);
+
+/* Kernel timing of subsequent encodes: when on, CUDA events are recorded on
+ * the encode stream around the encode kernel (k_encode).  gpubpe_kernel_ms
+ * synchronises on the last encode and writes its kernel duration in ms to
+ * ms[0] (n >= 1). */
+int gpubpe_set_profiling(gpubpe_ctx *ctx, int on);
+int gpubpe_kernel_ms(gpubpe_ctx *ctx, float *ms, int n);
 
 const char *gpubpe_last_error(gpubpe_ctx *ctx);
 void gpubpe_ctx_destroy(gpubpe_ctx *ctx);

@@ -43,6 +43,8 @@ SIGNATURES = {
     "gpubpe_query": (_int, [_vp, _vp, ctypes.POINTER(Stats)]),
     "gpubpe_launches_per_encode": (_int, []),
     "gpubpe_lookup_pairs": (_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),
+    "gpubpe_set_profiling": (_int, [_vp, _int]),
+    "gpubpe_kernel_ms": (_int, [_vp, ctypes.POINTER(ctypes.c_float), _int]),
     "gpubpe_last_error": (ctypes.c_char_p, [_vp]),
     "gpubpe_ctx_destroy": (None, [_vp]),
 }

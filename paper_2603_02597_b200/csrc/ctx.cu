@@ -19,7 +19,8 @@
 #include "kernels.cuh"
 
 size_t tile_smem_bytes();
-cudaError_t launch_encode(const EncodeParams &P, int grid_tile, int grid_giant, cudaStream_t s);
+cudaError_t launch_encode(const EncodeParams &P, int grid, cudaStream_t s, cudaEvent_t *ev,
+                          const cudaAccessPolicyWindow *win);
 cudaError_t setup_kernels();
 cudaError_t tile_occupancy(int *blocks);
 cudaError_t launch_lookup(const DevTables &T, const uint32_t *l, const uint32_t *r,
@@ -40,14 +41,21 @@ struct gpubpe_ctx {
     int tile_blocks_per_sm = 1;
     uint32_t flags = 0;
     DevTables T{};
-    // owned table buffers
-    std::vector<void *> owned;
+    // all device tables live in one allocation, pinned in L2 by an access
+    // policy window on every encode launch
+    uint8_t *tables = nullptr;
+    size_t tables_bytes = 0, tables_used = 0;
+    cudaAccessPolicyWindow win{};
     // workspace
-    DevBuf ws_state, ws_wdoc, ws_wclear, ws_gat, ws_recs, ws_status, ws_med, ws_arena;
+    DevBuf ws_state, ws_status, ws_med, ws_arena;
     unsigned int epoch = 0;
+    uint64_t calls = 0;  // selects the EncodeState slot (two, alternating)
     EncodeState *h_state = nullptr;  // pinned
     std::string err;
-    uint64_t n_ids_identity = 0;
+    bool profiling = false;
+    uint64_t last_n_bytes = 0;
+    bool timed = false;  // events of the last encode are valid
+    cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 
 static int fail(gpubpe_ctx *c, int code, const char *fmt, ...) {
@@ -68,14 +76,18 @@ static int fail(gpubpe_ctx *c, int code, const char *fmt, ...) {
                         "%s: %s", #call, cudaGetErrorString(e_));                         \
     } while (0)
 
+static size_t table_slot(size_t bytes) { return (std::max<size_t>(bytes, 16) + 255) & ~(size_t)255; }
+
 template <typename V>
 static int upload(gpubpe_ctx *ctx, const std::vector<V> &h, const V **out) {
-    void *d = nullptr;
-    size_t bytes = std::max<size_t>(h.size() * sizeof(V), 16);
-    CK(cudaMalloc(&d, bytes));
-    ctx->owned.push_back(d);
+    size_t bytes = table_slot(h.size() * sizeof(V));
+    if (ctx->tables_used + bytes > ctx->tables_bytes)
+        return fail(ctx, GPUBPE_ENOMEM, "table arena too small (%zu + %zu > %zu)", ctx->tables_used,
+                    bytes, ctx->tables_bytes);
+    uint8_t *d = ctx->tables + ctx->tables_used;
+    ctx->tables_used += bytes;
     if (!h.empty()) CK(cudaMemcpy(d, h.data(), h.size() * sizeof(V), cudaMemcpyHostToDevice));
-    *out = static_cast<const V *>(d);
+    *out = reinterpret_cast<const V *>(d);
     return GPUBPE_OK;
 }
 
@@ -230,6 +242,28 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
     std::vector<uint32_t> jbits(2048);
     for (int k = 0; k < 2048; ++k) jbits[k] = (uint32_t)(J[k >> 1] >> (32 * (k & 1)));
 
+    // memo upper bounds (the memo is built after a verification encode)
+    uint64_t memo_cand = 0, blob_max = 0;
+    if (!(flags & GPUBPE_F_NO_MEMO) && n_vocab && vocab_ids && vocab_bytes && vocab_offs)
+        for (uint64_t v = 0; v < n_vocab; ++v) {
+            uint64_t len = vocab_offs[v + 1] - vocab_offs[v];
+            if (len < 2 || len > SHORT_MAX) continue;
+            ++memo_cand;
+            if (len > 8) blob_max += len;
+        }
+    uint64_t memo_cap_max = 2;
+    while (memo_cap_max < 2 * memo_cand) memo_cap_max <<= 1;
+    {
+        size_t need = table_slot(slots.size() * sizeof(uint4)) + 2 * table_slot(n_ids * 4) +
+                      table_slot(jbits.size() * 4) + table_slot(256 * 4) +
+                      (identity ? 0 : table_slot(ext.size() * 4)) +
+                      table_slot(memo_cap_max * sizeof(uint4)) + table_slot(blob_max);
+        void *d = nullptr;
+        cudaError_t e = cudaMalloc(&d, need);
+        if (e != cudaSuccess) return bail(fail(ctx, GPUBPE_ENOMEM, "tables (%zu B): %s", need, cudaGetErrorString(e)));
+        ctx->tables = static_cast<uint8_t *>(d);
+        ctx->tables_bytes = need;
+    }
     const uint32_t *d_rl, *d_rr, *d_j, *d_base;
     const uint4 *d_pairs;
     if ((rc = upload(ctx, slots, &d_pairs))) return bail(rc);
@@ -256,6 +290,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
     ctx->h_state = nullptr;
     {
         cudaError_t e = cudaMallocHost(&ctx->h_state, sizeof(EncodeState));
+        (void)0;
         if (e != cudaSuccess) return bail(fail(ctx, GPUBPE_ENOMEM, "pinned state: %s", cudaGetErrorString(e)));
         memset(ctx->h_state, 0, sizeof(EncodeState));
     }
@@ -341,6 +376,24 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
             ctx->T.blob = d_blob;
         }
     }
+    // ---- keep the tables resident in L2 across unrelated traffic
+    {
+        cudaDeviceProp prop;
+        cudaGetDeviceProperties(&prop, device);
+        size_t want = std::min<size_t>(ctx->tables_used, (size_t)prop.persistingL2CacheMaxSize);
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        cudaGetLastError();
+        size_t win = std::min<size_t>(ctx->tables_used, (size_t)prop.accessPolicyMaxWindowSize);
+        if (want && win) {
+            ctx->win.base_ptr = ctx->tables;
+            ctx->win.num_bytes = win;
+            ctx->win.hitRatio = std::min(1.0f, (float)want / (float)win);
+            ctx->win.hitProp = cudaAccessPropertyPersisting;
+            ctx->win.missProp = cudaAccessPropertyStreaming;
+        }
+    }
     *out = ctx;
     return GPUBPE_OK;
 }
@@ -350,25 +403,21 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
                        uint64_t chunk_budget, uint32_t *d_out_ids, int64_t *d_out_offs,
                        cudaStream_t s, bool *checked) {
     *checked = false;
-    const uint64_t n_win = (n_bytes + WIN - 1) / WIN;
     const uint64_t n_tiles = (n_bytes + TILE - 1) / TILE;
-    int grid_tile = (int)std::min<uint64_t>(n_tiles, (uint64_t)ctx->num_sms * ctx->tile_blocks_per_sm);
-    int grid_giant = std::max(1, (int)std::min<uint64_t>((n_win + NT - 1) / NT, (uint64_t)ctx->num_sms * 2));
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(n_tiles, (uint64_t)ctx->num_sms * ctx->tile_blocks_per_sm));
     int rc;
-    if ((rc = ensure(ctx, ctx->ws_state, sizeof(EncodeState), true))) return rc;
-    if ((rc = ensure(ctx, ctx->ws_wdoc, n_win * 8, false))) return rc;
-    if ((rc = ensure(ctx, ctx->ws_wclear, n_win, false))) return rc;
-    if ((rc = ensure(ctx, ctx->ws_gat, n_win * 4, false))) return rc;
-    if ((rc = ensure(ctx, ctx->ws_recs, n_win * sizeof(GiantRec), false))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_state, 2 * sizeof(EncodeState), true))) return rc;
     if (ctx->ws_status.bytes < n_tiles * 8) ctx->epoch = 0;
     if ((rc = ensure(ctx, ctx->ws_status, n_tiles * 8, true))) return rc;
-    if ((rc = ensure(ctx, ctx->ws_med, (size_t)std::max(grid_tile, 1) * MED_BYTES, false))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_med, (size_t)grid * MED_BYTES, false))) return rc;
     if ((rc = ensure(ctx, ctx->ws_arena, 64ull << 20, false))) return rc;
-    if (++ctx->epoch >= (1u << 20)) {
-        CK(cudaMemsetAsync(ctx->ws_status.p, 0, ctx->ws_status.bytes, s));
-        ctx->epoch = 1;
-    }
     for (int attempt = 0; attempt < 3; ++attempt) {
+        if (++ctx->epoch >= (1u << 20)) {
+            CK(cudaMemsetAsync(ctx->ws_status.p, 0, ctx->ws_status.bytes, s));
+            ctx->epoch = 1;
+        }
+        EncodeState *slots = static_cast<EncodeState *>(ctx->ws_state.p);
+        const uint64_t k = ctx->calls++;
         EncodeParams P{};
         P.T = ctx->T;
         P.bytes = d_bytes;
@@ -379,34 +428,27 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.chunk_budget = chunk_budget;
         P.out_ids = d_out_ids;
         P.out_offs = reinterpret_cast<long long *>(d_out_offs);
-        P.st = static_cast<EncodeState *>(ctx->ws_state.p);
-        P.window_doc = static_cast<long long *>(ctx->ws_wdoc.p);
-        P.wclear = static_cast<uint8_t *>(ctx->ws_wclear.p);
-        P.giant_at = static_cast<int *>(ctx->ws_gat.p);
-        P.recs = static_cast<GiantRec *>(ctx->ws_recs.p);
+        P.st = slots + (k & 1);
+        P.st_next = slots + ((k + 1) & 1);
         P.status = static_cast<unsigned long long *>(ctx->ws_status.p);
         P.med_scratch = static_cast<uint8_t *>(ctx->ws_med.p);
         P.arena = static_cast<uint8_t *>(ctx->ws_arena.p);
         P.arena_cap = ctx->ws_arena.bytes;
-        P.n_win = n_win;
         P.n_tiles = n_tiles;
         P.epoch = ctx->epoch;
         P.strict = (ctx->flags & GPUBPE_F_STRICT) ? 1 : 0;
-        cudaError_t e = launch_encode(P, grid_tile, grid_giant, s);
+        cudaError_t e = launch_encode(P, grid, s, ctx->profiling ? ctx->ev : nullptr, &ctx->win);
+        ctx->timed = ctx->profiling;
         if (e != cudaSuccess) return fail(ctx, GPUBPE_ECUDA, "encode launch: %s", cudaGetErrorString(e));
-        // The arena can only overflow if giant segments exceed its capacity;
-        // 25 bytes of arena per input byte always suffice.
-        if (n_bytes * 25 <= ctx->ws_arena.bytes) return GPUBPE_OK;
+        // Giant segments need ENGINE_BYTES(len) of arena; 25 B per input byte
+        // (+64 per segment) always suffices, else check and re-run.
+        if (n_bytes * 25 + 4096 <= ctx->ws_arena.bytes) return GPUBPE_OK;
         *checked = true;
-        CK(cudaMemcpyAsync(ctx->h_state, ctx->ws_state.p, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->h_state, P.st, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (!ctx->h_state->overflow) return GPUBPE_OK;
         size_t need = (size_t)ctx->h_state->arena_used * 4;
         if ((rc = ensure(ctx, ctx->ws_arena, need, false))) return rc;
-        if (++ctx->epoch >= (1u << 20)) {
-            CK(cudaMemsetAsync(ctx->ws_status.p, 0, ctx->ws_status.bytes, s));
-            ctx->epoch = 1;
-        }
     }
     return fail(ctx, GPUBPE_ENOMEM, "giant-segment arena kept overflowing");
 }
@@ -421,11 +463,15 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *
     if (n_docs && (!d_doc_offs || !d_out_offs)) return fail(ctx, GPUBPE_EINVAL, "null offsets");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CK(cudaSetDevice(ctx->device));
+    ctx->last_n_bytes = n_docs ? n_bytes : 0;
+    ctx->timed = false;
     if (n_bytes == 0 || n_docs == 0) {
         if (n_docs) CK(cudaMemsetAsync(d_out_offs, 0, (n_docs + 1) * 8, s));
-        int rc = ensure(ctx, ctx->ws_state, sizeof(EncodeState), true);
+        int rc = ensure(ctx, ctx->ws_state, 2 * sizeof(EncodeState), true);
         if (rc) return rc;
-        CK(cudaMemsetAsync(ctx->ws_state.p, 0, sizeof(EncodeState), s));
+        const uint64_t k = ctx->calls++;
+        CK(cudaMemsetAsync(static_cast<EncodeState *>(ctx->ws_state.p) + (k & 1), 0, sizeof(EncodeState), s));
+        CK(cudaMemsetAsync(static_cast<EncodeState *>(ctx->ws_state.p) + ((k + 1) & 1), 0, sizeof(EncodeState), s));
         return GPUBPE_OK;
     }
     if (!d_bytes || !d_out_ids) return fail(ctx, GPUBPE_EINVAL, "null data pointer");
@@ -438,14 +484,19 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_query(gpubpe_ctx *c
     if (!ctx || !out) return GPUBPE_EINVAL;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     memset(out, 0, sizeof *out);
-    if (ctx->ws_state.p) {
-        CK(cudaMemcpyAsync(ctx->h_state, ctx->ws_state.p, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
+    if (ctx->ws_state.p && ctx->calls) {
+        const EncodeState *last = static_cast<const EncodeState *>(ctx->ws_state.p) + ((ctx->calls - 1) & 1);
+        CK(cudaMemcpyAsync(ctx->h_state, last, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
+    } else {
+        memset(ctx->h_state, 0, sizeof(EncodeState));
     }
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
     const EncodeState &st = *ctx->h_state;
     if (st.error) return fail(ctx, GPUBPE_ECUDA, "device reported an internal error (segment bound)");
+    out->n_bytes = ctx->last_n_bytes;
     out->n_ids = st.n_ids;
+    out->passes = out->n_bytes - st.n_ids;
     out->n_segments = st.n_segments;
     out->memo_hits = st.memo_hits;
     out->short_merges = st.short_merges;
@@ -459,7 +510,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_query(gpubpe_ctx *c
     return GPUBPE_OK;
 }
 
-extern "C" __attribute__((visibility("default"))) int gpubpe_launches_per_encode(void) { return 3; }
+extern "C" __attribute__((visibility("default"))) int gpubpe_launches_per_encode(void) { return 1; }
 
 extern "C" __attribute__((visibility("default"))) int gpubpe_lookup_pairs(gpubpe_ctx *ctx, const uint32_t *d_left, const uint32_t *d_right,
                                    uint64_t n, uint32_t *d_new, uint32_t *d_rank, void *stream) {
@@ -470,16 +521,34 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_lookup_pairs(gpubpe
     return GPUBPE_OK;
 }
 
+extern "C" __attribute__((visibility("default"))) int gpubpe_set_profiling(gpubpe_ctx *ctx, int on) {
+    if (!ctx) return GPUBPE_EINVAL;
+    CK(cudaSetDevice(ctx->device));
+    if (on && !ctx->ev[0])
+        for (auto &e : ctx->ev) CK(cudaEventCreate(&e));
+    ctx->profiling = on != 0;
+    return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_kernel_ms(gpubpe_ctx *ctx, float *ms, int n) {
+    if (!ctx || !ms) return GPUBPE_EINVAL;
+    if (!ctx->timed) return fail(ctx, GPUBPE_EINVAL, "no profiled encode yet (gpubpe_set_profiling)");
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    if (n >= 1) CK(cudaEventElapsedTime(&ms[0], ctx->ev[0], ctx->ev[1]));
+    return GPUBPE_OK;
+}
+
 extern "C" __attribute__((visibility("default"))) const char *gpubpe_last_error(gpubpe_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    for (void *p : ctx->owned) cudaFree(p);
-    for (DevBuf *b : {&ctx->ws_state, &ctx->ws_wdoc, &ctx->ws_wclear, &ctx->ws_gat, &ctx->ws_recs,
-                      &ctx->ws_status, &ctx->ws_med, &ctx->ws_arena})
+    if (ctx->tables) cudaFree(ctx->tables);
+    for (DevBuf *b : {&ctx->ws_state, &ctx->ws_status, &ctx->ws_med, &ctx->ws_arena})
         if (b->p) cudaFree(b->p);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
     delete ctx;
 }

@@ -1,41 +1,39 @@
-// kernels.cuh -- the encode kernels and their launch parameters.
+// kernels.cuh -- the fused encode kernel and its launch parameters.
 //
-//   K0 k_windows  one thread per WIN-byte window: owning document (binary
-//                 search of the doc offsets), and whether the window holds no
-//                 segment boundary at all ("clear").  A segment containing a
-//                 clear window is "giant"; every other segment is < 2*WIN bytes.
-//   K1 k_giant    finds runs of clear windows (= giant segments), resolves
-//                 their exact extent and runs the CTA engine on each in a
-//                 global-memory arena.
-//   K2 k_tile     persistent, one TILE of bytes per iteration: byte -> id map,
-//                 junction/document/chunk boundaries, per-segment BPE (memo
-//                 probe, per-thread greedy, CTA engine for medium segments),
-//                 decoupled look-back for the output offset, coalesced id
-//                 store, document offsets.
+// k_encode is ONE persistent launch per batch.  Each CTA repeatedly takes the
+// next TILE bytes (dynamic tile counter, so tiles are taken in order) and:
+//   1. stages the tile (+HALO) in shared memory, maps bytes to ids,
+//   2. marks segment boundaries: junction bitmap misses, document starts,
+//      fixed-offset chunk cuts (P-default semantics),
+//   3. encodes every segment that STARTS in the tile:
+//        len 1                    base id
+//        2..32, vocab string      one memo probe
+//        2..32, other             one warp, exact multi-merge in registers
+//        33..MED_MAX              whole CTA, exact multi-merge in scratch
+//        longer ("giant")         whole CTA, exact multi-merge in the arena
+//   4. publishes its id count and finds its output offset by decoupled
+//      look-back over the tile status words,
+//   5. stores ids (coalesced) and the CSR offsets of documents starting in it.
 #pragma once
-#include <cuda/atomic>
-
 #include "common.cuh"
 #include "engine.cuh"
+#include "warp_engine.cuh"
 
 #define TILE 2048            // bytes per tile
-#define WIN 1024             // giant-detection window (TILE % WIN == 0)
-#define HALO 256             // bytes loaded past the tile end
-#define LD (TILE + HALO)     // bytes held in shared memory per tile
-#define NT 256               // threads per CTA (all kernels)
-#define SHORT_MAX 32         // longest segment merged by one thread
-#define MED_MAX (2 * WIN)    // longest non-giant segment (+1)
-#define NOSEG 0xFFFFu        // "segment end beyond the loaded bytes"
-#define PENDING 0xFFFFFFFFu  // count filled by the cooperative phase
+#define HALO 256             // bytes staged past the tile end
+#define LD (TILE + HALO)     // bytes staged per tile
+#define NT 256               // threads per CTA
+#define SHORT_MAX 32         // longest segment a warp encodes in registers
+#define MED_MAX LD           // longest segment encoded in per-CTA scratch
+#define NOSEG 0xFFFFu        // segment end lies past the staged bytes
 
-// Per-call device state, zeroed by k_windows.
+// Per-call device state, zeroed at the start of every encode.
 struct EncodeState {
     unsigned long long tile_counter;
-    unsigned long long n_giant;
-    unsigned long long arena_used;
+    unsigned long long arena_used;  // u32 words requested from the arena
     unsigned long long overflow;
     unsigned long long error;
-    // stats
+    // counters
     unsigned long long n_ids;
     unsigned long long n_segments;
     unsigned long long memo_hits;
@@ -44,12 +42,6 @@ struct EncodeState {
     unsigned long long giant_segments;
     unsigned long long giant_bytes;
     unsigned long long engine_passes;
-};
-
-struct GiantRec {
-    unsigned long long start, end;  // byte positions [start, end)
-    unsigned long long out_off;     // element offset of the result in the arena (u32 units)
-    unsigned long long count;       // ids produced
 };
 
 struct EncodeParams {
@@ -61,19 +53,17 @@ struct EncodeParams {
     unsigned long long max_seq_len, chunk_budget;
     uint32_t *out_ids;
     long long *out_offs;
-    // workspace
-    EncodeState *st;
-    long long *window_doc;       // [n_win]
-    uint8_t *wclear;             // [n_win]
-    int *giant_at;               // [n_win] record index of the giant segment starting in window
-    GiantRec *recs;              // [n_win]
+    EncodeState *st;       // this call's state (zeroed by the previous call)
+    EncodeState *st_next;  // the next call's state, zeroed here by CTA 0
     unsigned long long *status;  // [n_tiles] look-back words
-    uint8_t *med_scratch;        // [grid_tile * MED_BYTES]
-    uint8_t *arena;
+    uint8_t *med_scratch;        // [grid * MED_BYTES]
+    uint8_t *arena;              // giant segments
     unsigned long long arena_cap;
-    unsigned long long n_win, n_tiles;
-    unsigned int epoch;  // look-back tag (20 bits)
+    unsigned long long n_tiles;
+    unsigned int epoch;          // look-back tag (20 bits)
     int strict;
 };
 
-#define MED_BYTES ((size_t)MED_MAX * 25 + 64)
+// engine scratch for n tokens: tok, tok2 (u32) + pr, pr2 (uint2) + sel (u8)
+#define ENGINE_BYTES(n) ((size_t)(n) * 25 + 64)
+#define MED_BYTES ENGINE_BYTES(MED_MAX)

@@ -103,6 +103,15 @@ class DeviceEncoder:
                                      out_offs.data_ptr(), s.cuda_stream)
         _native.check(rc, self._h, "gpubpe_encode")
 
+    def set_profiling(self, on: bool) -> None:
+        _native.check(self._lib.gpubpe_set_profiling(self._h, int(on)), self._h, "set_profiling")
+
+    def kernel_ms(self) -> float:
+        """Duration (ms) of the encode kernel of the last profiled encode."""
+        arr = (ctypes.c_float * 1)()
+        _native.check(self._lib.gpubpe_kernel_ms(self._h, arr, 1), self._h, "kernel_ms")
+        return float(arr[0])
+
     def query(self, stream=None) -> dict:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         st = _native.Stats()

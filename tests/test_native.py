@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing
     assert set(_native.SIGNATURES) == declared_symbols()
     _native.load()
-    assert lib.gpubpe_launches_per_encode() == 3
+    assert lib.gpubpe_launches_per_encode() == 1
 
 
 def test_stats_struct_matches_header():
