@@ -10,7 +10,7 @@ Mirrors /root/reference/pkg/src/lanebpe/merge_table.py:
     table built by either package can be handed to the other.
 
 The device never probes this table: the context (device.py) re-packs the rules
-into its own L2-resident layout (csrc/tables.cu).  `rule_arrays()` recovers the
+into its own L2-resident layout (csrc/ctx.cu).  `rule_arrays()` recovers the
 rules from any object with the reference's `keys` / `values` / `count` fields.
 """
 

@@ -1,0 +1,97 @@
+#!/usr/bin/env python3
+"""Aggregate an ncu SASS source page by CUDA source line.
+
+  python tools/ncu_lines.py REPORT.ncu-rep [--kernel k_encode] [--top 40]
+
+ncu's CUDA-source view needs the source on the profiling box; the SASS view
+does not.  This maps SASS offsets to file:line with `nvdisasm -g` on the cubin
+inside libgpubpe.so (built with -lineinfo) and sums warp-stall samples and
+executed instructions per line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import re
+import subprocess
+import tempfile
+from collections import defaultdict
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+LIB = ROOT / "paper_2603_02597_b200" / "libgpubpe.so"
+
+
+def line_map(kernel: str) -> dict[int, tuple[str, int]]:
+    tmp = Path(tempfile.mkdtemp())
+    subprocess.run(["cuobjdump", "-xelf", "all", str(LIB)], cwd=tmp, check=True, capture_output=True)
+    out: dict[int, tuple[str, int]] = {}
+    for cub in tmp.glob("*.cubin"):
+        txt = subprocess.run(["nvdisasm", "-g", str(cub)], capture_output=True, text=True).stdout
+        inside, cur = False, None
+        for ln in txt.splitlines():
+            if ln.startswith(".text."):
+                inside = kernel in ln
+                continue
+            if not inside:
+                continue
+            m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
+            if m:
+                cur = (Path(m.group(1)).name, int(m.group(2)))
+                continue
+            m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
+            if m and cur:
+                out[int(m.group(1), 16)] = cur
+        if out:
+            break
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("report")
+    ap.add_argument("--kernel", default="k_encode")
+    ap.add_argument("--top", type=int, default=40)
+    args = ap.parse_args()
+    raw = subprocess.run(["ncu", "-i", args.report, "--page", "source", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    hdr = rows[hdr_i]
+    ci = {n: hdr.index(n) for n in ("Address", "Source", "Warp Stall Sampling (All Samples)",
+                                     "Instructions Executed")}
+    body = [r for r in rows[hdr_i + 1:] if len(r) == len(hdr)]
+    base = int(body[0][ci["Address"]], 16)
+    lm = line_map(args.kernel)
+    samples, insts = defaultdict(int), defaultdict(int)
+    tot_s = tot_i = 0
+    for r in body:
+        off = int(r[ci["Address"]], 16) - base
+        key = lm.get(off, ("?", 0))
+        s = int(r[ci["Warp Stall Sampling (All Samples)"]] or 0)
+        n = int(r[ci["Instructions Executed"]] or 0)
+        samples[key] += s
+        insts[key] += n
+        tot_s += s
+        tot_i += n
+    src_cache: dict[str, list[str]] = {}
+
+    def text(f, l):
+        if f not in src_cache:
+            p = ROOT / "paper_2603_02597_b200" / "csrc" / f
+            src_cache[f] = p.read_text().splitlines() if p.exists() else []
+        lines = src_cache[f]
+        return lines[l - 1].strip()[:70] if 0 < l <= len(lines) else ""
+
+    print(f"total stall samples {tot_s}, warp instructions {tot_i}")
+    print(f"{'file:line':28s} {'stall%':>7s} {'inst%':>7s}  source")
+    for key in sorted(samples, key=lambda k: -samples[k])[: args.top]:
+        f, l = key
+        print(f"{f + ':' + str(l):28s} {100 * samples[key] / max(tot_s, 1):6.2f}% "
+              f"{100 * insts[key] / max(tot_i, 1):6.2f}%  {text(f, l)}")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,142 @@
+#!/usr/bin/env python3
+"""Device-time sweep of the encode kernel over the SURVEY §8(d) workloads.
+
+  python tools/perf.py [--iters K] [--only name,...] [--memo 0|1] [--json out.json]
+
+For each workload: input resident in HBM, W warm-ups, then K encodes each
+preceded by an L2 flush (256 MiB write); CUDA events on the launching stream
+around the encode only.  Prints p50 kernel time, tokens/s, input GB/s and the
+HBM-roofline fraction of the algorithmic bytes (n_bytes + 4 n_ids + 16 (n_docs+1)).
+Also the profiling driver for ncu (--iters 3 --no-flush).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tools"))
+
+WHOLE = 1 << 40
+
+
+def workloads():
+    import numpy as np
+
+    import fixtures
+    import synth_corpus
+
+    sizes = fixtures.synth_sizes()
+
+    def single(name):
+        spec = sizes[name]
+        doc = synth_corpus.english_bytes(spec["n_bytes"], spec["seed"])
+        return np.frombuffer(doc, np.uint8), np.array([0, len(doc)], np.int64), spec["tokens_whole"]
+
+    def batch(n_docs, doc_bytes, seed):
+        pool = np.frombuffer(synth_corpus.english_bytes(n_docs * doc_bytes + (1 << 20), seed), np.uint8)
+        offs = np.arange(n_docs + 1, dtype=np.int64) * doc_bytes
+        return pool[: n_docs * doc_bytes].copy(), offs, None
+
+    def corpus(mb):
+        data, offs = synth_corpus.corpus_docs(mb << 20, seed=0)
+        return data, offs, None
+
+    def adversarial(kind, n):
+        rng = np.random.default_rng(0)
+        if kind == "digits":
+            d = rng.integers(48, 58, n, dtype=np.uint8)
+        elif kind == "letters":
+            d = rng.integers(97, 123, n, dtype=np.uint8)
+        else:
+            d = np.full(n, {"newlines": 10, "aaaa": 97}[kind], np.uint8)
+        return d, np.array([0, n], np.int64), None
+
+    return {
+        "c1_8k": lambda: single("c1_8k"),
+        "c1_32k": lambda: single("c1_32k"),
+        "c1_131k": lambda: single("c1_131k"),
+        "c3_1m": lambda: single("c3_1m"),
+        "c2_4096x512": lambda: batch(4096, 2300, 5),
+        "corpus_256m": lambda: corpus(256),
+        "adv_digits_1m": lambda: adversarial("digits", 1 << 20),
+        "adv_letters_1m": lambda: adversarial("letters", 1 << 20),
+        "adv_newlines_1m": lambda: adversarial("newlines", 1 << 20),
+        "adv_aaaa_1m": lambda: adversarial("aaaa", 1 << 20),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--only", default="")
+    ap.add_argument("--memo", type=int, default=1)
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--json", default="")
+    args = ap.parse_args()
+
+    import numpy as np
+    import torch
+
+    import fixtures
+    import paper_2603_02597_b200 as bpe
+
+    peaks_p = ROOT / "MEASURED_PEAKS.json"
+    peak = json.loads(peaks_p.read_text())["hbm_gbs"] if peaks_p.exists() else 6650.0
+    tok = bpe.Tokenizer.from_files(*fixtures.gpt2_paths(), bpe.BlockConfig(max_seq_len=WHOLE, chunk_budget=WHOLE))
+    enc = tok.device_encoder(0, memo=bool(args.memo))
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    wl = workloads()
+    names = args.only.split(",") if args.only else list(wl)
+    rows = []
+    for name in names:
+        data, offs, want = wl[name]()
+        n = int(data.size)
+        d_data = torch.from_numpy(data.copy()).to(dev)
+        d_offs = torch.from_numpy(offs).to(dev)
+        out_ids = torch.empty(n, dtype=torch.int32, device=dev)
+        out_offs = torch.empty(len(offs), dtype=torch.int64, device=dev)
+        for _ in range(args.warmup):
+            enc.encode_into(d_data, d_offs, out_ids, out_offs, WHOLE, WHOLE, stream)
+        st = enc.query()
+        n_ids = int(out_offs[-1].item())
+        if want is not None:
+            assert n_ids == want, (name, n_ids, want)
+        times = []
+        for _ in range(args.iters):
+            if not args.no_flush:
+                flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            enc.encode_into(d_data, d_offs, out_ids, out_offs, WHOLE, WHOLE, stream)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = statistics.median(times)
+        b_alg = n + 4 * n_ids + 16 * len(offs)
+        row = {"workload": name, "bytes": n, "docs": len(offs) - 1, "ids": n_ids, "p50_ms": ms,
+               "min_ms": min(times), "tokens_per_s": n_ids / ms * 1e3, "in_GBps": n / ms / 1e6,
+               "alg_GBps": b_alg / ms / 1e6, "frac": b_alg / ms / 1e6 / peak,
+               "engine_passes": st["engine_passes"], "memo_hits": st["memo_hits"],
+               "short_merges": st["short_merges"], "medium": st["medium_segments"],
+               "giant": st["giant_segments"], "segments": st["n_segments"]}
+        rows.append(row)
+        print(f"{name:18s} {n:>11,d} B {len(offs)-1:>6d} docs {n_ids:>10,d} ids  p50 {ms*1e3:9.1f} us  "
+              f"{row['tokens_per_s']/1e9:7.3f} Gtok/s  in {row['in_GBps']:8.1f} GB/s  "
+              f"frac {row['frac']:.4f}  passes {st['engine_passes']}", flush=True)
+        del d_data, d_offs, out_ids, out_offs
+    if args.json:
+        Path(args.json).write_text(json.dumps(rows, indent=1))
+
+
+if __name__ == "__main__":
+    main()
