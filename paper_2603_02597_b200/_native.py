@@ -16,7 +16,10 @@ from pathlib import Path
 
 from .errors import DeviceError
 
-LIB_PATH = Path(__file__).resolve().parent / "libgpubpe.so"
+import os
+
+# GPUBPE_LIB selects an alternative in-tree build (tuning experiments only)
+LIB_PATH = Path(__file__).resolve().parent / os.environ.get("GPUBPE_LIB", "libgpubpe.so")
 
 OK, EINVAL, ECUDA, ENOMEM, ETABLE = 0, 1, 2, 3, 4
 F_NO_MEMO, F_STRICT = 1, 2

@@ -15,12 +15,14 @@
 //   base         byte -> internal id (byte_codec.py:97-111)
 //   memo         uint4 slots {bytes0-3, bytes4-7, id, len | blob_off<<8} keyed
 //                by the byte string of a vocab token whose BPE is itself;
-//                blob holds the full strings (for tokens longer than 8 bytes).
+//                blob holds bytes 8.. of tokens longer than 8 bytes as
+//                zero-padded 8-byte chunks (blob_off counts chunks).
 //   ext_id       internal -> external id (NULL when ids are used as-is).
 #pragma once
 #include <cstdint>
 
 #define GPUBPE_INF 0xFFFFFFFFu
+#define FULL_MASK 0xffffffffu
 
 struct DevTables {
     const uint4 *pairs;
@@ -31,7 +33,7 @@ struct DevTables {
     const uint32_t *base;
     const uint4 *memo;
     uint32_t memo_mask;  // 0 with memo == nullptr disables the memo
-    const uint8_t *blob;
+    const unsigned long long *blob;
     const uint32_t *ext_id;
     int well_formed;  // exact multi-merge allowed (else one global-min merge per pass)
 };
@@ -58,6 +60,16 @@ __host__ __device__ __forceinline__ uint64_t memo_hash_init(uint32_t len) {
 }
 
 #ifdef __CUDACC__
+
+// Skewed shared-memory layouts of a warp tile.  Lane L owns bytes [16L,
+// 16L+16), so plain layouts put every lane's k-th slot in the same bank
+// (16-way conflicts for u32 slots, 8-way for byte words).  One pad word per
+// 16 slots / per 4 byte-words spreads the lanes over all 32 banks.
+__host__ __device__ constexpr uint32_t SI(uint32_t p) { return p + (p >> 4); }  // slot of position p
+__host__ __device__ constexpr uint32_t SW(uint32_t w) { return w + (w >> 2); }  // word of byte-word w
+__device__ __forceinline__ uint32_t sb_byte(const uint32_t *sbw, uint32_t p) {
+    return (sbw[SW(p >> 2)] >> (8 * (p & 3))) & 0xFFu;
+}
 
 struct PairHit {
     uint32_t rank;  // GPUBPE_INF on miss

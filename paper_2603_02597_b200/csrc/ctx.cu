@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -20,7 +21,7 @@
 
 size_t tile_smem_bytes();
 cudaError_t launch_encode(const EncodeParams &P, int grid, cudaStream_t s, cudaEvent_t *ev,
-                          const cudaAccessPolicyWindow *win);
+                          const cudaAccessPolicyWindow *win, bool coop);
 cudaError_t setup_kernels();
 cudaError_t tile_occupancy(int *blocks);
 cudaError_t launch_lookup(const DevTables &T, const uint32_t *l, const uint32_t *r,
@@ -47,7 +48,8 @@ struct gpubpe_ctx {
     size_t tables_bytes = 0, tables_used = 0;
     cudaAccessPolicyWindow win{};
     // workspace
-    DevBuf ws_state, ws_status, ws_med, ws_arena;
+    DevBuf ws_state, ws_status, ws_recs, ws_scratch, ws_tiles, ws_arena;
+    uint64_t last_n_tiles = 0;
     unsigned int epoch = 0;
     uint64_t calls = 0;  // selects the EncodeState slot (two, alternating)
     EncodeState *h_state = nullptr;  // pinned
@@ -129,6 +131,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
     if (!out) return GPUBPE_EINVAL;
     *out = nullptr;
     gpubpe_ctx *ctx = new gpubpe_ctx();
+    *out = ctx;  // on failure the caller reads the message, then destroys
     ctx->device = device;
     ctx->flags = flags;
     int rc = GPUBPE_OK;
@@ -146,9 +149,19 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
         ctx->num_sms = prop.multiProcessorCount;
         if ((e = setup_kernels()) != cudaSuccess)
             return bail(fail(ctx, GPUBPE_ECUDA, "kernel setup: %s", cudaGetErrorString(e)));
-        int blocks = 1;
-        tile_occupancy(&blocks);
-        ctx->tile_blocks_per_sm = std::max(1, blocks);
+        // the per-lane engine keeps its token arrays on the thread stack
+        size_t stack = 0;
+        cudaDeviceGetLimit(&stack, cudaLimitStackSize);
+        if (stack < 4096 && (e = cudaDeviceSetLimit(cudaLimitStackSize, 4096)) != cudaSuccess)
+            return bail(fail(ctx, GPUBPE_ECUDA, "stack limit: %s", cudaGetErrorString(e)));
+        int blocks = 0;
+        if ((e = tile_occupancy(&blocks)) != cudaSuccess || blocks < 1)
+            return bail(fail(ctx, GPUBPE_ECUDA, "encode kernel does not fit an SM (%d blocks, %s)", blocks,
+                             cudaGetErrorString(e)));
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+        if (!coop) return bail(fail(ctx, GPUBPE_ECUDA, "device %d lacks cooperative launch", device));
+        ctx->tile_blocks_per_sm = blocks;
     }
 
     // ---- internal ids: used as-is when every id < 2^24, else densely remapped
@@ -181,6 +194,8 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
         NW[i] = intern(new_tok[i]);
     }
     const uint64_t n_ids = identity ? max_id + 1 : ext.size();
+    if (n_ids >= (1ull << 24))
+        return bail(fail(ctx, GPUBPE_EINVAL, "more than 2^24 distinct token ids (%llu)", (unsigned long long)n_ids));
 
     // ---- pair table
     uint64_t cap = 2;
@@ -249,7 +264,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
             uint64_t len = vocab_offs[v + 1] - vocab_offs[v];
             if (len < 2 || len > SHORT_MAX) continue;
             ++memo_cand;
-            if (len > 8) blob_max += len;
+            if (len > 8) blob_max += (len - 1) / 8 * 8;
         }
     uint64_t memo_cap_max = 2;
     while (memo_cap_max < 2 * memo_cand) memo_cap_max <<= 1;
@@ -351,7 +366,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
             uint64_t mcap = 2;
             while (mcap < 2 * keep.size()) mcap <<= 1;
             std::vector<uint4> memo(mcap, make_uint4(0, 0, 0, 0));
-            std::vector<uint8_t> blob;
+            std::vector<unsigned long long> blob;  // bytes 8.. as zero-padded 8-byte chunks
             for (size_t k : keep) {
                 const uint8_t *sv = hb.data() + ho[k];
                 uint32_t len = (uint32_t)(ho[k + 1] - ho[k]);
@@ -360,7 +375,11 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
                 uint32_t boff = (uint32_t)blob.size();
                 if (len > 8) {
                     if (boff >= (1u << 24)) continue;  // blob offset field is 24 bits
-                    blob.insert(blob.end(), sv, sv + len);
+                    for (uint32_t c = 8; c < len; c += 8) {
+                        unsigned long long ch = 0;
+                        for (uint32_t j = c; j < len && j < c + 8; ++j) ch |= (unsigned long long)sv[j] << (8 * (j - c));
+                        blob.push_back(ch);
+                    }
                 }
                 uint32_t h = (uint32_t)memo_hash_bytes(sv, len) & (uint32_t)(mcap - 1);
                 while (memo[h].w != 0) h = (h + 1) & (uint32_t)(mcap - 1);
@@ -368,7 +387,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
                                      len | (len > 8 ? boff << 8 : 0u));
             }
             const uint4 *d_memo;
-            const uint8_t *d_blob;
+            const unsigned long long *d_blob;
             if ((rc = upload(ctx, memo, &d_memo))) return bail(rc);
             if ((rc = upload(ctx, blob, &d_blob))) return bail(rc);
             ctx->T.memo = d_memo;
@@ -403,15 +422,30 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
                        uint64_t chunk_budget, uint32_t *d_out_ids, int64_t *d_out_offs,
                        cudaStream_t s, bool *checked) {
     *checked = false;
-    const uint64_t n_tiles = (n_bytes + TILE - 1) / TILE;
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(n_tiles, (uint64_t)ctx->num_sms * ctx->tile_blocks_per_sm));
+    // one CTA of NW autonomous warps per SM, all co-resident (cooperative)
+    const int grid = ctx->num_sms * ctx->tile_blocks_per_sm;
+    // tile width: the largest of 512/256/128 bytes that still gives every
+    // warp of the grid two tiles (small inputs get more, smaller tiles)
+    const uint64_t n_warps = (uint64_t)grid * NW;
+    int wt = 128;
+    if (n_bytes >= 2 * n_warps * 512) wt = 512;
+    else if (n_bytes >= 2 * n_warps * 256) wt = 256;
+    const uint64_t n_tiles = (n_bytes + wt - 1) / wt;
+    const uint64_t R = std::min<uint64_t>(n_tiles, (uint64_t)UNIT_MAX * grid);
+    const uint64_t n_rounds = (n_tiles + R - 1) / R;
+    // deferred segments (> SHORT_MAX bytes) start at least SHORT_MAX + 1 apart
+    const uint64_t def_max = n_bytes / (SHORT_MAX + 1) + 1;
     int rc;
     if ((rc = ensure(ctx, ctx->ws_state, 2 * sizeof(EncodeState), true))) return rc;
-    if (ctx->ws_status.bytes < n_tiles * 8) ctx->epoch = 0;
-    if ((rc = ensure(ctx, ctx->ws_status, n_tiles * 8, true))) return rc;
-    if ((rc = ensure(ctx, ctx->ws_med, (size_t)grid * MED_BYTES, false))) return rc;
+    const uint64_t n_units = n_rounds * grid;
+    if (ctx->ws_status.bytes < n_units * 8) ctx->epoch = 0;
+    if ((rc = ensure(ctx, ctx->ws_status, n_units * 8, true))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_scratch, 2 * R * SLOT * 4, false))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_tiles, 2 * R * 8, false))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_recs, std::max<uint64_t>(1 << 16, std::min<uint64_t>(def_max, 1 << 20)) * sizeof(DefRec), false))) return rc;
     if ((rc = ensure(ctx, ctx->ws_arena, 64ull << 20, false))) return rc;
-    for (int attempt = 0; attempt < 3; ++attempt) {
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        const uint64_t rec_cap = ctx->ws_recs.bytes / sizeof(DefRec);
         if (++ctx->epoch >= (1u << 20)) {
             CK(cudaMemsetAsync(ctx->ws_status.p, 0, ctx->ws_status.bytes, s));
             ctx->epoch = 1;
@@ -430,27 +464,57 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.out_offs = reinterpret_cast<long long *>(d_out_offs);
         P.st = slots + (k & 1);
         P.st_next = slots + ((k + 1) & 1);
+        P.scratch = static_cast<uint32_t *>(ctx->ws_scratch.p);
+        P.tiles = static_cast<unsigned long long *>(ctx->ws_tiles.p);
         P.status = static_cast<unsigned long long *>(ctx->ws_status.p);
-        P.med_scratch = static_cast<uint8_t *>(ctx->ws_med.p);
-        P.arena = static_cast<uint8_t *>(ctx->ws_arena.p);
-        P.arena_cap = ctx->ws_arena.bytes;
+        P.recs = static_cast<DefRec *>(ctx->ws_recs.p);
+        P.rec_cap = rec_cap;
+        P.arena = static_cast<uint32_t *>(ctx->ws_arena.p);
+        P.arena_words = ctx->ws_arena.bytes / 4;
         P.n_tiles = n_tiles;
+        P.round_tiles = R;
+        P.prefetch = ctx->tables;
+        P.prefetch_bytes = ctx->tables_used;
         P.epoch = ctx->epoch;
         P.strict = (ctx->flags & GPUBPE_F_STRICT) ? 1 : 0;
-        cudaError_t e = launch_encode(P, grid, s, ctx->profiling ? ctx->ev : nullptr, &ctx->win);
+        P.aligned = (reinterpret_cast<uintptr_t>(d_bytes) & 15) == 0;
+        P.tile_bytes = wt;
+        ctx->last_n_tiles = n_tiles;
+        // debug knobs (tuning only) never apply to the memo verification encode
+        const int dbg = (ctx->T.memo && getenv("GPUBPE_DEBUG")) ? atoi(getenv("GPUBPE_DEBUG")) : 0;
+        if (dbg & 1) P.prefetch_bytes = 0;
+        P.dbg_phase_a_only = (dbg & 16) ? 1 : (dbg & 32) ? 2 : 0;
+        static unsigned long long *dbuf = nullptr;
+        if (dbg & 8) {
+            if (!dbuf) cudaMalloc(&dbuf, 32768 * 8);
+            cudaMemsetAsync(dbuf, 0, 32768 * 8, s);
+            P.dbg = dbuf;
+        }
+        cudaError_t e = launch_encode(P, grid, s, ctx->profiling ? ctx->ev : nullptr, (dbg & 4) ? nullptr : &ctx->win, !(dbg & 2));
         ctx->timed = ctx->profiling;
         if (e != cudaSuccess) return fail(ctx, GPUBPE_ECUDA, "encode launch: %s", cudaGetErrorString(e));
-        // Giant segments need ENGINE_BYTES(len) of arena; 25 B per input byte
-        // (+64 per segment) always suffices, else check and re-run.
-        if (n_bytes * 25 + 4096 <= ctx->ws_arena.bytes) return GPUBPE_OK;
+        // Overflow is impossible when every deferred segment fits the record
+        // list and the arena (ENGINE_BYTES(len) rounded to 16 B per segment);
+        // otherwise check after the call and re-run with larger buffers.
+        const uint64_t arena_need = 26 * n_bytes + 96 * def_max;
+        if ((dbg & 8) && getenv("GPUBPE_DEBUG_OUT")) {
+            std::vector<unsigned long long> h(32768);
+            cudaMemcpyAsync(h.data(), dbuf, h.size() * 8, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            FILE *f = fopen(getenv("GPUBPE_DEBUG_OUT"), "wb");
+            if (f) { fwrite(h.data(), 8, h.size(), f); fclose(f); }
+        }
+        if (def_max <= rec_cap && arena_need <= ctx->ws_arena.bytes) return GPUBPE_OK;
         *checked = true;
         CK(cudaMemcpyAsync(ctx->h_state, P.st, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (!ctx->h_state->overflow) return GPUBPE_OK;
-        size_t need = (size_t)ctx->h_state->arena_used * 4;
-        if ((rc = ensure(ctx, ctx->ws_arena, need, false))) return rc;
+        const uint64_t nd = ctx->h_state->n_def;
+        if (nd > rec_cap && (rc = ensure(ctx, ctx->ws_recs, nd * sizeof(DefRec), false))) return rc;
+        const uint64_t used = ctx->h_state->arena_used * 4;
+        if (used > ctx->ws_arena.bytes && (rc = ensure(ctx, ctx->ws_arena, used, false))) return rc;
     }
-    return fail(ctx, GPUBPE_ENOMEM, "giant-segment arena kept overflowing");
+    return fail(ctx, GPUBPE_ENOMEM, "deferred-segment buffers kept overflowing");
 }
 
 extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes,
@@ -493,18 +557,18 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_query(gpubpe_ctx *c
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
     const EncodeState &st = *ctx->h_state;
-    if (st.error) return fail(ctx, GPUBPE_ECUDA, "device reported an internal error (segment bound)");
+    if (st.overflow) return fail(ctx, GPUBPE_ECUDA, "device reported an unrecovered buffer overflow");
     out->n_bytes = ctx->last_n_bytes;
     out->n_ids = st.n_ids;
     out->passes = out->n_bytes - st.n_ids;
-    out->n_segments = st.n_segments;
-    out->memo_hits = st.memo_hits;
-    out->short_merges = st.short_merges;
-    out->medium_segments = st.medium_segments;
-    out->giant_segments = st.giant_segments;
-    out->giant_bytes = st.giant_bytes;
-    out->engine_passes = st.engine_passes;
-    out->tiles = st.tile_counter;
+    out->n_segments = st.c.n_segments;
+    out->memo_hits = st.c.memo_hits;
+    out->short_merges = st.c.short_merges;
+    out->medium_segments = st.c.medium_segments;
+    out->giant_segments = st.c.giant_segments;
+    out->giant_bytes = st.c.giant_bytes;
+    out->engine_passes = st.c.engine_passes;
+    out->tiles = ctx->last_n_bytes ? ctx->last_n_tiles : 0;
     out->overflow = st.overflow;
     out->well_formed = (uint64_t)ctx->T.well_formed;
     return GPUBPE_OK;
@@ -545,7 +609,7 @@ extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     if (ctx->tables) cudaFree(ctx->tables);
-    for (DevBuf *b : {&ctx->ws_state, &ctx->ws_status, &ctx->ws_med, &ctx->ws_arena})
+    for (DevBuf *b : {&ctx->ws_state, &ctx->ws_status, &ctx->ws_recs, &ctx->ws_scratch, &ctx->ws_tiles, &ctx->ws_arena})
         if (b->p) cudaFree(b->p);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);
     for (auto &e : ctx->ev)

@@ -8,14 +8,93 @@
 //   ordered reassembly             src/lanebpe/chunker.py:166-179
 // Segment boundaries (junction bitmap, document starts, chunk cuts) are exact
 // cut points: no merge of the reference can ever span them, so segments are
-// encoded independently and concatenated in order.
+// encoded independently and concatenated in order (DESIGN.md section 3).
 #include <cuda_runtime.h>
 
 #include <cuda/atomic>
 
 #include "kernels.cuh"
 
+// ------------------------------------------------------------------ smem
+
+struct __align__(16) WarpSmem {
+    union {
+        struct {
+            uint32_t sbw[SW((LD + 16) / 4) + 1];  // staged bytes, skewed words (+ slack for 8-B reads)
+            uint32_t miss[WT / 2 + 2];      // memo misses: start | len << 16
+        } a;
+        uint32_t outbuf[SLOT];              // scratch entries in output order
+    } u;
+    uint32_t sid[SI(SLOT) + 2];  // at SI(p): ids of the segment starting at p; first tagged count << 24
+                          // (0xFF: deferred, record index in the next slot)
+    uint16_t seg[WT];           // starts of the segments beginning in the tile, in order
+    uint32_t cm[NGRP / 2 + 1];  // cut bits, position k = cut before byte a + k
+    uint32_t n_miss, n_def;
+};
+
+struct CtaSmem {
+    uint32_t jb[2048];  // junction bitmap
+    uint32_t base[256];
+    EngineShared es;
+    unsigned long long bcast[4];
+    PassCounters pc;
+    unsigned long long tb[UNIT_MAX];  // phase B: tile output offsets inside the unit
+    unsigned long long tw[UNIT_MAX];  // phase B: tile words
+    WarpSmem w[NW];
+};
+
+struct WarpCtx {
+    long long dcur;  // document cursor: tiles of one warp are increasing
+    unsigned long long n_segments, memo_hits, short_merges, engine_passes;  // per lane
+};
+
 // ------------------------------------------------------------------ helpers
+
+__device__ __forceinline__ void st_relaxed(unsigned long long *w, unsigned long long v) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(*w);
+    r.store(v, cuda::memory_order_relaxed);
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(unsigned long long *w) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(*w);
+    return r.load(cuda::memory_order_relaxed);
+}
+// Relaxed polling: an acquire load would invalidate the SM's L1 (CCTL.IVALL)
+// on every iteration and stall the other warps' L1/shared-memory traffic.
+__device__ __forceinline__ unsigned int ld_relaxed_u32(unsigned int *w) {
+    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> r(*w);
+    return r.load(cuda::memory_order_relaxed);
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Debug cycle stamp k of tile t after value v is available (GPUBPE_DEBUG & 8).
+#ifdef GPUBPE_DEBUG_STAMPS
+#define TSTAMP(k, v)                                                                     \
+    do {                                                                                 \
+        if (P.dbg && t < 2048) {                                                         \
+            uint32_t d_;                                                                 \
+            asm volatile("mov.b32 %0, %1;" : "=r"(d_) : "r"((uint32_t)(v)));            \
+            __syncwarp();                                                                \
+            long long c_;                                                                \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_) : "r"(d_));               \
+            if (lane == 0) P.dbg[16384 + 8 * t + (k)] = (unsigned long long)(c_ - dbg_c0); \
+        }                                                                                \
+    } while (0)
+#else
+#define TSTAMP(k, v) do { } while (0)
+#endif
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
 
 // Smallest structural cut (doc end or chunk cut) strictly after p; doc d holds p.
 __device__ __forceinline__ long long next_struct_cut(const EncodeParams &P, long long d, long long p) {
@@ -30,10 +109,18 @@ __device__ __forceinline__ long long next_struct_cut(const EncodeParams &P, long
 }
 
 // Warp: last document d with offs[d] <= p (p < n_bytes), i.e. the non-empty
-// document holding byte p.  32-ary search, all lanes get the result.
-__device__ long long warp_doc_of(const long long *offs, unsigned long long n_docs, long long p) {
+// document holding byte p.  32-ary search in [lo, n_docs), offs[lo] <= p.
+__device__ long long warp_doc_from(const long long *offs, long long lo, unsigned long long n_docs,
+                                   long long p) {
     const int lane = threadIdx.x & 31;
-    long long lo = 0, hi = (long long)n_docs - 1;  // answer in [lo, hi]
+    long long hi = (long long)n_docs - 1;
+    {   // the next 31 documents first: tiles of one warp move forward slowly
+        const long long idx = lo + lane;
+        const bool ok = idx <= hi && __ldg(&offs[idx]) <= p;
+        const unsigned m = __ballot_sync(FULL_MASK, ok);
+        if (m != FULL_MASK) return lo + 31 - __clz(m);
+        lo += 31;
+    }
     while (hi > lo) {
         const long long step = (hi - lo + 32) / 32;
         const long long idx = lo + (long long)lane * step;
@@ -47,9 +134,8 @@ __device__ long long warp_doc_of(const long long *offs, unsigned long long n_doc
 }
 
 // CTA: first p in [lo, hi) whose cut slot is a junction miss, else hi.
-// Each thread checks 16 consecutive slots per round (4096 per round).
-__device__ long long cta_first_nonjunction(const EncodeParams &P, long long lo, long long hi,
-                                           EngineShared &sh) {
+__device__ long long cta_first_nonjunction(const EncodeParams &P, const uint32_t *jb, long long lo,
+                                           long long hi, EngineShared &sh) {
     for (long long b = lo; b < hi; b += 16 * NT) {
         const long long p0 = b + 16 * (long long)threadIdx.x;
         unsigned long long k = ~0ull;
@@ -58,7 +144,8 @@ __device__ long long cta_first_nonjunction(const EncodeParams &P, long long lo, 
             const long long pe = min(p0 + 16, hi);
             for (long long p = p0; p < pe; ++p) {
                 const uint32_t y = __ldg(&P.bytes[p]);
-                if (!is_junction(P.T.jbits, x, y)) { k = (unsigned long long)p; break; }
+                const uint32_t idx = (x << 8) | y;
+                if (!((jb[idx >> 5] >> (idx & 31)) & 1u)) { k = (unsigned long long)p; break; }
                 x = y;
             }
         }
@@ -68,390 +155,723 @@ __device__ long long cta_first_nonjunction(const EncodeParams &P, long long lo, 
     return hi;
 }
 
-__device__ __forceinline__ void st_relaxed(unsigned long long *w, unsigned long long v) {
-    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(*w);
-    r.store(v, cuda::memory_order_relaxed);
-}
-__device__ __forceinline__ unsigned long long ld_relaxed(unsigned long long *w) {
-    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(*w);
-    return r.load(cuda::memory_order_relaxed);
+// Cut bits of the 16 positions of group g (position k: cut before byte k).
+__device__ __forceinline__ uint32_t group_cuts(const uint32_t *jb, const uint32_t *sbw, int g,
+                                               uint32_t prevb) {
+    uint32_t x = g ? sb_byte(sbw, 16 * g - 1) : prevb;
+    const uint32_t w[4] = {sbw[SW(4 * g)], sbw[SW(4 * g + 1)], sbw[SW(4 * g + 2)], sbw[SW(4 * g + 3)]};
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t y = (w[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+        const uint32_t idx = (x << 8) | y;
+        m |= ((jb[idx >> 5] >> (idx & 31)) & 1u) << k;
+        x = y;
+    }
+    return ~m & 0xFFFFu;
 }
 
-// Memo probe for sb[0..len), 2 <= len <= SHORT_MAX.  Returns the id or INF.
-__device__ uint32_t memo_lookup(const DevTables &T, const uint8_t *sb, uint32_t len) {
-    unsigned long long lo = 0;
-    const uint32_t m = len < 8 ? len : 8;
-    for (uint32_t j = 0; j < m; ++j) lo |= (unsigned long long)sb[j] << (8 * j);
-    unsigned long long h = memo_hash_step(memo_hash_init(len), lo);
-    for (uint32_t c = 8; c < len; c += 8) {
-        unsigned long long ch = 0;
-        for (uint32_t j = c; j < len && j < c + 8; ++j) ch |= (unsigned long long)sb[j] << (8 * (j - c));
-        h = memo_hash_step(h, ch);
+// First cut in [q, lim], lim - q < 32; -1 if none.
+__device__ __forceinline__ int next_cut(const uint32_t *cm, int q, int lim) {
+    int w = q >> 5;
+    uint32_t bits = cm[w] & (0xFFFFFFFFu << (q & 31));
+    if (!bits) {
+        ++w;
+        if (w * 32 > lim) return -1;
+        bits = cm[w];
+        if (!bits) return -1;
     }
-    uint32_t slot = (uint32_t)h & T.memo_mask;
+    const int c = w * 32 + __ffs(bits) - 1;
+    return c <= lim ? c : -1;
+}
+
+// 8 bytes of the staged tile starting at byte p (little endian).
+__device__ __forceinline__ unsigned long long sb_load8(const uint32_t *sbw, uint32_t p) {
+    const uint32_t w = p >> 2;
+    const uint32_t sh = (p & 3) * 8;
+    const uint32_t w0 = sbw[SW(w)], w1 = sbw[SW(w + 1)], w2 = sbw[SW(w + 2)];
+    const uint32_t lo = __funnelshift_r(w0, w1, sh);
+    const uint32_t hi = __funnelshift_r(w1, w2, sh);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
+__device__ __forceinline__ unsigned long long low_bytes(unsigned long long v, uint32_t n) {
+    return n >= 8 ? v : (v & ((1ull << (8 * n)) - 1));
+}
+
+// Memo home slot for staged bytes [p, p + len), 2 <= len <= SHORT_MAX.
+__device__ __forceinline__ uint32_t memo_slot(const uint32_t *sb, uint32_t p, uint32_t len, uint32_t mask) {
+    unsigned long long h = memo_hash_step(memo_hash_init(len), low_bytes(sb_load8(sb, p), len));
+    for (uint32_t c = 8; c < len; c += 8) h = memo_hash_step(h, low_bytes(sb_load8(sb, p + c), len - c));
+    return (uint32_t)h & mask;
+}
+
+// Memo lookup continuing from slot `slot` whose entry `e` is already loaded.
+// The id, or INF when the string is not a memoised vocab token.
+__device__ uint32_t memo_resolve(const DevTables &T, const uint32_t *sb, uint32_t p, uint32_t len,
+                                 uint32_t slot, uint4 e) {
+    const unsigned long long c0 = low_bytes(sb_load8(sb, p), len);
     for (;;) {
-        const uint4 e = __ldg(&T.memo[slot]);
         if (e.w == 0) return GPUBPE_INF;
-        if ((e.w & 0xFFu) == len && e.x == (uint32_t)lo && e.y == (uint32_t)(lo >> 32)) {
+        if ((e.w & 0xFFu) == len && e.x == (uint32_t)c0 && e.y == (uint32_t)(c0 >> 32)) {
             bool eq = true;
-            if (len > 8) {
-                const uint8_t *tail = T.blob + (e.w >> 8);
-                for (uint32_t j = 8; j < len; ++j)
-                    if (__ldg(&tail[j]) != sb[j]) { eq = false; break; }
-            }
+            const unsigned long long *tail = T.blob + (e.w >> 8);
+            for (uint32_t c = 8, k = 0; c < len; c += 8, ++k)
+                eq &= __ldg(&tail[k]) == low_bytes(sb_load8(sb, p + c), len - c);
             if (eq) return e.z;
         }
         slot = (slot + 1) & T.memo_mask;
+        e = __ldg(&T.memo[slot]);
+    }
+}
+
+// Warp decoupled look-back: publishes this tile's total, returns its base.
+#define LB_AGG 1ull
+#define LB_INC 2ull
+#define LB_VALUE_MASK ((1ull << 42) - 1)
+
+__device__ __forceinline__ unsigned long long warp_lookback(unsigned long long *status, unsigned long long t,
+                                                            unsigned long long total, unsigned int epoch) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long tag = (unsigned long long)epoch << 44;
+    if (t == 0) {
+        if (lane == 0) st_relaxed(&status[0], tag | (LB_INC << 42) | total);
+        return 0;
+    }
+    if (lane == 0) st_relaxed(&status[t], tag | (LB_AGG << 42) | total);
+    unsigned long long excl = 0;
+    long long pos = (long long)t - 1;
+    for (;;) {
+        const long long j = pos - lane;
+        unsigned long long v, flag;
+        if (j >= 0) {
+            for (;;) {
+                v = ld_relaxed(&status[j]);
+                flag = ((v >> 44) == epoch) ? ((v >> 42) & 3ull) : 0ull;
+                if (flag) break;
+                __nanosleep(32);
+            }
+        } else {
+            v = LB_INC << 42;
+            flag = LB_INC;
+        }
+        const unsigned inc = __ballot_sync(FULL_MASK, flag == LB_INC);
+        const int stop = inc ? __ffs(inc) - 1 : 31;
+        unsigned long long val = lane <= stop ? (v & LB_VALUE_MASK) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(FULL_MASK, val, o);
+        excl += val;
+        if (inc) break;
+        pos -= 32;
+    }
+    if (lane == 0) st_relaxed(&status[t], tag | (LB_INC << 42) | (excl + total));
+    return excl;
+}
+
+// Cut bits of the 16 positions owned by lane L (explicit 16-bit load: the
+// shift-and-mask form was once widened by the compiler into a misaligned
+// 32-bit shared load at cm + 2L).
+__device__ __forceinline__ uint32_t lane_cuts(const WarpSmem &S, int L) {
+    return reinterpret_cast<const uint16_t *>(S.cm)[L];
+}
+
+// Count of the scratch entries of the segment whose sid tag is v.
+__device__ __forceinline__ uint32_t seg_entries(uint32_t v) {
+    const uint32_t cc = v >> 24;
+    return cc == 0xFFu ? 1u : cc;
+}
+
+__device__ __forceinline__ void l2_discard(const void *p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+// ------------------------------------------------------------------ phase A
+
+// Encode tile t (bytes [t * wt, t * wt + wt)) into scratch slot `slot` (see
+// kernels.cuh, phase A).  The segments starting in the tile are gathered
+// into a position-ordered list and dealt round-robin to the lanes, so every
+// lane handles ~1/32 of them (a warp's latency is its slowest lane's chain).
+__device__ __noinline__ void encode_tile(const EncodeParams &P, CtaSmem &C, WarpSmem &S, unsigned long long t,
+                                         unsigned long long slot, WarpCtx &X) {
+    const int lane = threadIdx.x & 31;
+    const DevTables &T = P.T;
+    const int wt = P.tile_bytes;
+    const int ld = wt + HALO;
+    const long long N = (long long)P.n_bytes;
+    const long long a = (long long)t * wt;
+    const int nst = (int)min((long long)ld, N - a);
+    const int nin = min(wt, nst);
+    const bool last = a + wt >= N;
+    uint32_t *sb = S.u.a.sbw;
+    uint32_t c_seg = 0, c_memo = 0, c_miss = 0, c_pass = 0;
+
+    // ---- 1. stage the tile and its halo (16-B loads, both rounds in flight)
+    if (P.aligned && nst == ld) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(P.bytes + a);
+        const int nv = ld / 16;
+        uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
+        if (lane < nv) v0 = ldg_stream(src + lane);
+        if (lane + 32 < nv) v1 = ldg_stream(src + 32 + lane);
+        if (lane < nv) {
+            uint32_t *d = sb + SW(4 * lane);  // a lane's 4 words are contiguous after skewing
+            d[0] = v0.x; d[1] = v0.y; d[2] = v0.z; d[3] = v0.w;
+        }
+        if (lane + 32 < nv) {
+            uint32_t *d = sb + SW(4 * (32 + lane));
+            d[0] = v1.x; d[1] = v1.y; d[2] = v1.z; d[3] = v1.w;
+        }
+    } else {
+        uint8_t *b8 = reinterpret_cast<uint8_t *>(sb);
+#pragma unroll 1
+        for (int k = lane; k < ld; k += 32) b8[4 * SW(k >> 2) + (k & 3)] = k < nst ? __ldg(&P.bytes[a + k]) : 0;
+    }
+#ifdef GPUBPE_DEBUG_STAMPS
+    long long dbg_c0 = 0;
+    if (P.dbg) asm volatile("mov.u64 %0, %%clock64;" : "=l"(dbg_c0));
+#endif
+    const uint32_t prevb = a > 0 ? __ldg(&P.bytes[a - 1]) : 0u;
+    if (lane == 0) {
+        S.n_miss = 0;
+        S.n_def = 0;
+    }
+    __syncwarp();
+    TSTAMP(0, sb[SW(4 * lane)] + prevb);
+
+    // ---- 2. cut bits: junction misses, start and end of input
+    {
+        const int ng = ld / 16;
+        uint32_t m[2] = {0u, 0u};
+#pragma unroll 1
+        for (int g = lane, i = 0; g < ng; g += 32, ++i) {
+            uint32_t mg = group_cuts(C.jb, sb, g, prevb);
+            const int p0 = 16 * g;
+            if (p0 >= nst) mg = 0;
+            else if (p0 + 16 > nst) mg &= (1u << (nst - p0)) - 1;
+            if (a + nst == N && nst >= p0 && nst < p0 + 16) mg |= 1u << (nst - p0);
+            if (g == 0 && a == 0) mg |= 1u;
+            if (i == 0) m[0] = mg; else m[1] = mg;
+        }
+        const uint32_t n0 = __shfl_down_sync(FULL_MASK, m[0], 1);
+        const uint32_t nh = __shfl_down_sync(FULL_MASK, m[1], 1);
+        if (!(lane & 1)) S.cm[lane >> 1] = (m[0] & 0xFFFFu) | (n0 << 16);
+        if (lane == 0) {
+            S.cm[16] = (m[1] & 0xFFFFu) | (nh << 16);
+            S.cm[17] = 0;
+        }
+    }
+    __syncwarp();
+    TSTAMP(1, S.cm[lane & 15]);
+
+    // ---- 3. document starts and chunk cuts inside the staged bytes
+    long long dc = 0;  // document holding byte a
+    if (P.n_docs > 1) dc = X.dcur = warp_doc_from(P.doc_offs, X.dcur, P.n_docs, a);
+    if (P.n_docs > 1 || (unsigned long long)N > P.max_seq_len) {
+#pragma unroll 1
+        for (long long d0 = dc;; d0 += 32) {
+            const long long d = d0 + lane;
+            bool in = false;
+            if (d < (long long)P.n_docs) {
+                const long long s = __ldg(&P.doc_offs[d]);
+                if (s < a + nst) {
+                    in = true;
+                    if (s >= a) atomicOr(&S.cm[(s - a) >> 5], 1u << ((s - a) & 31));
+                    const long long e = __ldg(&P.doc_offs[d + 1]);
+                    if ((unsigned long long)(e - s) > P.max_seq_len) {
+                        const long long cb = (long long)P.chunk_budget;
+                        long long k = s < a ? (a - s + cb - 1) / cb : 1;
+                        if (k < 1) k = 1;
+#pragma unroll 1
+                        for (long long c = s + k * cb; c < e && c < a + nst; c += cb)
+                            atomicOr(&S.cm[(c - a) >> 5], 1u << ((c - a) & 31));
+                    }
+                }
+            }
+            if (__ballot_sync(FULL_MASK, in) != FULL_MASK) break;
+        }
+        __syncwarp();
+    }
+
+    // ---- 4. position-ordered list of the segments starting in the tile
+    uint32_t nseg;
+    {
+        uint32_t mine = lane_cuts(S, lane);
+        const int p0 = 16 * lane;
+        if (p0 >= nin) mine = 0;
+        else if (p0 + 16 > nin) mine &= (1u << (nin - p0)) - 1;
+        const uint32_t c = __popc(mine);
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o) incl += y;
+        }
+        nseg = __shfl_sync(FULL_MASK, incl, 31);
+        uint32_t k = incl - c;
+#pragma unroll 1
+        for (uint32_t bits = mine; bits; bits &= bits - 1) S.seg[k++] = (uint16_t)(p0 + __ffs(bits) - 1);
+    }
+    __syncwarp();
+
+    // ---- 5. classify; memo candidates park their slot in sid and prefetch
+    //         its line into L1 (pass 1), then resolve (pass 2)
+    const bool use_memo = T.memo_mask != 0;
+#pragma unroll 1
+    for (uint32_t i = lane; i < nseg; i += 32) {
+        const int p = S.seg[i];
+        const int e = next_cut(S.cm, p + 1, p + SHORT_MAX);
+        ++c_seg;
+        if (e < 0) {  // longer than SHORT_MAX: deferred to the CTA engine
+            const unsigned long long r = atomicAdd(&P.st->n_def, 1ull);
+            if (r < P.rec_cap) P.recs[r].start = (unsigned long long)(a + p);
+            S.sid[SI(p)] = 0xFF000000u;
+            S.sid[SI(p + 1)] = (uint32_t)r;
+            S.n_def = 1;
+            continue;
+        }
+        const uint32_t len = (uint32_t)(e - p);
+        if (len == 1) {
+            S.sid[SI(p)] = (1u << 24) | C.base[sb_byte(sb, p)];
+        } else if (use_memo) {
+            const uint32_t ms = memo_slot(sb, (uint32_t)p, len, T.memo_mask);
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(T.memo + ms));
+            S.sid[SI(p)] = ms;  // tag 0: memo pending (slots < 2^24)
+            S.sid[SI(p + 1)] = len;
+        } else {
+            S.u.a.miss[atomicAdd(&S.n_miss, 1u)] = (uint32_t)p | (len << 16);
+            ++c_miss;
+        }
+    }
+    TSTAMP(7, c_seg);
+    if (use_memo) {
+#pragma unroll 1
+        for (uint32_t i = lane; i < nseg; i += 32) {
+            const int p = S.seg[i];
+            const uint32_t ms = S.sid[SI(p)];
+            if (ms >> 24) continue;
+            const uint32_t len = S.sid[SI(p + 1)];
+            const uint32_t id = memo_resolve(T, sb, (uint32_t)p, len, ms, __ldg(&T.memo[ms]));
+            if (id == GPUBPE_INF) {  // not a vocab string: the warp engine below
+                S.u.a.miss[atomicAdd(&S.n_miss, 1u)] = (uint32_t)p | (len << 16);
+                ++c_miss;
+                continue;
+            }
+            ++c_memo;
+            S.sid[SI(p)] = (1u << 24) | id;
+        }
+    }
+    __syncwarp();
+    TSTAMP(2, c_memo);
+
+    // ---- 6. memo misses: packed into the lanes, exact multi-merge passes
+    {
+        const bool strict = P.strict || !T.well_formed;
+        const uint32_t nm = S.n_miss;
+#pragma unroll 1
+        for (uint32_t i = 0; i < nm;) {
+            uint32_t k = 1, tot = S.u.a.miss[i] >> 16;
+            if (!strict)
+                while (i + k < nm && tot + (S.u.a.miss[i + k] >> 16) <= 32) tot += S.u.a.miss[i + k++] >> 16;
+            c_pass += warp_pack_bpe(T, C.base, sb, S.sid, S.u.a.miss + i, k, strict);
+            i += k;
+        }
+    }
+    TSTAMP(3, c_pass);
+#ifdef GPUBPE_DEBUG_STAMPS
+    if (P.dbg && t < 2048 && lane == 0) P.dbg[16384 + 8 * t + 6] = S.n_miss;
+#endif
+
+    // ---- 7. entries in output order (chunked scan over the list) -> outbuf;
+    //         each segment's sid slot then holds its entry offset
+    uint32_t total = 0;
+#pragma unroll 1
+    for (uint32_t i0 = 0; i0 < nseg; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const bool valid = i < nseg;
+        const int p = valid ? S.seg[i] : 0;
+        const uint32_t v = valid ? S.sid[SI(p)] : 0u;
+        const uint32_t cc = valid ? seg_entries(v) : 0u;
+        uint32_t incl = cc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t o = total + incl - cc;
+        if (valid) {
+            if ((v >> 24) == 0xFFu) {
+                S.u.outbuf[o] = MARK | S.sid[SI(p + 1)];
+            } else {
+                S.u.outbuf[o] = v & 0xFFFFFFu;
+#pragma unroll 1
+                for (uint32_t j = 1; j < cc; ++j) S.u.outbuf[o + j] = S.sid[SI(p + j)];
+            }
+            S.sid[SI(p)] = o;
+        }
+        total += __shfl_sync(FULL_MASK, incl, 31);
+    }
+    __syncwarp();
+    {
+        uint4 *dst = reinterpret_cast<uint4 *>(P.scratch + slot * SLOT);
+        const uint4 *src = reinterpret_cast<const uint4 *>(S.u.outbuf);
+#pragma unroll 1
+        for (uint32_t k = lane; k < (total + 3) / 4; k += 32) dst[k] = src[k];
+        if (lane == 0) P.tiles[slot] = (unsigned long long)total | ((unsigned long long)S.n_def << 16);
+    }
+    TSTAMP(4, total);
+
+    // ---- 8. tile-local entry offsets of the documents starting in this tile
+    if (P.n_docs > 1 || a == 0 || last) {
+        long long dlb;  // first document with offs >= a
+        if (__ldg(&P.doc_offs[dc]) < a) {
+            dlb = dc + 1;
+        } else {
+            dlb = dc;
+#pragma unroll 1
+            for (;;) {  // empty documents just before dc also start at a
+                const long long d = dlb - 1 - lane;
+                const bool eq = d >= 0 && __ldg(&P.doc_offs[d]) == a;
+                const unsigned m = __ballot_sync(FULL_MASK, eq);
+                const int run = m == FULL_MASK ? 32 : __ffs(~m) - 1;
+                dlb -= run;
+                if (run < 32) break;
+            }
+        }
+#pragma unroll 1
+        for (long long d0 = dlb;; d0 += 32) {
+            const long long d = d0 + lane;
+            bool in = false;
+            if (d <= (long long)P.n_docs) {
+                const long long s = __ldg(&P.doc_offs[d]);
+                if (s < a + nin || last) {
+                    in = true;
+                    const int q = (int)(s - a);
+                    P.out_offs[d] = (long long)(q >= nin ? total : S.sid[SI(q)]);
+                }
+            }
+            if (__ballot_sync(FULL_MASK, in) != FULL_MASK) break;
+        }
+    }
+    __syncwarp();
+    TSTAMP(5, 0);
+    X.n_segments += c_seg;
+    X.memo_hits += c_memo;
+    X.short_merges += c_miss;
+    if (lane == 0) X.engine_passes += c_pass;
+}
+
+// ------------------------------------------------------------------ phase B
+
+// Extra ids of the deferred markers among the first n entries of a slot
+// (one thread; only for tiles that hold markers).
+__device__ unsigned long long marker_extra(const EncodeParams &P, const uint32_t *src, uint32_t n) {
+    unsigned long long x = 0;
+    for (uint32_t k = 0; k < n; ++k) {
+        const uint32_t e = __ldcg(&src[k]);
+        if (e & MARK) x += (unsigned long long)__ldcg(&P.recs[e & ~MARK].count) - 1;
+    }
+    return x;
+}
+
+// Warp: copy one tile's slot to out_ids[base ...], expanding deferred markers.
+__device__ void place_tile(const EncodeParams &P, const uint32_t *src, unsigned long long w,
+                           unsigned long long base) {
+    const int lane = threadIdx.x & 31;
+    const DevTables &T = P.T;
+    const uint32_t n = TW_ENTRIES(w);
+    uint32_t *dst = P.out_ids + base;
+    if (!TW_HASDEF(w)) {
+        for (uint32_t k = lane; k < n; k += 32) dst[k] = out_id(T, __ldcg(&src[k]));
+    } else {
+        unsigned long long o = 0;
+        for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const uint32_t e = k < n ? __ldcg(&src[k]) : 0u;
+            const bool mark = k < n && (e & MARK);
+            uint32_t cntk = 0, res = 0;
+            if (mark) {
+                cntk = __ldcg(&P.recs[e & ~MARK].count);
+                res = __ldcg(&P.recs[e & ~MARK].res);
+            } else if (k < n) {
+                cntk = 1;
+            }
+            unsigned long long incl = cntk;
+#pragma unroll
+            for (int s = 1; s < 32; s <<= 1) {
+                const unsigned long long y = __shfl_up_sync(FULL_MASK, incl, s);
+                if (lane >= s) incl += y;
+            }
+            const unsigned long long ex = o + incl - cntk;
+            if (k < n && !mark) dst[ex] = out_id(T, e);
+            for (unsigned mk = __ballot_sync(FULL_MASK, mark); mk; mk &= mk - 1) {
+                const int src_lane = __ffs(mk) - 1;
+                const unsigned long long at = __shfl_sync(FULL_MASK, ex, src_lane);
+                const uint32_t c = __shfl_sync(FULL_MASK, cntk, src_lane);
+                const uint32_t r = __shfl_sync(FULL_MASK, res, src_lane);
+                for (uint32_t j = lane; j < c; j += 32) dst[at + j] = out_id(T, __ldcg(&P.arena[r + j]));
+            }
+            o += __shfl_sync(FULL_MASK, incl, 31);
+        }
+    }
+    __syncwarp();
+    // the slot is dead: drop its lines from L2 without write-back (tiles with
+    // markers are re-read by the document fix-up)
+    if (!TW_HASDEF(w))
+        for (uint32_t k = lane; k < (n * 4 + 127) / 128; k += 32) l2_discard(src + 32 * k);
+}
+
+// CTA: place the tiles [lo, hi) of round r (unit u = r * grid + blockIdx.x).
+__device__ __noinline__ void place_range(const EncodeParams &P, CtaSmem &C, unsigned long long r,
+                            unsigned long long t0, unsigned long long lo, unsigned long long hi) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const unsigned long long par = r & 1;
+    const unsigned long long *tw = P.tiles + par * P.round_tiles + (lo - t0);
+    const uint32_t *slots = P.scratch + (par * P.round_tiles + (lo - t0)) * SLOT;
+    const int nt = (int)(hi - lo);
+    const unsigned long long u = r * gridDim.x + blockIdx.x;
+    if (wid == 0) {
+        constexpr int PER = UNIT_MAX / 32;
+        unsigned long long v[PER], sum = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int k = lane * PER + j;
+            unsigned long long w = k < nt ? __ldcg(&tw[k]) : 0ull;
+            C.tw[k] = w;
+            v[j] = TW_ENTRIES(w) + TW_EXTRA(w);
+            sum += v[j];
+        }
+        unsigned long long incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const unsigned long long total = __shfl_sync(FULL_MASK, incl, 31);
+        unsigned long long o = incl - sum;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            C.tb[lane * PER + j] = o;
+            o += v[j];
+        }
+        unsigned long long base = 0;
+        if (nt > 0) {
+            base = warp_lookback(P.status, u, total, P.epoch);
+        } else if (lane == 0) {  // empty unit: an aggregate of 0 keeps the chain moving
+            st_relaxed(&P.status[u], ((unsigned long long)P.epoch << 44) | (LB_AGG << 42));
+        }
+        if (lane == 0) {
+            C.bcast[0] = base;
+            if (nt > 0 && hi == P.n_tiles) P.st->n_ids = base + total;
+        }
+    }
+    __syncthreads();
+    const unsigned long long base = C.bcast[0];
+    for (int k = wid; k < nt; k += NW) place_tile(P, slots + (size_t)k * SLOT, C.tw[k], base + C.tb[k]);
+    // CSR offsets of the documents starting in [lo, hi): tile-local -> global
+    if (wid == 0 && nt > 0 && (P.n_docs > 1 || lo == 0 || hi == P.n_tiles)) {
+        const long long blo = (long long)lo * P.tile_bytes;
+        long long d = 0;
+        if (blo > 0) {  // first document with offs >= blo (lower bound)
+            long long lo_d = 0, hi_d = (long long)P.n_docs;  // answer in [lo_d, hi_d]
+            while (hi_d > lo_d) {
+                const long long step = (hi_d - lo_d + 31) / 32;
+                const long long idx = lo_d + (long long)lane * step;
+                const bool lt = idx < hi_d && __ldg(&P.doc_offs[idx]) < blo;
+                const unsigned m = __ballot_sync(FULL_MASK, lt);
+                if (!m) { hi_d = lo_d; break; }
+                const int l = 31 - __clz(m);
+                lo_d = lo_d + (long long)l * step + 1;
+                hi_d = min(hi_d, lo_d - 1 + step);
+            }
+            d = lo_d;
+        }
+        for (long long d0 = d;; d0 += 32) {
+            const long long dd = d0 + lane;
+            bool in = false;
+            if (dd <= (long long)P.n_docs) {
+                const long long s = __ldg(&P.doc_offs[dd]);
+                if (s < (long long)hi * P.tile_bytes || hi == P.n_tiles) in = s >= blo;
+                if (in) {
+                    const long long t = min(s / P.tile_bytes, (long long)P.n_tiles - 1);
+                    const int k = (int)(t - (long long)lo);
+                    const uint32_t local = (uint32_t)__ldcg(&P.out_offs[dd]);
+                    unsigned long long v = base + C.tb[k] + local;
+                    if (TW_HASDEF(C.tw[k])) v += marker_extra(P, slots + (size_t)k * SLOT, local);
+                    P.out_offs[dd] = (long long)v;
+                }
+            }
+            if (__ballot_sync(FULL_MASK, in) != FULL_MASK) break;
+        }
+    }
+    __syncthreads();
+}
+
+// All CTAs (co-resident: cooperative launch).  k = 1, 2, ... per use.
+__device__ void grid_sync(EncodeState *st, unsigned int k) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(&st->bar, 1u);
+        const unsigned int target = k * gridDim.x;
+        while (ld_relaxed_u32(&st->bar) < target) __nanosleep(128);
+        __threadfence();  // acquire side of the barrier, once
+    }
+    __syncthreads();
+}
+
+// Sum the warps' counters into the CTA, then into the call's global set.
+__device__ void publish_counters(CtaSmem &C, WarpCtx &X, PassCounters *dst) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long seg = X.n_segments, memo = X.memo_hits, sm = X.short_merges, ep = X.engine_passes;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        seg += __shfl_xor_sync(FULL_MASK, seg, o);
+        memo += __shfl_xor_sync(FULL_MASK, memo, o);
+        sm += __shfl_xor_sync(FULL_MASK, sm, o);
+        ep += __shfl_xor_sync(FULL_MASK, ep, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&C.pc.n_segments, seg);
+        atomicAdd(&C.pc.memo_hits, memo);
+        atomicAdd(&C.pc.short_merges, sm);
+        atomicAdd(&C.pc.engine_passes, ep);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long *s = &C.pc.n_segments;
+        unsigned long long *d = &dst->n_segments;
+        for (int i = 0; i < (int)(sizeof(PassCounters) / 8); ++i)
+            if (s[i]) atomicAdd(&d[i], s[i]);
+    }
+}
+
+// Deferred records [d0, d1) of round r: encode each with the CTA engine into
+// the arena and add its extra ids to its tile word.
+__device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, unsigned long long d0,
+                                unsigned long long d1, unsigned long long t0, unsigned long long par) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    EncodeState *st = P.st;
+    const long long N = (long long)P.n_bytes;
+    const bool strict = P.strict || !P.T.well_formed;
+    for (;;) {
+        if (tid == 0) C.bcast[0] = d0 + atomicAdd(&st->rec_ctr, 1ull);
+        __syncthreads();
+        const unsigned long long r = C.bcast[0];
+        if (r >= d1) break;
+        const long long s0 = (long long)__ldcg(&P.recs[r].start);
+        if (wid == 0) {
+            const long long d = P.n_docs > 1 ? warp_doc_from(P.doc_offs, 0, P.n_docs, s0) : 0;
+            if (lane == 0) C.bcast[1] = (unsigned long long)d;
+        }
+        __syncthreads();
+        long long lim = next_struct_cut(P, (long long)C.bcast[1], s0);
+        if (lim > N) lim = N;
+        const long long send = cta_first_nonjunction(P, C.jb, s0 + 1, lim, C.es);
+        const unsigned long long len = (unsigned long long)(send - s0);
+        if (tid == 0) {
+            const unsigned long long words = (ENGINE_BYTES(len) + 15) / 16 * 4;
+            unsigned long long off = atomicAdd(&st->arena_used, words);
+            if (off + words > P.arena_words) {
+                atomicExch(&st->overflow, 1ull);
+                off = ~0ull;
+            }
+            C.bcast[2] = off;
+        }
+        __syncthreads();
+        const unsigned long long off = C.bcast[2];
+        if (off == ~0ull) continue;
+        EngineMem M;
+        M.tok = P.arena + off;
+        M.tok2 = M.tok + len;
+        M.pr = reinterpret_cast<uint2 *>(M.tok2 + len);
+        M.pr2 = M.pr + len;
+        M.sel = reinterpret_cast<uint8_t *>(M.pr2 + len);
+        for (unsigned long long j = tid; j < len; j += NT) M.tok[j] = C.base[__ldg(&P.bytes[s0 + j])];
+        __syncthreads();
+        uint32_t passes;
+        const uint32_t *res;
+        const uint32_t cnt = engine_run(P.T, M, (uint32_t)len, strict, C.es, &passes, &res);
+        if (tid == 0) {
+            P.recs[r].count = cnt;
+            P.recs[r].res = (uint32_t)(res - P.arena);
+            const unsigned long long t = (unsigned long long)s0 / (unsigned long long)P.tile_bytes;
+            atomicAdd(&P.tiles[par * P.round_tiles + (t - t0)], ((unsigned long long)cnt - 1) << 17);
+            if (len >= GIANT_MIN) {
+                atomicAdd(&C.pc.giant_segments, 1ull);
+                atomicAdd(&C.pc.giant_bytes, len);
+            } else {
+                atomicAdd(&C.pc.medium_segments, 1ull);
+            }
+            atomicAdd(&C.pc.engine_passes, (unsigned long long)passes);
+        }
+        __syncthreads();
     }
 }
 
 // ------------------------------------------------------------------ kernel
 
-struct TileSmem {
-    uint8_t sb[LD + 16];
-    uint32_t bits[(LD + 31) / 32 + 2];
-    uint32_t sid[LD];  // ids of each segment, stored from the segment's start slot
-    uint16_t seg_start[TILE];
-    uint16_t seg_end[TILE];
-    uint32_t seg_cnt[TILE];  // counts, then exclusive offsets
-    uint16_t miss[TILE];     // segments for the warp engine
-    uint16_t pend[TILE / (SHORT_MAX + 1) + 4];
-    EngineShared es;
-    unsigned long long tile;
-    unsigned long long base;
-    unsigned long long arena_off;
-    long long d0;
-    const uint32_t *ovh_src;  // result of the overhang segment (scratch or arena)
-    unsigned int n_seg, n_miss, n_pend, total, ovh_seg;
-    unsigned int c_memo, c_warp, c_med, c_giant, c_passes;
-    unsigned long long c_giant_bytes;
-};
-
-__device__ __forceinline__ void set_bit(uint32_t *bits, int k) { atomicOr(&bits[k >> 5], 1u << (k & 31)); }
-
-#define LB_AGG 1ull
-#define LB_INC 2ull
-#define LB_VALUE_MASK ((1ull << 42) - 1)
-
-__global__ void __launch_bounds__(NT) k_encode(EncodeParams P) {
+__global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ EncodeParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
+    CtaSmem &C = *reinterpret_cast<CtaSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const long long N = (long long)P.n_bytes;
-    const DevTables &T = P.T;
-    const bool strict = P.strict || !T.well_formed;
-    const bool use_memo = T.memo_mask != 0;
-    uint8_t *medp = P.med_scratch + (size_t)blockIdx.x * MED_BYTES;
+    EncodeState *st = P.st;
     if (blockIdx.x == 0 && tid == 0) *P.st_next = EncodeState{};
-
-    for (;;) {
-        if (tid == 0) {
-            S.tile = atomicAdd(&P.st->tile_counter, 1ull);
-            S.n_miss = S.n_pend = 0;
-            S.ovh_src = nullptr;
-            S.ovh_seg = 0xFFFFFFFFu;
-            S.c_memo = S.c_warp = S.c_med = S.c_giant = S.c_passes = 0;
-            S.c_giant_bytes = 0;
+    // warm the probe tables into L2 (they were flushed or evicted since the last call)
+    for (unsigned long long off = ((unsigned long long)blockIdx.x * NT + tid) * 128ull; off < P.prefetch_bytes;
+         off += (unsigned long long)gridDim.x * NT * 128ull)
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(P.prefetch + off));
+    for (int k = tid; k < 2048; k += NT) C.jb[k] = __ldg(&P.T.jbits[k]);
+    for (int k = tid; k < 256; k += NT) C.base[k] = __ldg(&P.T.base[k]);
+    if (tid < (int)(sizeof(PassCounters) / 8)) (&C.pc.n_segments)[tid] = 0;
+    __syncthreads();
+    if (P.dbg && tid == 0) P.dbg[4 * blockIdx.x] = gtimer();
+    WarpSmem &S = C.w[wid];
+    WarpCtx X{};
+    unsigned int nbar = 0;
+    unsigned long long d_done = 0;
+    const unsigned long long R = P.round_tiles;
+    const unsigned long long G = gridDim.x;
+    for (unsigned long long r = 0, t0 = 0; t0 < P.n_tiles; ++r, t0 += R) {
+        const unsigned long long t1 = min(P.n_tiles, t0 + R), par = r & 1;
+        // ---- phase A: encode tiles of the round into their slots
+        for (;;) {
+            unsigned long long t = 0;
+            if (lane == 0) t = t0 + atomicAdd(&st->actr[par], 1ull);
+            t = __shfl_sync(FULL_MASK, t, 0);
+            if (t >= t1) break;
+            const unsigned long long g0 = P.dbg ? gtimer() : 0;
+            encode_tile(P, C, S, t, par * R + (t - t0), X);
+            if (P.dbg && lane == 0 && t < 4096) {
+                P.dbg[1024 + 2 * t] = g0;
+                P.dbg[1024 + 2 * t + 1] = gtimer();
+            }
         }
+        if (P.dbg_phase_a_only) return;
+        if (blockIdx.x == 0 && tid == 0) st->actr[par ^ 1] = 0;
+        if (P.dbg && tid == 0 && r == 0) P.dbg[4 * blockIdx.x + 1] = gtimer();
+        grid_sync(st, ++nbar);
+        if (P.dbg && tid == 0 && r == 0) P.dbg[4 * blockIdx.x + 2] = gtimer();
+        // ---- rare: deferred segments recorded in this round
+        if (tid == 0) C.bcast[3] = __ldcg(&st->n_def);
         __syncthreads();
-        const unsigned long long t = S.tile;
-        if (t >= P.n_tiles) break;
-        const long long a = (long long)(t * TILE);
-        const long long b = min(a + TILE, N);
-        const long long el = min(b + HALO, N);
-        const int nld = (int)(el - a);
-        const int ntile = (int)(b - a);
-
-        // ---- stage bytes; warp 0 finds the document holding byte a
-        for (int k = tid; k < nld; k += NT) S.sb[k] = __ldg(&P.bytes[a + k]);
-        const uint32_t prev = a > 0 ? __ldg(&P.bytes[a - 1]) : 0u;
-        if (wid == 0) {
-            const long long d = P.n_docs > 1 ? warp_doc_of(P.doc_offs, P.n_docs, a) : 0;
-            if (lane == 0) S.d0 = d;
+        const unsigned long long D = C.bcast[3];
+        if (D > d_done) {
+            if (D > P.rec_cap) {
+                if (blockIdx.x == 0 && tid == 0) atomicExch(&st->overflow, 1ull);
+                return;
+            }
+            encode_deferred(P, C, d_done, D, t0, par);
+            grid_sync(st, ++nbar);
+            if (blockIdx.x == 0 && tid == 0) st->rec_ctr = 0;
+            if (__ldcg(&st->overflow)) return;
+            d_done = D;
         }
-        __syncthreads();
-        // ---- junction-miss bits for slots [0, nld); slot k = cut before byte a+k
-        for (int w = wid; w * 32 < nld + 1; w += NT / 32) {
-            const int k = w * 32 + lane;
-            bool cut;
-            if (k < nld) {
-                const uint32_t x = k ? S.sb[k - 1] : prev;
-                cut = (a + k == 0) || !is_junction(T.jbits, x, S.sb[k]);
-            } else {
-                cut = (k == nld) && (el == N);
-            }
-            const unsigned m = __ballot_sync(FULL_MASK, cut);
-            if (lane == 0) S.bits[w] = m;
-        }
-        __syncthreads();
-        // ---- document starts and chunk cuts inside [a, el)
-        const long long d0 = S.d0;
-        for (long long d = d0 + tid; d < (long long)P.n_docs; d += NT) {
-            const long long s = __ldg(&P.doc_offs[d]);
-            if (s >= el) break;
-            const long long e = __ldg(&P.doc_offs[d + 1]);
-            if (s >= a) set_bit(S.bits, (int)(s - a));
-            if ((unsigned long long)(e - s) > P.max_seq_len) {
-                const long long cb = (long long)P.chunk_budget;
-                long long m = s < a ? (a - s + cb - 1) / cb : 1;
-                if (m < 1) m = 1;
-                for (long long c = s + m * cb; c < e && c < el; c += cb) set_bit(S.bits, (int)(c - a));
-            }
-        }
-        __syncthreads();
-        // ---- segments starting in [0, ntile): start and end slot
-        {
-            const int per = TILE / NT;
-            const int k0 = tid * per;
-            uint32_t mine = (S.bits[k0 >> 5] >> (k0 & 31)) & ((1u << per) - 1);
-            if (k0 >= ntile) mine = 0;
-            else if (k0 + per > ntile) mine &= (1u << (ntile - k0)) - 1;
-            uint32_t tot;
-            uint32_t idx = block_excl_sum(__popc(mine), S.es, &tot);
-            const int lim = el == N ? nld : nld - 1;  // last slot whose cut status is known
-            while (mine) {
-                const int k = k0 + __ffs(mine) - 1;
-                mine &= mine - 1;
-                int q = k + 1, end = NOSEG;
-                while (q <= lim) {
-                    const uint32_t wv = S.bits[q >> 5] >> (q & 31);
-                    if (wv) {
-                        const int c = q + __ffs(wv) - 1;
-                        if (c <= lim) end = c;
-                        break;
-                    }
-                    q = (q | 31) + 1;
-                }
-                S.seg_start[idx] = (uint16_t)k;
-                S.seg_end[idx] = (uint16_t)end;
-                ++idx;
-            }
-            if (tid == 0) S.n_seg = tot;
-        }
-        __syncthreads();
-        const unsigned int n_seg = S.n_seg;
-        // ---- one thread per segment: base id, memo, or defer
-        for (unsigned int i = tid; i < n_seg; i += NT) {
-            const uint32_t k0 = S.seg_start[i], e = S.seg_end[i];
-            if (e == NOSEG || e - k0 > SHORT_MAX) {
-                S.pend[atomicAdd(&S.n_pend, 1u)] = (uint16_t)i;
-                continue;
-            }
-            const uint32_t len = e - k0;
-            if (len == 1) {
-                S.sid[k0] = __ldg(&T.base[S.sb[k0]]);
-                S.seg_cnt[i] = 1;
-                continue;
-            }
-            const uint32_t id = use_memo ? memo_lookup(T, S.sb + k0, len) : GPUBPE_INF;
-            if (id != GPUBPE_INF) {
-                S.sid[k0] = id;
-                S.seg_cnt[i] = 1;
-                atomicAdd(&S.c_memo, 1u);
-            } else {
-                S.miss[atomicAdd(&S.n_miss, 1u)] = (uint16_t)i;
-            }
-        }
-        __syncthreads();
-        // ---- one warp per memo miss: exact multi-merge in registers
-        {
-            const unsigned int n_miss = S.n_miss;
-            unsigned int wp = 0, ws = 0;
-            for (unsigned int m = wid; m < n_miss; m += NT / 32) {
-                const unsigned int i = S.miss[m];
-                const uint32_t k0 = S.seg_start[i], len = S.seg_end[i] - k0;
-                const uint32_t tk = lane < len ? __ldg(&T.base[S.sb[k0 + lane]]) : 0u;
-                uint32_t np;
-                const uint32_t cnt = warp_bpe(T, tk, len, strict, S.sid + k0, &np);
-                wp += np;
-                ++ws;
-                if (lane == 0) S.seg_cnt[i] = cnt;
-            }
-            if (lane == 0 && ws) {
-                atomicAdd(&S.c_passes, wp);
-                atomicAdd(&S.c_warp, ws);
-            }
-        }
-        __syncthreads();
-        // ---- long segments: whole CTA, in-tile ones first, the overhang last
-        const unsigned int n_pend = S.n_pend;
-        for (int phase = 0; phase < 2; ++phase) {
-            for (unsigned int pi = 0; pi < n_pend; ++pi) {
-                const unsigned int i = S.pend[pi];
-                const uint32_t k0 = S.seg_start[i], e = S.seg_end[i];
-                if ((e == NOSEG) != (phase == 1)) continue;
-                const long long s = a + k0;
-                long long send;
-                if (e != NOSEG) {
-                    send = s + (e - k0);
-                } else {
-                    long long d = d0;
-                    while (__ldg(&P.doc_offs[d + 1]) <= s) ++d;  // docs overlapping the tile
-                    long long lim = next_struct_cut(P, d, s);
-                    if (lim > N) lim = N;
-                    send = cta_first_nonjunction(P, a + nld, lim, S.es);
-                }
-                const unsigned long long len = (unsigned long long)(send - s);
-                uint8_t *buf = medp;
-                if (len > MED_MAX) {
-                    if (tid == 0) {
-                        const unsigned long long words = (ENGINE_BYTES(len) + 15) / 16 * 4;
-                        unsigned long long off = atomicAdd(&P.st->arena_used, words);
-                        if ((off + words) * 4 > P.arena_cap) {
-                            atomicExch(&P.st->overflow, 1ull);
-                            off = ~0ull;
-                        }
-                        S.arena_off = off;
-                        S.c_giant++;
-                        S.c_giant_bytes += len;
-                    }
-                    __syncthreads();
-                    if (S.arena_off == ~0ull) {  // the host re-runs with a larger arena
-                        if (tid == 0) S.seg_cnt[i] = 0;
-                        __syncthreads();
-                        continue;
-                    }
-                    buf = P.arena + S.arena_off * 4;
-                } else if (tid == 0) {
-                    S.c_med++;
-                }
-                EngineMem M;
-                M.tok = reinterpret_cast<uint32_t *>(buf);
-                M.tok2 = M.tok + len;
-                M.pr = reinterpret_cast<uint2 *>(M.tok2 + len);  // 2*len words: 8-B aligned
-                M.pr2 = M.pr + len;
-                M.sel = reinterpret_cast<uint8_t *>(M.pr2 + len);
-                for (unsigned long long j = tid; j < len; j += NT)
-                    M.tok[j] = __ldg(&T.base[e != NOSEG ? S.sb[k0 + j] : __ldg(&P.bytes[s + j])]);
-                __syncthreads();
-                uint32_t passes;
-                const uint32_t *res;
-                const uint32_t cnt = engine_run(T, M, (uint32_t)len, strict, S.es, &passes, &res);
-                if (e != NOSEG)
-                    for (uint32_t j = tid; j < cnt; j += NT) S.sid[k0 + j] = res[j];
-                if (tid == 0) {
-                    S.seg_cnt[i] = cnt;
-                    S.c_passes += passes;
-                    if (e == NOSEG) {
-                        S.ovh_seg = i;
-                        S.ovh_src = res;
-                    }
-                }
-                __syncthreads();
-            }
-        }
-        // ---- exclusive scan of counts -> seg_cnt becomes offsets
-        {
-            const int per = TILE / NT;
-            uint32_t v[TILE / NT];
-            uint32_t sum = 0;
-#pragma unroll
-            for (int j = 0; j < per; ++j) {
-                const unsigned int i = tid * per + j;
-                v[j] = i < n_seg ? S.seg_cnt[i] : 0u;
-                sum += v[j];
-            }
-            uint32_t tot;
-            uint32_t off = block_excl_sum(sum, S.es, &tot);
-#pragma unroll
-            for (int j = 0; j < per; ++j) {
-                const unsigned int i = tid * per + j;
-                if (i < n_seg) S.seg_cnt[i] = off;
-                off += v[j];
-            }
-            if (tid == 0) S.total = tot;
-        }
-        __syncthreads();
-        // ---- decoupled look-back (status words carry the value: relaxed is enough)
-        const unsigned long long total = S.total;
-        if (wid == 0) {
-            const unsigned long long tag = (unsigned long long)P.epoch << 44;
-            unsigned long long excl = 0;
-            if (t == 0) {
-                if (lane == 0) st_relaxed(&P.status[0], tag | (LB_INC << 42) | total);
-            } else {
-                if (lane == 0) st_relaxed(&P.status[t], tag | (LB_AGG << 42) | total);
-                long long pos = (long long)t - 1;
-                for (;;) {
-                    const long long j = pos - lane;
-                    unsigned long long v, flag;
-                    if (j >= 0) {
-                        do {
-                            v = ld_relaxed(&P.status[j]);
-                            flag = ((v >> 44) == P.epoch) ? ((v >> 42) & 3ull) : 0ull;
-                        } while (flag == 0);
-                    } else {
-                        v = LB_INC << 42;
-                        flag = LB_INC;
-                    }
-                    const unsigned inc = __ballot_sync(FULL_MASK, flag == LB_INC);
-                    const int stop = inc ? __ffs(inc) - 1 : 31;
-                    unsigned long long val = lane <= stop ? (v & LB_VALUE_MASK) : 0ull;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(FULL_MASK, val, o);
-                    excl += val;
-                    if (inc) break;
-                    pos -= 32;
-                }
-                if (lane == 0) st_relaxed(&P.status[t], tag | (LB_INC << 42) | (excl + total));
-            }
-            if (lane == 0) S.base = excl;
-        }
-        __syncthreads();
-        const unsigned long long base = S.base;
-        // ---- store ids
-        uint32_t *out = P.out_ids + base;
-        const unsigned int oseg = S.ovh_seg;
-        for (unsigned int i = tid; i < n_seg; i += NT) {
-            if (i == oseg) continue;
-            const uint32_t k0 = S.seg_start[i];
-            const uint32_t o = S.seg_cnt[i];
-            const uint32_t c = (i + 1 < n_seg ? S.seg_cnt[i + 1] : S.total) - o;
-            for (uint32_t j = 0; j < c; ++j) out[o + j] = out_id(T, S.sid[k0 + j]);
-        }
-        if (oseg != 0xFFFFFFFFu) {
-            const uint32_t o = S.seg_cnt[oseg];
-            const uint32_t c = (oseg + 1 < n_seg ? S.seg_cnt[oseg + 1] : S.total) - o;
-            const uint32_t *src = S.ovh_src;
-            for (uint32_t j = tid; j < c; j += NT) out[o + j] = out_id(T, src[j]);
-        }
-        // ---- CSR offsets of documents starting in [a, b) (and at N for the last tile)
-        {
-            const long long hi = (b == N) ? N + 1 : b;
-            for (long long d = d0 + tid; d <= (long long)P.n_docs; d += NT) {
-                const long long s = __ldg(&P.doc_offs[d]);
-                if (s >= hi) break;
-                if (s < a) continue;
-                unsigned long long v;
-                if (s == N) {
-                    v = base + total;
-                } else {
-                    const int k = (int)(s - a);
-                    unsigned int lo = 0, h2 = n_seg;
-                    while (lo < h2) {
-                        const unsigned int mid = (lo + h2) >> 1;
-                        if (S.seg_start[mid] < k) lo = mid + 1; else h2 = mid;
-                    }
-                    v = base + (lo < n_seg ? S.seg_cnt[lo] : S.total);
-                }
-                P.out_offs[d] = (long long)v;
-            }
-        }
-        if (tid == 0) {
-            EncodeState *st = P.st;
-            atomicAdd(&st->n_segments, (unsigned long long)n_seg);
-            if (S.c_memo) atomicAdd(&st->memo_hits, (unsigned long long)S.c_memo);
-            if (S.c_warp) atomicAdd(&st->short_merges, (unsigned long long)S.c_warp);
-            if (S.c_med) atomicAdd(&st->medium_segments, (unsigned long long)S.c_med);
-            if (S.c_giant) {
-                atomicAdd(&st->giant_segments, (unsigned long long)S.c_giant);
-                atomicAdd(&st->giant_bytes, S.c_giant_bytes);
-            }
-            if (S.c_passes) atomicAdd(&st->engine_passes, (unsigned long long)S.c_passes);
-            if (b == N) atomicAdd(&st->n_ids, base + total);
-        }
-        __syncthreads();
+        // ---- phase B: place this CTA's contiguous range of the round's tiles
+        const unsigned long long q = (t1 - t0 + G - 1) / G;
+        const unsigned long long lo = min(t1, t0 + blockIdx.x * q), hi = min(t1, lo + q);
+        place_range(P, C, r, t0, lo, hi);
     }
+    publish_counters(C, X, &st->c);
+    if (P.dbg && tid == 0) P.dbg[4 * blockIdx.x + 3] = gtimer();
 }
 
 // ------------------------------------------------------------------ lookup
@@ -467,23 +887,31 @@ __global__ void k_lookup_pairs(DevTables T, const uint32_t *l, const uint32_t *r
 
 // ------------------------------------------------------------------ launchers
 
-size_t tile_smem_bytes() { return sizeof(TileSmem); }
+size_t tile_smem_bytes() { return sizeof(CtaSmem); }
+int unit_max() { return UNIT_MAX; }
 
 cudaError_t launch_encode(const EncodeParams &P, int grid, cudaStream_t s, cudaEvent_t *ev,
-                          const cudaAccessPolicyWindow *win) {
+                          const cudaAccessPolicyWindow *win, bool coop) {
     if (ev) cudaEventRecord(ev[0], s);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = sizeof(TileSmem);
+    cfg.dynamicSmemBytes = sizeof(CtaSmem);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    if (win && win->num_bytes) {
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow = *win;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (coop) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
     }
+    if (win && win->num_bytes) {
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow = *win;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_encode, P);
     if (ev) cudaEventRecord(ev[1], s);
     return e != cudaSuccess ? e : cudaGetLastError();
@@ -491,11 +919,11 @@ cudaError_t launch_encode(const EncodeParams &P, int grid, cudaStream_t s, cudaE
 
 cudaError_t setup_kernels() {
     return cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(TileSmem));
+                                (int)sizeof(CtaSmem));
 }
 
 cudaError_t tile_occupancy(int *blocks) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_encode, NT, sizeof(TileSmem));
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_encode, NT, sizeof(CtaSmem));
 }
 
 cudaError_t launch_lookup(const DevTables &T, const uint32_t *l, const uint32_t *r,

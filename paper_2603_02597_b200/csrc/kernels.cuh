@@ -1,40 +1,59 @@
 // kernels.cuh -- the fused encode kernel and its launch parameters.
 //
-// k_encode is ONE persistent launch per batch.  Each CTA repeatedly takes the
-// next TILE bytes (dynamic tile counter, so tiles are taken in order) and:
-//   1. stages the tile (+HALO) in shared memory, maps bytes to ids,
-//   2. marks segment boundaries: junction bitmap misses, document starts,
-//      fixed-offset chunk cuts (P-default semantics),
-//   3. encodes every segment that STARTS in the tile:
-//        len 1                    base id
-//        2..32, vocab string      one memo probe
-//        2..32, other             one warp, exact multi-merge in registers
-//        33..MED_MAX              whole CTA, exact multi-merge in scratch
-//        longer ("giant")         whole CTA, exact multi-merge in the arena
-//   4. publishes its id count and finds its output offset by decoupled
-//      look-back over the tile status words,
-//   5. stores ids (coalesced) and the CSR offsets of documents starting in it.
+// k_encode is ONE cooperative persistent launch per batch (grid = one CTA of
+// NW warps per SM).  The input is processed in ROUNDS of up to R tiles of WT
+// bytes; each round has two phases separated by one grid barrier.
+//
+// Phase A (encode; every WARP autonomous, no waiting): a warp takes the next
+// tile of the round from a counter and
+//   1. stages the tile (+HALO) in its own shared memory (16-B loads),
+//   2. marks cut positions: junction-bitmap misses (bitmap in smem), document
+//      starts, fixed-offset chunk cuts (P-default semantics), end of input,
+//   3. encodes every segment that STARTS in the tile, lane L owning the
+//      segments that start in bytes [16L, 16L+16):
+//        len 1               base id
+//        2..SHORT_MAX        one memo probe (vocab strings whose BPE is
+//                            themselves); on a miss the whole warp runs the
+//                            exact multi-merge in registers (warp_engine.cuh)
+//        longer              "deferred": a marker entry + a record
+//   4. writes the tile's ids in order to its scratch SLOT (L2-resident) with
+//      coalesced 16-B stores, its entry count, and the tile-local offsets of
+//      the documents that start in it.
+// Deferred segments (longer than SHORT_MAX: never in prose, which tops out at
+// 14 bytes; digit/letter/newline runs) are then encoded by whole CTAs with the
+// exact engine (engine.cuh) into the arena, and a second barrier follows.
+// Phase B (place): CTA c owns a contiguous range of the round's tiles: it
+// scans their counts, finds the range's output offset by a CTA-granular
+// decoupled look-back (G units per round), copies the slots to the output
+// (expanding deferred markers), fixes the documents' CSR offsets and discards
+// the scratch lines from L2 without write-back.
 #pragma once
 #include "common.cuh"
 #include "engine.cuh"
 #include "warp_engine.cuh"
 
-#define TILE 2048            // bytes per tile
-#define HALO 256             // bytes staged past the tile end
-#define LD (TILE + HALO)     // bytes staged per tile
-#define NT 256               // threads per CTA
-#define SHORT_MAX 32         // longest segment a warp encodes in registers
-#define MED_MAX LD           // longest segment encoded in per-CTA scratch
-#define NOSEG 0xFFFFu        // segment end lies past the staged bytes
+constexpr int WT = 512;         // bytes per warp tile (16 per lane)
+constexpr int HALO = 32;        // bytes staged past the tile: any short segment ends inside
+constexpr int LD = WT + HALO;   // staged bytes
+constexpr int NGRP = LD / 16;   // 16-position groups whose cut bits are computed
+#ifndef GPUBPE_NW
+#define GPUBPE_NW 32
+#endif
+constexpr int NW = GPUBPE_NW;   // warps per CTA
+constexpr int NT = NW * 32;     // threads per CTA
+constexpr int SHORT_MAX = 32;   // longest segment encoded inside the tile loop
+constexpr int GIANT_MIN = 2305; // deferred segments at least this long count as "giant"
+constexpr int SLOT = WT + SHORT_MAX;  // scratch entries per tile (ids of segments starting in it)
+constexpr int UNIT_MAX = 128;   // tiles per CTA per round in phase B
+constexpr unsigned int MARK = 0x80000000u;  // scratch entry: deferred record index follows
 
-// Per-call device state, zeroed at the start of every encode.
-struct EncodeState {
-    unsigned long long tile_counter;
-    unsigned long long arena_used;  // u32 words requested from the arena
-    unsigned long long overflow;
-    unsigned long long error;
-    // counters
-    unsigned long long n_ids;
+// tile word: bits 0-15 entries, bit 16 has deferred markers, bits 17.. extra ids
+// of the deferred segments beyond their one marker entry
+#define TW_ENTRIES(w) ((uint32_t)((w) & 0xFFFFull))
+#define TW_HASDEF(w) (((w) >> 16) & 1ull)
+#define TW_EXTRA(w) ((w) >> 17)
+
+struct PassCounters {
     unsigned long long n_segments;
     unsigned long long memo_hits;
     unsigned long long short_merges;
@@ -42,6 +61,28 @@ struct EncodeState {
     unsigned long long giant_segments;
     unsigned long long giant_bytes;
     unsigned long long engine_passes;
+};
+
+// Per-call device state, zeroed before the call (each call zeroes the next
+// call's slot; two slots alternate).  Hot words get their own 128-B lines.
+struct EncodeState {
+    unsigned long long actr[2];      // phase-A tile counters by round parity
+    unsigned long long pad0[14];
+    unsigned int bar;                // grid barrier arrivals
+    unsigned int pad1[31];
+    unsigned long long n_def;        // deferred segments recorded
+    unsigned long long rec_ctr;      // deferred records taken by CTAs
+    unsigned long long arena_used;   // u32 words requested from the arena
+    unsigned long long overflow;     // arena or record list overflowed: host re-runs
+    unsigned long long n_ids;
+    unsigned long long pad2[3];
+    PassCounters c;
+};
+
+struct DefRec {
+    unsigned long long start;  // first byte of the segment
+    unsigned int count;        // ids it encodes to
+    unsigned int res;          // arena word offset of its ids
 };
 
 struct EncodeParams {
@@ -55,15 +96,24 @@ struct EncodeParams {
     long long *out_offs;
     EncodeState *st;       // this call's state (zeroed by the previous call)
     EncodeState *st_next;  // the next call's state, zeroed here by CTA 0
-    unsigned long long *status;  // [n_tiles] look-back words
-    uint8_t *med_scratch;        // [grid * MED_BYTES]
-    uint8_t *arena;              // giant segments
-    unsigned long long arena_cap;
+    uint32_t *scratch;     // [2][R][SLOT] tile slots by round parity
+    unsigned long long *tiles;   // [2][R] tile words by round parity
+    unsigned long long *status;  // [n_rounds * grid] unit look-back words
+    DefRec *recs;                // [rec_cap]
+    unsigned long long rec_cap;
+    uint32_t *arena;             // deferred-segment engine scratch + results
+    unsigned long long arena_words;
     unsigned long long n_tiles;
-    unsigned int epoch;          // look-back tag (20 bits)
+    unsigned long long round_tiles;  // R
+    const uint8_t *prefetch;     // table region warmed into L2 at kernel start
+    unsigned long long prefetch_bytes;
+    unsigned int epoch;          // look-back tag
     int strict;
+    int aligned;                 // bytes pointer is 16-B aligned
+    int tile_bytes;              // wt: 128, 256 or 512 (host picks by input size)
+    unsigned long long *dbg;     // debug timestamps (GPUBPE_DEBUG & 8), else null
+    int dbg_phase_a_only;        // GPUBPE_DEBUG & 16: profile phase A alone (output invalid)
 };
 
 // engine scratch for n tokens: tok, tok2 (u32) + pr, pr2 (uint2) + sel (u8)
 #define ENGINE_BYTES(n) ((size_t)(n) * 25 + 64)
-#define MED_BYTES ENGINE_BYTES(MED_MAX)

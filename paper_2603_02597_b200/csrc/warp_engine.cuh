@@ -1,116 +1,180 @@
-// warp_engine.cuh -- exact BPE of one short segment (<= 32 tokens) by one warp.
+// warp_engine.cuh -- exact BPE of SEVERAL short segments at once by one warp.
 //
-// Lane j holds token j; pair j = (tok_j, tok_{j+1}) is probed by lane j.  Each
-// pass applies the same selection rule as the CTA engine (engine.cuh: strict
-// single global-min merge, or for well-formed tables every pair that is the
-// global min or passes both blocking walks, with run parity), entirely in
-// registers: run starts by a shuffle max-scan, walks by indexed shuffles,
-// compaction by ballot + __fns + shuffle.  One round of table probes per pass
-// (all lanes in parallel) instead of one dependent probe chain per merge.
+// The memo misses of a tile (segments of <= SHORT_MAX bytes that are not a
+// vocab string whose BPE is itself; ~1.3% of prose segments) are packed
+// back to back into the 32 lanes, lane j holding token j.  Each pass is one
+// round of table probes plus register/shuffle work:
+//   * strict mode (table not well-formed, or forced; one segment per pack):
+//     the single leftmost minimum-rank pair -- the reference's own order
+//     (engines.py:269-335), one merge per pass;
+//   * well-formed tables (every rule using token T ranks above the rule
+//     producing T; GPT-2 is): in every segment, all occurrences of the
+//     segment's minimum rank (even offset inside runs of equal pairs: the
+//     reference's leftmost-first pairing), plus any pair whose bounded
+//     blocking walks succeed (no lower-rank merge can
+//     reach it before its turn; a truncated walk only defers a merge).
+// Pairs never span two packed segments: the last token of a segment has no
+// pair and walks stop at segment ends, exactly as at the ends of a sequence.
 #pragma once
 #include "common.cuh"
 
-#define FULL_MASK 0xffffffffu
+#define WALK_STEPS 8
 
-__device__ __forceinline__ unsigned long long wmin64(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long u = __shfl_xor_sync(FULL_MASK, v, o);
-        v = u < v ? u : v;
-    }
-    return v;
+// Segment boundaries in lane order: bit j of `heads` marks a segment's first
+// lane.  Last lane of the segment holding lane j (n = lanes in use).
+__device__ __forceinline__ uint32_t seg_last_lane(uint32_t heads, uint32_t j, uint32_t n) {
+    const uint32_t after = j >= 31 ? 0u : (heads & (0xFFFFFFFEu << j));
+    return after ? (uint32_t)(__ffs(after) - 2) : n - 1;
 }
 
-// tok: this lane's token (lanes >= n ignored).  Writes the result to
-// out[0..ret) (lane j writes out[j]); returns the output length.  All 32
-// lanes must call.  *passes receives the number of passes.
-__device__ __forceinline__ uint32_t warp_bpe(const DevTables &T, uint32_t tok, uint32_t n, bool strict,
-                                             uint32_t *out, uint32_t *passes) {
+// list[0..k): start | len << 16 of the segments (staged bytes sb), sum len <=
+// 32.  Writes each segment's ids to sid[SI(start..)], tags the first with the
+// count << 24.  Returns the passes run.
+static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *base, const uint32_t *sbw,
+                                  uint32_t *sid, const uint32_t *list, uint32_t k,
+                                  bool strict) {
     const uint32_t lane = threadIdx.x & 31;
-    uint32_t rk = GPUBPE_INF, nw = 0;
+    const uint32_t ent_l = lane < k ? list[lane] : 0u;
+    const uint32_t len_l = ent_l >> 16;
+    uint32_t off = len_l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL_MASK, off, o);
+        if (lane >= (uint32_t)o) off += y;
+    }
+    const uint32_t total = __shfl_sync(FULL_MASK, off, 31);
+    off -= len_l;  // first lane of segment `lane`
+    const uint32_t heads0 = __reduce_or_sync(FULL_MASK, lane < k ? (1u << off) : 0u);
+    // lane j: its segment, token, flags
+    bool valid = lane < total;
+    const uint32_t le = (lane >= 31) ? 0xFFFFFFFFu : ((2u << lane) - 1);
+    const uint32_t seg = (uint32_t)__popc(heads0 & le) - 1;
+    const uint32_t f = 31 - __clz(heads0 & le);
+    const uint32_t ent = __shfl_sync(FULL_MASK, ent_l, seg & 31);
+    uint32_t tok = valid ? base[sb_byte(sbw, (ent & 0xFFFFu) + lane - f)] : 0u;
+    bool first = valid && ((heads0 >> lane) & 1u);
+    bool last = valid && seg_last_lane(heads0, lane, total) == lane;
+    uint32_t n = total;
+
+    // initial pair probes and blocking ranks, one round
+    uint32_t rk = GPUBPE_INF, nw = 0, rl = GPUBPE_INF, rr = GPUBPE_INF;
     {
-        uint32_t t1 = __shfl_down_sync(FULL_MASK, tok, 1);
-        if (lane + 1 < n) {
-            PairHit h = probe_pair(T, tok, t1);
+        const uint32_t t1 = __shfl_down_sync(FULL_MASK, tok, 1);
+        if (valid && !last) {
+            const PairHit h = probe_pair(T, tok, t1);
             rk = h.rank;
             nw = h.nw;
+        }
+        if (valid && !strict) {
+            rl = __ldg(&T.rl[tok]);
+            rr = __ldg(&T.rr[tok]);
         }
     }
     uint32_t np = 0;
     for (;;) {
-        unsigned long long key = rk != GPUBPE_INF ? (((unsigned long long)rk << 32) | lane) : ~0ull;
-        key = wmin64(key);
-        if (key == ~0ull) break;
+        const bool live = valid && !last && rk != GPUBPE_INF;
+        if (!__any_sync(FULL_MASK, live)) break;
         ++np;
-        const uint32_t rmin = (uint32_t)(key >> 32);
         bool sel;
         if (strict) {
-            sel = lane == (uint32_t)key;
+            const uint32_t m = __reduce_min_sync(FULL_MASK, live ? rk : GPUBPE_INF);
+            const unsigned b = __ballot_sync(FULL_MASK, live && rk == m);
+            sel = lane == (uint32_t)(__ffs(b) - 1);
         } else {
-            const bool pair = lane + 1 < n;
-            const uint32_t rprev = __shfl_up_sync(FULL_MASK, rk, 1);
-            const bool start = pair && (lane == 0 || rprev != rk);
-            uint32_t s = start ? lane : 0u;
+            // segmented minimum rank (forward segmented scan, then the
+            // value at the segment's last lane)
+            uint32_t v = live ? rk : GPUBPE_INF;
+            bool fl = first || !valid;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                uint32_t v = __shfl_up_sync(FULL_MASK, s, o);
-                if (lane >= (uint32_t)o) s = max(s, v);
+                const uint32_t yv = __shfl_up_sync(FULL_MASK, v, o);
+                const bool yf = __shfl_up_sync(FULL_MASK, fl, o);
+                if (lane >= (uint32_t)o) {
+                    if (!fl) v = min(v, yv);
+                    fl = fl || yf;
+                }
             }
-            bool ok = pair && rk != GPUBPE_INF && ((lane - s) & 1u) == 0;
-            const bool need = ok && rk != rmin;
+            const uint32_t heads = __ballot_sync(FULL_MASK, first);
+            const uint32_t segmin = __shfl_sync(FULL_MASK, v, valid ? seg_last_lane(heads, lane, n) : lane);
+            // runs of equal pairs (identical tokens, e.g. "aaaa") pair up
+            // leftmost-first: even offset inside the run
+            const uint32_t rprev = __shfl_up_sync(FULL_MASK, rk, 1);
+            const bool same = live && !first && rprev == rk;
+            uint32_t s = lane;
+            if (__any_sync(FULL_MASK, same)) {
+                uint32_t st = (live && !same) ? lane : 0u;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL_MASK, st, o);
+                    if (lane >= (uint32_t)o) st = max(st, y);
+                }
+                s = st;
+            }
+            bool ok = live && ((lane - s) & 1u) == 0;
+            const bool need = ok && rk != segmin;
             if (__any_sync(FULL_MASK, need)) {
-                const uint32_t rrv = lane < n ? __ldg(&T.rr[tok]) : GPUBPE_INF;
-                const uint32_t rlv = lane < n ? __ldg(&T.rl[tok]) : GPUBPE_INF;
                 // left walk from the run start s
-                uint32_t j = s;
+                uint32_t q = s;
                 bool done = !need, res = true;
-                for (int it = 0; it < 32; ++it) {
-                    uint32_t rrj = __shfl_sync(FULL_MASK, rrv, j & 31);
-                    uint32_t rkm = __shfl_sync(FULL_MASK, rk, (j - 1) & 31);
+#pragma unroll 1
+                for (int it = 0; it < WALK_STEPS; ++it) {
+                    const bool qfirst = __shfl_sync(FULL_MASK, first, q & 31);
+                    const uint32_t rrq = __shfl_sync(FULL_MASK, rr, q & 31);
+                    const uint32_t rkm = __shfl_sync(FULL_MASK, rk, (q - 1) & 31);
                     if (!done) {
-                        if (j == 0 || rrj > rk) done = true;
+                        if (qfirst || rrq > rk) done = true;
                         else if (rkm < rk) { done = true; res = false; }
-                        else --j;
+                        else --q;
                     }
                     if (!__any_sync(FULL_MASK, !done)) break;
                 }
-                bool lres = res;
+                const bool lres = done && res;
                 // right walk from lane + 1
-                j = lane + 1;
+                q = lane + 1;
                 done = !need;
                 res = true;
-                for (int it = 0; it < 32; ++it) {
-                    uint32_t rlj = __shfl_sync(FULL_MASK, rlv, j & 31);
-                    uint32_t rkj = __shfl_sync(FULL_MASK, rk, j & 31);
+#pragma unroll 1
+                for (int it = 0; it < WALK_STEPS; ++it) {
+                    const bool qlast = __shfl_sync(FULL_MASK, last, q & 31);
+                    const uint32_t rlq = __shfl_sync(FULL_MASK, rl, q & 31);
+                    const uint32_t rkq = __shfl_sync(FULL_MASK, rk, q & 31);
                     if (!done) {
-                        if (j + 1 >= n || rlj > rk) done = true;
-                        else if (rkj < rk) { done = true; res = false; }
-                        else ++j;
+                        if (qlast || rlq > rk) done = true;
+                        else if (rkq < rk) { done = true; res = false; }
+                        else ++q;
                     }
                     if (!__any_sync(FULL_MASK, !done)) break;
                 }
-                if (need) ok = lres && res;
+                if (need) ok = lres && done && res;
             }
             sel = ok;
         }
         // apply: token j+1 disappears when pair j is selected
-        const bool selprev = __shfl_up_sync(FULL_MASK, sel, 1) && lane > 0;
-        const bool keep = lane < n && !selprev;
+        const bool selprev = __shfl_up_sync(FULL_MASK, sel, 1) && lane > 0 && !first;
+        const bool keep = valid && !selprev;
         const uint32_t newtok = sel ? nw : tok;
+        const bool lastnext = __shfl_down_sync(FULL_MASK, last, 1);  // every lane shuffles
+        const bool newlast = sel ? lastnext : last;
         const unsigned km = __ballot_sync(FULL_MASK, keep);
         const uint32_t n2 = __popc(km);
         const uint32_t src = lane < n2 ? __fns(km, 0, (int)lane + 1) : 0u;
-        const uint32_t t2 = __shfl_sync(FULL_MASK, newtok, src);
-        const bool m2 = __shfl_sync(FULL_MASK, sel, src) && lane < n2;
+        tok = __shfl_sync(FULL_MASK, newtok, src);
+        valid = lane < n2;
+        first = __shfl_sync(FULL_MASK, first, src) && valid;
+        last = __shfl_sync(FULL_MASK, newlast, src) && valid;
+        const bool m2 = __shfl_sync(FULL_MASK, sel, src) && valid;
         const uint32_t rk_src = __shfl_sync(FULL_MASK, rk, src);
         const uint32_t nw_src = __shfl_sync(FULL_MASK, nw, src);
+        const uint32_t rl_src = __shfl_sync(FULL_MASK, rl, src);
+        const uint32_t rr_src = __shfl_sync(FULL_MASK, rr, src);
         const bool mnext = __shfl_down_sync(FULL_MASK, m2, 1);
-        tok = t2;
-        n = n2;
         const uint32_t tnext = __shfl_down_sync(FULL_MASK, tok, 1);
-        if (lane + 1 < n) {
+        n = n2;
+        rl = rl_src;
+        rr = rr_src;
+        if (valid && !last) {
             if (m2 || mnext) {
-                PairHit h = probe_pair(T, tok, tnext);
+                const PairHit h = probe_pair(T, tok, tnext);
                 rk = h.rank;
                 nw = h.nw;
             } else {
@@ -120,8 +184,24 @@ __device__ __forceinline__ uint32_t warp_bpe(const DevTables &T, uint32_t tok, u
         } else {
             rk = GPUBPE_INF;
         }
+        if (m2 && !strict) {
+            rl = __ldg(&T.rl[tok]);
+            rr = __ldg(&T.rr[tok]);
+        }
     }
-    if (lane < n) out[lane] = tok;
-    *passes = np;
-    return n;
+    // write back: segment order is preserved by the compaction
+    const uint32_t heads = __ballot_sync(FULL_MASK, first);
+    const uint32_t le2 = (lane >= 31) ? 0xFFFFFFFFu : ((2u << lane) - 1);
+    const uint32_t sg = (uint32_t)__popc(heads & le2) - 1;
+    const uint32_t f2 = 31 - __clz(heads & le2);
+    const uint32_t e2 = __shfl_sync(FULL_MASK, ent_l, sg & 31);
+    const uint32_t p = e2 & 0xFFFFu;
+    if (valid) sid[SI(p + lane - f2)] = tok;
+    __syncwarp();
+    if (first) {
+        const uint32_t cnt = seg_last_lane(heads, lane, n) - lane + 1;
+        sid[SI(p)] |= cnt << 24;
+    }
+    __syncwarp();
+    return np;
 }

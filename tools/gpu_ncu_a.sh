@@ -1,0 +1,8 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
+cp paper_2603_02597_b200/libgpubpe.so gpurun_out/lib_${TAG:-iter}.so
+for W in ${WORKLOADS:-c1_131k}; do
+GPUBPE_PROFILE_TIMED=1 GPUBPE_DEBUG=16 timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_encode -c 1 \
+    -o gpurun_out/prof_${TAG}_${W} -f python tools/perf.py --only $W --iters 1 --warmup 1 ${PERF_ARGS} > gpurun_out/ncu_${TAG}_${W}.log 2>&1
+tail -2 gpurun_out/ncu_${TAG}_${W}.log
+done

@@ -24,9 +24,10 @@ ROOT = Path(__file__).resolve().parent.parent
 LIB = ROOT / "paper_2603_02597_b200" / "libgpubpe.so"
 
 
-def line_map(kernel: str) -> dict[int, tuple[str, int]]:
+def line_map(kernel: str, lib: Path = LIB) -> dict[int, tuple[str, int]]:
     tmp = Path(tempfile.mkdtemp())
-    subprocess.run(["cuobjdump", "-xelf", "all", str(LIB)], cwd=tmp, check=True, capture_output=True)
+    subprocess.run(["cuobjdump", "-xelf", "all", str(Path(lib).resolve())], cwd=tmp, check=True,
+                   capture_output=True)
     out: dict[int, tuple[str, int]] = {}
     for cub in tmp.glob("*.cubin"):
         txt = subprocess.run(["nvdisasm", "-g", str(cub)], capture_output=True, text=True).stdout
@@ -54,6 +55,8 @@ def main():
     ap.add_argument("report")
     ap.add_argument("--kernel", default="k_encode")
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--lib", default=str(LIB), help="the .so the report was captured with")
+    ap.add_argument("--reasons", action="store_true", help="per-line stall reasons (no barrier)")
     args = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", args.report, "--page", "source", "--csv"], capture_output=True,
                          text=True).stdout
@@ -64,7 +67,9 @@ def main():
                                      "Instructions Executed")}
     body = [r for r in rows[hdr_i + 1:] if len(r) == len(hdr)]
     base = int(body[0][ci["Address"]], 16)
-    lm = line_map(args.kernel)
+    lm = line_map(args.kernel, Path(args.lib))
+    reason_cols = [n for n in hdr if n.startswith("stall_") and "Not Issued" not in n]
+    reasons = defaultdict(lambda: defaultdict(int))
     samples, insts = defaultdict(int), defaultdict(int)
     tot_s = tot_i = 0
     for r in body:
@@ -72,6 +77,12 @@ def main():
         key = lm.get(off, ("?", 0))
         s = int(r[ci["Warp Stall Sampling (All Samples)"]] or 0)
         n = int(r[ci["Instructions Executed"]] or 0)
+        if args.reasons:
+            s = sum(int(r[hdr.index(c)] or 0) for c in reason_cols if c != "stall_barrier")
+            for c in reason_cols:
+                v = int(r[hdr.index(c)] or 0)
+                if v and c != "stall_barrier":
+                    reasons[key][c[6:]] += v
         samples[key] += s
         insts[key] += n
         tot_s += s
@@ -89,8 +100,12 @@ def main():
     print(f"{'file:line':28s} {'stall%':>7s} {'inst%':>7s}  source")
     for key in sorted(samples, key=lambda k: -samples[k])[: args.top]:
         f, l = key
+        extra = ""
+        if args.reasons:
+            top = sorted(reasons[key].items(), key=lambda kv: -kv[1])[:3]
+            extra = "  [" + " ".join(f"{k}:{v}" for k, v in top) + "]"
         print(f"{f + ':' + str(l):28s} {100 * samples[key] / max(tot_s, 1):6.2f}% "
-              f"{100 * insts[key] / max(tot_i, 1):6.2f}%  {text(f, l)}")
+              f"{100 * insts[key] / max(tot_i, 1):6.2f}%  {text(f, l)}{extra}")
 
 
 if __name__ == "__main__":
