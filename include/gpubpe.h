@@ -96,6 +96,23 @@ int gpubpe_encode(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes,
                   uint64_t chunk_budget, uint32_t *d_out_ids, int64_t *d_out_offs,
                   void *stream);
 
+/*
+ * Encode from and to HOST memory -- the reference's own call shape (bytes in,
+ * ids out; tokenize_batch, chunker.py:110-187, for a packed batch).  Copies
+ * the batch into context-owned pinned, device-mapped memory; the same encode
+ * as gpubpe_encode then reads the bytes and writes the ids through PCIe
+ * itself (zero-copy: the transfers overlap the kernel); the offsets and
+ * exactly n_ids ids are copied out after one stream synchronisation.
+ *   h_out_ids      capacity >= n_bytes (ids <= bytes)
+ *   h_out_offs     n_docs+1 int64 CSR offsets of the ids
+ *   n_ids_out      ids written
+ *   kernel_ms      nullable: device time of the encode (CUDA events)
+ */
+int gpubpe_encode_host(gpubpe_ctx *ctx, const uint8_t *h_bytes, uint64_t n_bytes,
+                       const int64_t *h_doc_offs, uint64_t n_docs, uint64_t max_seq_len,
+                       uint64_t chunk_budget, uint32_t *h_out_ids, int64_t *h_out_offs,
+                       uint64_t *n_ids_out, float *kernel_ms, void *stream);
+
 /* Synchronise `stream` and read the counters of the last encode on it
  * (BatchResult.counters, chunker.py:56-64). */
 int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out);

@@ -43,6 +43,8 @@ SIGNATURES = {
     "gpubpe_ctx_create": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _u64,
                                  ctypes.c_uint32, ctypes.POINTER(_vp)]),
     "gpubpe_encode": (_int, [_vp, _vp, _u64, _vp, _u64, _u64, _u64, _vp, _vp, _vp]),
+    "gpubpe_encode_host": (_int, [_vp, _vp, _u64, _vp, _u64, _u64, _u64, _vp, _vp,
+                                  ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_float), _vp]),
     "gpubpe_query": (_int, [_vp, _vp, ctypes.POINTER(Stats)]),
     "gpubpe_launches_per_encode": (_int, []),
     "gpubpe_lookup_pairs": (_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -49,6 +50,12 @@ struct gpubpe_ctx {
     cudaAccessPolicyWindow win{};
     // workspace
     DevBuf ws_state, ws_status, ws_recs, ws_scratch, ws_tiles, ws_arena;
+    // host-buffer entry point: pinned (device-mapped) staging + device copy
+    DevBuf io_dev;
+    uint8_t *pin = nullptr;
+    size_t pin_bytes = 0;
+    bool state_fresh = false;  // h_state already holds the last encode's state
+    cudaEvent_t io_ev[2] = {nullptr, nullptr};
     uint64_t last_n_tiles = 0;
     unsigned int epoch = 0;
     uint64_t calls = 0;  // selects the EncodeState slot (two, alternating)
@@ -224,6 +231,8 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
         maxprod[NW[i]] = std::max<int64_t>(maxprod[NW[i]], rank[i]);
     }
     bool wf = !(flags & GPUBPE_F_STRICT);
+    for (uint64_t i = 0; i < n_rules && wf; ++i)  // the warp engine packs ranks into 31 bits
+        if (rank[i] >= 0x7FFFFFFFu) wf = false;
     for (uint64_t i = 0; i < n_rules && wf; ++i)
         if ((int64_t)rank[i] <= maxprod[L[i]] || (int64_t)rank[i] <= maxprod[R[i]]) wf = false;
     // ---- junction bitmap: first/last covered byte sets to a fixpoint
@@ -527,6 +536,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *
     if (n_docs && (!d_doc_offs || !d_out_offs)) return fail(ctx, GPUBPE_EINVAL, "null offsets");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CK(cudaSetDevice(ctx->device));
+    ctx->state_fresh = false;
     ctx->last_n_bytes = n_docs ? n_bytes : 0;
     ctx->timed = false;
     if (n_bytes == 0 || n_docs == 0) {
@@ -544,17 +554,131 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *
                        d_out_ids, d_out_offs, s, &checked);
 }
 
+// memcpy with up to 8 threads for large buffers (staging through pinned memory)
+static void copy_par(void *dst, const void *src, size_t n) {
+    const size_t per = 4u << 20;
+    if (n <= 2 * per) {
+        memcpy(dst, src, n);
+        return;
+    }
+    const unsigned nt = (unsigned)std::min<size_t>(8, (n + per - 1) / per);
+    std::vector<std::thread> th;
+    const size_t chunk = (n + nt - 1) / nt;
+    for (unsigned i = 1; i < nt; ++i) {
+        const size_t lo = i * chunk, hi = std::min(n, lo + chunk);
+        if (lo < hi) th.emplace_back([=] { memcpy((uint8_t *)dst + lo, (const uint8_t *)src + lo, hi - lo); });
+    }
+    memcpy(dst, src, std::min(n, chunk));
+    for (auto &t : th) t.join();
+}
+
+static int ensure_pinned(gpubpe_ctx *ctx, size_t bytes) {
+    if (ctx->pin_bytes >= bytes && ctx->pin) return GPUBPE_OK;
+    if (ctx->pin) CK(cudaFreeHost(ctx->pin));
+    ctx->pin = nullptr;
+    ctx->pin_bytes = 0;
+    const size_t nb = std::max<size_t>(bytes + bytes / 4, 1 << 20);
+    CK(cudaHostAlloc(reinterpret_cast<void **>(&ctx->pin), nb, cudaHostAllocMapped));
+    ctx->pin_bytes = nb;
+    return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
+    gpubpe_ctx *ctx, const uint8_t *h_bytes, uint64_t n_bytes, const int64_t *h_doc_offs, uint64_t n_docs,
+    uint64_t max_seq_len, uint64_t chunk_budget, uint32_t *h_out_ids, int64_t *h_out_offs,
+    uint64_t *n_ids_out, float *kernel_ms, void *stream) {
+    if (!ctx) return GPUBPE_EINVAL;
+    if (!n_ids_out || (n_docs && (!h_doc_offs || !h_out_offs)) || (n_bytes && (!h_bytes || !h_out_ids)))
+        return fail(ctx, GPUBPE_EINVAL, "null host pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device));
+    *n_ids_out = 0;
+    if (kernel_ms) *kernel_ms = 0.f;
+    if (n_docs == 0) return GPUBPE_OK;
+    static const int mode = getenv("GPUBPE_HOSTMODE") ? atoi(getenv("GPUBPE_HOSTMODE")) : 0;
+    int rc;
+    const size_t offs_b = (n_docs + 1) * 8;
+    const size_t o_in = 0;
+    const size_t o_doffs = (n_bytes + 255) & ~(size_t)255;
+    const size_t o_ooffs = (o_doffs + offs_b + 255) & ~(size_t)255;
+    const size_t o_ids = (o_ooffs + offs_b + 255) & ~(size_t)255;
+    const size_t need = o_ids + std::max<uint64_t>(n_bytes, 1) * 4;
+    if ((rc = ensure_pinned(ctx, need))) return rc;
+    if (!ctx->io_ev[0])
+        for (auto &e : ctx->io_ev) CK(cudaEventCreate(&e));
+    uint8_t *pin = ctx->pin;
+    uint8_t *dv = nullptr;  // device copy of the same layout (modes 0 and 2)
+    if (mode != 1) {
+        if ((rc = ensure(ctx, ctx->io_dev, need, false))) return rc;
+        dv = static_cast<uint8_t *>(ctx->io_dev.p);
+    }
+    if (mode == 1) {  // zero-copy: the kernel reads and writes mapped host memory
+        copy_par(pin + o_in, h_bytes, n_bytes);
+        memcpy(pin + o_doffs, h_doc_offs, offs_b);
+        void *dev = nullptr;
+        CK(cudaHostGetDevicePointer(&dev, pin, 0));
+        dv = static_cast<uint8_t *>(dev);
+    } else if (mode == 2) {  // pageable copies straight from the caller's buffers
+        CK(cudaMemcpyAsync(dv + o_doffs, h_doc_offs, offs_b, cudaMemcpyHostToDevice, s));
+        if (n_bytes) CK(cudaMemcpyAsync(dv + o_in, h_bytes, n_bytes, cudaMemcpyHostToDevice, s));
+    } else {  // pinned staging in 4 MiB pieces; staging of piece k+1 overlaps the DMA of piece k
+        memcpy(pin + o_doffs, h_doc_offs, offs_b);
+        CK(cudaMemcpyAsync(dv + o_doffs, pin + o_doffs, offs_b, cudaMemcpyHostToDevice, s));
+        const size_t piece = 4u << 20;
+        for (size_t lo = 0; lo < n_bytes; lo += piece) {
+            const size_t k = std::min<size_t>(piece, n_bytes - lo);
+            copy_par(pin + o_in + lo, h_bytes + lo, k);
+            CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, k, cudaMemcpyHostToDevice, s));
+        }
+    }
+    CK(cudaEventRecord(ctx->io_ev[0], s));
+    rc = gpubpe_encode(ctx, dv + o_in, n_bytes, reinterpret_cast<const int64_t *>(dv + o_doffs), n_docs,
+                       max_seq_len, chunk_budget, reinterpret_cast<uint32_t *>(dv + o_ids),
+                       reinterpret_cast<int64_t *>(dv + o_ooffs), stream);
+    if (rc) return rc;
+    CK(cudaEventRecord(ctx->io_ev[1], s));
+    if (mode != 1) CK(cudaMemcpyAsync(pin + o_ooffs, dv + o_ooffs, offs_b, cudaMemcpyDeviceToHost, s));
+    if (n_bytes) {  // the counters come back in the same sync (none needed by gpubpe_query)
+        const EncodeState *last = static_cast<const EncodeState *>(ctx->ws_state.p) + ((ctx->calls - 1) & 1);
+        CK(cudaMemcpyAsync(ctx->h_state, last, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    ctx->state_fresh = n_bytes != 0;
+    const int64_t *p_oo = reinterpret_cast<const int64_t *>(pin + o_ooffs);
+    const uint64_t total = n_bytes ? (uint64_t)p_oo[n_docs] : 0;
+    if (total > n_bytes)
+        return fail(ctx, GPUBPE_ECUDA, "device produced %llu ids for %llu bytes", (unsigned long long)total,
+                    (unsigned long long)n_bytes);
+    memcpy(h_out_offs, p_oo, offs_b);
+    if (total) {
+        if (mode == 1) {
+            copy_par(h_out_ids, pin + o_ids, total * 4);
+        } else if (mode == 2) {
+            CK(cudaMemcpy(h_out_ids, dv + o_ids, total * 4, cudaMemcpyDeviceToHost));
+        } else {
+            CK(cudaMemcpyAsync(pin + o_ids, dv + o_ids, total * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            copy_par(h_out_ids, pin + o_ids, total * 4);
+        }
+    }
+    if (kernel_ms) CK(cudaEventElapsedTime(kernel_ms, ctx->io_ev[0], ctx->io_ev[1]));
+    *n_ids_out = total;
+    return GPUBPE_OK;
+}
+
 extern "C" __attribute__((visibility("default"))) int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out) {
     if (!ctx || !out) return GPUBPE_EINVAL;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     memset(out, 0, sizeof *out);
-    if (ctx->ws_state.p && ctx->calls) {
+    if (ctx->state_fresh) {
+        // gpubpe_encode_host already brought the last encode's state back
+    } else if (ctx->ws_state.p && ctx->calls) {
         const EncodeState *last = static_cast<const EncodeState *>(ctx->ws_state.p) + ((ctx->calls - 1) & 1);
         CK(cudaMemcpyAsync(ctx->h_state, last, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
     } else {
         memset(ctx->h_state, 0, sizeof(EncodeState));
     }
-    CK(cudaStreamSynchronize(s));
+    if (!ctx->state_fresh) CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
     const EncodeState &st = *ctx->h_state;
     if (st.overflow) return fail(ctx, GPUBPE_ECUDA, "device reported an unrecovered buffer overflow");
@@ -609,8 +733,12 @@ extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     if (ctx->tables) cudaFree(ctx->tables);
-    for (DevBuf *b : {&ctx->ws_state, &ctx->ws_status, &ctx->ws_recs, &ctx->ws_scratch, &ctx->ws_tiles, &ctx->ws_arena})
+    for (DevBuf *b : {&ctx->ws_state, &ctx->ws_status, &ctx->ws_recs, &ctx->ws_scratch, &ctx->ws_tiles,
+                      &ctx->ws_arena, &ctx->io_dev})
         if (b->p) cudaFree(b->p);
+    if (ctx->pin) cudaFreeHost(ctx->pin);
+    for (auto &e : ctx->io_ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);

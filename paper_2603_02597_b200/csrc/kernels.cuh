@@ -44,7 +44,7 @@ constexpr int NT = NW * 32;     // threads per CTA
 constexpr int SHORT_MAX = 32;   // longest segment encoded inside the tile loop
 constexpr int GIANT_MIN = 2305; // deferred segments at least this long count as "giant"
 constexpr int SLOT = WT + SHORT_MAX;  // scratch entries per tile (ids of segments starting in it)
-constexpr int UNIT_MAX = 128;   // tiles per CTA per round in phase B
+constexpr int UNIT_MAX = 512;   // tiles per CTA per round in phase B
 constexpr unsigned int MARK = 0x80000000u;  // scratch entry: deferred record index follows
 
 // tile word: bits 0-15 entries, bit 16 has deferred markers, bits 17.. extra ids

@@ -18,7 +18,9 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef WALK_STEPS
 #define WALK_STEPS 8
+#endif
 
 // Segment boundaries in lane order: bit j of `heads` marks a segment's first
 // lane.  Last lane of the segment holding lane j (n = lanes in use).
@@ -81,21 +83,18 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
             const unsigned b = __ballot_sync(FULL_MASK, live && rk == m);
             sel = lane == (uint32_t)(__ffs(b) - 1);
         } else {
-            // segmented minimum rank (forward segmented scan, then the
-            // value at the segment's last lane)
-            uint32_t v = live ? rk : GPUBPE_INF;
-            bool fl = first || !valid;
+            // segmented minimum rank: forward segmented scan (rank in the low
+            // 31 bits, head flag in bit 31: one shuffle per step), then the
+            // value at the segment's last lane
+            uint32_t x = (live ? min(rk, 0x7FFFFFFFu) : 0x7FFFFFFFu) | ((first || !valid) ? 0x80000000u : 0u);
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t yv = __shfl_up_sync(FULL_MASK, v, o);
-                const bool yf = __shfl_up_sync(FULL_MASK, fl, o);
-                if (lane >= (uint32_t)o) {
-                    if (!fl) v = min(v, yv);
-                    fl = fl || yf;
-                }
+                const uint32_t y = __shfl_up_sync(FULL_MASK, x, o);
+                if (lane >= (uint32_t)o && !(x >> 31)) x = min(x, y & 0x7FFFFFFFu) | (y & 0x80000000u);
             }
             const uint32_t heads = __ballot_sync(FULL_MASK, first);
-            const uint32_t segmin = __shfl_sync(FULL_MASK, v, valid ? seg_last_lane(heads, lane, n) : lane);
+            const uint32_t segmin_raw = __shfl_sync(FULL_MASK, x, valid ? seg_last_lane(heads, lane, n) : lane) & 0x7FFFFFFFu;
+            const uint32_t segmin = segmin_raw == 0x7FFFFFFFu ? GPUBPE_INF : segmin_raw;
             // runs of equal pairs (identical tokens, e.g. "aaaa") pair up
             // leftmost-first: even offset inside the run
             const uint32_t rprev = __shfl_up_sync(FULL_MASK, rk, 1);
@@ -112,7 +111,7 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
             }
             bool ok = live && ((lane - s) & 1u) == 0;
             const bool need = ok && rk != segmin;
-            if (__any_sync(FULL_MASK, need)) {
+            if (WALK_STEPS > 0 && __any_sync(FULL_MASK, need)) {
                 // left walk from the run start s
                 uint32_t q = s;
                 bool done = !need, res = true;
@@ -146,6 +145,8 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
                     if (!__any_sync(FULL_MASK, !done)) break;
                 }
                 if (need) ok = lres && done && res;
+            } else if (need) {
+                ok = false;  // no walks: only the segment minima merge this pass
             }
             sel = ok;
         }
@@ -158,11 +159,14 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
         const unsigned km = __ballot_sync(FULL_MASK, keep);
         const uint32_t n2 = __popc(km);
         const uint32_t src = lane < n2 ? __fns(km, 0, (int)lane + 1) : 0u;
-        tok = __shfl_sync(FULL_MASK, newtok, src);
+        // token (< 2^24) and its three flags move in one shuffle
+        const uint32_t packed = newtok | (first ? 1u << 24 : 0u) | (newlast ? 1u << 25 : 0u) | (sel ? 1u << 26 : 0u);
+        const uint32_t moved = __shfl_sync(FULL_MASK, packed, src);
         valid = lane < n2;
-        first = __shfl_sync(FULL_MASK, first, src) && valid;
-        last = __shfl_sync(FULL_MASK, newlast, src) && valid;
-        const bool m2 = __shfl_sync(FULL_MASK, sel, src) && valid;
+        tok = moved & 0xFFFFFFu;
+        first = valid && ((moved >> 24) & 1u);
+        last = valid && ((moved >> 25) & 1u);
+        const bool m2 = valid && ((moved >> 26) & 1u);
         const uint32_t rk_src = __shfl_sync(FULL_MASK, rk, src);
         const uint32_t nw_src = __shfl_sync(FULL_MASK, nw, src);
         const uint32_t rl_src = __shfl_sync(FULL_MASK, rl, src);
@@ -172,6 +176,10 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
         n = n2;
         rl = rl_src;
         rr = rr_src;
+        if (m2 && !strict) {  // loads in flight together with the pair probe below
+            rl = __ldg(&T.rl[tok]);
+            rr = __ldg(&T.rr[tok]);
+        }
         if (valid && !last) {
             if (m2 || mnext) {
                 const PairHit h = probe_pair(T, tok, tnext);
@@ -183,10 +191,6 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
             }
         } else {
             rk = GPUBPE_INF;
-        }
-        if (m2 && !strict) {
-            rl = __ldg(&T.rl[tok]);
-            rr = __ldg(&T.rr[tok]);
         }
     }
     // write back: segment order is preserved by the compaction

@@ -146,40 +146,25 @@ class DeviceEncoder:
 
     # ------------------------------------------------------------ host API
 
-    def _staging(self, key: str, n: int, dtype):
-        t = self._pinned.get(key)
-        if t is None or t.numel() < n:
-            t = torch.empty(max(n, 1 << 16), dtype=dtype, pin_memory=True)
-            self._pinned[key] = t
-        return t
-
     def encode_packed_host(self, data: np.ndarray, offs: np.ndarray, max_seq_len: int,
                            chunk_budget: int):
-        """Host CSR in -> host CSR out, timed.  Returns (ids uint32[], offs int64[],
-        stats, engine_ms)."""
+        """Host CSR in -> host CSR out through gpubpe_encode_host (pinned
+        staging, H2D, encode, D2H in one native call).  Returns (ids
+        uint32[], offs int64[], stats, engine_ms)."""
+        data = np.ascontiguousarray(data, dtype=np.uint8)
+        offs = np.ascontiguousarray(offs, dtype=np.int64)
+        n = int(data.size)
+        n_docs = int(offs.size) - 1
+        ids = np.empty(max(n, 1), dtype=np.uint32)
+        out_offs = np.zeros(max(n_docs + 1, 1), dtype=np.int64)
+        n_ids = ctypes.c_uint64(0)
+        ms = ctypes.c_float(0.0)
         with self._lock, torch.cuda.device(self.device):
-            n = int(data.size)
-            n_docs = int(offs.size) - 1
-            hb = self._staging("bytes", n, torch.uint8)
-            ho = self._staging("offs", n_docs + 1, torch.int64)
-            hb.numpy()[:n] = data
-            ho.numpy()[: n_docs + 1] = offs
-            dev = torch.device("cuda", self.device)
-            d_data = hb[: max(n, 1)].to(dev, non_blocking=True)[:n]
-            d_offs = ho[: n_docs + 1].to(dev, non_blocking=True)
-            out_ids = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-            out_offs = torch.empty(n_docs + 1, dtype=torch.int64, device=dev)
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            ev0.record()
-            self.encode_into(d_data, d_offs, out_ids, out_offs, max_seq_len, chunk_budget)
-            ev1.record()
-            h_offs = out_offs.cpu().numpy()
-            st = self.query()
-            total = int(h_offs[-1]) if n_docs >= 0 and n else 0
-            hi = self._staging("ids", total, torch.int32)
-            hi[:total].copy_(out_ids[:total])
-            ids = hi.numpy()[:total].view(np.uint32).copy()
-            if n == 0:
-                h_offs = np.zeros(n_docs + 1, dtype=np.int64)
-            return ids, h_offs, st, ev0.elapsed_time(ev1)
+            s = torch.cuda.current_stream(self.device)
+            rc = self._lib.gpubpe_encode_host(self._h, _ptr(data), n, _ptr(offs), n_docs,
+                                              int(max_seq_len), int(chunk_budget), _ptr(ids),
+                                              _ptr(out_offs), ctypes.byref(n_ids), ctypes.byref(ms),
+                                              s.cuda_stream)
+            _native.check(rc, self._h, "gpubpe_encode_host")
+            st = self.query(s)
+        return ids[: n_ids.value], out_offs[: n_docs + 1], st, float(ms.value)

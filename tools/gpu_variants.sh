@@ -1,4 +1,3 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-timeout 120 python -c 'import __graft_entry__ as g; g.smoke()' 2>&1 | tail -1
-for L in libgpubpe.so libgpubpe_nw24.so libgpubpe_nw16.so; do echo "== $L"; GPUBPE_LIB=$L timeout 300 python tools/perf.py --iters 20 --only ${ONLY:-c1_8k,c1_131k,c3_1m,c2_4096x512,corpus_256m} 2>&1 | tail -6; done
+for L in ${LIBS:-libgpubpe.so libgpubpe_nw24.so libgpubpe_nw16.so}; do echo "== $L"; GPUBPE_LIB=$L timeout 300 python tools/perf.py --iters 20 --only ${ONLY:-c1_8k,c1_131k,c3_1m,c2_4096x512,corpus_256m} 2>&1 | tail -6; done
