@@ -279,10 +279,12 @@ def main():
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = b_alg / t_tile / 1e9
+    # DRAM bytes of one k_encode launch on this workload, from the committed
+    # `ncu --set full` capture (profiles/ncu_summary.json, tools/ncu_summary.py)
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get(args.workload, {}).get("k_tile_dram_bytes")
+        traffic = json.loads(prof.read_text()).get(args.workload, {}).get("traffic_bytes")
 
     # e2e through the public API: host bytes in, host ids out
     e2e = None

@@ -482,8 +482,6 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.arena_words = ctx->ws_arena.bytes / 4;
         P.n_tiles = n_tiles;
         P.round_tiles = R;
-        P.prefetch = ctx->tables;
-        P.prefetch_bytes = ctx->tables_used;
         P.epoch = ctx->epoch;
         P.strict = (ctx->flags & GPUBPE_F_STRICT) ? 1 : 0;
         P.aligned = (reinterpret_cast<uintptr_t>(d_bytes) & 15) == 0;
@@ -491,7 +489,6 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         ctx->last_n_tiles = n_tiles;
         // debug knobs (tuning only) never apply to the memo verification encode
         const int dbg = (ctx->T.memo && getenv("GPUBPE_DEBUG")) ? atoi(getenv("GPUBPE_DEBUG")) : 0;
-        if (dbg & 1) P.prefetch_bytes = 0;
         P.dbg_phase_a_only = (dbg & 16) ? 1 : (dbg & 32) ? 2 : 0;
         static unsigned long long *dbuf = nullptr;
         if (dbg & 8) {

@@ -815,10 +815,6 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     EncodeState *st = P.st;
     if (blockIdx.x == 0 && tid == 0) *P.st_next = EncodeState{};
-    // warm the probe tables into L2 (they were flushed or evicted since the last call)
-    for (unsigned long long off = ((unsigned long long)blockIdx.x * NT + tid) * 128ull; off < P.prefetch_bytes;
-         off += (unsigned long long)gridDim.x * NT * 128ull)
-        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(P.prefetch + off));
     for (int k = tid; k < 2048; k += NT) C.jb[k] = __ldg(&P.T.jbits[k]);
     for (int k = tid; k < 256; k += NT) C.base[k] = __ldg(&P.T.base[k]);
     if (tid < (int)(sizeof(PassCounters) / 8)) (&C.pc.n_segments)[tid] = 0;

@@ -105,8 +105,6 @@ struct EncodeParams {
     unsigned long long arena_words;
     unsigned long long n_tiles;
     unsigned long long round_tiles;  // R
-    const uint8_t *prefetch;     // table region warmed into L2 at kernel start
-    unsigned long long prefetch_bytes;
     unsigned int epoch;          // look-back tag
     int strict;
     int aligned;                 // bytes pointer is 16-B aligned
