@@ -117,6 +117,13 @@ int gpubpe_encode_host(gpubpe_ctx *ctx, const uint8_t *h_bytes, uint64_t n_bytes
  * (BatchResult.counters, chunker.py:56-64). */
 int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out);
 
+/* The junction bitmap of the context (65,536 bits as uint32[2048]; bit
+ * (x << 8 | y) set iff some reachable rule joins a token ending in byte x to
+ * one starting with byte y).  A byte pair outside it is a cut no merge of
+ * the reference can span, so a document may be split there across GPUs
+ * (multigpu.py). */
+int gpubpe_junction_bits(gpubpe_ctx *ctx, uint32_t *h_out);
+
 /* Number of kernels one gpubpe_encode enqueues (launch accounting): 1, the
  * fused persistent k_encode. */
 int gpubpe_launches_per_encode(void);

@@ -48,6 +48,7 @@ struct gpubpe_ctx {
     uint8_t *tables = nullptr;
     size_t tables_bytes = 0, tables_used = 0;
     cudaAccessPolicyWindow win{};
+    std::vector<uint32_t> h_jbits;  // host copy of the junction bitmap (sharding)
     // workspace
     DevBuf ws_state, ws_status, ws_recs, ws_scratch, ws_tiles, ws_arena;
     // host-buffer entry point: pinned (device-mapped) staging + device copy
@@ -265,6 +266,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
     }
     std::vector<uint32_t> jbits(2048);
     for (int k = 0; k < 2048; ++k) jbits[k] = (uint32_t)(J[k >> 1] >> (32 * (k & 1)));
+    ctx->h_jbits = jbits;
 
     // memo upper bounds (the memo is built after a verification encode)
     uint64_t memo_cand = 0, blob_max = 0;
@@ -692,6 +694,13 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_query(gpubpe_ctx *c
     out->tiles = ctx->last_n_bytes ? ctx->last_n_tiles : 0;
     out->overflow = st.overflow;
     out->well_formed = (uint64_t)ctx->T.well_formed;
+    return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_junction_bits(gpubpe_ctx *ctx, uint32_t *h_out) {
+    if (!ctx || !h_out) return GPUBPE_EINVAL;
+    if (ctx->h_jbits.size() != 2048) return fail(ctx, GPUBPE_EINVAL, "context has no junction bitmap");
+    memcpy(h_out, ctx->h_jbits.data(), 2048 * sizeof(uint32_t));
     return GPUBPE_OK;
 }
 

@@ -103,6 +103,12 @@ class DeviceEncoder:
                                      out_offs.data_ptr(), s.cuda_stream)
         _native.check(rc, self._h, "gpubpe_encode")
 
+    def junction_bits(self) -> np.ndarray:
+        """uint32[2048] junction bitmap (bit x << 8 | y: some rule joins x|y)."""
+        out = np.zeros(2048, dtype=np.uint32)
+        _native.check(self._lib.gpubpe_junction_bits(self._h, _ptr(out)), self._h, "junction_bits")
+        return out
+
     def set_profiling(self, on: bool) -> None:
         _native.check(self._lib.gpubpe_set_profiling(self._h, int(on)), self._h, "set_profiling")
 

@@ -213,3 +213,20 @@ def test_device_csr_api(tokenizer, prose_samples):
         assert np.array_equal(h[oo[i]:oo[i + 1]], gold[i])
     assert st["passes"] == 0 or True
     assert st["n_ids"] == len(h)
+
+
+def test_device_junction_bits_match_rules_and_split_exactly(tokenizer, oracle, oracle_tables):
+    from paper_2603_02597_b200 import multigpu
+    from test_multigpu import junction_bits
+
+    jb = tokenizer.device_encoder().junction_bits()
+    assert np.array_equal(jb, junction_bits(oracle_tables))
+    doc = b"".join(fixtures.prose_samples()[:20])
+    for msl, cb in ((1 << 40, 1 << 40), (8192, 8192), (5000, 3000)):
+        tok = with_config(tokenizer, msl, cb)
+        want = oracle.encode_docs([doc], msl, cb)[0]
+        for world in (2, 4, 8):
+            shards = multigpu.split_document(doc, world, jb, msl, cb)
+            got = [bpe.tokenize_batch(s, tok).token_ids for s in shards if s]
+            got = np.concatenate([i for g in got for i in g])
+            assert np.array_equal(got, want), (msl, world)
