@@ -113,6 +113,12 @@ int gpubpe_encode_host(gpubpe_ctx *ctx, const uint8_t *h_bytes, uint64_t n_bytes
                        uint64_t chunk_budget, uint32_t *h_out_ids, int64_t *h_out_offs,
                        uint64_t *n_ids_out, float *kernel_ms, void *stream);
 
+/* Pinned, device-mapped host memory for results: when gpubpe_encode_host's
+ * h_out_ids points into such a buffer the kernel writes the ids there
+ * directly (no copy-out).  Free with gpubpe_host_free. */
+int gpubpe_host_alloc(int device, uint64_t bytes, void **out);
+void gpubpe_host_free(void *p);
+
 /* Synchronise `stream` and read the counters of the last encode on it
  * (BatchResult.counters, chunker.py:56-64). */
 int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out);

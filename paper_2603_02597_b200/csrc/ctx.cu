@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <thread>
 #include <cstdarg>
 #include <cstdio>
@@ -54,6 +55,7 @@ struct gpubpe_ctx {
     // host-buffer entry point: pinned (device-mapped) staging + device copy
     DevBuf io_dev;
     uint8_t *pin = nullptr;
+    uint8_t *pin_dev = nullptr;  // device alias of pin (mapped)
     size_t pin_bytes = 0;
     bool state_fresh = false;  // h_state already holds the last encode's state
     cudaEvent_t io_ev[2] = {nullptr, nullptr};
@@ -578,6 +580,9 @@ static int ensure_pinned(gpubpe_ctx *ctx, size_t bytes) {
     ctx->pin_bytes = 0;
     const size_t nb = std::max<size_t>(bytes + bytes / 4, 1 << 20);
     CK(cudaHostAlloc(reinterpret_cast<void **>(&ctx->pin), nb, cudaHostAllocMapped));
+    void *dev = nullptr;
+    CK(cudaHostGetDevicePointer(&dev, ctx->pin, 0));
+    ctx->pin_dev = static_cast<uint8_t *>(dev);
     ctx->pin_bytes = nb;
     return GPUBPE_OK;
 }
@@ -594,7 +599,10 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     *n_ids_out = 0;
     if (kernel_ms) *kernel_ms = 0.f;
     if (n_docs == 0) return GPUBPE_OK;
-    static const int mode = getenv("GPUBPE_HOSTMODE") ? atoi(getenv("GPUBPE_HOSTMODE")) : 0;
+    static const bool htime = getenv("GPUBPE_HOSTTIME") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t_a = now();
+    static const int mode = getenv("GPUBPE_HOSTMODE") ? atoi(getenv("GPUBPE_HOSTMODE")) : 3;
     int rc;
     const size_t offs_b = (n_docs + 1) * 8;
     const size_t o_in = 0;
@@ -614,34 +622,50 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     if (mode == 1) {  // zero-copy: the kernel reads and writes mapped host memory
         copy_par(pin + o_in, h_bytes, n_bytes);
         memcpy(pin + o_doffs, h_doc_offs, offs_b);
-        void *dev = nullptr;
-        CK(cudaHostGetDevicePointer(&dev, pin, 0));
-        dv = static_cast<uint8_t *>(dev);
+        dv = ctx->pin_dev;
     } else if (mode == 2) {  // pageable copies straight from the caller's buffers
         CK(cudaMemcpyAsync(dv + o_doffs, h_doc_offs, offs_b, cudaMemcpyHostToDevice, s));
         if (n_bytes) CK(cudaMemcpyAsync(dv + o_in, h_bytes, n_bytes, cudaMemcpyHostToDevice, s));
-    } else {  // pinned staging in 4 MiB pieces; staging of piece k+1 overlaps the DMA of piece k
+    } else {  // pinned staging in 4 MiB pieces; staging of piece k+1 overlaps the DMA of piece k;
+              // the doc offsets ride with the last piece (they follow the bytes in the layout)
         memcpy(pin + o_doffs, h_doc_offs, offs_b);
-        CK(cudaMemcpyAsync(dv + o_doffs, pin + o_doffs, offs_b, cudaMemcpyHostToDevice, s));
         const size_t piece = 4u << 20;
-        for (size_t lo = 0; lo < n_bytes; lo += piece) {
-            const size_t k = std::min<size_t>(piece, n_bytes - lo);
-            copy_par(pin + o_in + lo, h_bytes + lo, k);
-            CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, k, cudaMemcpyHostToDevice, s));
+        size_t lo = 0;
+        for (; lo + piece < n_bytes; lo += piece) {
+            copy_par(pin + o_in + lo, h_bytes + lo, piece);
+            CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, piece, cudaMemcpyHostToDevice, s));
         }
+        copy_par(pin + o_in + lo, h_bytes + lo, n_bytes - lo);
+        CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, o_doffs + offs_b - lo, cudaMemcpyHostToDevice, s));
     }
+    auto t_b = now();
     CK(cudaEventRecord(ctx->io_ev[0], s));
+    uint8_t *dout = dv;  // where the kernel writes ids and offsets
+    if (mode == 3) dout = ctx->pin_dev;  // outputs straight into mapped pinned memory (stores overlap the kernel)
+    // A caller buffer that is itself pinned and device-mapped (gpubpe_host_alloc)
+    // receives the ids directly: no copy-out at all.
+    uint32_t *d_ids_direct = nullptr;
+    if (mode == 3 && n_bytes) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, h_out_ids) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer)
+            d_ids_direct = static_cast<uint32_t *>(pa.devicePointer);
+        cudaGetLastError();
+    }
     rc = gpubpe_encode(ctx, dv + o_in, n_bytes, reinterpret_cast<const int64_t *>(dv + o_doffs), n_docs,
-                       max_seq_len, chunk_budget, reinterpret_cast<uint32_t *>(dv + o_ids),
-                       reinterpret_cast<int64_t *>(dv + o_ooffs), stream);
+                       max_seq_len, chunk_budget,
+                       d_ids_direct ? d_ids_direct : reinterpret_cast<uint32_t *>(dout + o_ids),
+                       reinterpret_cast<int64_t *>(dout + o_ooffs), stream);
     if (rc) return rc;
     CK(cudaEventRecord(ctx->io_ev[1], s));
-    if (mode != 1) CK(cudaMemcpyAsync(pin + o_ooffs, dv + o_ooffs, offs_b, cudaMemcpyDeviceToHost, s));
+    if (mode != 1 && mode != 3) CK(cudaMemcpyAsync(pin + o_ooffs, dv + o_ooffs, offs_b, cudaMemcpyDeviceToHost, s));
     if (n_bytes) {  // the counters come back in the same sync (none needed by gpubpe_query)
         const EncodeState *last = static_cast<const EncodeState *>(ctx->ws_state.p) + ((ctx->calls - 1) & 1);
         CK(cudaMemcpyAsync(ctx->h_state, last, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
     }
+    auto t_c = now();
     CK(cudaStreamSynchronize(s));
+    auto t_d = now();
     ctx->state_fresh = n_bytes != 0;
     const int64_t *p_oo = reinterpret_cast<const int64_t *>(pin + o_ooffs);
     const uint64_t total = n_bytes ? (uint64_t)p_oo[n_docs] : 0;
@@ -650,7 +674,9 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
                     (unsigned long long)n_bytes);
     memcpy(h_out_offs, p_oo, offs_b);
     if (total) {
-        if (mode == 1) {
+        if (d_ids_direct) {
+            // already in place
+        } else if (mode == 1 || mode == 3) {
             copy_par(h_out_ids, pin + o_ids, total * 4);
         } else if (mode == 2) {
             CK(cudaMemcpy(h_out_ids, dv + o_ids, total * 4, cudaMemcpyDeviceToHost));
@@ -662,7 +688,28 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     }
     if (kernel_ms) CK(cudaEventElapsedTime(kernel_ms, ctx->io_ev[0], ctx->io_ev[1]));
     *n_ids_out = total;
+    if (htime) {
+        auto t_e = now();
+        auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
+        fprintf(stderr, "encode_host: stage+h2d enqueue %.1f | encode enqueue %.1f | sync wait %.1f | copy-out %.1f us\n",
+                us(t_a, t_b), us(t_b, t_c), us(t_c, t_d), us(t_d, t_e));
+    }
     return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_host_alloc(int device, uint64_t bytes, void **out) {
+    if (!out) return GPUBPE_EINVAL;
+    *out = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess) return GPUBPE_ECUDA;
+    void *p = nullptr;
+    const cudaError_t e = cudaHostAlloc(&p, std::max<uint64_t>(bytes, 1), cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? GPUBPE_ENOMEM : GPUBPE_ECUDA;
+    *out = p;
+    return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) void gpubpe_host_free(void *p) {
+    if (p) cudaFreeHost(p);
 }
 
 extern "C" __attribute__((visibility("default"))) int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out) {

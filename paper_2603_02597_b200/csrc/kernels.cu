@@ -628,6 +628,24 @@ __device__ __noinline__ void place_range(const EncodeParams &P, CtaSmem &C, unsi
     const uint32_t *slots = P.scratch + (par * P.round_tiles + (lo - t0)) * SLOT;
     const int nt = (int)(hi - lo);
     const unsigned long long u = r * gridDim.x + blockIdx.x;
+    // A call that fits one round needs no look-back: warps 1.. sum the words
+    // of all tiles before this range directly (L2 reads, no CTA waits on
+    // another) while warp 0 scans the range.
+    const bool direct = r == 0 && P.n_tiles <= P.round_tiles;
+    if (direct) {
+        if (tid == 0) C.bcast[1] = 0;
+        __syncthreads();
+        if (wid > 0) {
+            unsigned long long acc = 0;
+            for (unsigned long long t = (unsigned long long)(tid - 32); t < lo; t += NT - 32) {
+                const unsigned long long w = __ldcg(&P.tiles[t]);  // round 0: parity 0, t0 == 0
+                acc += TW_ENTRIES(w) + TW_EXTRA(w);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
+            if (lane == 0 && acc) atomicAdd(&C.bcast[1], acc);
+        }
+    }
     if (wid == 0) {
         constexpr int PER = UNIT_MAX / 32;
         unsigned long long v[PER], sum = 0;
@@ -653,18 +671,21 @@ __device__ __noinline__ void place_range(const EncodeParams &P, CtaSmem &C, unsi
             o += v[j];
         }
         unsigned long long base = 0;
-        if (nt > 0) {
+        if (direct) {
+            // base comes from warps 1.. (C.bcast[1]) after the barrier below
+        } else if (nt > 0) {
             base = warp_lookback(P.status, u, total, P.epoch);
         } else if (lane == 0) {  // empty unit: an aggregate of 0 keeps the chain moving
             st_relaxed(&P.status[u], ((unsigned long long)P.epoch << 44) | (LB_AGG << 42));
         }
         if (lane == 0) {
             C.bcast[0] = base;
-            if (nt > 0 && hi == P.n_tiles) P.st->n_ids = base + total;
+            C.bcast[2] = total;
         }
     }
     __syncthreads();
-    const unsigned long long base = C.bcast[0];
+    const unsigned long long base = direct ? C.bcast[1] : C.bcast[0];
+    if (tid == 0 && nt > 0 && hi == P.n_tiles) P.st->n_ids = base + C.bcast[2];
     for (int k = wid; k < nt; k += NW) place_tile(P, slots + (size_t)k * SLOT, C.tw[k], base + C.tb[k]);
     // CSR offsets of the documents starting in [lo, hi): tile-local -> global
     if (wid == 0 && nt > 0 && (P.n_docs > 1 || lo == 0 || hi == P.n_tiles)) {

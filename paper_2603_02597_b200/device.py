@@ -31,6 +31,75 @@ def _ptr(a: np.ndarray):
     return ctypes.c_void_p(a.ctypes.data) if a.size else None
 
 
+class _Lease:
+    """A pooled host buffer lent to result arrays (PEP 688): numpy views of it
+    keep it alive, and when the last one is released the buffer goes back to
+    the pool instead of to the allocator."""
+
+    __slots__ = ("buf", "pool")
+
+    def __init__(self, buf: np.ndarray, pool: "_HostPool"):
+        self.buf, self.pool = buf, pool
+
+    def __buffer__(self, flags):
+        return memoryview(self.buf)
+
+    def __release_buffer__(self, view):
+        self.pool.put(self.buf)
+
+
+class _PinnedBlock:
+    """Owner of one gpubpe_host_alloc block (freed with the last reference)."""
+
+    __slots__ = ("ptr", "lib")
+
+    def __init__(self, ptr: int, lib):
+        self.ptr, self.lib = ptr, lib
+
+    def __del__(self):
+        try:
+            self.lib.gpubpe_host_free(ctypes.c_void_p(self.ptr))
+        except Exception:
+            pass
+
+
+class _HostPool:
+    """Recycled result buffers: pinned and device-mapped (gpubpe_host_alloc),
+    so the kernel writes the ids straight into them and nothing is copied out
+    on the host; reused across calls, so neither pinning nor page faults are
+    paid per call.  A buffer returns here when its last result array dies."""
+
+    def __init__(self, keep: int = 4):
+        self._free: dict[int, list[np.ndarray]] = {}
+        self._keep = keep
+        self._lock = threading.Lock()
+
+    def take(self, nbytes: int, lib, device: int) -> np.ndarray:
+        cls = 1 << max(20, int(nbytes - 1).bit_length())
+        with self._lock:
+            lst = self._free.get(cls)
+            if lst:
+                return lst.pop()
+        p = ctypes.c_void_p()
+        if lib.gpubpe_host_alloc(device, cls, ctypes.byref(p)) == _native.OK and p.value:
+            raw = (ctypes.c_uint8 * cls).from_address(p.value)
+            raw._owner = _PinnedBlock(p.value, lib)  # freed when the last view of raw dies
+            return np.frombuffer(raw, dtype=np.uint8)
+        return np.zeros(cls, dtype=np.uint8)  # pinned memory exhausted: the encode copies out
+
+    def put(self, buf: np.ndarray) -> None:
+        with self._lock:
+            lst = self._free.setdefault(buf.size, [])
+            if len(lst) < self._keep:
+                lst.append(buf)
+
+    def array(self, buf: np.ndarray, dtype, count: int) -> np.ndarray:
+        return np.frombuffer(_Lease(buf, self), dtype=dtype, count=count)
+
+
+_RESULTS = _HostPool()
+
+
 class DeviceEncoder:
     """Device-resident tables for one merge table on one GPU."""
 
@@ -161,7 +230,8 @@ class DeviceEncoder:
         offs = np.ascontiguousarray(offs, dtype=np.int64)
         n = int(data.size)
         n_docs = int(offs.size) - 1
-        ids = np.empty(max(n, 1), dtype=np.uint32)
+        buf = _RESULTS.take(4 * max(n, 1), self._lib, self.device)
+        ids = buf.view(np.uint32)
         out_offs = np.zeros(max(n_docs + 1, 1), dtype=np.int64)
         n_ids = ctypes.c_uint64(0)
         ms = ctypes.c_float(0.0)
@@ -173,4 +243,4 @@ class DeviceEncoder:
                                               s.cuda_stream)
             _native.check(rc, self._h, "gpubpe_encode_host")
             st = self.query(s)
-        return ids[: n_ids.value], out_offs[: n_docs + 1], st, float(ms.value)
+        return _RESULTS.array(buf, np.uint32, n_ids.value), out_offs[: n_docs + 1], st, float(ms.value)

@@ -47,3 +47,18 @@ buf = np.empty(n, np.uint8)
 print("memcpy 588KB        %8.1f us" % t(lambda: np.copyto(buf, data)))
 def sync(): torch.cuda.synchronize()
 print("empty sync          %8.1f us" % t(sync))
+def enq(): enc.encode_into(d, o, out, oo2, W, W)
+for _ in range(5): enq()
+torch.cuda.synchronize()
+ts = []
+for _ in range(100):
+    t0 = time.perf_counter(); enq(); ts.append(time.perf_counter() - t0)
+torch.cuda.synchronize()
+print("enqueue encode_into %8.1f us (host time per call, no sync)" % (1e6 * statistics.median(ts)))
+raw_enq = []
+for _ in range(100):
+    t0 = time.perf_counter()
+    enc._lib.gpubpe_encode(enc._h, d.data_ptr(), n, o.data_ptr(), 1, W, W, out.data_ptr(), oo2.data_ptr(), s.cuda_stream)
+    raw_enq.append(time.perf_counter() - t0)
+torch.cuda.synchronize()
+print("enqueue C gpubpe_encode %6.1f us" % (1e6 * statistics.median(raw_enq)))
