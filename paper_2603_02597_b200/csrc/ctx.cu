@@ -496,8 +496,8 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.dbg_phase_a_only = (dbg & 16) ? 1 : (dbg & 32) ? 2 : 0;
         static unsigned long long *dbuf = nullptr;
         if (dbg & 8) {
-            if (!dbuf) cudaMalloc(&dbuf, 32768 * 8);
-            cudaMemsetAsync(dbuf, 0, 32768 * 8, s);
+            if (!dbuf) cudaMalloc(&dbuf, 40960 * 8);
+            cudaMemsetAsync(dbuf, 0, 40960 * 8, s);
             P.dbg = dbuf;
         }
         cudaError_t e = launch_encode(P, grid, s, ctx->profiling ? ctx->ev : nullptr, (dbg & 4) ? nullptr : &ctx->win, !(dbg & 2));
@@ -508,7 +508,7 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         // otherwise check after the call and re-run with larger buffers.
         const uint64_t arena_need = 26 * n_bytes + 96 * def_max;
         if ((dbg & 8) && getenv("GPUBPE_DEBUG_OUT")) {
-            std::vector<unsigned long long> h(32768);
+            std::vector<unsigned long long> h(40960);
             cudaMemcpyAsync(h.data(), dbuf, h.size() * 8, cudaMemcpyDeviceToHost, s);
             cudaStreamSynchronize(s);
             FILE *f = fopen(getenv("GPUBPE_DEBUG_OUT"), "wb");

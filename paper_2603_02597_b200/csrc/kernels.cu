@@ -471,7 +471,18 @@ __device__ __noinline__ void encode_tile(const EncodeParams &P, CtaSmem &C, Warp
             uint32_t k = 1, tot = S.u.a.miss[i] >> 16;
             if (!strict)
                 while (i + k < nm && tot + (S.u.a.miss[i + k] >> 16) <= 32) tot += S.u.a.miss[i + k++] >> 16;
+#ifdef GPUBPE_DEBUG_STAMPS
+            long long eng_acc[6] = {0, 0, 0, 0, 0, 0};
+            const uint32_t np_ = warp_pack_bpe(T, C.base, sb, S.sid, S.u.a.miss + i, k, strict, eng_acc);
+            if (P.dbg && lane == 0) {
+                for (int q = 0; q < 6; ++q) atomicAdd(&P.dbg[32768 + q], (unsigned long long)eng_acc[q]);
+                atomicAdd(&P.dbg[32768 + 6], (unsigned long long)np_);
+                atomicAdd(&P.dbg[32768 + 7], 1ull);
+            }
+            c_pass += np_;
+#else
             c_pass += warp_pack_bpe(T, C.base, sb, S.sid, S.u.a.miss + i, k, strict);
+#endif
             i += k;
         }
     }

@@ -18,6 +18,18 @@
 #pragma once
 #include "common.cuh"
 
+#ifdef GPUBPE_DEBUG_STAMPS
+#define ENG_MARK(k)                                                         \
+    do {                                                                    \
+        long long c_;                                                       \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_));                  \
+        eng_acc[k] += c_ - eng_prev;                                        \
+        eng_prev = c_;                                                      \
+    } while (0)
+#else
+#define ENG_MARK(k) do { } while (0)
+#endif
+
 #ifndef WALK_STEPS
 #define WALK_STEPS 8
 #endif
@@ -34,8 +46,12 @@ __device__ __forceinline__ uint32_t seg_last_lane(uint32_t heads, uint32_t j, ui
 // count << 24.  Returns the passes run.
 static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *base, const uint32_t *sbw,
                                   uint32_t *sid, const uint32_t *list, uint32_t k,
-                                  bool strict) {
+                                  bool strict, long long *eng_acc = nullptr) {
     const uint32_t lane = threadIdx.x & 31;
+#ifdef GPUBPE_DEBUG_STAMPS
+    long long eng_prev;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(eng_prev));
+#endif
     const uint32_t ent_l = lane < k ? list[lane] : 0u;
     const uint32_t len_l = ent_l >> 16;
     uint32_t off = len_l;
@@ -72,6 +88,7 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
             rr = __ldg(&T.rr[tok]);
         }
     }
+    ENG_MARK(0);  // setup + initial probes
     uint32_t np = 0;
     for (;;) {
         const bool live = valid && !last && rk != GPUBPE_INF;
@@ -83,18 +100,25 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
             const unsigned b = __ballot_sync(FULL_MASK, live && rk == m);
             sel = lane == (uint32_t)(__ffs(b) - 1);
         } else {
-            // segmented minimum rank: forward segmented scan (rank in the low
-            // 31 bits, head flag in bit 31: one shuffle per step), then the
-            // value at the segment's last lane
-            uint32_t x = (live ? min(rk, 0x7FFFFFFFu) : 0x7FFFFFFFu) | ((first || !valid) ? 0x80000000u : 0u);
+            // minimum rank of each packed segment: one REDUX when the pack holds
+            // a single segment, else a forward segmented scan (rank in the low
+            // 31 bits, head flag in bit 31: one shuffle per step) read at the
+            // segment's last lane
+            uint32_t segmin;
+            if (k == 1) {
+                segmin = __reduce_min_sync(FULL_MASK, live ? rk : GPUBPE_INF);
+            } else {
+                uint32_t x = (live ? min(rk, 0x7FFFFFFFu) : 0x7FFFFFFFu) | ((first || !valid) ? 0x80000000u : 0u);
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(FULL_MASK, x, o);
-                if (lane >= (uint32_t)o && !(x >> 31)) x = min(x, y & 0x7FFFFFFFu) | (y & 0x80000000u);
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL_MASK, x, o);
+                    if (lane >= (uint32_t)o && !(x >> 31)) x = min(x, y & 0x7FFFFFFFu) | (y & 0x80000000u);
+                }
+                const uint32_t heads = __ballot_sync(FULL_MASK, first);
+                const uint32_t sm = __shfl_sync(FULL_MASK, x, valid ? seg_last_lane(heads, lane, n) : lane) & 0x7FFFFFFFu;
+                segmin = sm == 0x7FFFFFFFu ? GPUBPE_INF : sm;
             }
-            const uint32_t heads = __ballot_sync(FULL_MASK, first);
-            const uint32_t segmin_raw = __shfl_sync(FULL_MASK, x, valid ? seg_last_lane(heads, lane, n) : lane) & 0x7FFFFFFFu;
-            const uint32_t segmin = segmin_raw == 0x7FFFFFFFu ? GPUBPE_INF : segmin_raw;
+            ENG_MARK(1);  // segment minima
             // runs of equal pairs (identical tokens, e.g. "aaaa") pair up
             // leftmost-first: even offset inside the run
             const uint32_t rprev = __shfl_up_sync(FULL_MASK, rk, 1);
@@ -111,44 +135,38 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
             }
             bool ok = live && ((lane - s) & 1u) == 0;
             const bool need = ok && rk != segmin;
+            ENG_MARK(2);  // segmin + runs
             if (WALK_STEPS > 0 && __any_sync(FULL_MASK, need)) {
-                // left walk from the run start s
-                uint32_t q = s;
-                bool done = !need, res = true;
+                // both blocking walks, one step of each per iteration: left
+                // from the run start s, right from lane + 1
+                uint32_t ql = s, qr = lane + 1;
+                bool ldone = !need, lres = true, rdone = !need, rres = true;
 #pragma unroll 1
                 for (int it = 0; it < WALK_STEPS; ++it) {
-                    const bool qfirst = __shfl_sync(FULL_MASK, first, q & 31);
-                    const uint32_t rrq = __shfl_sync(FULL_MASK, rr, q & 31);
-                    const uint32_t rkm = __shfl_sync(FULL_MASK, rk, (q - 1) & 31);
-                    if (!done) {
-                        if (qfirst || rrq > rk) done = true;
-                        else if (rkm < rk) { done = true; res = false; }
-                        else --q;
+                    const bool qfirst = __shfl_sync(FULL_MASK, first, ql & 31);
+                    const uint32_t rrq = __shfl_sync(FULL_MASK, rr, ql & 31);
+                    const uint32_t rkm = __shfl_sync(FULL_MASK, rk, (ql - 1) & 31);
+                    const bool qlast = __shfl_sync(FULL_MASK, last, qr & 31);
+                    const uint32_t rlq = __shfl_sync(FULL_MASK, rl, qr & 31);
+                    const uint32_t rkq = __shfl_sync(FULL_MASK, rk, qr & 31);
+                    if (!ldone) {
+                        if (qfirst || rrq > rk) ldone = true;
+                        else if (rkm < rk) { ldone = true; lres = false; }
+                        else --ql;
                     }
-                    if (!__any_sync(FULL_MASK, !done)) break;
-                }
-                const bool lres = done && res;
-                // right walk from lane + 1
-                q = lane + 1;
-                done = !need;
-                res = true;
-#pragma unroll 1
-                for (int it = 0; it < WALK_STEPS; ++it) {
-                    const bool qlast = __shfl_sync(FULL_MASK, last, q & 31);
-                    const uint32_t rlq = __shfl_sync(FULL_MASK, rl, q & 31);
-                    const uint32_t rkq = __shfl_sync(FULL_MASK, rk, q & 31);
-                    if (!done) {
-                        if (qlast || rlq > rk) done = true;
-                        else if (rkq < rk) { done = true; res = false; }
-                        else ++q;
+                    if (!rdone) {
+                        if (qlast || rlq > rk) rdone = true;
+                        else if (rkq < rk) { rdone = true; rres = false; }
+                        else ++qr;
                     }
-                    if (!__any_sync(FULL_MASK, !done)) break;
+                    if (!__any_sync(FULL_MASK, !(ldone && rdone) && !(ldone && !lres) && !(rdone && !rres))) break;
                 }
-                if (need) ok = lres && done && res;
+                if (need) ok = ldone && lres && rdone && rres;
             } else if (need) {
                 ok = false;  // no walks: only the segment minima merge this pass
             }
             sel = ok;
+            ENG_MARK(3);  // walks
         }
         // apply: token j+1 disappears when pair j is selected
         const bool selprev = __shfl_up_sync(FULL_MASK, sel, 1) && lane > 0 && !first;
@@ -176,6 +194,7 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
         n = n2;
         rl = rl_src;
         rr = rr_src;
+        ENG_MARK(4);  // compaction
         if (m2 && !strict) {  // loads in flight together with the pair probe below
             rl = __ldg(&T.rl[tok]);
             rr = __ldg(&T.rr[tok]);
@@ -192,6 +211,8 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
         } else {
             rk = GPUBPE_INF;
         }
+        (void)__any_sync(FULL_MASK, rk == 0);  // (stamps: wait for the probe)
+        ENG_MARK(5);  // re-probe
     }
     // write back: segment order is preserved by the compaction
     const uint32_t heads = __ballot_sync(FULL_MASK, first);
