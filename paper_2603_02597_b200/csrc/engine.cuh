@@ -146,25 +146,67 @@ __device__ __forceinline__ bool walk_right(const DevTables &T, const uint32_t *t
     return false;
 }
 
+// Cooperating groups the engine runs on: the whole CTA (giant segments) or
+// one warp (medium segments, 32 encoded per CTA at a time).
+struct BlockGroup {
+    EngineShared &sh;
+    __device__ uint32_t rank() const { return threadIdx.x; }
+    __device__ uint32_t size() const { return blockDim.x; }
+    __device__ void sync() const { __syncthreads(); }
+    __device__ unsigned long long min_u64(unsigned long long v) const { return block_min_u64(v, sh); }
+    __device__ uint32_t excl_sum(uint32_t v, uint32_t *total) const { return block_excl_sum(v, sh, total); }
+    __device__ uint32_t incl_max(uint32_t v, uint32_t *total) const { return block_incl_max(v, sh, total); }
+};
+
+struct WarpGroup {
+    __device__ uint32_t rank() const { return threadIdx.x & 31; }
+    __device__ uint32_t size() const { return 32; }
+    __device__ void sync() const { __syncwarp(); }
+    __device__ unsigned long long min_u64(unsigned long long v) const { return warp_min_u64(v); }
+    __device__ uint32_t excl_sum(uint32_t v, uint32_t *total) const {
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        *total = __shfl_sync(0xffffffffu, x, 31);
+        return x - v;
+    }
+    __device__ uint32_t incl_max(uint32_t v, uint32_t *total) const {
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x = max(x, y);
+        }
+        *total = __shfl_sync(0xffffffffu, x, 31);
+        return x;
+    }
+};
+
 // Runs the engine on M.tok[0..n).  Returns the output length; *out points at
-// the buffer holding the result.  Must be called by every thread of the CTA.
-static __device__ uint32_t engine_run(const DevTables &T, EngineMem M, uint32_t n, bool strict,
-                               EngineShared &sh, uint32_t *passes_out, const uint32_t **out) {
-    const uint32_t nt = blockDim.x;
+// the buffer holding the result.  Every thread of the group must call.
+template <class G>
+static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_t n, bool strict, const G &g,
+                                        uint32_t *passes_out, const uint32_t **out) {
+    const uint32_t nt = g.size(), me = g.rank();
     uint32_t passes = 0;
     for (uint32_t b = 0; b < n; b += nt) {
-        uint32_t i = b + threadIdx.x;
+        uint32_t i = b + me;
         if (i + 1 < n) {
             PairHit h = probe_pair(T, M.tok[i], M.tok[i + 1]);
             M.pr[i] = make_uint2(h.rank, h.nw);
         }
     }
-    __syncthreads();
+    g.sync();
     while (n >= 2) {
         // 1. min (rank, position)
         unsigned long long mine = ~0ull;
         for (uint32_t b = 0; b < n - 1; b += nt) {
-            uint32_t i = b + threadIdx.x;
+            uint32_t i = b + me;
             if (i < n - 1) {
                 uint32_t r = M.pr[i].x;
                 if (r != GPUBPE_INF) {
@@ -173,25 +215,25 @@ static __device__ uint32_t engine_run(const DevTables &T, EngineMem M, uint32_t 
                 }
             }
         }
-        unsigned long long kmin = block_min_u64(mine, sh);
+        unsigned long long kmin = g.min_u64(mine);
         if (kmin == ~0ull) break;
         const uint32_t rmin = (uint32_t)(kmin >> 32);
         const uint32_t pmin = (uint32_t)kmin;
         // 2. selection
         if (strict) {
             for (uint32_t b = 0; b < n; b += nt) {
-                uint32_t i = b + threadIdx.x;
+                uint32_t i = b + me;
                 if (i < n) M.sel[i] = (i == pmin);
             }
         } else {
             uint32_t carry = 0;
             for (uint32_t b = 0; b < n; b += nt) {
-                uint32_t i = b + threadIdx.x;
+                uint32_t i = b + me;
                 bool pair = i + 1 < n;
                 uint32_t r = pair ? M.pr[i].x : GPUBPE_INF;
                 bool start = pair && (i == 0 || M.pr[i - 1].x != r);
                 uint32_t chunk_max;
-                uint32_t s = block_incl_max(start ? i : 0u, sh, &chunk_max);
+                uint32_t s = g.incl_max(start ? i : 0u, &chunk_max);
                 s = max(s, carry);
                 carry = max(carry, chunk_max);
                 bool ok = pair && r != GPUBPE_INF && ((i - s) & 1u) == 0;
@@ -200,14 +242,14 @@ static __device__ uint32_t engine_run(const DevTables &T, EngineMem M, uint32_t 
                 if (i < n) M.sel[i] = ok;
             }
         }
-        __syncthreads();
+        g.sync();
         // 3. apply + compact
         uint32_t carry = 0;
         for (uint32_t b = 0; b < n; b += nt) {
-            uint32_t j = b + threadIdx.x;
+            uint32_t j = b + me;
             bool keep = j < n && !(j > 0 && M.sel[j - 1]);
             uint32_t total;
-            uint32_t pos = carry + block_excl_sum(keep ? 1u : 0u, sh, &total);
+            uint32_t pos = carry + g.excl_sum(keep ? 1u : 0u, &total);
             carry += total;
             if (keep) {
                 bool sj = M.sel[j];
@@ -227,7 +269,7 @@ static __device__ uint32_t engine_run(const DevTables &T, EngineMem M, uint32_t 
                 }
             }
         }
-        __syncthreads();
+        g.sync();
         n = carry;
         uint32_t *tt = M.tok; M.tok = M.tok2; M.tok2 = tt;
         uint2 *pp = M.pr; M.pr = M.pr2; M.pr2 = pp;
@@ -236,4 +278,10 @@ static __device__ uint32_t engine_run(const DevTables &T, EngineMem M, uint32_t 
     *passes_out = passes;
     *out = M.tok;
     return n;
+}
+
+// The CTA-wide engine (all threads of the CTA must call).
+static __device__ uint32_t engine_run(const DevTables &T, EngineMem M, uint32_t n, bool strict,
+                                      EngineShared &sh, uint32_t *passes_out, const uint32_t **out) {
+    return engine_run_g(T, M, n, strict, BlockGroup{sh}, passes_out, out);
 }

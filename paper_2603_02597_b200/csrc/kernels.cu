@@ -30,6 +30,7 @@ struct __align__(16) WarpSmem {
     uint16_t seg[WT];           // starts of the segments beginning in the tile, in order
     uint32_t cm[NGRP / 2 + 1];  // cut bits, position k = cut before byte a + k
     uint32_t n_miss, n_def;
+    unsigned long long dl_arena;  // deferred pass: this warp's arena offset broadcast
 };
 
 struct CtaSmem {
@@ -776,19 +777,118 @@ __device__ void publish_counters(CtaSmem &C, WarpCtx &X, PassCounters *dst) {
     }
 }
 
-// Deferred records [d0, d1) of round r: encode each with the CTA engine into
-// the arena and add its extra ids to its tile word.
+// Warp: first p in [lo, hi) whose cut slot is a junction miss, else hi.
+__device__ long long warp_first_nonjunction(const EncodeParams &P, const uint32_t *jb, long long lo, long long hi) {
+    const int lane = threadIdx.x & 31;
+    for (long long b = lo; b < hi; b += 16 * 32) {
+        const long long p0 = b + 16 * (long long)lane;
+        long long k = hi;
+        if (p0 < hi) {
+            uint32_t x = __ldg(&P.bytes[p0 - 1]);
+            const long long pe = min(p0 + 16, hi);
+            for (long long p = p0; p < pe; ++p) {
+                const uint32_t y = __ldg(&P.bytes[p]);
+                const uint32_t idx = (x << 8) | y;
+                if (!((jb[idx >> 5] >> (idx & 31)) & 1u)) { k = p; break; }
+                x = y;
+            }
+        }
+        const unsigned m = __ballot_sync(FULL_MASK, k < hi);
+        if (m) return __shfl_sync(FULL_MASK, k, __ffs(m) - 1);
+    }
+    return hi;
+}
+
+// Group-engine encode of one deferred segment [s0, s0 + len) into the arena;
+// the record gets its count and result offset, its tile word the extra ids.
+template <class G>
+__device__ void encode_record(const EncodeParams &P, CtaSmem &C, const G &g, unsigned long long r, long long s0,
+                              unsigned long long len, unsigned long long t0, unsigned long long par, bool lead,
+                              unsigned long long *arena_off_bcast) {
+    EncodeState *st = P.st;
+    if (lead) {
+        const unsigned long long words = (ENGINE_BYTES(len) + 15) / 16 * 4;
+        unsigned long long off = atomicAdd(&st->arena_used, words);
+        if (off + words > P.arena_words) {
+            atomicExch(&st->overflow, 1ull);
+            off = ~0ull;
+        }
+        *arena_off_bcast = off;
+    }
+    g.sync();
+    const unsigned long long off = *arena_off_bcast;
+    if (off == ~0ull) return;  // the host re-runs with a larger arena
+    EngineMem M;
+    M.tok = P.arena + off;
+    M.tok2 = M.tok + len;
+    M.pr = reinterpret_cast<uint2 *>(M.tok2 + len);
+    M.pr2 = M.pr + len;
+    M.sel = reinterpret_cast<uint8_t *>(M.pr2 + len);
+    for (unsigned long long j = g.rank(); j < len; j += g.size()) M.tok[j] = C.base[__ldg(&P.bytes[s0 + j])];
+    g.sync();
+    uint32_t passes;
+    const uint32_t *res;
+    const bool strict = P.strict || !P.T.well_formed;
+    const uint32_t cnt = engine_run_g(P.T, M, (uint32_t)len, strict, g, &passes, &res);
+    if (lead) {
+        P.recs[r].count = cnt;
+        P.recs[r].res = (uint32_t)(res - P.arena);
+        const unsigned long long t = (unsigned long long)s0 / (unsigned long long)P.tile_bytes;
+        atomicAdd(&P.tiles[par * P.round_tiles + (t - t0)], ((unsigned long long)cnt - 1) << 17);
+        if (len >= GIANT_MIN) {
+            atomicAdd(&C.pc.giant_segments, 1ull);
+            atomicAdd(&C.pc.giant_bytes, len);
+        } else {
+            atomicAdd(&C.pc.medium_segments, 1ull);
+        }
+        atomicAdd(&C.pc.engine_passes, (unsigned long long)passes);
+    }
+    g.sync();
+}
+
+#define REC_GIANT 0xFFFFFFFFu
+
+// Deferred records [d0, d1) of round r.  Pass 1: every warp takes records,
+// finds each segment's end (first cut after its start, looked for within
+// GIANT_MIN bytes) and encodes the medium ones with the warp engine; longer
+// ones are marked.  Pass 2 (after a grid barrier): whole CTAs take the marked
+// giants.  Both write results to the arena and extra ids to the tile words.
 __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, unsigned long long d0,
-                                unsigned long long d1, unsigned long long t0, unsigned long long par) {
+                                             unsigned long long d1, unsigned long long t0, unsigned long long par,
+                                             unsigned int &nbar) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     EncodeState *st = P.st;
     const long long N = (long long)P.n_bytes;
-    const bool strict = P.strict || !P.T.well_formed;
+    // ---- pass 1: warps
     for (;;) {
-        if (tid == 0) C.bcast[0] = d0 + atomicAdd(&st->rec_ctr, 1ull);
+        unsigned long long r = 0;
+        if (lane == 0) r = d0 + atomicAdd(&st->rec_ctr, 1ull);
+        r = __shfl_sync(FULL_MASK, r, 0);
+        if (r >= d1) break;
+        const long long s0 = (long long)__ldcg(&P.recs[r].start);
+        const long long d = P.n_docs > 1 ? warp_doc_from(P.doc_offs, 0, P.n_docs, s0) : 0;
+        long long lim = next_struct_cut(P, d, s0);
+        if (lim > N) lim = N;
+        const long long scan_hi = min(lim, s0 + (long long)GIANT_MIN);
+        const long long send = warp_first_nonjunction(P, C.jb, s0 + 1, scan_hi);
+        if (send >= scan_hi && scan_hi < lim) {  // no cut within GIANT_MIN bytes: a CTA's job
+            if (lane == 0) P.recs[r].count = REC_GIANT;
+            continue;
+        }
+        encode_record(P, C, WarpGroup{}, r, s0, (unsigned long long)(send - s0), t0, par, lane == 0,
+                      &C.w[wid].dl_arena);
+    }
+    grid_sync(st, ++nbar);
+    // ---- pass 2: whole CTAs for the giants
+    for (;;) {
+        if (tid == 0) C.bcast[0] = d0 + atomicAdd(&st->rec_ctr2, 1ull);
         __syncthreads();
         const unsigned long long r = C.bcast[0];
         if (r >= d1) break;
+        if (__ldcg(&P.recs[r].count) != REC_GIANT) {
+            __syncthreads();
+            continue;
+        }
         const long long s0 = (long long)__ldcg(&P.recs[r].start);
         if (wid == 0) {
             const long long d = P.n_docs > 1 ? warp_doc_from(P.doc_offs, 0, P.n_docs, s0) : 0;
@@ -797,45 +897,9 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
         __syncthreads();
         long long lim = next_struct_cut(P, (long long)C.bcast[1], s0);
         if (lim > N) lim = N;
-        const long long send = cta_first_nonjunction(P, C.jb, s0 + 1, lim, C.es);
-        const unsigned long long len = (unsigned long long)(send - s0);
-        if (tid == 0) {
-            const unsigned long long words = (ENGINE_BYTES(len) + 15) / 16 * 4;
-            unsigned long long off = atomicAdd(&st->arena_used, words);
-            if (off + words > P.arena_words) {
-                atomicExch(&st->overflow, 1ull);
-                off = ~0ull;
-            }
-            C.bcast[2] = off;
-        }
-        __syncthreads();
-        const unsigned long long off = C.bcast[2];
-        if (off == ~0ull) continue;
-        EngineMem M;
-        M.tok = P.arena + off;
-        M.tok2 = M.tok + len;
-        M.pr = reinterpret_cast<uint2 *>(M.tok2 + len);
-        M.pr2 = M.pr + len;
-        M.sel = reinterpret_cast<uint8_t *>(M.pr2 + len);
-        for (unsigned long long j = tid; j < len; j += NT) M.tok[j] = C.base[__ldg(&P.bytes[s0 + j])];
-        __syncthreads();
-        uint32_t passes;
-        const uint32_t *res;
-        const uint32_t cnt = engine_run(P.T, M, (uint32_t)len, strict, C.es, &passes, &res);
-        if (tid == 0) {
-            P.recs[r].count = cnt;
-            P.recs[r].res = (uint32_t)(res - P.arena);
-            const unsigned long long t = (unsigned long long)s0 / (unsigned long long)P.tile_bytes;
-            atomicAdd(&P.tiles[par * P.round_tiles + (t - t0)], ((unsigned long long)cnt - 1) << 17);
-            if (len >= GIANT_MIN) {
-                atomicAdd(&C.pc.giant_segments, 1ull);
-                atomicAdd(&C.pc.giant_bytes, len);
-            } else {
-                atomicAdd(&C.pc.medium_segments, 1ull);
-            }
-            atomicAdd(&C.pc.engine_passes, (unsigned long long)passes);
-        }
-        __syncthreads();
+        const long long send = cta_first_nonjunction(P, C.jb, s0 + GIANT_MIN, lim, C.es);
+        encode_record(P, C, BlockGroup{C.es}, r, s0, (unsigned long long)(send - s0), t0, par, tid == 0,
+                      &C.bcast[2]);
     }
 }
 
@@ -887,9 +951,12 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
                 if (blockIdx.x == 0 && tid == 0) atomicExch(&st->overflow, 1ull);
                 return;
             }
-            encode_deferred(P, C, d_done, D, t0, par);
+            encode_deferred(P, C, d_done, D, t0, par, nbar);
             grid_sync(st, ++nbar);
-            if (blockIdx.x == 0 && tid == 0) st->rec_ctr = 0;
+            if (blockIdx.x == 0 && tid == 0) {
+                st->rec_ctr = 0;
+                st->rec_ctr2 = 0;
+            }
             if (__ldcg(&st->overflow)) return;
             d_done = D;
         }

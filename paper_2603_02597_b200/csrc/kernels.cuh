@@ -42,7 +42,7 @@ constexpr int NGRP = LD / 16;   // 16-position groups whose cut bits are compute
 constexpr int NW = GPUBPE_NW;   // warps per CTA
 constexpr int NT = NW * 32;     // threads per CTA
 constexpr int SHORT_MAX = 32;   // longest segment encoded inside the tile loop
-constexpr int GIANT_MIN = 2305; // deferred segments at least this long count as "giant"
+constexpr int GIANT_MIN = 4097; // deferred segments this long are encoded by a whole CTA (else a warp)
 constexpr int SLOT = WT + SHORT_MAX;  // scratch entries per tile (ids of segments starting in it)
 constexpr int UNIT_MAX = 512;   // tiles per CTA per round in phase B
 constexpr unsigned int MARK = 0x80000000u;  // scratch entry: deferred record index follows
@@ -71,7 +71,8 @@ struct EncodeState {
     unsigned int bar;                // grid barrier arrivals
     unsigned int pad1[31];
     unsigned long long n_def;        // deferred segments recorded
-    unsigned long long rec_ctr;      // deferred records taken by CTAs
+    unsigned long long rec_ctr;      // deferred records taken by warps (medium pass)
+    unsigned long long rec_ctr2;     // deferred records scanned by CTAs (giant pass)
     unsigned long long arena_used;   // u32 words requested from the arena
     unsigned long long overflow;     // arena or record list overflowed: host re-runs
     unsigned long long n_ids;
