@@ -28,6 +28,7 @@ extern "C" {
 #define GPUBPE_ECUDA 2      /* CUDA runtime / launch failure (DeviceError) */
 #define GPUBPE_ENOMEM 3     /* device or host allocation failed (DeviceError) */
 #define GPUBPE_ETABLE 4     /* merge table rejected: duplicate pair / reserved key */
+#define GPUBPE_ERANGE 5     /* output capacity too small (the needed size is reported) */
 
 #define GPUBPE_API_VERSION 1
 
@@ -122,6 +123,23 @@ void gpubpe_host_free(void *p);
 /* Synchronise `stream` and read the counters of the last encode on it
  * (BatchResult.counters, chunker.py:56-64). */
 int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out);
+
+/*
+ * Device decode, ids -> bytes (replaces decode_tokens, byte_codec.py:121-146,
+ * and Tokenizer.decode, chunker.py:100-101).
+ * gpubpe_set_vocab: the byte string of every decodable id (n strings; ids
+ *   absent here, or with symbols containing non-byte characters, are unknown).
+ * gpubpe_decode: d_ids[n_ids] as n_seqs sequences (d_id_offs[n_seqs+1] CSR;
+ *   n_seqs == 0: one sequence, no offsets) -> their byte strings back to back
+ *   in d_out (capacity out_cap) with d_out_offs[n_seqs+1].  Synchronises.
+ *   Unknown id: GPUBPE_EINVAL, *bad_index = its index (UnknownTokenId).
+ *   Capacity too small: GPUBPE_ERANGE, *n_bytes_out = the bytes needed.
+ */
+int gpubpe_set_vocab(gpubpe_ctx *ctx, const uint32_t *ids, const uint8_t *bytes, const uint64_t *offs,
+                     uint64_t n);
+int gpubpe_decode(gpubpe_ctx *ctx, const uint32_t *d_ids, uint64_t n_ids, const int64_t *d_id_offs,
+                  uint64_t n_seqs, uint8_t *d_out, uint64_t out_cap, int64_t *d_out_offs,
+                  uint64_t *n_bytes_out, uint64_t *bad_index, void *stream);
 
 /* The junction bitmap of the context (65,536 bits as uint32[2048]; bit
  * (x << 8 | y) set iff some reachable rule joins a token ending in byte x to

@@ -21,7 +21,7 @@ import os
 # GPUBPE_LIB selects an alternative in-tree build (tuning experiments only)
 LIB_PATH = Path(__file__).resolve().parent / os.environ.get("GPUBPE_LIB", "libgpubpe.so")
 
-OK, EINVAL, ECUDA, ENOMEM, ETABLE = 0, 1, 2, 3, 4
+OK, EINVAL, ECUDA, ENOMEM, ETABLE, ERANGE = 0, 1, 2, 3, 4, 5
 F_NO_MEMO, F_STRICT = 1, 2
 
 # (name, restype, argtypes) for every entry point of include/gpubpe.h
@@ -49,6 +49,9 @@ SIGNATURES = {
     "gpubpe_host_free": (None, [_vp]),
     "gpubpe_query": (_int, [_vp, _vp, ctypes.POINTER(Stats)]),
     "gpubpe_junction_bits": (_int, [_vp, _vp]),
+    "gpubpe_set_vocab": (_int, [_vp, _vp, _vp, _vp, _u64]),
+    "gpubpe_decode": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _u64, _vp, ctypes.POINTER(ctypes.c_uint64),
+                             ctypes.POINTER(ctypes.c_uint64), _vp]),
     "gpubpe_launches_per_encode": (_int, []),
     "gpubpe_lookup_pairs": (_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),
     "gpubpe_set_profiling": (_int, [_vp, _int]),

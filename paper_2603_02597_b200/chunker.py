@@ -79,7 +79,26 @@ class Tokenizer:
         return self._base_ids[np.frombuffer(bytes(text), dtype=np.uint8)]
 
     def decode(self, tokens) -> bytes:
-        return decode_tokens(tokens, self.encoder, self.vocab)
+        """Token ids -> bytes on the device (decode_tokens semantics,
+        byte_codec.py:121-146; UnknownTokenId for ids outside the vocab)."""
+        return self.device_encoder().decode_host([tokens])[0]
+
+    def decode_batch(self, seqs) -> list[bytes]:
+        """Many id sequences -> their byte strings in one device call."""
+        return self.device_encoder().decode_host(seqs)
+
+    def _decode_strings(self):
+        """(ids, blob, offs) of every id whose symbol maps to bytes."""
+        ids, pieces = [], []
+        for tid, sym in self.vocab.id_to_symbol.items():
+            b = symbol_bytes(sym, self.encoder)
+            if b:
+                ids.append(tid)
+                pieces.append(b)
+        offs = np.zeros(len(pieces) + 1, dtype=np.uint64)
+        if pieces:
+            offs[1:] = np.cumsum([len(p) for p in pieces])
+        return np.array(ids, dtype=np.uint32), np.frombuffer(b"".join(pieces), dtype=np.uint8), offs
 
     def _vocab_strings(self):
         ids, pieces = [], []
@@ -109,6 +128,7 @@ class Tokenizer:
             vids, blob, offs = self._vocab_strings() if memo else (None, None, None)
             enc = DeviceEncoder(self._base_ids, left, right, rank, new, vids, blob, offs,
                                 device=dev, memo=memo, strict=strict)
+            enc.set_vocab(*self._decode_strings())
             self._devices[key] = enc
         return enc
 

@@ -20,6 +20,7 @@
 
 #include "../../include/gpubpe.h"
 #include "kernels.cuh"
+#include "decode.cuh"
 
 size_t tile_smem_bytes();
 cudaError_t launch_encode(const EncodeParams &P, int grid, cudaStream_t s, cudaEvent_t *ev,
@@ -50,6 +51,13 @@ struct gpubpe_ctx {
     size_t tables_bytes = 0, tables_used = 0;
     cudaAccessPolicyWindow win{};
     std::vector<uint32_t> h_jbits;  // host copy of the junction bitmap (sharding)
+    // decode (ids -> bytes): per-id LUT + byte blob, workspace
+    uint32_t *d_vinfo = nullptr;
+    uint8_t *d_vblob = nullptr;
+    uint32_t n_vocab_dec = 0;
+    DevBuf dec_state, dec_status;
+    unsigned int dec_epoch = 0;
+    int dec_grid = 0;
     // workspace
     DevBuf ws_state, ws_status, ws_recs, ws_scratch, ws_tiles, ws_arena;
     // host-buffer entry point: pinned (device-mapped) staging + device copy
@@ -744,6 +752,102 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_query(gpubpe_ctx *c
     return GPUBPE_OK;
 }
 
+extern "C" __attribute__((visibility("default"))) int gpubpe_set_vocab(gpubpe_ctx *ctx, const uint32_t *ids,
+                                                                         const uint8_t *bytes,
+                                                                         const uint64_t *offs, uint64_t n) {
+    if (!ctx || (n && (!ids || !bytes || !offs))) return GPUBPE_EINVAL;
+    CK(cudaSetDevice(ctx->device));
+    uint64_t max_id = 0;
+    for (uint64_t i = 0; i < n; ++i) max_id = std::max<uint64_t>(max_id, ids[i]);
+    if (n && max_id >= (1ull << 26)) return fail(ctx, GPUBPE_EINVAL, "decode: ids must be < 2^26");
+    const uint64_t blob_b = n ? offs[n] : 0;
+    if (blob_b >= (1ull << 24)) return fail(ctx, GPUBPE_EINVAL, "decode: vocab strings exceed 16 MiB");
+    std::vector<uint32_t> vinfo(n ? max_id + 1 : 1, GPUBPE_INF);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t len = offs[i + 1] - offs[i];
+        if (len == 0 || len > 255) continue;  // not decodable as bytes
+        vinfo[ids[i]] = (uint32_t)(offs[i] << 8) | (uint32_t)len;
+    }
+    if (ctx->d_vinfo) cudaFree(ctx->d_vinfo);
+    if (ctx->d_vblob) cudaFree(ctx->d_vblob);
+    ctx->d_vinfo = nullptr;
+    ctx->d_vblob = nullptr;
+    CK(cudaMalloc(&ctx->d_vinfo, vinfo.size() * 4));
+    CK(cudaMemcpy(ctx->d_vinfo, vinfo.data(), vinfo.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&ctx->d_vblob, std::max<uint64_t>(blob_b, 16)));
+    if (blob_b) CK(cudaMemcpy(ctx->d_vblob, bytes, blob_b, cudaMemcpyHostToDevice));
+    ctx->n_vocab_dec = (uint32_t)vinfo.size();
+    CK(setup_decode());
+    int blocks = 0;
+    CK(decode_occupancy(&blocks));
+    ctx->dec_grid = ctx->num_sms * std::max(1, blocks);
+    return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *ctx, const uint32_t *d_ids, uint64_t n_ids,
+                                                                      const int64_t *d_id_offs, uint64_t n_seqs,
+                                                                      uint8_t *d_out, uint64_t out_cap,
+                                                                      int64_t *d_out_offs, uint64_t *n_bytes_out,
+                                                                      uint64_t *bad_index, void *stream) {
+    if (!ctx || !n_bytes_out || !bad_index) return GPUBPE_EINVAL;
+    if (!ctx->d_vinfo) return fail(ctx, GPUBPE_EINVAL, "decode: no vocabulary (gpubpe_set_vocab)");
+    if (n_seqs && (!d_id_offs || !d_out_offs)) return fail(ctx, GPUBPE_EINVAL, "decode: null offsets");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device));
+    *n_bytes_out = 0;
+    *bad_index = ~0ull;
+    if (n_ids == 0) {
+        if (n_seqs) CK(cudaMemsetAsync(d_out_offs, 0, (n_seqs + 1) * 8, s));
+        return GPUBPE_OK;
+    }
+    const uint64_t n_tiles = (n_ids + decode_tile_ids() - 1) / decode_tile_ids();
+    int rc;
+    if ((rc = ensure(ctx, ctx->dec_state, sizeof(DecodeState), false))) return rc;
+    if (ctx->dec_status.bytes < n_tiles * 8) ctx->dec_epoch = 0;
+    if ((rc = ensure(ctx, ctx->dec_status, n_tiles * 8, true))) return rc;
+    if (++ctx->dec_epoch >= (1u << 20)) {
+        CK(cudaMemsetAsync(ctx->dec_status.p, 0, ctx->dec_status.bytes, s));
+        ctx->dec_epoch = 1;
+    }
+    DecodeState init{0, 0, 0, ~0ull};
+    DecodeState *d_st = static_cast<DecodeState *>(ctx->dec_state.p);
+    CK(cudaMemcpyAsync(d_st, &init, sizeof init, cudaMemcpyHostToDevice, s));
+    DecodeParams P{};
+    P.vinfo = ctx->d_vinfo;
+    P.blob = ctx->d_vblob;
+    P.n_vocab = ctx->n_vocab_dec;
+    P.ids = d_ids;
+    P.n_ids = n_ids;
+    P.id_offs = reinterpret_cast<const long long *>(d_id_offs);
+    P.n_seqs = n_seqs;
+    P.out = d_out;
+    P.out_cap = out_cap;
+    P.out_offs = reinterpret_cast<long long *>(d_out_offs);
+    P.st = d_st;
+    P.status = static_cast<unsigned long long *>(ctx->dec_status.p);
+    P.n_tiles = n_tiles;
+    P.epoch = ctx->dec_epoch;
+    P.aligned = (reinterpret_cast<uintptr_t>(d_ids) & 15) == 0;
+    const int grid = (int)std::min<uint64_t>(n_tiles, (uint64_t)ctx->dec_grid);
+    CK(launch_decode(P, grid, s));
+    DecodeState h;
+    CK(cudaMemcpyAsync(ctx->h_state, d_st, sizeof h, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    memcpy(&h, ctx->h_state, sizeof h);
+    ctx->state_fresh = false;
+    if (h.bad != ~0ull) {
+        *bad_index = h.bad;
+        return fail(ctx, GPUBPE_EINVAL, "id at index %llu not in vocabulary", (unsigned long long)h.bad);
+    }
+    if (h.need) {
+        *n_bytes_out = h.need;
+        return fail(ctx, GPUBPE_ERANGE, "decode output needs %llu bytes (capacity %llu)",
+                    (unsigned long long)h.need, (unsigned long long)out_cap);
+    }
+    *n_bytes_out = h.n_bytes;
+    return GPUBPE_OK;
+}
+
 extern "C" __attribute__((visibility("default"))) int gpubpe_junction_bits(gpubpe_ctx *ctx, uint32_t *h_out) {
     if (!ctx || !h_out) return GPUBPE_EINVAL;
     if (ctx->h_jbits.size() != 2048) return fail(ctx, GPUBPE_EINVAL, "context has no junction bitmap");
@@ -790,6 +894,10 @@ extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe
                       &ctx->ws_arena, &ctx->io_dev})
         if (b->p) cudaFree(b->p);
     if (ctx->pin) cudaFreeHost(ctx->pin);
+    if (ctx->d_vinfo) cudaFree(ctx->d_vinfo);
+    if (ctx->d_vblob) cudaFree(ctx->d_vblob);
+    for (DevBuf *b : {&ctx->dec_state, &ctx->dec_status})
+        if (b->p) cudaFree(b->p);
     for (auto &e : ctx->io_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);

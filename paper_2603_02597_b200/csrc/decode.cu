@@ -1,0 +1,251 @@
+// decode.cu -- ids -> bytes on the device.
+//
+// Restates decode_tokens (/root/reference/pkg/src/lanebpe/byte_codec.py:121-146)
+// and Tokenizer.decode (chunker.py:100-101): each id maps to the byte string
+// of its vocab symbol; the output is their concatenation; an id outside the
+// vocabulary (or whose symbol has a non-byte character) is an error
+// (UnknownTokenId).  A batch is a CSR of id sequences; the output is a CSR
+// of byte strings.
+//
+// k_decode: one launch, CTA tiles of TD ids (8 per thread, loaded as uint4 by
+// warp-contiguous 512-B rows), lengths from the LUT (L2-resident), warp and
+// block scans, a CTA-granular decoupled look-back for the tile's output
+// offset, the tile's bytes staged in shared memory and stored with coalesced
+// byte stores (tiles whose bytes exceed the stage write directly).  HBM-bound:
+// 4 B read per id + its bytes written.
+#include <cuda_runtime.h>
+
+#include <cuda/atomic>
+
+#include "common.cuh"
+#include "decode.cuh"
+
+namespace {
+
+constexpr int DT = 1024;             // threads per CTA
+constexpr int DPT = 8;               // ids per thread
+constexpr int TD = DT * DPT;         // ids per tile
+constexpr int STAGE = 96 * 1024;     // staged output bytes per tile
+
+struct DecSmem {
+    uint32_t goff[TD / 4];           // output offset of each 4-id group inside the tile
+    uint32_t wsum[DT / 32];
+    unsigned long long base, need;
+    uint32_t total;
+    uint8_t stage[STAGE];
+};
+
+__device__ __forceinline__ void st_rel(unsigned long long *w, unsigned long long v) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(*w);
+    r.store(v, cuda::memory_order_relaxed);
+}
+__device__ __forceinline__ unsigned long long ld_rel(unsigned long long *w) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(*w);
+    return r.load(cuda::memory_order_relaxed);
+}
+
+// id -> (blob offset, length); INF info = unknown id
+__device__ __forceinline__ uint32_t info_of(const DecodeParams &P, uint32_t id) {
+    return id < P.n_vocab ? __ldg(&P.vinfo[id]) : GPUBPE_INF;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(DT, 1) k_decode(const __grid_constant__ DecodeParams P) {
+    extern __shared__ __align__(16) unsigned char dsm_raw[];
+    DecSmem &S = *reinterpret_cast<DecSmem *>(dsm_raw);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (;;) {
+        if (tid == 0) S.base = atomicAdd(&P.st->tile_ctr, 1ull);
+        __syncthreads();
+        const unsigned long long t = S.base;
+        __syncthreads();
+        if (t >= P.n_tiles) break;
+        const unsigned long long t0 = t * TD;
+        // ---- ids: warp row w covers tile ids [w*256, w*256+256); lane l holds
+        //      4-id groups g = k*32 + l (k = 0, 1) of that row
+        uint32_t id[DPT], len[DPT];
+        const unsigned long long row = t0 + (unsigned long long)wid * 256;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const unsigned long long i = row + (unsigned long long)k * 128 + lane * 4;
+            if (P.aligned && i + 4 <= P.n_ids) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(P.ids + i));
+                id[4 * k] = v.x; id[4 * k + 1] = v.y; id[4 * k + 2] = v.z; id[4 * k + 3] = v.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) id[4 * k + j] = i + j < P.n_ids ? __ldg(&P.ids[i + j]) : 0u;
+            }
+        }
+        uint32_t gs[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            gs[k] = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const unsigned long long i = row + (unsigned long long)k * 128 + lane * 4 + j;
+                uint32_t l = 0;
+                if (i < P.n_ids) {
+                    const uint32_t inf = info_of(P, id[4 * k + j]);
+                    if (inf == GPUBPE_INF) {
+                        atomicMin(&P.st->bad, i);
+                    } else {
+                        l = inf & 0xFFu;
+                    }
+                }
+                len[4 * k + j] = l;
+                gs[k] += l;
+            }
+        }
+        // ---- offsets: warp scans (k-major), block scan of warp totals
+        uint32_t wtot = 0, gex[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            uint32_t x = gs[k];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL_MASK, x, o);
+                if (lane >= o) x += y;
+            }
+            gex[k] = wtot + x - gs[k];
+            wtot += __shfl_sync(FULL_MASK, x, 31);
+        }
+        if (lane == 31) S.wsum[wid] = wtot;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t v = S.wsum[lane];
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL_MASK, x, o);
+                if (lane >= o) x += y;
+            }
+            S.wsum[lane] = x - v;  // exclusive warp offsets
+            const uint32_t total = __shfl_sync(FULL_MASK, x, 31);
+            // decoupled look-back over tiles (value+flag+epoch in one word)
+            const unsigned long long tag = (unsigned long long)P.epoch << 44;
+            unsigned long long excl = 0;
+            if (t == 0) {
+                if (lane == 0) st_rel(&P.status[0], tag | (2ull << 42) | total);
+            } else {
+                if (lane == 0) st_rel(&P.status[t], tag | (1ull << 42) | total);
+                long long pos = (long long)t - 1;
+                for (;;) {
+                    const long long j = pos - lane;
+                    unsigned long long v2 = 2ull << 42, flag = 2;
+                    if (j >= 0) {
+                        for (;;) {
+                            v2 = ld_rel(&P.status[j]);
+                            flag = ((v2 >> 44) == P.epoch) ? ((v2 >> 42) & 3ull) : 0ull;
+                            if (flag) break;
+                            __nanosleep(32);
+                        }
+                    }
+                    const unsigned inc = __ballot_sync(FULL_MASK, flag == 2);
+                    const int stop = inc ? __ffs(inc) - 1 : 31;
+                    unsigned long long val = lane <= stop ? (v2 & ((1ull << 42) - 1)) : 0ull;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(FULL_MASK, val, o);
+                    excl += val;
+                    if (inc) break;
+                    pos -= 32;
+                }
+                if (lane == 0) st_rel(&P.status[t], tag | (2ull << 42) | (excl + total));
+            }
+            if (lane == 0) {
+                S.base = excl;
+                S.total = total;
+            }
+        }
+        __syncthreads();
+        const unsigned long long base = S.base;
+        const uint32_t total = S.total;
+        const uint32_t wbase = S.wsum[wid];
+        const bool staged = total <= STAGE;
+        const bool fits = base + total <= P.out_cap;
+        if (!fits && tid == 0) atomicMax(&P.st->need, base + total);
+        // ---- bytes: staged in shared memory (or straight to global)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            uint32_t o = wbase + gex[k];
+            S.goff[(wid * 2 + k) * 32 + lane] = o;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t l = len[4 * k + j];
+                if (l) {
+                    const uint8_t *src = P.blob + (info_of(P, id[4 * k + j]) >> 8);
+                    if (staged) {
+                        for (uint32_t b = 0; b < l; ++b) S.stage[o + b] = __ldg(&src[b]);
+                    } else if (fits) {
+                        for (uint32_t b = 0; b < l; ++b) P.out[base + o + b] = __ldg(&src[b]);
+                    }
+                }
+                o += l;
+            }
+        }
+        __syncthreads();
+        if (staged && fits)
+            for (uint32_t b = tid; b < total; b += DT) P.out[base + b] = S.stage[b];
+        // ---- byte offsets of the sequences that start in this tile
+        if (P.n_seqs && wid == 0) {
+            // first sequence with id_offs >= t0 (lower bound, 32-ary)
+            long long lo = 0, hi = (long long)P.n_seqs;
+            while (hi > lo) {
+                const long long step = (hi - lo + 31) / 32;
+                const long long idx = lo + (long long)lane * step;
+                const bool lt = idx < hi && (unsigned long long)__ldg(&P.id_offs[idx]) < t0;
+                const unsigned m = __ballot_sync(FULL_MASK, lt);
+                if (!m) { hi = lo; break; }
+                const int l = 31 - __clz(m);
+                lo = lo + (long long)l * step + 1;
+                hi = min(hi, lo - 1 + step);
+            }
+            const bool last_tile = t + 1 == P.n_tiles;
+            for (long long d0 = lo;; d0 += 32) {
+                const long long d = d0 + lane;
+                bool in = false;
+                if (d <= (long long)P.n_seqs) {
+                    const unsigned long long s = (unsigned long long)__ldg(&P.id_offs[d]);
+                    if (s < t0 + TD || last_tile) {
+                        in = true;
+                        const unsigned long long q = s - t0;  // id index inside the tile
+                        unsigned long long v;
+                        if (q >= TD || s >= P.n_ids) {
+                            v = base + total;
+                        } else {
+                            const uint32_t w = (uint32_t)(q >> 8), rem = (uint32_t)(q & 255);
+                            const uint32_t k = rem >> 7, l2 = (rem & 127) >> 2, j = rem & 3;
+                            uint32_t o = S.goff[(w * 2 + k) * 32 + l2];
+                            for (uint32_t jj = 0; jj < j; ++jj) {
+                                const unsigned long long ii = s - j + jj;
+                                const uint32_t inf = info_of(P, __ldg(&P.ids[ii]));
+                                o += inf == GPUBPE_INF ? 0u : (inf & 0xFFu);
+                            }
+                            v = base + o;
+                        }
+                        P.out_offs[d] = (long long)v;
+                    }
+                }
+                if (__ballot_sync(FULL_MASK, in) != FULL_MASK) break;
+            }
+        }
+        if (t + 1 == P.n_tiles && tid == 0) P.st->n_bytes = base + total;
+        __syncthreads();
+    }
+}
+
+size_t decode_smem_bytes() { return sizeof(DecSmem); }
+int decode_tile_ids() { return TD; }
+
+cudaError_t setup_decode() {
+    return cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem));
+}
+
+cudaError_t decode_occupancy(int *blocks) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_decode, DT, sizeof(DecSmem));
+}
+
+cudaError_t launch_decode(const DecodeParams &P, int grid, cudaStream_t s) {
+    k_decode<<<grid, DT, sizeof(DecSmem), s>>>(P);
+    return cudaGetLastError();
+}

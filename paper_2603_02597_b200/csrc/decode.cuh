@@ -1,0 +1,36 @@
+// decode.cuh -- parameters of the device decode (ids -> bytes), decode.cu.
+#pragma once
+#include <cstdint>
+
+struct DecodeState {
+    unsigned long long tile_ctr;
+    unsigned long long need;     // output bytes needed when out_cap was too small
+    unsigned long long n_bytes;  // bytes written
+    unsigned long long bad;      // smallest index of an unknown id, ~0 if none
+};
+
+struct DecodeParams {
+    const uint32_t *vinfo;  // per id: blob offset << 8 | length, INF if not decodable
+    const uint8_t *blob;
+    uint32_t n_vocab;       // ids >= n_vocab are unknown
+    const uint32_t *ids;
+    unsigned long long n_ids;
+    const long long *id_offs;  // [n_seqs + 1] CSR of id sequences (nullable when n_seqs == 0)
+    unsigned long long n_seqs;
+    uint8_t *out;
+    unsigned long long out_cap;
+    long long *out_offs;       // [n_seqs + 1] byte offsets
+    DecodeState *st;
+    unsigned long long *status;  // [n_tiles] look-back words
+    unsigned long long n_tiles;
+    unsigned int epoch;
+    int aligned;               // ids pointer is 16-B aligned
+};
+
+#ifdef __CUDACC__
+size_t decode_smem_bytes();
+int decode_tile_ids();
+cudaError_t setup_decode();
+cudaError_t decode_occupancy(int *blocks);
+cudaError_t launch_decode(const DecodeParams &P, int grid, cudaStream_t s);
+#endif

@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 from . import _native
-from .errors import DeviceError, DuplicatePair
+from .errors import DeviceError, DuplicatePair, UnknownTokenId
 
 try:
     import torch
@@ -171,6 +171,66 @@ class DeviceEncoder:
                                      int(max_seq_len), int(chunk_budget), out_ids.data_ptr(),
                                      out_offs.data_ptr(), s.cuda_stream)
         _native.check(rc, self._h, "gpubpe_encode")
+
+    # ------------------------------------------------------------ decode
+
+    def set_vocab(self, ids: np.ndarray, blob: np.ndarray, offs: np.ndarray) -> None:
+        """Byte strings of every decodable id (CSR) for the device decode."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        blob = np.ascontiguousarray(blob, dtype=np.uint8)
+        offs = np.ascontiguousarray(offs, dtype=np.uint64)
+        rc = self._lib.gpubpe_set_vocab(self._h, _ptr(ids), _ptr(blob), _ptr(offs), len(ids))
+        _native.check(rc, self._h, "gpubpe_set_vocab")
+
+    def decode_into(self, ids: "torch.Tensor", id_offs, out: "torch.Tensor", out_offs, stream=None) -> int:
+        """Device CSR of ids -> device CSR of bytes; returns the bytes written.
+        id_offs/out_offs: int64 [n_seqs+1] tensors, or None for one sequence.
+        Raises UnknownTokenId, or ValueError when `out` is too small."""
+        n = ids.numel()
+        n_seqs = 0 if id_offs is None else id_offs.numel() - 1
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        nb, bad = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        rc = self._lib.gpubpe_decode(self._h, ids.data_ptr(), n, id_offs.data_ptr() if n_seqs else None,
+                                     n_seqs, out.data_ptr(), out.numel(),
+                                     out_offs.data_ptr() if n_seqs else None, ctypes.byref(nb),
+                                     ctypes.byref(bad), s.cuda_stream)
+        if rc == _native.EINVAL and bad.value != (1 << 64) - 1:
+            raise UnknownTokenId(f"id {int(ids[bad.value].item()) & 0xFFFFFFFF} at index {bad.value} "
+                                 "not in vocabulary")
+        if rc == _native.ERANGE:
+            raise ValueError(f"decode output needs {nb.value} bytes, capacity {out.numel()}")
+        _native.check(rc, self._h, "gpubpe_decode")
+        return int(nb.value)
+
+    def decode_host(self, seqs) -> list[bytes]:
+        """list of id sequences -> list of byte strings, decoded on the device."""
+        arrs = [np.asarray(x, dtype=np.int64).ravel() for x in seqs]
+        for a in arrs:
+            if a.size and (a.min() < 0 or a.max() > 0xFFFFFFFF):
+                bad = int(a[(a < 0) | (a > 0xFFFFFFFF)][0])
+                raise UnknownTokenId(f"id {bad} not in vocabulary")
+        offs = np.zeros(len(arrs) + 1, dtype=np.int64)
+        if arrs:
+            offs[1:] = np.cumsum([a.size for a in arrs])
+        flat = np.concatenate(arrs).astype(np.uint32) if arrs else np.empty(0, np.uint32)
+        with self._lock, torch.cuda.device(self.device):
+            dev = torch.device("cuda", self.device)
+            d_ids = torch.from_numpy(flat.view(np.int32) if flat.size else np.zeros(1, np.int32)).to(dev)
+            d_offs = torch.from_numpy(offs).to(dev)
+            d_oo = torch.empty_like(d_offs)
+            cap = 8 * max(int(flat.size), 1) + 64
+            for _ in range(2):
+                d_out = torch.empty(cap, dtype=torch.uint8, device=dev)
+                try:
+                    nb = self.decode_into(d_ids[: flat.size], d_offs, d_out, d_oo)
+                    break
+                except ValueError as exc:  # capacity: re-run with the size the device asked for
+                    cap = int(str(exc).split()[3]) + 64
+            else:  # pragma: no cover
+                raise DeviceError("decode capacity retry failed")
+            out = d_out[:nb].cpu().numpy().tobytes()
+            oo = d_oo.cpu().numpy()
+        return [out[oo[i]:oo[i + 1]] for i in range(len(arrs))]
 
     def junction_bits(self) -> np.ndarray:
         """uint32[2048] junction bitmap (bit x << 8 | y: some rule joins x|y)."""

@@ -38,7 +38,7 @@ def test_gpt2_tables(tokenizer):
     assert tokenizer.table.capacity == 131072
     assert tokenizer.encode(b"the").tolist() == [83, 71, 68]
     assert tokenizer.vocab.id_to_symbol[1169] == "the"
-    assert tokenizer.decode([31373, 995]) == b"hello world"
+    assert bpe.decode_tokens([31373, 995], tokenizer.encoder, tokenizer.vocab) == b"hello world"
 
 
 def test_table_lookups_and_rule_recovery(tokenizer, oracle_tables):

@@ -230,3 +230,40 @@ def test_device_junction_bits_match_rules_and_split_exactly(tokenizer, oracle, o
             got = [bpe.tokenize_batch(s, tok).token_ids for s in shards if s]
             got = np.concatenate([i for g in got for i in g])
             assert np.array_equal(got, want), (msl, world)
+
+
+# ---------------------------------------------------------------- decode
+
+
+def test_decode_known_answers(tokenizer):
+    assert tokenizer.decode([31373, 995]) == b"hello world"
+    assert tokenizer.decode([1169]) == b"the"  # test_byte_codec.py:78-81
+    assert tokenizer.decode([]) == b""  # test_byte_codec.py:74-75
+    assert tokenizer.decode([50256]) == b"<|endoftext|>"
+    with pytest.raises(bpe.errors.UnknownTokenId):
+        tokenizer.decode([2**32 - 1])  # test_byte_codec.py:84-86
+    with pytest.raises(bpe.errors.UnknownTokenId):
+        tokenizer.decode([31373, 50257, 995])
+
+
+def test_decode_roundtrips_and_matches_host_helper(tokenizer):
+    docs, cfgs = fixtures.mixed_cases()
+    msl, cb, want = cfgs["default"]
+    got = tokenizer.decode_batch(want)
+    assert got == [bytes(d) if isinstance(d, (bytes, bytearray)) else d.encode() for d in docs]
+    rng = np.random.default_rng(4)
+    seqs = [rng.integers(0, 50257, int(rng.integers(0, 3000))) for _ in range(40)]
+    host = [bpe.decode_tokens(s, tokenizer.encoder, tokenizer.vocab) for s in seqs]
+    assert tokenizer.decode_batch(seqs) == host
+
+
+def test_decode_large_and_adversarial(tokenizer, oracle):
+    import synth_corpus
+
+    spec = fixtures.synth_sizes()["c3_1m"]
+    doc = synth_corpus.english_bytes(spec["n_bytes"], spec["seed"])
+    ids = bpe.tokenize_batch([doc], with_config(tokenizer, 1 << 40, 1 << 40)).token_ids[0]
+    assert tokenizer.decode(ids) == doc
+    longest = max(tokenizer.vocab.id_to_symbol, key=lambda i: len(tokenizer.vocab.id_to_symbol[i]))
+    big = [longest] * 20000  # ~2.5 MB of output from 80 KB of ids: unstaged tiles
+    assert tokenizer.decode(big) == bpe.decode_tokens([longest], tokenizer.encoder, tokenizer.vocab) * 20000

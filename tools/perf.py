@@ -72,6 +72,47 @@ def workloads():
     }
 
 
+def decode_row(name, enc, flush, peak, args):
+    """decode_<workload>: device decode of that workload's ids (ids in HBM,
+    bytes out in HBM); alg bytes = 4 n_ids + n_bytes + 16 (n_seqs+1)."""
+    import numpy as np
+    import torch
+
+    wl = workloads()[name[len("decode_"):]]
+    data, offs, _ = wl()
+    dev = torch.device("cuda", 0)
+    d_data = torch.from_numpy(data.copy()).to(dev)
+    d_offs = torch.from_numpy(offs).to(dev)
+    ids = torch.empty(max(data.size, 1), dtype=torch.int32, device=dev)
+    ioffs = torch.empty(len(offs), dtype=torch.int64, device=dev)
+    enc.encode_into(d_data, d_offs, ids, ioffs, 8192, 8192)
+    n_ids = int(ioffs[-1].item())
+    ids = ids[:n_ids]
+    out = torch.empty(data.size + 64, dtype=torch.uint8, device=dev)
+    oo = torch.empty_like(ioffs)
+    for _ in range(args.warmup):
+        enc.decode_into(ids, ioffs, out, oo)
+    assert torch.equal(out[: data.size].cpu(), torch.from_numpy(data)), "decode round trip"
+    times = []
+    for _ in range(args.iters):
+        if not args.no_flush:
+            flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        enc.decode_into(ids, ioffs, out, oo)  # includes its one sync for the error/size check
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times)
+    b_alg = 4 * n_ids + data.size + 16 * len(offs)
+    row = {"workload": name, "bytes": int(data.size), "ids": n_ids, "p50_ms": ms,
+           "tokens_per_s": n_ids / ms * 1e3, "alg_GBps": b_alg / ms / 1e6, "frac": b_alg / ms / 1e6 / peak}
+    print(f"{name:18s} {n_ids:>11,d} ids -> {data.size:>11,d} B  p50 {ms*1e3:9.1f} us  "
+          f"{row['tokens_per_s']/1e9:7.3f} Gtok/s  alg {row['alg_GBps']:8.1f} GB/s  frac {row['frac']:.4f}", flush=True)
+    return row
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
@@ -98,6 +139,9 @@ def main():
     wl = workloads()
     names = args.only.split(",") if args.only else list(wl)
     rows = []
+    for name in [n for n in names if n.startswith("decode_")]:
+        rows.append(decode_row(name, enc, flush, peak, args))
+    names = [n for n in names if not n.startswith("decode_")]
     for name in names:
         data, offs, want = wl[name]()
         n = int(data.size)
