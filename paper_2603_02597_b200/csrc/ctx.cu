@@ -760,22 +760,29 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_set_vocab(gpubpe_ct
     uint64_t max_id = 0;
     for (uint64_t i = 0; i < n; ++i) max_id = std::max<uint64_t>(max_id, ids[i]);
     if (n && max_id >= (1ull << 26)) return fail(ctx, GPUBPE_EINVAL, "decode: ids must be < 2^26");
-    const uint64_t blob_b = n ? offs[n] : 0;
-    if (blob_b >= (1ull << 24)) return fail(ctx, GPUBPE_EINVAL, "decode: vocab strings exceed 16 MiB");
+    // strings 16-B aligned and zero-padded: the kernel fetches them with 16-B loads;
+    // vinfo = (offset / 16) << 8 | length
     std::vector<uint32_t> vinfo(n ? max_id + 1 : 1, GPUBPE_INF);
+    std::vector<uint8_t> blob;
     for (uint64_t i = 0; i < n; ++i) {
         const uint64_t len = offs[i + 1] - offs[i];
         if (len == 0 || len > 255) continue;  // not decodable as bytes
-        vinfo[ids[i]] = (uint32_t)(offs[i] << 8) | (uint32_t)len;
+        const uint64_t at = blob.size();
+        if ((at >> 4) >= (1ull << 24)) return fail(ctx, GPUBPE_EINVAL, "decode: vocab strings exceed 256 MiB");
+        blob.insert(blob.end(), bytes + offs[i], bytes + offs[i + 1]);
+        blob.resize((blob.size() + 15) & ~(size_t)15, 0);
+        vinfo[ids[i]] = (uint32_t)((at >> 4) << 8) | (uint32_t)len;
     }
+    blob.resize(blob.size() + 16, 0);
+    const uint64_t blob_b = blob.size();
     if (ctx->d_vinfo) cudaFree(ctx->d_vinfo);
     if (ctx->d_vblob) cudaFree(ctx->d_vblob);
     ctx->d_vinfo = nullptr;
     ctx->d_vblob = nullptr;
     CK(cudaMalloc(&ctx->d_vinfo, vinfo.size() * 4));
     CK(cudaMemcpy(ctx->d_vinfo, vinfo.data(), vinfo.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&ctx->d_vblob, std::max<uint64_t>(blob_b, 16)));
-    if (blob_b) CK(cudaMemcpy(ctx->d_vblob, bytes, blob_b, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&ctx->d_vblob, blob_b));
+    CK(cudaMemcpy(ctx->d_vblob, blob.data(), blob_b, cudaMemcpyHostToDevice));
     ctx->n_vocab_dec = (uint32_t)vinfo.size();
     CK(setup_decode());
     int blocks = 0;

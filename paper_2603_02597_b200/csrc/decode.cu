@@ -24,15 +24,17 @@ namespace {
 
 constexpr int DT = 1024;             // threads per CTA
 constexpr int DPT = 8;               // ids per thread
+constexpr int KG = DPT / 4;          // 4-id groups per lane
+constexpr int ROW = 32 * DPT;        // ids per warp row
 constexpr int TD = DT * DPT;         // ids per tile
-constexpr int STAGE = 96 * 1024;     // staged output bytes per tile
+constexpr int STAGE = 96 * 1024;     // staged output bytes per tile (+16 alignment slack)
 
 struct DecSmem {
     uint32_t goff[TD / 4];           // output offset of each 4-id group inside the tile
     uint32_t wsum[DT / 32];
     unsigned long long base, need;
     uint32_t total;
-    uint8_t stage[STAGE];
+    __align__(16) uint8_t stage[STAGE + 32];
 };
 
 __device__ __forceinline__ void st_rel(unsigned long long *w, unsigned long long v) {
@@ -62,12 +64,12 @@ __global__ void __launch_bounds__(DT, 1) k_decode(const __grid_constant__ Decode
         __syncthreads();
         if (t >= P.n_tiles) break;
         const unsigned long long t0 = t * TD;
-        // ---- ids: warp row w covers tile ids [w*256, w*256+256); lane l holds
-        //      4-id groups g = k*32 + l (k = 0, 1) of that row
+        // ---- ids: warp row w covers tile ids [w*ROW, (w+1)*ROW); lane l holds
+        //      4-id groups g = k*32 + l (k < KG) of that row
         uint32_t id[DPT], len[DPT];
-        const unsigned long long row = t0 + (unsigned long long)wid * 256;
+        const unsigned long long row = t0 + (unsigned long long)wid * ROW;
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < KG; ++k) {
             const unsigned long long i = row + (unsigned long long)k * 128 + lane * 4;
             if (P.aligned && i + 4 <= P.n_ids) {
                 const uint4 v = __ldg(reinterpret_cast<const uint4 *>(P.ids + i));
@@ -77,30 +79,29 @@ __global__ void __launch_bounds__(DT, 1) k_decode(const __grid_constant__ Decode
                 for (int j = 0; j < 4; ++j) id[4 * k + j] = i + j < P.n_ids ? __ldg(&P.ids[i + j]) : 0u;
             }
         }
-        uint32_t gs[2];
+        uint32_t gs[KG];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < KG; ++k) {
             gs[k] = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const unsigned long long i = row + (unsigned long long)k * 128 + lane * 4 + j;
-                uint32_t l = 0;
+                uint32_t inf = 0;  // length 0: past the end or unknown
                 if (i < P.n_ids) {
-                    const uint32_t inf = info_of(P, id[4 * k + j]);
+                    inf = info_of(P, id[4 * k + j]);
                     if (inf == GPUBPE_INF) {
                         atomicMin(&P.st->bad, i);
-                    } else {
-                        l = inf & 0xFFu;
+                        inf = 0;
                     }
                 }
-                len[4 * k + j] = l;
-                gs[k] += l;
+                len[4 * k + j] = inf;  // blob chunk << 8 | length
+                gs[k] += inf & 0xFFu;
             }
         }
         // ---- offsets: warp scans (k-major), block scan of warp totals
-        uint32_t wtot = 0, gex[2];
+        uint32_t wtot = 0, gex[KG];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < KG; ++k) {
             uint32_t x = gs[k];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -113,14 +114,14 @@ __global__ void __launch_bounds__(DT, 1) k_decode(const __grid_constant__ Decode
         if (lane == 31) S.wsum[wid] = wtot;
         __syncthreads();
         if (wid == 0) {
-            uint32_t v = S.wsum[lane];
+            uint32_t v = lane < DT / 32 ? S.wsum[lane] : 0u;
             uint32_t x = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(FULL_MASK, x, o);
                 if (lane >= o) x += y;
             }
-            S.wsum[lane] = x - v;  // exclusive warp offsets
+            if (lane < DT / 32) S.wsum[lane] = x - v;  // exclusive warp offsets
             const uint32_t total = __shfl_sync(FULL_MASK, x, 31);
             // decoupled look-back over tiles (value+flag+epoch in one word)
             const unsigned long long tag = (unsigned long long)P.epoch << 44;
@@ -164,28 +165,56 @@ __global__ void __launch_bounds__(DT, 1) k_decode(const __grid_constant__ Decode
         const bool staged = total <= STAGE;
         const bool fits = base + total <= P.out_cap;
         if (!fits && tid == 0) atomicMax(&P.st->need, base + total);
-        // ---- bytes: staged in shared memory (or straight to global)
+        // ---- bytes: one 16-B load per id (strings are 16-B aligned and
+        //      zero-padded), staged at shift = base & 15 so 16-B chunks of the
+        //      stage land on 16-B aligned global addresses
+        const uint32_t shift = (uint32_t)(base & 15);
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < KG; ++k) {
             uint32_t o = wbase + gex[k];
-            S.goff[(wid * 2 + k) * 32 + lane] = o;
+            S.goff[(wid * KG + k) * 32 + lane] = o;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const uint32_t l = len[4 * k + j];
+                const uint32_t inf = len[4 * k + j], l = inf & 0xFFu;
                 if (l) {
-                    const uint8_t *src = P.blob + (info_of(P, id[4 * k + j]) >> 8);
-                    if (staged) {
-                        for (uint32_t b = 0; b < l; ++b) S.stage[o + b] = __ldg(&src[b]);
-                    } else if (fits) {
-                        for (uint32_t b = 0; b < l; ++b) P.out[base + o + b] = __ldg(&src[b]);
+                    const uint4 *src = reinterpret_cast<const uint4 *>(P.blob) + (inf >> 8);
+                    if (staged) {  // shared-memory stores (the common case)
+                        uint8_t *dst = S.stage + shift + o;
+                        for (uint32_t c = 0; c < l; c += 16) {
+                            const uint4 v = __ldg(src + (c >> 4));
+                            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                            const uint32_t m = min(16u, l - c);
+#pragma unroll
+                            for (uint32_t b = 0; b < 16; ++b)
+                                if (b < m) dst[c + b] = (uint8_t)(w[b >> 2] >> (8 * (b & 3)));
+                        }
+                    } else if (fits) {  // tile larger than the stage: straight to global
+                        uint8_t *dst = P.out + base + o;
+                        for (uint32_t c = 0; c < l; c += 16) {
+                            const uint4 v = __ldg(src + (c >> 4));
+                            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                            const uint32_t m = min(16u, l - c);
+                            for (uint32_t b = 0; b < m; ++b) dst[c + b] = (uint8_t)(w[b >> 2] >> (8 * (b & 3)));
+                        }
                     }
                 }
                 o += l;
             }
         }
         __syncthreads();
-        if (staged && fits)
-            for (uint32_t b = tid; b < total; b += DT) P.out[base + b] = S.stage[b];
+        if (staged && fits) {
+            // chunk q of the stage covers global [(base & ~15) + 16q, +16)
+            const uint32_t end = shift + total, nq = (end + 15) >> 4;
+            uint8_t *gdst = P.out + (base & ~15ull);
+            for (uint32_t q = tid; q < nq; q += DT) {
+                const uint32_t lo = q * 16, hi = lo + 16;
+                if (lo >= shift && hi <= end) {
+                    reinterpret_cast<uint4 *>(gdst)[q] = reinterpret_cast<const uint4 *>(S.stage)[q];
+                } else {
+                    for (uint32_t b = max(lo, shift); b < min(hi, end); ++b) gdst[b] = S.stage[b];
+                }
+            }
+        }
         // ---- byte offsets of the sequences that start in this tile
         if (P.n_seqs && wid == 0) {
             // first sequence with id_offs >= t0 (lower bound, 32-ary)
@@ -213,9 +242,9 @@ __global__ void __launch_bounds__(DT, 1) k_decode(const __grid_constant__ Decode
                         if (q >= TD || s >= P.n_ids) {
                             v = base + total;
                         } else {
-                            const uint32_t w = (uint32_t)(q >> 8), rem = (uint32_t)(q & 255);
+                            const uint32_t w = (uint32_t)(q / ROW), rem = (uint32_t)(q % ROW);
                             const uint32_t k = rem >> 7, l2 = (rem & 127) >> 2, j = rem & 3;
-                            uint32_t o = S.goff[(w * 2 + k) * 32 + l2];
+                            uint32_t o = S.goff[(w * KG + k) * 32 + l2];
                             for (uint32_t jj = 0; jj < j; ++jj) {
                                 const unsigned long long ii = s - j + jj;
                                 const uint32_t inf = info_of(P, __ldg(&P.ids[ii]));

@@ -94,6 +94,10 @@ def decode_row(name, enc, flush, peak, args):
         enc.decode_into(ids, ioffs, out, oo)
     assert torch.equal(out[: data.size].cpu(), torch.from_numpy(data)), "decode round trip"
     times = []
+    prof = os.environ.get("GPUBPE_PROFILE_TIMED")
+    if prof:
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
     for _ in range(args.iters):
         if not args.no_flush:
             flush.fill_(1)
@@ -104,6 +108,8 @@ def decode_row(name, enc, flush, peak, args):
         e1.record()
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
+    if prof:
+        torch.cuda.cudart().cudaProfilerStop()
     ms = statistics.median(times)
     b_alg = 4 * n_ids + data.size + 16 * len(offs)
     row = {"workload": name, "bytes": int(data.size), "ids": n_ids, "p50_ms": ms,
