@@ -13,6 +13,7 @@ from .bindings import TokenizerHandle
 from .byte_codec import ByteEncoder, Vocab, base_id_table, build_byte_encoder, decode_tokens, encode_bytes
 from .chunker import ENGINE_NAMES, BatchResult, Chunk, Tokenizer, chunk_tokens, pack_texts, tokenize_batch
 from .engine import BlockConfig, PassCounters
+from .windows import DEFAULT_LENGTHS, SweepSpec, make_windows
 from .merge_table import (
     MergeRule,
     PackedPairTable,
@@ -27,7 +28,7 @@ from .merge_table import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "BatchResult", "BlockConfig", "ByteEncoder", "Chunk", "ENGINE_NAMES", "MergeRule",
+    "BatchResult", "BlockConfig", "DEFAULT_LENGTHS", "SweepSpec", "make_windows", "ByteEncoder", "Chunk", "ENGINE_NAMES", "MergeRule",
     "PackedPairTable", "PassCounters", "Tokenizer", "TokenizerHandle", "Vocab", "base_id_table",
     "build_byte_encoder", "build_table", "chunk_tokens", "decode_tokens", "encode_bytes", "errors",
     "pack_key", "pack_texts", "pack_value", "parse_merges", "rule_arrays", "tokenize_batch",

@@ -115,3 +115,63 @@ def test_pack_texts():
 def test_empty_batch_needs_no_device(tokenizer):
     res = bpe.tokenize_batch([], tokenizer)
     assert res.token_ids == [] and res.counters.passes == 0
+
+
+# ------------------------------------------------------------- make_windows
+
+
+def _windows_fixture():
+    import gzip
+    import json
+    from pathlib import Path
+
+    here = Path(__file__).resolve().parent / "golden"
+    fx = json.loads((here / "windows.json").read_text())
+    lines = gzip.decompress((here / "prose_corpus.txt.gz").read_bytes()).split(b"\n")
+    return fx, b"\n".join(lines[: fx["corpus_lines"]])
+
+
+def test_sweep_spec_validation():
+    with pytest.raises(ValueError):
+        bpe.SweepSpec(lengths=())
+    with pytest.raises(ValueError):
+        bpe.SweepSpec(lengths=(64, 16))
+    with pytest.raises(ValueError):
+        bpe.SweepSpec(measured_runs=0)
+    bpe.SweepSpec(warmup_runs=0)
+
+
+def test_make_windows_byte_mode_matches_reference():
+    fx, corpus = _windows_fixture()
+    for case in fx["cases"]:
+        if case["mode"] != "byte":
+            continue
+        spec = bpe.SweepSpec(lengths=tuple(case["lengths"]), samples_per_length=case["samples"])
+        got = bpe.make_windows(corpus, None, spec, seed=case["seed"])
+        assert {str(k): [w.hex() for w in v] for k, v in got.items()} == case["windows"]
+    with pytest.raises(errors.CorpusTooSmall):
+        bpe.make_windows(b"short", None, bpe.SweepSpec(lengths=(256,)))
+    with pytest.raises(errors.CorpusTooSmall):
+        bpe.make_windows(b"", None, bpe.SweepSpec(lengths=(256,)))
+    with pytest.raises(ValueError):
+        bpe.make_windows(corpus, [1, 2, 3], bpe.SweepSpec(lengths=(1,)))
+
+
+class _HostDecoder:
+    """Stands in for the device decode on CPU (the reference's own algorithm)."""
+
+    def __init__(self, tok):
+        self.tok = tok
+
+    def decode_batch(self, seqs):
+        return [bpe.decode_tokens(s, self.tok.encoder, self.tok.vocab) for s in seqs]
+
+
+def test_make_windows_token_mode_matches_reference_cpu(tokenizer):
+    fx, corpus = _windows_fixture()
+    for case in fx["cases"]:
+        if case["mode"] != "token":
+            continue
+        spec = bpe.SweepSpec(lengths=tuple(case["lengths"]), samples_per_length=case["samples"])
+        got = bpe.make_windows(corpus, fx["stream"], spec, tokenizer=_HostDecoder(tokenizer), seed=case["seed"])
+        assert {str(k): [w.hex() for w in v] for k, v in got.items()} == case["windows"]

@@ -267,3 +267,15 @@ def test_decode_large_and_adversarial(tokenizer, oracle):
     longest = max(tokenizer.vocab.id_to_symbol, key=lambda i: len(tokenizer.vocab.id_to_symbol[i]))
     big = [longest] * 20000  # ~2.5 MB of output from 80 KB of ids: unstaged tiles
     assert tokenizer.decode(big) == bpe.decode_tokens([longest], tokenizer.encoder, tokenizer.vocab) * 20000
+
+
+def test_make_windows_token_mode_device_decode_matches_reference(tokenizer):
+    from test_api import _windows_fixture
+
+    fx, corpus = _windows_fixture()
+    for case in fx["cases"]:
+        if case["mode"] != "token":
+            continue
+        spec = bpe.SweepSpec(lengths=tuple(case["lengths"]), samples_per_length=case["samples"])
+        got = bpe.make_windows(corpus, fx["stream"], spec, tokenizer=tokenizer, seed=case["seed"])
+        assert {str(k): [w.hex() for w in v] for k, v in got.items()} == case["windows"]
