@@ -59,7 +59,7 @@ struct gpubpe_ctx {
     unsigned int dec_epoch = 0;
     int dec_grid = 0;
     // workspace
-    DevBuf ws_state, ws_status, ws_recs, ws_scratch, ws_tiles, ws_arena;
+    DevBuf ws_state, ws_status, ws_recs, ws_scratch, ws_tiles, ws_arena, ws_gscr, ws_glist;
     // host-buffer entry point: pinned (device-mapped) staging + device copy
     DevBuf io_dev;
     uint8_t *pin = nullptr;
@@ -465,8 +465,10 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
     if ((rc = ensure(ctx, ctx->ws_tiles, 2 * R * 8, false))) return rc;
     if ((rc = ensure(ctx, ctx->ws_recs, std::max<uint64_t>(1 << 16, std::min<uint64_t>(def_max, 1 << 20)) * sizeof(DefRec), false))) return rc;
     if ((rc = ensure(ctx, ctx->ws_arena, 64ull << 20, false))) return rc;
+    if ((rc = ensure(ctx, ctx->ws_gscr, (8 + 2 * (size_t)grid) * 8, false))) return rc;
     for (int attempt = 0; attempt < 4; ++attempt) {
         const uint64_t rec_cap = ctx->ws_recs.bytes / sizeof(DefRec);
+        if ((rc = ensure(ctx, ctx->ws_glist, rec_cap * 4, false))) return rc;
         if (++ctx->epoch >= (1u << 20)) {
             CK(cudaMemsetAsync(ctx->ws_status.p, 0, ctx->ws_status.bytes, s));
             ctx->epoch = 1;
@@ -498,6 +500,8 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.strict = (ctx->flags & GPUBPE_F_STRICT) ? 1 : 0;
         P.aligned = (reinterpret_cast<uintptr_t>(d_bytes) & 15) == 0;
         P.tile_bytes = wt;
+        P.gscr = static_cast<unsigned long long *>(ctx->ws_gscr.p);
+        P.glist = static_cast<uint32_t *>(ctx->ws_glist.p);
         ctx->last_n_tiles = n_tiles;
         // debug knobs (tuning only) never apply to the memo verification encode
         const int dbg = (ctx->T.memo && getenv("GPUBPE_DEBUG")) ? atoi(getenv("GPUBPE_DEBUG")) : 0;
@@ -898,7 +902,7 @@ extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe
     cudaDeviceSynchronize();
     if (ctx->tables) cudaFree(ctx->tables);
     for (DevBuf *b : {&ctx->ws_state, &ctx->ws_status, &ctx->ws_recs, &ctx->ws_scratch, &ctx->ws_tiles,
-                      &ctx->ws_arena, &ctx->io_dev})
+                      &ctx->ws_arena, &ctx->io_dev, &ctx->ws_gscr, &ctx->ws_glist})
         if (b->p) cudaFree(b->p);
     if (ctx->pin) cudaFreeHost(ctx->pin);
     if (ctx->d_vinfo) cudaFree(ctx->d_vinfo);

@@ -619,6 +619,11 @@ __device__ void place_tile(const EncodeParams &P, const uint32_t *src, unsigned 
                 const unsigned long long at = __shfl_sync(FULL_MASK, ex, src_lane);
                 const uint32_t c = __shfl_sync(FULL_MASK, cntk, src_lane);
                 const uint32_t r = __shfl_sync(FULL_MASK, res, src_lane);
+                if (c >= GIANT_MIN - 1) {  // a giant's ids: copied by the whole grid after placement
+                    const uint32_t rec = __shfl_sync(FULL_MASK, e & ~MARK, src_lane);
+                    if (lane == 0) P.recs[rec].dst = base + at;
+                    continue;
+                }
                 for (uint32_t j = lane; j < c; j += 32) dst[at + j] = out_id(T, __ldcg(&P.arena[r + j]));
             }
             o += __shfl_sync(FULL_MASK, incl, 31);
@@ -777,6 +782,222 @@ __device__ void publish_counters(CtaSmem &C, WarpCtx &X, PassCounters *dst) {
     }
 }
 
+#define REC_GIANT 0xFFFFFFFFu  // record marked by the warp pass: a whole-grid job
+
+// ------------------------------------------------------------------ grid engine
+//
+// Exact multi-merge BPE of ONE giant segment by all CTAs (engine.cuh's
+// selection rule, same arena layout).  CTA c owns elements [c*n/G, (c+1)*n/G)
+// of the current sequence; a pass costs three grid barriers:
+//   A  block min (rank, pos) -> atomicMin; last run start of the range -> gscr;
+//   B  selection with the run-start carry of the ranges before; the pair just
+//      before the range is re-selected redundantly (same inputs, same rule),
+//      so keep counts need no extra barrier; counts -> gscr;
+//   C  compaction at the global prefix of the counts (neighbours' selections
+//      were written before barrier B).
+// gscr: [0], [1] alternating kmin slots, [2] giant end, [3] arena offset,
+// [8 + c] last run start + 1 of range c, [8 + G + c] kept tokens of range c.
+
+__device__ __forceinline__ bool grid_select(const DevTables &T, const EngineMem &M, uint32_t i, uint32_t n,
+                                            uint32_t s, uint32_t rmin, uint32_t pmin, bool strict) {
+    if (i + 1 >= n) return false;
+    const uint32_t r = M.pr[i].x;
+    if (strict) return i == pmin;
+    bool ok = r != GPUBPE_INF && ((i - s) & 1u) == 0;
+    if (ok && r != rmin) ok = walk_left(T, M.tok, M.pr, s, r) && walk_right(T, M.tok, M.pr, i + 1, n, r);
+    return ok;
+}
+
+__device__ uint32_t grid_engine_run(const EncodeParams &P, CtaSmem &C, EngineMem M, uint32_t n, bool strict,
+                                    unsigned int &nbar, uint32_t *passes_out, const uint32_t **out) {
+    const uint32_t tid = threadIdx.x, G = gridDim.x, c = blockIdx.x;
+    const DevTables &T = P.T;
+    EncodeState *st = P.st;
+    unsigned long long *g = P.gscr;
+    for (unsigned long long i = (unsigned long long)c * NT + tid; i + 1 < n; i += (unsigned long long)G * NT) {
+        const PairHit h = probe_pair(T, M.tok[i], M.tok[i + 1]);
+        M.pr[i] = make_uint2(h.rank, h.nw);
+    }
+    if (c == 0 && tid == 0) g[0] = g[1] = ~0ull;
+    grid_sync(st, ++nbar);
+    uint32_t passes = 0;
+    while (n >= 2) {
+        const uint32_t lo = (uint32_t)((unsigned long long)n * c / G), hi = (uint32_t)((unsigned long long)n * (c + 1) / G);
+        // ---- A: min and the range's last run start
+        unsigned long long mine = ~0ull;
+        uint32_t ls = 0;  // last start + 1 (0: none)
+        for (uint32_t i = lo + tid; i < hi; i += NT) {
+            if (i + 1 < n) {
+                const uint32_t r = M.pr[i].x;
+                if (r != GPUBPE_INF) mine = min(mine, ((unsigned long long)r << 32) | i);
+                if (i == 0 || M.pr[i - 1].x != r) ls = i + 1;
+            }
+        }
+        const unsigned long long bmin = block_min_u64(mine, C.es);
+        uint32_t dummy;
+        const uint32_t bls = block_incl_max(ls, C.es, &dummy);
+        if (tid == NT - 1) {
+            if (bmin != ~0ull) atomicMin(&g[passes & 1], bmin);
+            g[8 + c] = bls;  // inclusive max of the last thread = the range's last start + 1
+        }
+        grid_sync(st, ++nbar);
+        if (c == 0 && tid == 0) g[(passes + 1) & 1] = ~0ull;  // the next pass's slot
+        const unsigned long long kmin = __ldcg(&g[passes & 1]);
+        if (kmin == ~0ull) break;  // (every CTA sees the same value)
+        const uint32_t rmin = (uint32_t)(kmin >> 32), pmin = (uint32_t)kmin;
+        // carry: last run start before this range
+        uint32_t carry = 0;
+        for (uint32_t q = tid; q < c; q += NT) carry = max(carry, (uint32_t)__ldcg(&g[8 + q]));
+        carry = block_incl_max(carry, C.es, &dummy);
+        if (tid == 0) C.bcast[1] = dummy;
+        __syncthreads();
+        carry = (uint32_t)C.bcast[1];
+        const uint32_t s_before = carry ? carry - 1 : 0u;  // run start covering lo - 1
+        // ---- B: selection of [lo, hi), redundant selection of lo - 1, keep counts
+        const bool sel_prev = lo > 0 && grid_select(T, M, lo - 1, n, s_before, rmin, pmin, strict);
+        uint32_t runs = carry;  // max start + 1 seen so far
+        for (uint32_t b = lo; b < hi; b += NT) {
+            const uint32_t i = b + tid;
+            const bool pair = i < hi && i + 1 < n;
+            const uint32_t r = pair ? M.pr[i].x : GPUBPE_INF;
+            const bool start = pair && (i == 0 || M.pr[i - 1].x != r);
+            uint32_t chunk_max;
+            uint32_t sv = block_incl_max(start ? i + 1 : 0u, C.es, &chunk_max);
+            sv = max(sv, runs);
+            runs = max(runs, chunk_max);
+            if (i < hi) M.sel[i] = grid_select(T, M, i, n, sv ? sv - 1 : 0u, rmin, pmin, strict);
+        }
+        __syncthreads();
+        uint32_t kept = 0;
+        for (uint32_t j = lo + tid; j < hi; j += NT) {
+            const bool sp = j == lo ? sel_prev : (M.sel[j - 1] != 0);
+            kept += (j > 0 && sp) ? 0u : 1u;
+        }
+        uint32_t ktot;
+        (void)block_excl_sum(kept, C.es, &ktot);
+        if (tid == 0) g[8 + G + c] = ktot;
+        grid_sync(st, ++nbar);
+        // ---- C: compaction at the global prefix
+        uint32_t pre = 0, tot = 0;
+        for (uint32_t q = tid; q < G; q += NT) {
+            const uint32_t v = (uint32_t)__ldcg(&g[8 + G + q]);
+            tot += v;
+            if (q < c) pre += v;
+        }
+        uint32_t ptot;
+        pre = block_excl_sum(pre, C.es, &ptot);  // (sum over threads)
+        pre = ptot;
+        (void)block_excl_sum(tot, C.es, &tot);
+        uint32_t carry2 = pre;
+        for (uint32_t b = lo; b < hi; b += NT) {
+            const uint32_t j = b + tid;
+            bool keep = false;
+            if (j < hi) {
+                const bool sp = j == lo ? sel_prev : (__ldcg(&M.sel[j - 1]) != 0);
+                keep = !(j > 0 && sp);
+            }
+            uint32_t total;
+            const uint32_t pos = carry2 + block_excl_sum(keep ? 1u : 0u, C.es, &total);
+            carry2 += total;
+            if (keep) {
+                const bool sj = __ldcg(&M.sel[j]) != 0;
+                const uint2 pj = (j + 1 < n) ? M.pr[j] : make_uint2(GPUBPE_INF, 0);
+                const uint32_t t = sj ? pj.y : M.tok[j];
+                M.tok2[pos] = t;
+                const uint32_t jn = sj ? j + 2 : j + 1;
+                if (jn < n) {
+                    const bool sn = __ldcg(&M.sel[jn]) != 0;
+                    const uint32_t tn = sn ? M.pr[jn].y : M.tok[jn];
+                    if (sj || sn) {
+                        const PairHit h = probe_pair(T, t, tn);
+                        M.pr2[pos] = make_uint2(h.rank, h.nw);
+                    } else {
+                        M.pr2[pos] = pj;
+                    }
+                }
+            }
+        }
+        grid_sync(st, ++nbar);
+        n = tot;
+        uint32_t *tt = M.tok; M.tok = M.tok2; M.tok2 = tt;
+        uint2 *pp = M.pr; M.pr = M.pr2; M.pr2 = pp;
+        ++passes;
+    }
+    *passes_out = passes;
+    *out = M.tok;
+    return n;
+}
+
+// All CTAs: encode the giant records of [d0, d1) one after another.
+__device__ void grid_giants(const EncodeParams &P, CtaSmem &C, unsigned long long t0, unsigned long long par,
+                            unsigned int &nbar) {
+    const int tid = threadIdx.x;
+    EncodeState *st = P.st;
+    unsigned long long *g = P.gscr;
+    const long long N = (long long)P.n_bytes;
+    const bool strict = P.strict || !P.T.well_formed;
+    const unsigned long long ng = __ldcg(&g[4]);  // giants of this round (same in every CTA)
+    for (unsigned long long gi = 0; gi < ng; ++gi) {
+        const unsigned long long r = __ldcg(&P.glist[gi]);
+        const long long s0 = (long long)__ldcg(&P.recs[r].start);
+        // the segment's end: each CTA scans a slice of [s0 + GIANT_MIN, lim)
+        long long d = 0;
+        if (P.n_docs > 1) {
+            if ((threadIdx.x >> 5) == 0) {
+                const long long dd = warp_doc_from(P.doc_offs, 0, P.n_docs, s0);
+                if ((threadIdx.x & 31) == 0) C.bcast[1] = (unsigned long long)dd;
+            }
+            __syncthreads();
+            d = (long long)C.bcast[1];
+        }
+        long long lim = next_struct_cut(P, d, s0);
+        if (lim > N) lim = N;
+        const long long from = s0 + GIANT_MIN, span = lim - from;
+        const long long lo = from + span * blockIdx.x / gridDim.x, hi = from + span * (blockIdx.x + 1) / gridDim.x;
+        if (blockIdx.x == 0 && tid == 0) g[2] = (unsigned long long)lim;
+        grid_sync(st, ++nbar);
+        const long long e = cta_first_nonjunction(P, C.jb, lo, hi, C.es);
+        if (tid == 0 && e < hi) atomicMin(&g[2], (unsigned long long)e);
+        if (blockIdx.x == 0 && tid == 0) {
+            // arena for the engine (the length is not known yet: bound it by lim)
+            const unsigned long long words = (ENGINE_BYTES(lim - s0) + 15) / 16 * 4;
+            unsigned long long off = atomicAdd(&st->arena_used, words);
+            if (off + words > P.arena_words) {
+                atomicExch(&st->overflow, 1ull);
+                off = ~0ull;
+            }
+            g[3] = off;
+        }
+        grid_sync(st, ++nbar);
+        const unsigned long long off = __ldcg(&g[3]);
+        const long long send = (long long)__ldcg(&g[2]);
+        if (off == ~0ull) continue;  // the host re-runs with a larger arena (all CTAs alike)
+        const unsigned long long len = (unsigned long long)(send - s0);
+        EngineMem M;
+        M.tok = P.arena + off;
+        M.tok2 = M.tok + len;
+        M.pr = reinterpret_cast<uint2 *>(M.tok2 + len);
+        M.pr2 = M.pr + len;
+        M.sel = reinterpret_cast<uint8_t *>(M.pr2 + len);
+        for (unsigned long long j = (unsigned long long)blockIdx.x * NT + tid; j < len;
+             j += (unsigned long long)gridDim.x * NT)
+            M.tok[j] = C.base[__ldg(&P.bytes[s0 + j])];
+        grid_sync(st, ++nbar);
+        uint32_t passes;
+        const uint32_t *res;
+        const uint32_t cnt = grid_engine_run(P, C, M, (uint32_t)len, strict, nbar, &passes, &res);
+        if (blockIdx.x == 0 && tid == 0) {
+            P.recs[r].count = cnt;
+            P.recs[r].res = (uint32_t)(res - P.arena);
+            const unsigned long long t = (unsigned long long)s0 / (unsigned long long)P.tile_bytes;
+            atomicAdd(&P.tiles[par * P.round_tiles + (t - t0)], ((unsigned long long)cnt - 1) << 17);
+            atomicAdd(&C.pc.giant_segments, 1ull);
+            atomicAdd(&C.pc.giant_bytes, len);
+            atomicAdd(&C.pc.engine_passes, (unsigned long long)passes);
+        }
+    }
+}
+
 // Warp: first p in [lo, hi) whose cut slot is a junction miss, else hi.
 __device__ long long warp_first_nonjunction(const EncodeParams &P, const uint32_t *jb, long long lo, long long hi) {
     const int lane = threadIdx.x & 31;
@@ -846,7 +1067,6 @@ __device__ void encode_record(const EncodeParams &P, CtaSmem &C, const G &g, uns
     g.sync();
 }
 
-#define REC_GIANT 0xFFFFFFFFu
 
 // Deferred records [d0, d1) of round r.  Pass 1: every warp takes records,
 // finds each segment's end (first cut after its start, looked for within
@@ -871,36 +1091,19 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
         if (lim > N) lim = N;
         const long long scan_hi = min(lim, s0 + (long long)GIANT_MIN);
         const long long send = warp_first_nonjunction(P, C.jb, s0 + 1, scan_hi);
-        if (send >= scan_hi && scan_hi < lim) {  // no cut within GIANT_MIN bytes: a CTA's job
-            if (lane == 0) P.recs[r].count = REC_GIANT;
+        if (send >= scan_hi && scan_hi < lim) {  // no cut within GIANT_MIN bytes: a job for the grid
+            if (lane == 0) {
+                P.recs[r].count = REC_GIANT;
+                P.glist[atomicAdd(&P.gscr[4], 1ull)] = (uint32_t)r;
+            }
             continue;
         }
         encode_record(P, C, WarpGroup{}, r, s0, (unsigned long long)(send - s0), t0, par, lane == 0,
                       &C.w[wid].dl_arena);
     }
     grid_sync(st, ++nbar);
-    // ---- pass 2: whole CTAs for the giants
-    for (;;) {
-        if (tid == 0) C.bcast[0] = d0 + atomicAdd(&st->rec_ctr2, 1ull);
-        __syncthreads();
-        const unsigned long long r = C.bcast[0];
-        if (r >= d1) break;
-        if (__ldcg(&P.recs[r].count) != REC_GIANT) {
-            __syncthreads();
-            continue;
-        }
-        const long long s0 = (long long)__ldcg(&P.recs[r].start);
-        if (wid == 0) {
-            const long long d = P.n_docs > 1 ? warp_doc_from(P.doc_offs, 0, P.n_docs, s0) : 0;
-            if (lane == 0) C.bcast[1] = (unsigned long long)d;
-        }
-        __syncthreads();
-        long long lim = next_struct_cut(P, (long long)C.bcast[1], s0);
-        if (lim > N) lim = N;
-        const long long send = cta_first_nonjunction(P, C.jb, s0 + GIANT_MIN, lim, C.es);
-        encode_record(P, C, BlockGroup{C.es}, r, s0, (unsigned long long)(send - s0), t0, par, tid == 0,
-                      &C.bcast[2]);
-    }
+    // ---- pass 2: every CTA together on each giant, in record order
+    grid_giants(P, C, t0, par, nbar);
 }
 
 // ------------------------------------------------------------------ kernel
@@ -910,7 +1113,10 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
     CtaSmem &C = *reinterpret_cast<CtaSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     EncodeState *st = P.st;
-    if (blockIdx.x == 0 && tid == 0) *P.st_next = EncodeState{};
+    if (blockIdx.x == 0 && tid == 0) {
+        *P.st_next = EncodeState{};
+        P.gscr[4] = 0;  // giants of the round (appended after the round's first grid barrier)
+    }
     for (int k = tid; k < 2048; k += NT) C.jb[k] = __ldg(&P.T.jbits[k]);
     for (int k = tid; k < 256; k += NT) C.base[k] = __ldg(&P.T.base[k]);
     if (tid < (int)(sizeof(PassCounters) / 8)) (&C.pc.n_segments)[tid] = 0;
@@ -919,7 +1125,7 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
     WarpSmem &S = C.w[wid];
     WarpCtx X{};
     unsigned int nbar = 0;
-    unsigned long long d_done = 0;
+    unsigned long long d_done = 0, ng = 0;
     const unsigned long long R = P.round_tiles;
     const unsigned long long G = gridDim.x;
     for (unsigned long long r = 0, t0 = 0; t0 < P.n_tiles; ++r, t0 += R) {
@@ -953,6 +1159,7 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
             }
             encode_deferred(P, C, d_done, D, t0, par, nbar);
             grid_sync(st, ++nbar);
+            ng = __ldcg(&P.gscr[4]);
             if (blockIdx.x == 0 && tid == 0) {
                 st->rec_ctr = 0;
                 st->rec_ctr2 = 0;
@@ -964,6 +1171,21 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
         const unsigned long long q = (t1 - t0 + G - 1) / G;
         const unsigned long long lo = min(t1, t0 + blockIdx.x * q), hi = min(t1, lo + q);
         place_range(P, C, r, t0, lo, hi);
+        if (ng) {  // giants' ids: one grid-wide copy once their destinations are placed
+            grid_sync(st, ++nbar);
+            if (blockIdx.x == 0 && tid == 0) P.gscr[4] = 0;
+            for (unsigned long long gi = 0; gi < ng; ++gi) {
+                const DefRec *rec = &P.recs[__ldcg(&P.glist[gi])];
+                const uint32_t cnt = __ldcg(&rec->count);
+                if (cnt < GIANT_MIN - 1) continue;  // copied by its tile's warp
+                const uint32_t *src = P.arena + __ldcg(&rec->res);
+                uint32_t *dst = P.out_ids + __ldcg(&rec->dst);
+                for (unsigned long long j = (unsigned long long)blockIdx.x * NT + tid; j < cnt;
+                     j += (unsigned long long)gridDim.x * NT)
+                    dst[j] = out_id(P.T, __ldcg(&src[j]));
+            }
+            ng = 0;
+        }
     }
     publish_counters(C, X, &st->c);
     if (P.dbg && tid == 0) P.dbg[4 * blockIdx.x + 3] = gtimer();

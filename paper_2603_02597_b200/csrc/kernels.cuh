@@ -42,7 +42,7 @@ constexpr int NGRP = LD / 16;   // 16-position groups whose cut bits are compute
 constexpr int NW = GPUBPE_NW;   // warps per CTA
 constexpr int NT = NW * 32;     // threads per CTA
 constexpr int SHORT_MAX = 32;   // longest segment encoded inside the tile loop
-constexpr int GIANT_MIN = 4097; // deferred segments this long are encoded by a whole CTA (else a warp)
+constexpr int GIANT_MIN = 4097; // deferred segments this long are encoded by the whole grid (else a warp)
 constexpr int SLOT = WT + SHORT_MAX;  // scratch entries per tile (ids of segments starting in it)
 constexpr int UNIT_MAX = 512;   // tiles per CTA per round in phase B
 constexpr unsigned int MARK = 0x80000000u;  // scratch entry: deferred record index follows
@@ -84,6 +84,7 @@ struct DefRec {
     unsigned long long start;  // first byte of the segment
     unsigned int count;        // ids it encodes to
     unsigned int res;          // arena word offset of its ids
+    unsigned long long dst;    // giants: output position, copied grid-wide after placement
 };
 
 struct EncodeParams {
@@ -110,6 +111,8 @@ struct EncodeParams {
     int strict;
     int aligned;                 // bytes pointer is 16-B aligned
     int tile_bytes;              // wt: 128, 256 or 512 (host picks by input size)
+    unsigned long long *gscr;    // grid-engine scratch: [0..7] scalars, [8..8+2*grid) per-CTA
+    uint32_t *glist;             // [rec_cap] giant record indices of the round (count in gscr[4])
     unsigned long long *dbg;     // debug timestamps (GPUBPE_DEBUG & 8), else null
     int dbg_phase_a_only;        // GPUBPE_DEBUG & 16: profile phase A alone (output invalid)
 };
