@@ -57,6 +57,10 @@ typedef struct gpubpe_stats {
 #define GPUBPE_F_NO_MEMO 1u      /* disable the vocab-string memo (evidence runs) */
 #define GPUBPE_F_STRICT 2u       /* force one-merge-per-pass even if well-formed */
 
+/* Encode modes (gpubpe_set_mode) */
+#define GPUBPE_MODE_DEFAULT 0u     /* the reference's semantics: no pre-tokenization */
+#define GPUBPE_MODE_GPT2_REGEX 1u  /* tiktoken's GPT-2 regex pre-tokens are cuts too (optional) */
+
 /*
  * Build a device context (replaces Tokenizer.__init__ / Tokenizer.from_files,
  * chunker.py:74-93, and build_table, merge_table.py:246-278, as the place the
@@ -140,6 +144,19 @@ int gpubpe_set_vocab(gpubpe_ctx *ctx, const uint32_t *ids, const uint8_t *bytes,
 int gpubpe_decode(gpubpe_ctx *ctx, const uint32_t *d_ids, uint64_t n_ids, const int64_t *d_id_offs,
                   uint64_t n_seqs, uint8_t *d_out, uint64_t out_cap, int64_t *d_out_offs,
                   uint64_t *n_bytes_out, uint64_t *bad_index, void *stream);
+
+/*
+ * Optional GPT-2 regex pre-tokenization (not the reference's
+ * semantics, which has none -- SPEC.md:93,95 -- so never the default).
+ * gpubpe_set_pretok: 2-bit classes (0 other, 1 \p{L}, 2 \p{N}, 3 \s) of
+ *   code points 0..n_cps-1, four per byte.
+ * gpubpe_set_mode: GPUBPE_MODE_DEFAULT or GPUBPE_MODE_GPT2_REGEX for the
+ *   following encodes of this context (gpubpe_encode / gpubpe_encode_host):
+ *   the tokens of tiktoken's GPT-2 pattern become additional cut points, so
+ *   the ids are tiktoken's GPT-2 encode_ordinary ids for valid UTF-8 text.
+ */
+int gpubpe_set_pretok(gpubpe_ctx *ctx, const uint8_t *classes, uint64_t n_cps);
+int gpubpe_set_mode(gpubpe_ctx *ctx, uint32_t mode);
 
 /* The junction bitmap of the context (65,536 bits as uint32[2048]; bit
  * (x << 8 | y) set iff some reachable rule joins a token ending in byte x to

@@ -23,6 +23,7 @@ LIB_PATH = Path(__file__).resolve().parent / os.environ.get("GPUBPE_LIB", "libgp
 
 OK, EINVAL, ECUDA, ENOMEM, ETABLE, ERANGE = 0, 1, 2, 3, 4, 5
 F_NO_MEMO, F_STRICT = 1, 2
+MODE_DEFAULT, MODE_GPT2_REGEX = 0, 1
 
 # (name, restype, argtypes) for every entry point of include/gpubpe.h
 _vp, _u32p, _u8p, _u64p = ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32), ctypes.c_void_p, ctypes.c_void_p
@@ -49,6 +50,8 @@ SIGNATURES = {
     "gpubpe_host_free": (None, [_vp]),
     "gpubpe_query": (_int, [_vp, _vp, ctypes.POINTER(Stats)]),
     "gpubpe_junction_bits": (_int, [_vp, _vp]),
+    "gpubpe_set_pretok": (_int, [_vp, _vp, _u64]),
+    "gpubpe_set_mode": (_int, [_vp, ctypes.c_uint32]),
     "gpubpe_set_vocab": (_int, [_vp, _vp, _vp, _vp, _u64]),
     "gpubpe_decode": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _u64, _vp, ctypes.POINTER(ctypes.c_uint64),
                              ctypes.POINTER(ctypes.c_uint64), _vp]),

@@ -153,14 +153,19 @@ def pack_texts(texts) -> tuple[np.ndarray, np.ndarray]:
 
 
 def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
-                   workers: int | None = None) -> BatchResult:
+                   workers: int | None = None, pretokenize: str | None = None) -> BatchResult:
     """Tokenize a batch of str (UTF-8 encoded) or bytes documents on the GPU.
 
     `workers` is accepted for signature compatibility; the device engine
-    parallelises internally.
+    parallelises internally.  pretokenize=None is the reference's semantics
+    (no pre-tokenization); pretokenize="gpt2" splits at tiktoken's GPT-2
+    regex first (ids equal tiktoken's GPT-2 encode_ordinary for valid UTF-8;
+    an optional mode, never the default).
     """
     if variant not in ENGINE_NAMES:
         raise ValueError(f"unknown engine {variant!r}, expected one of {ENGINE_NAMES}")
+    if pretokenize not in (None, "gpt2"):
+        raise ValueError(f"unknown pretokenize {pretokenize!r}, expected None or 'gpt2'")
     cfg = tokenizer.config
     t0 = time.perf_counter()
     data, offs = pack_texts(texts)
@@ -170,8 +175,11 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
         return BatchResult([], 0.0, encode_ms, 0.0, PassCounters())
     try:
         enc = tokenizer.device_encoder()
-        ids, out_offs, st, engine_ms = enc.encode_packed_host(data, offs, cfg.max_seq_len,
-                                                              cfg.chunk_budget)
+        from ._native import MODE_DEFAULT, MODE_GPT2_REGEX
+
+        ids, out_offs, st, engine_ms = enc.encode_packed_host(
+            data, offs, cfg.max_seq_len, cfg.chunk_budget,
+            MODE_GPT2_REGEX if pretokenize == "gpt2" else MODE_DEFAULT)
     except DeviceError:
         raise
     except TokenizerError as exc:  # pragma: no cover - the device reports no per-input errors

@@ -21,6 +21,7 @@
 #include "../../include/gpubpe.h"
 #include "kernels.cuh"
 #include "decode.cuh"
+#include "pretok.cuh"
 
 size_t tile_smem_bytes();
 cudaError_t launch_encode(const EncodeParams &P, int grid, cudaStream_t s, cudaEvent_t *ev,
@@ -56,6 +57,13 @@ struct gpubpe_ctx {
     uint8_t *d_vblob = nullptr;
     uint32_t n_vocab_dec = 0;
     DevBuf dec_state, dec_status;
+    // GPT-2 regex pre-tokenization (optional mode)
+    uint8_t *d_pt_classes = nullptr;
+    uint32_t pt_n_cps = 0;
+    uint8_t pt_ascii[128] = {};
+    uint32_t mode = 0;
+    DevBuf pt_bits;
+    const uint32_t *cur_pretok = nullptr;  // bits for the encode being launched
     unsigned int dec_epoch = 0;
     int dec_grid = 0;
     // workspace
@@ -500,6 +508,7 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.strict = (ctx->flags & GPUBPE_F_STRICT) ? 1 : 0;
         P.aligned = (reinterpret_cast<uintptr_t>(d_bytes) & 15) == 0;
         P.tile_bytes = wt;
+        P.pretok = ctx->cur_pretok;
         P.gscr = static_cast<unsigned long long *>(ctx->ws_gscr.p);
         P.glist = static_cast<uint32_t *>(ctx->ws_glist.p);
         ctx->last_n_tiles = n_tiles;
@@ -562,6 +571,26 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *
         return GPUBPE_OK;
     }
     if (!d_bytes || !d_out_ids) return fail(ctx, GPUBPE_EINVAL, "null data pointer");
+    const uint32_t *pt = nullptr;
+    if (ctx->mode == GPUBPE_MODE_GPT2_REGEX) {  // pre-token starts, then the same encode
+        const uint64_t n_words = (n_bytes + 31) / 32;
+        int rc2;
+        if ((rc2 = ensure(ctx, ctx->pt_bits, (n_words + 64) * 4, false))) return rc2;
+        PretokParams Q{};
+        Q.bytes = d_bytes;
+        Q.n_bytes = n_bytes;
+        Q.doc_offs = reinterpret_cast<const long long *>(d_doc_offs);
+        Q.n_docs = n_docs;
+        Q.classes = ctx->d_pt_classes;
+        Q.n_cps = ctx->pt_n_cps;
+        memcpy(Q.ascii, ctx->pt_ascii, 128);
+        Q.out = static_cast<uint32_t *>(ctx->pt_bits.p);
+        Q.n_words = n_words;
+        CK(cudaMemsetAsync(Q.out + n_words, 0, 64 * 4, s));  // halo words past the end
+        CK(launch_pretok(Q, s));
+        pt = Q.out;
+    }
+    ctx->cur_pretok = pt;
     bool checked;
     return encode_impl(ctx, d_bytes, n_bytes, d_doc_offs, n_docs, max_seq_len, chunk_budget,
                        d_out_ids, d_out_offs, s, &checked);
@@ -859,6 +888,28 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *
     return GPUBPE_OK;
 }
 
+extern "C" __attribute__((visibility("default"))) int gpubpe_set_pretok(gpubpe_ctx *ctx, const uint8_t *classes,
+                                                                          uint64_t n_cps) {
+    if (!ctx || !classes || n_cps < 128 || n_cps > 0x110000) return GPUBPE_EINVAL;
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->d_pt_classes) cudaFree(ctx->d_pt_classes);
+    ctx->d_pt_classes = nullptr;
+    const size_t nb = (n_cps + 3) / 4;
+    CK(cudaMalloc(&ctx->d_pt_classes, nb));
+    CK(cudaMemcpy(ctx->d_pt_classes, classes, nb, cudaMemcpyHostToDevice));
+    for (int c = 0; c < 128; ++c) ctx->pt_ascii[c] = (classes[c >> 2] >> (2 * (c & 3))) & 3;
+    ctx->pt_n_cps = (uint32_t)n_cps;
+    return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_set_mode(gpubpe_ctx *ctx, uint32_t mode) {
+    if (!ctx || mode > GPUBPE_MODE_GPT2_REGEX) return GPUBPE_EINVAL;
+    if (mode == GPUBPE_MODE_GPT2_REGEX && !ctx->d_pt_classes)
+        return fail(ctx, GPUBPE_EINVAL, "GPT-2 regex mode needs gpubpe_set_pretok first");
+    ctx->mode = mode;
+    return GPUBPE_OK;
+}
+
 extern "C" __attribute__((visibility("default"))) int gpubpe_junction_bits(gpubpe_ctx *ctx, uint32_t *h_out) {
     if (!ctx || !h_out) return GPUBPE_EINVAL;
     if (ctx->h_jbits.size() != 2048) return fail(ctx, GPUBPE_EINVAL, "context has no junction bitmap");
@@ -907,8 +958,9 @@ extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe
     if (ctx->pin) cudaFreeHost(ctx->pin);
     if (ctx->d_vinfo) cudaFree(ctx->d_vinfo);
     if (ctx->d_vblob) cudaFree(ctx->d_vblob);
-    for (DevBuf *b : {&ctx->dec_state, &ctx->dec_status})
+    for (DevBuf *b : {&ctx->dec_state, &ctx->dec_status, &ctx->pt_bits})
         if (b->p) cudaFree(b->p);
+    if (ctx->d_pt_classes) cudaFree(ctx->d_pt_classes);
     for (auto &e : ctx->io_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);

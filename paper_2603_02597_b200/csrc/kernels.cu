@@ -134,7 +134,13 @@ __device__ long long warp_doc_from(const long long *offs, long long lo, unsigned
     return lo;
 }
 
-// CTA: first p in [lo, hi) whose cut slot is a junction miss, else hi.
+// GPT-2 regex mode: a pre-token starts at byte p.
+__device__ __forceinline__ bool pretok_cut(const EncodeParams &P, long long p) {
+    return P.pretok && ((__ldg(&P.pretok[p >> 5]) >> (p & 31)) & 1u);
+}
+
+// CTA: first p in [lo, hi) whose cut slot is a junction miss (or a pre-token
+// start in GPT-2 regex mode), else hi.
 __device__ long long cta_first_nonjunction(const EncodeParams &P, const uint32_t *jb, long long lo,
                                            long long hi, EngineShared &sh) {
     for (long long b = lo; b < hi; b += 16 * NT) {
@@ -146,7 +152,7 @@ __device__ long long cta_first_nonjunction(const EncodeParams &P, const uint32_t
             for (long long p = p0; p < pe; ++p) {
                 const uint32_t y = __ldg(&P.bytes[p]);
                 const uint32_t idx = (x << 8) | y;
-                if (!((jb[idx >> 5] >> (idx & 31)) & 1u)) { k = (unsigned long long)p; break; }
+                if (!((jb[idx >> 5] >> (idx & 31)) & 1u) || pretok_cut(P, p)) { k = (unsigned long long)p; break; }
                 x = y;
             }
         }
@@ -361,6 +367,11 @@ __device__ __noinline__ void encode_tile(const EncodeParams &P, CtaSmem &C, Warp
         }
     }
     __syncwarp();
+    if (P.pretok) {  // GPT-2 regex mode: pre-token starts are cuts too
+        const int nwords = (nst + 31) >> 5;
+        if (lane < nwords) S.cm[lane] |= __ldg(&P.pretok[(a >> 5) + lane]);
+        __syncwarp();
+    }
     TSTAMP(1, S.cm[lane & 15]);
 
     // ---- 3. document starts and chunk cuts inside the staged bytes
@@ -1010,7 +1021,7 @@ __device__ long long warp_first_nonjunction(const EncodeParams &P, const uint32_
             for (long long p = p0; p < pe; ++p) {
                 const uint32_t y = __ldg(&P.bytes[p]);
                 const uint32_t idx = (x << 8) | y;
-                if (!((jb[idx >> 5] >> (idx & 31)) & 1u)) { k = p; break; }
+                if (!((jb[idx >> 5] >> (idx & 31)) & 1u) || pretok_cut(P, p)) { k = p; break; }
                 x = y;
             }
         }

@@ -113,6 +113,7 @@ struct EncodeParams {
     int tile_bytes;              // wt: 128, 256 or 512 (host picks by input size)
     unsigned long long *gscr;    // grid-engine scratch: [0..7] scalars, [8..8+2*grid) per-CTA
     uint32_t *glist;             // [rec_cap] giant record indices of the round (count in gscr[4])
+    const uint32_t *pretok;      // GPT-2 regex token-start bits (pretok.cu), null in the default mode
     unsigned long long *dbg;     // debug timestamps (GPUBPE_DEBUG & 8), else null
     int dbg_phase_a_only;        // GPUBPE_DEBUG & 16: profile phase A alone (output invalid)
 };

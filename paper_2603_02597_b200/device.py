@@ -281,8 +281,18 @@ class DeviceEncoder:
 
     # ------------------------------------------------------------ host API
 
+    def set_mode(self, mode: int) -> None:
+        """_native.MODE_DEFAULT or MODE_GPT2_REGEX (loads the class table on first use)."""
+        if mode == _native.MODE_GPT2_REGEX and not getattr(self, "_pretok", False):
+            from .pretok import N_CPS, gpt2_classes
+
+            cls = gpt2_classes()
+            _native.check(self._lib.gpubpe_set_pretok(self._h, _ptr(cls), N_CPS), self._h, "set_pretok")
+            self._pretok = True
+        _native.check(self._lib.gpubpe_set_mode(self._h, int(mode)), self._h, "set_mode")
+
     def encode_packed_host(self, data: np.ndarray, offs: np.ndarray, max_seq_len: int,
-                           chunk_budget: int):
+                           chunk_budget: int, mode: int = 0):
         """Host CSR in -> host CSR out through gpubpe_encode_host (pinned
         staging, H2D, encode, D2H in one native call).  Returns (ids
         uint32[], offs int64[], stats, engine_ms)."""
@@ -296,11 +306,17 @@ class DeviceEncoder:
         n_ids = ctypes.c_uint64(0)
         ms = ctypes.c_float(0.0)
         with self._lock, torch.cuda.device(self.device):
+            if mode != _native.MODE_DEFAULT:
+                self.set_mode(mode)
             s = torch.cuda.current_stream(self.device)
-            rc = self._lib.gpubpe_encode_host(self._h, _ptr(data), n, _ptr(offs), n_docs,
-                                              int(max_seq_len), int(chunk_budget), _ptr(ids),
-                                              _ptr(out_offs), ctypes.byref(n_ids), ctypes.byref(ms),
-                                              s.cuda_stream)
+            try:
+                    rc = self._lib.gpubpe_encode_host(self._h, _ptr(data), n, _ptr(offs), n_docs,
+                                                  int(max_seq_len), int(chunk_budget), _ptr(ids),
+                                                  _ptr(out_offs), ctypes.byref(n_ids), ctypes.byref(ms),
+                                                  s.cuda_stream)
+            finally:
+                if mode != _native.MODE_DEFAULT:
+                    self.set_mode(_native.MODE_DEFAULT)
             _native.check(rc, self._h, "gpubpe_encode_host")
             st = self.query(s)
         return _RESULTS.array(buf, np.uint32, n_ids.value), out_offs[: n_docs + 1], st, float(ms.value)

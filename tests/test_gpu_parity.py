@@ -279,3 +279,43 @@ def test_make_windows_token_mode_device_decode_matches_reference(tokenizer):
         spec = bpe.SweepSpec(lengths=tuple(case["lengths"]), samples_per_length=case["samples"])
         got = bpe.make_windows(corpus, fx["stream"], spec, tokenizer=tokenizer, seed=case["seed"])
         assert {str(k): [w.hex() for w in v] for k, v in got.items()} == case["windows"]
+
+
+# ---------------------------------------------------------------- GPT-2 regex mode
+
+
+@pytest.fixture(scope="module")
+def tiktoken_gpt2(gpt2_paths):
+    from oracle.tiktoken_gpt2 import build
+
+    return build(gpt2_paths[0])
+
+
+def test_regex_mode_matches_tiktoken(tokenizer, tiktoken_gpt2):
+    import random as _r
+
+    docs = [d for d in fixtures.prose_samples()]
+    docs += [s.encode() for s in ["hello world", "it's", "IT'S don't we'll you've they're I'd I'm",
+                                  "\n\nhello", "  x  ", "x \n y", "日本語のテキスト、です。", "naïve café ½ ²",
+                                  "e.g. U.S.A. 3.14159 $1,000,000!!!", "\t\ttabs\tand nbsp　x", "",
+                                  "a" * 3000, "1234567890" * 50, "\n" * 100 + "x"]]
+    rng = _r.Random(3)
+    alphabet = "ab's dmtlvre'  \n\t1.?!,é日😀"
+    docs += ["".join(rng.choice(alphabet) for _ in range(rng.randint(0, 200))).encode() for _ in range(300)]
+    tok = with_config(tokenizer, 1 << 40, 1 << 40)
+    got = bpe.tokenize_batch(docs, tok, pretokenize="gpt2").token_ids
+    for i, (d, g) in enumerate(zip(docs, got)):
+        assert g.tolist() == tiktoken_gpt2.encode_ordinary(d.decode("utf-8")), i
+    # the default mode is untouched afterwards
+    assert bpe.tokenize_batch([b"\n\nhello"], tokenizer).token_ids[0].tolist() == [628, 31373]
+
+
+def test_regex_mode_large_document(tokenizer, tiktoken_gpt2):
+    import synth_corpus
+
+    spec = fixtures.synth_sizes()["c3_1m"]
+    doc = synth_corpus.english_bytes(spec["n_bytes"], spec["seed"])
+    got = bpe.tokenize_batch([doc], with_config(tokenizer, 1 << 40, 1 << 40), pretokenize="gpt2").token_ids[0]
+    assert got.tolist() == tiktoken_gpt2.encode_ordinary(doc.decode("utf-8"))
+    with pytest.raises(ValueError):
+        bpe.tokenize_batch([doc], tokenizer, pretokenize="o200k")

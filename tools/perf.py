@@ -149,7 +149,11 @@ def main():
         rows.append(decode_row(name, enc, flush, peak, args))
     names = [n for n in names if not n.startswith("decode_")]
     for name in names:
-        data, offs, want = wl[name]()
+        rx = name.startswith("rx_")  # GPT-2 regex pre-tokenization mode (ids differ: no check)
+        enc.set_mode(1 if rx else 0)
+        data, offs, want = wl[name[3:] if rx else name]()
+        if rx:
+            want = None
         n = int(data.size)
         d_data = torch.from_numpy(data.copy()).to(dev)
         d_offs = torch.from_numpy(offs).to(dev)
