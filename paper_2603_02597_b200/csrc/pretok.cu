@@ -59,6 +59,63 @@ __global__ void __launch_bounds__(PT) k_pretok(const __grid_constant__ PretokPar
     }
     long long d = lo;
     uint32_t bits = 0;
+    // ---- fast path: one document covers [p0, p1 + 2] and the bytes of
+    //      [max(ds, p0 - 4), min(de, p1 + 2)) are ASCII -> code points = bytes
+    {
+        long long dd = d;
+        while (__ldg(&Q.doc_offs[dd + 1]) <= p0) ++dd;
+        const long long ds = __ldg(&Q.doc_offs[dd]), de = __ldg(&Q.doc_offs[dd + 1]);
+        if (de >= min(n, p1 + 2) || de == n) {
+            const long long wlo = max(ds, p0 - 4), whi = min(de, p1 + 2);
+            uint8_t wb[40];  // byte p0 - 4 + i, 0 when outside the document
+            bool ascii = true;
+#pragma unroll
+            for (int i = 0; i < 40; ++i) {
+                const long long p = p0 - 4 + i;
+                const uint8_t b = (p >= wlo && p < whi) ? __ldg(&Q.bytes[p]) : 0u;
+                ascii &= b < 0x80u;
+                wb[i] = b;
+            }
+            if (ascii) {
+                auto has = [&](int i) { const long long p = p0 - 4 + i; return p >= ds && p < de; };
+                auto cls = [&](int i) -> uint8_t { return Q.ascii[wb[i]]; };
+                auto tstart = [&](int i) -> bool {
+                    if (!has(i - 1)) return true;
+                    const uint8_t c = cls(i - 1);
+                    return c == C_L || c == C_N || (c == C_S && wb[i - 1] != ' ');
+                };
+                auto clen = [&](int i) -> int {
+                    if (!has(i) || wb[i] != '\'' || !tstart(i)) return 0;
+                    const uint8_t a = has(i + 1) ? wb[i + 1] : 0, b = has(i + 2) ? wb[i + 2] : 0;
+                    if (a == 's' || a == 'd' || a == 'm' || a == 't') return 2;
+                    if ((a == 'l' && b == 'l') || (a == 'v' && b == 'e') || (a == 'r' && b == 'e')) return 3;
+                    return 0;
+                };
+#pragma unroll 4
+                for (int k = 0; k < 32; ++k) {
+                    const int i = k + 4;
+                    if (p0 + k >= p1) break;
+                    bool b;
+                    if (!has(i - 1)) {
+                        b = true;
+                    } else if (cls(i) == C_S) {
+                        b = cls(i - 1) != C_S || (has(i + 1) && cls(i + 1) != C_S);
+                    } else if (cls(i - 1) == C_S) {
+                        b = wb[i - 1] != ' ';
+                    } else if (clen(i - 1) || clen(i - 2) == 3) {
+                        b = false;
+                    } else if (clen(i - 2) == 2 || clen(i - 3) == 3) {
+                        b = true;
+                    } else {
+                        b = cls(i) != cls(i - 1);
+                    }
+                    if (b) bits |= 1u << k;
+                }
+                Q.out[w] = bits;
+                return;
+            }
+        }
+    }
     uint8_t cl[WIN], ch[WIN];
     int16_t at[WIN];
     for (long long pos = p0; pos < p1;) {
