@@ -584,6 +584,12 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *
         Q.classes = ctx->d_pt_classes;
         Q.n_cps = ctx->pt_n_cps;
         memcpy(Q.ascii, ctx->pt_ascii, 128);
+        Q.ascii_std = 1;
+        for (int c = 0; c < 128; ++c) {
+            const uint8_t want = ((c | 32) >= 'a' && (c | 32) <= 'z') ? 1 : (c >= '0' && c <= '9') ? 2
+                                 : ((c >= 9 && c <= 13) || c == ' ') ? 3 : 0;
+            if (ctx->pt_ascii[c] != want) Q.ascii_std = 0;
+        }
         Q.out = static_cast<uint32_t *>(ctx->pt_bits.p);
         Q.n_words = n_words;
         CK(cudaMemsetAsync(Q.out + n_words, 0, 64 * 4, s));  // halo words past the end

@@ -25,6 +25,13 @@
 // 10xxxxxx starts one (invalid sequences become single "other" code points;
 // stray continuation bytes join the preceding one).  Document starts are
 // text starts.
+//
+// Common case (the word lies in one document and its 48-byte window
+// [32w - 8, 32w + 40) is ASCII there): code points are bytes, and the rules
+// are evaluated bit-parallel on 48-bit masks (bit j = byte 32w - 8 + j) built
+// with SWAR byte-range tests; the word's bytes arrive in two coalesced 16-B
+// loads and the context bytes from the neighbouring lanes by shuffle.
+// Otherwise a per-code-point scalar path decodes UTF-8 around the word.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -44,78 +51,217 @@ __device__ __forceinline__ uint8_t cp_class(const PretokParams &Q, uint32_t cp) 
     return (uint8_t)((__ldg(&Q.classes[cp >> 2]) >> (2 * (cp & 3))) & 3u);
 }
 
+constexpr unsigned long long K1 = 0x0101010101010101ull, K80 = 0x8080808080808080ull;
+
+// 0x80 in every byte of x whose value lies in [lo, hi] (values < 0x80; x7 = x & 0x7F.., hb = x & 0x80..)
+__device__ __forceinline__ unsigned long long in_range(unsigned long long x7, unsigned long long hb,
+                                                       unsigned lo, unsigned hi) {
+    const unsigned long long ge = x7 + (0x80ull - lo) * K1;  // bit 7 set iff v >= lo (no carry out of a byte)
+    const unsigned long long gt = x7 + (0x7Full - hi) * K1;  // bit 7 set iff v > hi
+    return ge & ~gt & ~hb & K80;
+}
+
+// bit k = bit 7 of byte k (m has only bits 7 of its bytes set)
+__device__ __forceinline__ unsigned movemask8(unsigned long long m) {
+    return (unsigned)(((m >> 7) * 0x0102040810204080ull) >> 56);
+}
+
+struct Masks {
+    unsigned long long L, N, S, SP, AP, NA;
+};
+
+__device__ __forceinline__ Masks build_masks(const unsigned long long (&win)[6]) {
+    Masks M{0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const unsigned long long x = win[k], hb = x & K80, x7 = x & ~K80;
+        const unsigned long long sp = in_range(x7, hb, ' ', ' ');
+        M.L |= (unsigned long long)movemask8(in_range(x7 | 0x20 * K1, hb, 'a', 'z')) << (8 * k);
+        M.N |= (unsigned long long)movemask8(in_range(x7, hb, '0', '9')) << (8 * k);
+        M.S |= (unsigned long long)movemask8(in_range(x7, hb, 9, 13) | sp) << (8 * k);
+        M.SP |= (unsigned long long)movemask8(sp) << (8 * k);
+        M.AP |= (unsigned long long)movemask8(in_range(x7, hb, '\'', '\'')) << (8 * k);
+        M.NA |= (unsigned long long)movemask8(hb) << (8 * k);
+    }
+    return M;
+}
+
+__device__ __forceinline__ unsigned long long eq_mask(const unsigned long long (&win)[6], unsigned c) {
+    unsigned long long m = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const unsigned long long x = win[k], hb = x & K80;
+        m |= (unsigned long long)movemask8(in_range(x & ~K80, hb, c, c)) << (8 * k);
+    }
+    return m;
+}
+
+// Token-start bits of the 32 positions j in [8, 40) of a window whose bytes
+// are ASCII on E (bit j: byte j exists in the word's document).
+__device__ __forceinline__ uint32_t rules_bitparallel(const unsigned long long (&win)[6], const Masks &M0,
+                                                      unsigned long long E) {
+    const unsigned long long L = M0.L & E, N = M0.N & E, S = M0.S & E, SP = M0.SP & E, AP = M0.AP & E;
+    unsigned long long C2 = 0, C3 = 0;  // contractions starting at j: 's 'd 'm 't / 'll 've 're
+    if (AP) {
+        // an apostrophe starts one iff it is at a token start: text start, or prev in L/N, or prev \s other than ' '
+        const unsigned long long TS = ~(E << 1) | ((L | N | (S & ~SP)) << 1);
+        const unsigned long long a = AP & TS;
+        const unsigned long long sdmt = (eq_mask(win, 's') | eq_mask(win, 'd') | eq_mask(win, 'm') |
+                                         eq_mask(win, 't')) & E;
+        const unsigned long long l = eq_mask(win, 'l') & E, e = eq_mask(win, 'e') & E;
+        const unsigned long long vr = (eq_mask(win, 'v') | eq_mask(win, 'r')) & E;
+        C2 = a & (sdmt >> 1);
+        C3 = a & (((l >> 1) & (l >> 2)) | ((vr >> 1) & (e >> 2)));
+    }
+    const unsigned long long C = C2 | C3;
+    const unsigned long long B =
+        ~(E << 1)                                                    // text start
+        | (S & (~(S << 1) | ((E & ~S) >> 1)))                        // whitespace run start / last char of a run
+        | (~S & (S << 1) & ~(SP << 1))                               // after \s other than ' '
+        | (~S & ~(S << 1) & ~((C << 1) | (C3 << 2)) &                // not inside a contraction:
+           ((C2 << 2) | (C3 << 3) | (L ^ (L << 1)) | (N ^ (N << 1))));  // after one, or a class change
+    return (uint32_t)((B & E) >> 8);
+}
+
+// SWAR forms on 4 bytes: 0x80 in each byte whose value is in [lo, hi]
+// (x7 = x & 0x7F.., nh = ~x & 0x80.., so bytes >= 0x80 never match)
+__device__ __forceinline__ uint32_t rng4(uint32_t x7, uint32_t nh, uint32_t lo, uint32_t hi) {
+    return (x7 + (0x80u - lo) * 0x01010101u) & ~(x7 + (0x7Fu - hi) * 0x01010101u) & nh;
+}
+__device__ __forceinline__ uint32_t movemask4(uint32_t m) { return (((m >> 7) * 0x00204081u) >> 21) & 0xFu; }
+
+// Token-start bits of the word when bytes [p0 - 4, p0 + 36) all lie in its
+// document, are ASCII and hold no apostrophe: the rules without the
+// contraction terms, evaluated on bytes in place (bit 7 of each byte) with
+// funnel shifts for the neighbouring positions; x[i] = bytes p0 - 4 + 4i.
+__device__ __forceinline__ uint32_t rules_swar(const uint32_t (&x)[10]) {
+    uint32_t L[10], N[10], S[10], SP[10];
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const uint32_t x7 = x[i] & 0x7F7F7F7Fu, nh = ~x[i] & 0x80808080u;
+        L[i] = rng4(x7 | 0x20202020u, nh, 'a', 'z');
+        N[i] = rng4(x7, nh, '0', '9');
+        SP[i] = rng4(x7, nh, ' ', ' ');
+        S[i] = rng4(x7, nh, 9, 13) | SP[i];
+    }
+    uint32_t bits = 0;
+#pragma unroll
+    for (int i = 1; i < 9; ++i) {
+        const uint32_t pS = __funnelshift_l(S[i - 1], S[i], 8), nS = __funnelshift_r(S[i], S[i + 1], 8);
+        const uint32_t pSP = __funnelshift_l(SP[i - 1], SP[i], 8);
+        const uint32_t pL = __funnelshift_l(L[i - 1], L[i], 8), pN = __funnelshift_l(N[i - 1], N[i], 8);
+        const uint32_t B = (S[i] & (~pS | ~nS)) | (~S[i] & pS & ~pSP) | (~S[i] & ~pS & ((L[i] ^ pL) | (N[i] ^ pN)));
+        bits |= movemask4(B & 0x80808080u) << (4 * (i - 1));
+    }
+    return bits;
+}
+
 }  // namespace
 
-__global__ void __launch_bounds__(PT) k_pretok(const __grid_constant__ PretokParams Q) {
+__global__ void __launch_bounds__(PT, 4) k_pretok(const __grid_constant__ PretokParams Q) {
+    __shared__ uint8_t sasc[128];
+    __shared__ long long sdoc[2];  // documents holding the CTA's first and last byte
+    if (threadIdx.x < 128) sasc[threadIdx.x] = Q.ascii[threadIdx.x];
+    if (threadIdx.x < 2) {
+        const long long nb = (long long)Q.n_bytes;
+        const long long q = min(nb - 1, ((long long)blockIdx.x * PT + (threadIdx.x ? PT - 1 : 0)) * 32 +
+                                            (threadIdx.x ? 31 : 0));
+        long long lo = 0, hi = (long long)Q.n_docs - 1;
+        while (lo < hi) {  // last d with offs[d] <= q
+            const long long mid = (lo + hi + 1) >> 1;
+            if (__ldg(&Q.doc_offs[mid]) <= q) lo = mid; else hi = mid - 1;
+        }
+        sdoc[threadIdx.x] = lo;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
     const unsigned long long w = (unsigned long long)blockIdx.x * PT + threadIdx.x;
-    if (w >= Q.n_words) return;
     const long long n = (long long)Q.n_bytes;
     const long long p0 = (long long)w * 32, p1 = min(p0 + 32, n);
-    // the document holding byte p0 (last d with offs[d] <= p0)
-    long long lo = 0, hi = (long long)Q.n_docs - 1;
+    const bool active = w < Q.n_words;
+    // ---- the 48-byte window [p0 - 8, p0 + 40), 0 outside [0, n)
+    unsigned long long win[6];
+    const bool aligned = ((reinterpret_cast<uintptr_t>(Q.bytes) & 15) == 0);
+    if (active && aligned && p0 + 32 <= n) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(Q.bytes + p0);
+        const uint4 u = __ldg(src), v = __ldg(src + 1);
+        win[1] = ((unsigned long long)u.y << 32) | u.x;
+        win[2] = ((unsigned long long)u.w << 32) | u.z;
+        win[3] = ((unsigned long long)v.y << 32) | v.x;
+        win[4] = ((unsigned long long)v.w << 32) | v.z;
+    } else {
+#pragma unroll
+        for (int k = 1; k < 5; ++k) {
+            unsigned long long x = 0;
+            for (int b = 7; b >= 0; --b) {
+                const long long p = p0 + 8 * (k - 1) + b;
+                x = (x << 8) | ((active && p < n) ? __ldg(&Q.bytes[p]) : 0u);
+            }
+            win[k] = x;
+        }
+    }
+    win[0] = __shfl_up_sync(FULL_MASK, win[4], 1);
+    win[5] = __shfl_down_sync(FULL_MASK, win[1], 1);
+    if (lane == 0 || lane == 31) {
+        const int k = lane == 0 ? 0 : 5;
+        const long long q = lane == 0 ? p0 - 8 : p0 + 32;
+        unsigned long long x = 0;
+        if (aligned && q >= 0 && q + 8 <= n) {
+            x = __ldg(reinterpret_cast<const unsigned long long *>(Q.bytes + q));
+        } else {
+            for (int b = 7; b >= 0; --b) {
+                const long long p = q + b;
+                x = (x << 8) | ((active && p >= 0 && p < n) ? __ldg(&Q.bytes[p]) : 0u);
+            }
+        }
+        win[k] = x;
+    }
+    if (!active) return;
+    // the document holding byte p0 (last d with offs[d] <= p0; empty documents skipped)
+    long long lo = sdoc[0], hi = sdoc[1];
     while (lo < hi) {
         const long long mid = (lo + hi + 1) >> 1;
         if (__ldg(&Q.doc_offs[mid]) <= p0) lo = mid; else hi = mid - 1;
     }
     long long d = lo;
-    uint32_t bits = 0;
-    // ---- fast path: one document covers [p0, p1 + 2] and the bytes of
-    //      [max(ds, p0 - 4), min(de, p1 + 2)) are ASCII -> code points = bytes
-    {
-        long long dd = d;
-        while (__ldg(&Q.doc_offs[dd + 1]) <= p0) ++dd;
-        const long long ds = __ldg(&Q.doc_offs[dd]), de = __ldg(&Q.doc_offs[dd + 1]);
-        if (de >= min(n, p1 + 2) || de == n) {
-            const long long wlo = max(ds, p0 - 4), whi = min(de, p1 + 2);
-            uint8_t wb[40];  // byte p0 - 4 + i, 0 when outside the document
-            bool ascii = true;
+    while (__ldg(&Q.doc_offs[d + 1]) <= p0) ++d;
+    if (Q.ascii_std) {
+        const long long ds = __ldg(&Q.doc_offs[d]), de = __ldg(&Q.doc_offs[d + 1]);
+        if (ds <= p0 - 4 && de >= p0 + 36) {
+            uint32_t x[10], hb = 0, ap = 0;
 #pragma unroll
-            for (int i = 0; i < 40; ++i) {
-                const long long p = p0 - 4 + i;
-                const uint8_t b = (p >= wlo && p < whi) ? __ldg(&Q.bytes[p]) : 0u;
-                ascii &= b < 0x80u;
-                wb[i] = b;
+            for (int i = 0; i < 10; ++i) {
+                const int b = 4 + 4 * i;  // byte offset in the 48-byte window
+                x[i] = (uint32_t)(win[b >> 3] >> (8 * (b & 7)));
+                hb |= x[i];
+                ap |= rng4(x[i] & 0x7F7F7F7Fu, ~x[i] & 0x80808080u, '\'', '\'');
             }
-            if (ascii) {
-                auto has = [&](int i) { const long long p = p0 - 4 + i; return p >= ds && p < de; };
-                auto cls = [&](int i) -> uint8_t { return Q.ascii[wb[i]]; };
-                auto tstart = [&](int i) -> bool {
-                    if (!has(i - 1)) return true;
-                    const uint8_t c = cls(i - 1);
-                    return c == C_L || c == C_N || (c == C_S && wb[i - 1] != ' ');
-                };
-                auto clen = [&](int i) -> int {
-                    if (!has(i) || wb[i] != '\'' || !tstart(i)) return 0;
-                    const uint8_t a = has(i + 1) ? wb[i + 1] : 0, b = has(i + 2) ? wb[i + 2] : 0;
-                    if (a == 's' || a == 'd' || a == 'm' || a == 't') return 2;
-                    if ((a == 'l' && b == 'l') || (a == 'v' && b == 'e') || (a == 'r' && b == 'e')) return 3;
-                    return 0;
-                };
-#pragma unroll 4
-                for (int k = 0; k < 32; ++k) {
-                    const int i = k + 4;
-                    if (p0 + k >= p1) break;
-                    bool b;
-                    if (!has(i - 1)) {
-                        b = true;
-                    } else if (cls(i) == C_S) {
-                        b = cls(i - 1) != C_S || (has(i + 1) && cls(i + 1) != C_S);
-                    } else if (cls(i - 1) == C_S) {
-                        b = wb[i - 1] != ' ';
-                    } else if (clen(i - 1) || clen(i - 2) == 3) {
-                        b = false;
-                    } else if (clen(i - 2) == 2 || clen(i - 3) == 3) {
-                        b = true;
-                    } else {
-                        b = cls(i) != cls(i - 1);
-                    }
-                    if (b) bits |= 1u << k;
-                }
-                Q.out[w] = bits;
+            if (((hb & 0x80808080u) | ap) == 0) {
+                Q.out[w] = rules_swar(x);
                 return;
             }
         }
+        // every document meeting [p0, p1) in turn, on the bit-parallel masks restricted to it
+        const Masks M = build_masks(win);
+        uint32_t bits = 0;
+        bool ok = true;
+        for (long long dd = d;; ++dd) {
+            const long long s0 = __ldg(&Q.doc_offs[dd]), s1 = __ldg(&Q.doc_offs[dd + 1]);
+            if (s0 >= p1) break;
+            const long long jlo = max(0ll, s0 - (p0 - 8)), jhi = min(48ll, s1 - (p0 - 8));
+            if (jhi > jlo) {
+                const unsigned long long E = ((1ull << jhi) - 1) & ~((1ull << jlo) - 1);
+                if (M.NA & E) { ok = false; break; }
+                bits |= rules_bitparallel(win, M, E);
+            }
+            if (s1 >= p1) break;
+        }
+        if (ok) {
+            Q.out[w] = bits;
+            return;
+        }
     }
+    uint32_t bits = 0;
     uint8_t cl[WIN], ch[WIN];
     int16_t at[WIN];
     for (long long pos = p0; pos < p1;) {
@@ -133,7 +279,7 @@ __global__ void __launch_bounds__(PT) k_pretok(const __grid_constant__ PretokPar
             while (j < de && (__ldg(&Q.bytes[j]) & 0xC0u) == 0x80u) ++j;  // continuation bytes join
             uint8_t c = C_O, a = 0;
             if (b0 < 0x80u) {
-                c = Q.ascii[b0];
+                c = sasc[b0];
                 a = (uint8_t)b0;
             } else {
                 const int need = b0 >= 0xF0u ? 3 : b0 >= 0xE0u ? 2 : b0 >= 0xC0u ? 1 : -1;

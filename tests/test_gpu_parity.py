@@ -302,6 +302,15 @@ def test_regex_mode_matches_tiktoken(tokenizer, tiktoken_gpt2):
     rng = _r.Random(3)
     alphabet = "ab's dmtlvre'  \n\t1.?!,é日😀"
     docs += ["".join(rng.choice(alphabet) for _ in range(rng.randint(0, 200))).encode() for _ in range(300)]
+    # long ASCII documents: the bit-parallel paths of k_pretok (with and without apostrophes,
+    # every ASCII whitespace, controls and the class edges @ [ ` { / : 0x1c-0x1f 0x7f)
+    ascii_alpha = ["abZ zy  \n\t\r\x0b\x0c1909.?!,_@[`{/:\x1c\x1f\x7f", "ab's dmtlvre'  \n1."]
+    for k in range(120):
+        a = ascii_alpha[k % 2]
+        docs.append("".join(rng.choice(a) for _ in range(rng.randint(0, 3000))).encode())
+    for k in range(400):  # short ASCII documents: several per 32-byte word
+        a = ascii_alpha[k % 2]
+        docs.append("".join(rng.choice(a) for _ in range(rng.randint(0, 40))).encode())
     tok = with_config(tokenizer, 1 << 40, 1 << 40)
     got = bpe.tokenize_batch(docs, tok, pretokenize="gpt2").token_ids
     for i, (d, g) in enumerate(zip(docs, got)):
