@@ -27,10 +27,18 @@ from .merge_table import (
 
 __version__ = "0.1.0"
 
+
+def pinned_empty(nbytes: int, device: int = 0):
+    """uint8[nbytes] in pinned, device-mapped host memory; batches packed here
+    reach the GPU by DMA without a staging copy (see device.pinned_empty)."""
+    from .device import pinned_empty as _pinned_empty
+
+    return _pinned_empty(nbytes, device)
+
 __all__ = [
     "BatchResult", "BlockConfig", "DEFAULT_LENGTHS", "SweepSpec", "make_windows", "ByteEncoder", "Chunk", "ENGINE_NAMES", "MergeRule",
     "PackedPairTable", "PassCounters", "Tokenizer", "TokenizerHandle", "Vocab", "base_id_table",
     "build_byte_encoder", "build_table", "chunk_tokens", "decode_tokens", "encode_bytes", "errors",
-    "pack_key", "pack_texts", "pack_value", "parse_merges", "rule_arrays", "tokenize_batch",
+    "pack_key", "pack_texts", "pack_value", "pinned_empty", "parse_merges", "rule_arrays", "tokenize_batch",
     "unpack_value", "__version__",
 ]

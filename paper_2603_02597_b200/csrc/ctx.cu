@@ -75,6 +75,19 @@ struct gpubpe_ctx {
     size_t pin_bytes = 0;
     bool state_fresh = false;  // h_state already holds the last encode's state
     cudaEvent_t io_ev[2] = {nullptr, nullptr};
+    // streamed host encode (gpubpe_encode_host on large batches): two slots of
+    // pinned staging, device input and mapped pinned output; H2D on s_copy
+    struct StreamSlot {
+        uint8_t *pin_in = nullptr;
+        size_t pin_in_bytes = 0;
+        uint8_t *pin_out = nullptr, *pin_out_dev = nullptr;
+        size_t pin_out_bytes = 0;
+        DevBuf dev_in, dev_out;
+        cudaEvent_t ev_h2d = nullptr, ev_done = nullptr, ev_d2h = nullptr;
+    } ss[2];
+    cudaStream_t s_copy = nullptr, s_d2h = nullptr;
+    bool defer_check = false;  // the caller checks EncodeState.overflow itself (streamed encode)
+    EncodeState *h_state_ss = nullptr;  // pinned [2]: per-slot encode state
     uint64_t last_n_tiles = 0;
     unsigned int epoch = 0;
     uint64_t calls = 0;  // selects the EncodeState slot (two, alternating)
@@ -535,7 +548,7 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
             FILE *f = fopen(getenv("GPUBPE_DEBUG_OUT"), "wb");
             if (f) { fwrite(h.data(), 8, h.size(), f); fclose(f); }
         }
-        if (def_max <= rec_cap && arena_need <= ctx->ws_arena.bytes) return GPUBPE_OK;
+        if (ctx->defer_check || (def_max <= rec_cap && arena_need <= ctx->ws_arena.bytes)) return GPUBPE_OK;
         *checked = true;
         CK(cudaMemcpyAsync(ctx->h_state, P.st, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -634,6 +647,215 @@ static int ensure_pinned(gpubpe_ctx *ctx, size_t bytes) {
     return GPUBPE_OK;
 }
 
+static int ensure_host(gpubpe_ctx *ctx, uint8_t **p, uint8_t **p_dev, size_t *have, size_t bytes) {
+    if (*have >= bytes && *p) return GPUBPE_OK;
+    if (*p) CK(cudaFreeHost(*p));
+    *p = nullptr;
+    *have = 0;
+    const size_t nb = std::max<size_t>(bytes + bytes / 8, 1 << 20);
+    CK(cudaHostAlloc(reinterpret_cast<void **>(p), nb, p_dev ? cudaHostAllocMapped : 0));
+    if (p_dev) {
+        void *dev = nullptr;
+        CK(cudaHostGetDevicePointer(&dev, *p, 0));
+        *p_dev = static_cast<uint8_t *>(dev);
+    }
+    *have = nb;
+    return GPUBPE_OK;
+}
+
+// Device alias of a pinned, device-mapped host pointer (gpubpe_host_alloc), else null.
+static void *mapped_alias(const void *h) {
+    cudaPointerAttributes pa{};
+    void *d = nullptr;
+    if (h && cudaPointerGetAttributes(&pa, h) == cudaSuccess && pa.type == cudaMemoryTypeHost)
+        d = pa.devicePointer;
+    cudaGetLastError();
+    return d;
+}
+
+// gpubpe_encode_host for a large batch: parts of about `part_bytes` (whole
+// documents; a larger document is a part of its own) run through a two-slot
+// pipeline on three streams -- H2D of part i (s_copy), encode of part i-1
+// (the caller's stream) and D2H of part i-2's ids (s_d2h) overlap; the encodes
+// are enqueued back to back.  Documents are independent (chunker.py:139-179),
+// so the parts' results concatenate.
+//   input:  pinned caller bytes (gpubpe_host_alloc) are copied to the device
+//           directly; pageable ones are staged through the slot's pinned buffer;
+//   output: ids are DMA'd to a pinned caller buffer at their final position
+//           (known once the previous part's id count is: the host reads each
+//           part's offsets from mapped memory when it completes); a pageable
+//           caller buffer receives them through the slot's pinned buffer.
+// Overflow of the deferred-segment buffers is checked per part (drain) and
+// the part re-encoded synchronously after growing them.
+static int encode_host_streamed(gpubpe_ctx *ctx, const uint8_t *h_bytes, const int64_t *h_doc_offs,
+                                uint64_t n_docs, uint64_t max_seq_len, uint64_t chunk_budget,
+                                uint32_t *h_out_ids, int64_t *h_out_offs, uint64_t *n_ids_out,
+                                float *kernel_ms, void *stream, uint64_t part_bytes) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!ctx->s_copy) CK(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
+    if (!ctx->s_d2h) CK(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
+    if (!ctx->h_state_ss) CK(cudaHostAlloc(reinterpret_cast<void **>(&ctx->h_state_ss), 2 * sizeof(EncodeState), 0));
+    for (auto &S : ctx->ss) {
+        if (!S.ev_h2d) CK(cudaEventCreate(&S.ev_h2d));
+        if (!S.ev_done) CK(cudaEventCreate(&S.ev_done));
+        if (!S.ev_d2h) CK(cudaEventCreate(&S.ev_d2h));
+    }
+    const bool in_pinned = mapped_alias(h_bytes) != nullptr;
+    const bool out_pinned = mapped_alias(h_out_ids) != nullptr;
+    std::vector<std::pair<uint64_t, uint64_t>> parts;  // document ranges
+    for (uint64_t d = 0; d < n_docs;) {
+        uint64_t e = d + 1;
+        while (e < n_docs && (uint64_t)(h_doc_offs[e + 1] - h_doc_offs[d]) <= part_bytes) ++e;
+        parts.emplace_back(d, e);
+        d = e;
+    }
+    const size_t P = parts.size();
+    auto nb_of = [&](size_t i) { return (uint64_t)(h_doc_offs[parts[i].second] - h_doc_offs[parts[i].first]); };
+    auto nd_of = [&](size_t i) { return parts[i].second - parts[i].first; };
+    auto ids_off = [](uint64_t nd) { return ((nd + 1) * 8 + 255) & ~(size_t)255; };
+    std::vector<uint64_t> base_of(P, 0), cnt_of(P, 0);
+    EncodeState agg{};
+    uint64_t base = 0, tiles = 0;
+    const bool htime = getenv("GPUBPE_HOSTTIME") != nullptr;
+    double t_wait = 0, t_out = 0, t_in = 0, t_enq = 0;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
+    const auto t_start = now();
+    auto encode_part = [&](size_t i) -> int {  // enqueue the encode of part i on s
+        auto &S = ctx->ss[i & 1];
+        const uint64_t nd = nd_of(i), nb = nb_of(i);
+        uint8_t *din = static_cast<uint8_t *>(S.dev_in.p);
+        const size_t o_offs = (nb + 255) & ~(size_t)255;
+        int rc2 = gpubpe_encode(ctx, din, nb, reinterpret_cast<const int64_t *>(din + o_offs), nd, max_seq_len,
+                                chunk_budget, static_cast<uint32_t *>(S.dev_out.p),
+                                reinterpret_cast<int64_t *>(S.pin_out_dev), stream);
+        if (rc2) return rc2;
+        tiles += nb ? ctx->last_n_tiles : 0;
+        const EncodeState *last = static_cast<const EncodeState *>(ctx->ws_state.p) + ((ctx->calls - 1) & 1);
+        CK(cudaMemcpyAsync(&ctx->h_state_ss[i & 1], last, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(S.ev_done, s));
+        return GPUBPE_OK;
+    };
+    auto drain = [&](size_t i) -> int {  // part i encoded: offsets, counters, enqueue the D2H of its ids
+        auto &S = ctx->ss[i & 1];
+        auto t0 = now();
+        CK(cudaEventSynchronize(S.ev_done));
+        t_wait += us(t0, now());
+        const uint64_t d = parts[i].first, nd = nd_of(i), nb = nb_of(i);
+        if (nb && ctx->h_state_ss[i & 1].overflow) {
+            // deferred-segment buffers overflowed: grow them, redo this part with the
+            // synchronous check (its input is still in its slot)
+            const EncodeState &o = ctx->h_state_ss[i & 1];
+            int rc2;
+            ctx->defer_check = false;
+            tiles -= ctx->last_n_tiles;
+            if ((rc2 = ensure(ctx, ctx->ws_recs, o.n_def * sizeof(DefRec), false)) ||
+                (rc2 = ensure(ctx, ctx->ws_arena, o.arena_used * 4, false)) || (rc2 = encode_part(i))) {
+                ctx->defer_check = true;
+                return rc2;
+            }
+            ctx->defer_check = true;
+            CK(cudaStreamSynchronize(s));
+        }
+        const int64_t *lo = reinterpret_cast<const int64_t *>(S.pin_out);
+        const uint64_t cnt = nb ? (uint64_t)lo[nd] : 0;
+        if (cnt > nb)
+            return fail(ctx, GPUBPE_ECUDA, "device produced %llu ids for %llu bytes", (unsigned long long)cnt,
+                        (unsigned long long)nb);
+        for (uint64_t j = 0; j <= nd; ++j) h_out_offs[d + j] = (int64_t)base + (nb ? lo[j] : 0);
+        if (cnt) {
+            void *to = out_pinned ? static_cast<void *>(h_out_ids + base) : static_cast<void *>(S.pin_out + ids_off(nd));
+            CK(cudaMemcpyAsync(to, S.dev_out.p, cnt * 4, cudaMemcpyDeviceToHost, ctx->s_d2h));
+        }
+        CK(cudaEventRecord(S.ev_d2h, ctx->s_d2h));
+        const EncodeState &st = ctx->h_state_ss[i & 1];
+        if (nb) {
+            agg.overflow |= st.overflow;
+            agg.c.n_segments += st.c.n_segments;
+            agg.c.memo_hits += st.c.memo_hits;
+            agg.c.short_merges += st.c.short_merges;
+            agg.c.medium_segments += st.c.medium_segments;
+            agg.c.giant_segments += st.c.giant_segments;
+            agg.c.giant_bytes += st.c.giant_bytes;
+            agg.c.engine_passes += st.c.engine_passes;
+        }
+        base_of[i] = base;
+        cnt_of[i] = cnt;
+        base += cnt;
+        return GPUBPE_OK;
+    };
+    auto complete = [&](size_t i) -> int {  // part i's ids are in the caller's buffer afterwards
+        auto &S = ctx->ss[i & 1];
+        auto t0 = now();
+        CK(cudaEventSynchronize(S.ev_d2h));
+        auto t1 = now();
+        t_wait += us(t0, t1);
+        if (!out_pinned && cnt_of[i]) copy_par(h_out_ids + base_of[i], S.pin_out + ids_off(nd_of(i)), cnt_of[i] * 4);
+        t_out += us(t1, now());
+        return GPUBPE_OK;
+    };
+    struct DeferGuard {  // overflow is checked per part in drain(), not per launch
+        gpubpe_ctx *c;
+        explicit DeferGuard(gpubpe_ctx *c_) : c(c_) { c->defer_check = true; }
+        ~DeferGuard() { c->defer_check = false; }
+    } guard(ctx);
+    int rc;
+    for (size_t i = 0; i < P; ++i) {
+        auto &S = ctx->ss[i & 1];
+        // slot i & 1 is free again once part i-2's ids left it (device side: the stream
+        // wait below; a staged output also needs its host copy-out first)
+        if (i >= 2 && !out_pinned && (rc = complete(i - 2))) return rc;
+        const uint64_t d = parts[i].first, nd = nd_of(i), lo = (uint64_t)h_doc_offs[d], nb = nb_of(i);
+        const size_t o_offs = (nb + 255) & ~(size_t)255, need_in = o_offs + (nd + 1) * 8;
+        const size_t need_out = ids_off(nd) + (out_pinned ? 0 : std::max<uint64_t>(nb, 1) * 4);
+        if ((rc = ensure_host(ctx, &S.pin_in, nullptr, &S.pin_in_bytes, in_pinned ? (nd + 1) * 8 : need_in)))
+            return rc;
+        if ((rc = ensure_host(ctx, &S.pin_out, &S.pin_out_dev, &S.pin_out_bytes, need_out))) return rc;
+        if ((rc = ensure(ctx, S.dev_in, need_in, false))) return rc;
+        if ((rc = ensure(ctx, S.dev_out, std::max<uint64_t>(nb, 1) * 4, false))) return rc;
+        auto t0 = now();
+        uint8_t *din = static_cast<uint8_t *>(S.dev_in.p);
+        int64_t *po = reinterpret_cast<int64_t *>(in_pinned ? S.pin_in : S.pin_in + o_offs);
+        for (uint64_t j = 0; j <= nd; ++j) po[j] = h_doc_offs[d + j] - (int64_t)lo;
+        if (in_pinned) {
+            if (nb) CK(cudaMemcpyAsync(din, h_bytes + lo, nb, cudaMemcpyHostToDevice, ctx->s_copy));
+            CK(cudaMemcpyAsync(din + o_offs, po, (nd + 1) * 8, cudaMemcpyHostToDevice, ctx->s_copy));
+        } else {
+            copy_par(S.pin_in, h_bytes + lo, nb);
+            CK(cudaMemcpyAsync(din, S.pin_in, need_in, cudaMemcpyHostToDevice, ctx->s_copy));
+        }
+        CK(cudaEventRecord(S.ev_h2d, ctx->s_copy));
+        CK(cudaStreamWaitEvent(s, S.ev_h2d, 0));
+        if (i >= 2) CK(cudaStreamWaitEvent(s, S.ev_d2h, 0));  // the slot's device ids went out
+        auto t1 = now();
+        t_in += us(t0, t1);
+        if ((rc = encode_part(i))) return rc;
+        t_enq += us(t1, now());
+        if (i >= 1 && (rc = drain(i - 1))) return rc;
+    }
+    if (P && (rc = drain(P - 1))) return rc;
+    if (out_pinned) {
+        auto t0 = now();
+        CK(cudaStreamSynchronize(ctx->s_d2h));
+        t_wait += us(t0, now());
+    } else {
+        for (size_t i = P >= 2 ? P - 2 : 0; i < P; ++i)
+            if ((rc = complete(i))) return rc;
+    }
+    if (htime)
+        fprintf(stderr, "encode_host streamed: %zu parts (input %s, output %s), total %.0f us: stage+h2d %.0f | "
+                "enqueue %.0f | wait %.0f | copy-out %.0f\n", P, in_pinned ? "pinned" : "staged",
+                out_pinned ? "pinned" : "staged", us(t_start, now()), t_in, t_enq, t_wait, t_out);
+    if (kernel_ms && P) CK(cudaEventElapsedTime(kernel_ms, ctx->ss[0].ev_h2d, ctx->ss[(P - 1) & 1].ev_d2h));
+    agg.n_ids = base;
+    *ctx->h_state = agg;
+    ctx->state_fresh = true;
+    ctx->last_n_bytes = (uint64_t)(h_doc_offs[n_docs] - h_doc_offs[0]);
+    ctx->last_n_tiles = tiles;
+    *n_ids_out = base;
+    return GPUBPE_OK;
+}
+
 extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     gpubpe_ctx *ctx, const uint8_t *h_bytes, uint64_t n_bytes, const int64_t *h_doc_offs, uint64_t n_docs,
     uint64_t max_seq_len, uint64_t chunk_budget, uint32_t *h_out_ids, int64_t *h_out_offs,
@@ -646,6 +868,14 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     *n_ids_out = 0;
     if (kernel_ms) *kernel_ms = 0.f;
     if (n_docs == 0) return GPUBPE_OK;
+    {  // large batches stream through a two-slot pipeline (GPUBPE_STREAM_MB: part size, 0 = never)
+        const char *env = getenv("GPUBPE_STREAM_MB");
+        const long long part_mb = env ? atoll(env) : 32;
+        const uint64_t part = (uint64_t)std::max(part_mb, 0ll) << 20;
+        if (part && n_bytes > 2 * part && n_docs > 1)
+            return encode_host_streamed(ctx, h_bytes, h_doc_offs, n_docs, max_seq_len, chunk_budget, h_out_ids,
+                                        h_out_offs, n_ids_out, kernel_ms, stream, part);
+    }
     static const bool htime = getenv("GPUBPE_HOSTTIME") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto t_a = now();
@@ -673,6 +903,10 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     } else if (mode == 2) {  // pageable copies straight from the caller's buffers
         CK(cudaMemcpyAsync(dv + o_doffs, h_doc_offs, offs_b, cudaMemcpyHostToDevice, s));
         if (n_bytes) CK(cudaMemcpyAsync(dv + o_in, h_bytes, n_bytes, cudaMemcpyHostToDevice, s));
+    } else if (n_bytes && mapped_alias(h_bytes)) {  // caller bytes already pinned: no staging copy
+        memcpy(pin + o_doffs, h_doc_offs, offs_b);
+        CK(cudaMemcpyAsync(dv + o_in, h_bytes, n_bytes, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dv + o_doffs, pin + o_doffs, offs_b, cudaMemcpyHostToDevice, s));
     } else {  // pinned staging in 4 MiB pieces; staging of piece k+1 overlaps the DMA of piece k;
               // the doc offsets ride with the last piece (they follow the bytes in the layout)
         memcpy(pin + o_doffs, h_doc_offs, offs_b);
@@ -691,14 +925,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     if (mode == 3) dout = ctx->pin_dev;  // outputs straight into mapped pinned memory (stores overlap the kernel)
     // A caller buffer that is itself pinned and device-mapped (gpubpe_host_alloc)
     // receives the ids directly: no copy-out at all.
-    uint32_t *d_ids_direct = nullptr;
-    if (mode == 3 && n_bytes) {
-        cudaPointerAttributes pa{};
-        if (cudaPointerGetAttributes(&pa, h_out_ids) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-            pa.devicePointer)
-            d_ids_direct = static_cast<uint32_t *>(pa.devicePointer);
-        cudaGetLastError();
-    }
+    uint32_t *d_ids_direct = (mode == 3 && n_bytes) ? static_cast<uint32_t *>(mapped_alias(h_out_ids)) : nullptr;
     rc = gpubpe_encode(ctx, dv + o_in, n_bytes, reinterpret_cast<const int64_t *>(dv + o_doffs), n_docs,
                        max_seq_len, chunk_budget,
                        d_ids_direct ? d_ids_direct : reinterpret_cast<uint32_t *>(dout + o_ids),
@@ -962,6 +1189,17 @@ extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe
                       &ctx->ws_arena, &ctx->io_dev, &ctx->ws_gscr, &ctx->ws_glist})
         if (b->p) cudaFree(b->p);
     if (ctx->pin) cudaFreeHost(ctx->pin);
+    for (auto &S : ctx->ss) {
+        if (S.pin_in) cudaFreeHost(S.pin_in);
+        if (S.pin_out) cudaFreeHost(S.pin_out);
+        if (S.dev_in.p) cudaFree(S.dev_in.p);
+        if (S.dev_out.p) cudaFree(S.dev_out.p);
+        for (cudaEvent_t e : {S.ev_h2d, S.ev_done, S.ev_d2h})
+            if (e) cudaEventDestroy(e);
+    }
+    if (ctx->s_copy) cudaStreamDestroy(ctx->s_copy);
+    if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
+    if (ctx->h_state_ss) cudaFreeHost(ctx->h_state_ss);
     if (ctx->d_vinfo) cudaFree(ctx->d_vinfo);
     if (ctx->d_vblob) cudaFree(ctx->d_vblob);
     for (DevBuf *b : {&ctx->dec_state, &ctx->dec_status, &ctx->pt_bits})

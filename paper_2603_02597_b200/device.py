@@ -87,10 +87,21 @@ class _HostPool:
             return np.frombuffer(raw, dtype=np.uint8)
         return np.zeros(cls, dtype=np.uint8)  # pinned memory exhausted: the encode copies out
 
-    def put(self, buf: np.ndarray) -> None:
+    def take_pageable(self, nbytes: int) -> np.ndarray:
+        """A plain host buffer (for results too large to pin), recycled like the
+        pinned ones so its pages are faulted in once, not on every call."""
+        cls = 1 << max(20, int(nbytes - 1).bit_length())
         with self._lock:
-            lst = self._free.setdefault(buf.size, [])
-            if len(lst) < self._keep:
+            lst = self._free.get(-cls)
+            if lst:
+                return lst.pop()
+        return np.empty(cls, dtype=np.uint8)
+
+    def put(self, buf: np.ndarray) -> None:
+        key = buf.size if buf.size <= _POOLED_MAX else -buf.size
+        with self._lock:
+            lst = self._free.setdefault(key, [])
+            if len(lst) < (self._keep if 0 < key <= (256 << 20) else 1):
                 lst.append(buf)
 
     def array(self, buf: np.ndarray, dtype, count: int) -> np.ndarray:
@@ -98,6 +109,22 @@ class _HostPool:
 
 
 _RESULTS = _HostPool()
+_POOLED_MAX = 8 << 30  # result buffers above this are plain host arrays
+
+
+def pinned_empty(nbytes: int, device: int = 0) -> np.ndarray:
+    """uint8[nbytes] in pinned, device-mapped host memory (gpubpe_host_alloc),
+    freed when the last view dies.  Input batches held here skip the staging
+    copy of encode_packed_host / tokenize paths (the DMA reads them directly)."""
+    _require_cuda()
+    lib = _native.load()
+    p = ctypes.c_void_p()
+    rc = lib.gpubpe_host_alloc(int(device), max(int(nbytes), 1), ctypes.byref(p))
+    if rc != _native.OK or not p.value:
+        raise DeviceError(f"gpubpe_host_alloc({nbytes}) failed ({rc})")
+    raw = (ctypes.c_uint8 * max(int(nbytes), 1)).from_address(p.value)
+    raw._owner = _PinnedBlock(p.value, lib)
+    return np.frombuffer(raw, dtype=np.uint8, count=int(nbytes))
 
 
 class DeviceEncoder:
@@ -300,7 +327,11 @@ class DeviceEncoder:
         offs = np.ascontiguousarray(offs, dtype=np.int64)
         n = int(data.size)
         n_docs = int(offs.size) - 1
-        buf = _RESULTS.take(4 * max(n, 1), self._lib, self.device)
+        # large batches stream through the native pipeline, which copies the ids
+        # out part by part: a plain (recycled) host array is enough there
+        pinned = 4 * n <= _POOLED_MAX
+        buf = (_RESULTS.take(4 * max(n, 1), self._lib, self.device) if pinned
+               else _RESULTS.take_pageable(4 * max(n, 1)))
         ids = buf.view(np.uint32)
         out_offs = np.zeros(max(n_docs + 1, 1), dtype=np.int64)
         n_ids = ctypes.c_uint64(0)

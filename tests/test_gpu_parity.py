@@ -328,3 +328,56 @@ def test_regex_mode_large_document(tokenizer, tiktoken_gpt2):
     assert got.tolist() == tiktoken_gpt2.encode_ordinary(doc.decode("utf-8"))
     with pytest.raises(ValueError):
         bpe.tokenize_batch([doc], tokenizer, pretokenize="o200k")
+
+
+@pytest.mark.parametrize("regex,pinned_in,pinned_out", [(False, False, True), (True, False, True),
+                                                         (False, True, True), (False, True, False),
+                                                         (False, False, False)])
+def test_streamed_host_encode_matches_device_encode(tokenizer, oracle, monkeypatch, regex, pinned_in,
+                                                    pinned_out):
+    """gpubpe_encode_host on a batch larger than two parts runs the two-slot
+    pipeline (parts of GPUBPE_STREAM_MB MiB, here 1): its ids, offsets and
+    counters equal one device-resident encode of the whole batch; docs of every
+    size, empty ones and a document larger than a part included."""
+    import torch
+    import synth_corpus
+
+    rng = np.random.default_rng(11)
+    pool = synth_corpus.english_bytes(3 << 20, 4)
+    docs, at = [], 0
+    for k in range(700):
+        n = int(rng.choice([0, 1, 17, 300, 5000, 20000])) if k != 350 else (2 << 20) + 12345
+        docs.append(pool[at % (1 << 20): at % (1 << 20) + n] if k != 350 else pool[:n])
+        at += 7919
+    data, offs = bpe.pack_texts(docs)
+    assert data.size > (2 << 20)
+    enc = tokenizer.device_encoder()
+    mode = 1 if regex else 0
+    monkeypatch.setenv("GPUBPE_STREAM_MB", "0")
+    d = torch.from_numpy(data.copy()).cuda()
+    o = torch.from_numpy(offs).cuda()
+    enc.set_mode(mode)
+    try:
+        ids_d, offs_d, st_d = enc.encode_tensors(d, o, 8192, 8192)
+    finally:
+        enc.set_mode(0)
+    want_ids, want_offs = ids_d.cpu().numpy().view(np.uint32), offs_d.cpu().numpy()
+    monkeypatch.setenv("GPUBPE_STREAM_MB", "1")
+    if pinned_in:  # the DMA reads the caller's bytes directly
+        pd = bpe.pinned_empty(data.size)
+        pd[:] = data
+        data = pd
+    if not pinned_out:  # result buffer in pageable memory: ids staged through the slots
+        from paper_2603_02597_b200 import device
+
+        monkeypatch.setattr(device, "_POOLED_MAX", 0)
+    ids, oo, st, _ = enc.encode_packed_host(data, offs, 8192, 8192, mode=mode)
+    assert np.array_equal(oo, want_offs)
+    assert np.array_equal(ids, want_ids)
+    for k in ("n_ids", "passes"):  # (segment/pass counters depend on the tiling)
+        assert st[k] == st_d[k], k
+    if not regex:  # and against the oracle on a sample of documents
+        sample = list(range(0, 700, 37)) + [350]
+        want = oracle.encode_docs([docs[i] for i in sample], 8192, 8192)
+        for i, w in zip(sample, want):
+            assert np.array_equal(ids[oo[i]:oo[i + 1]], w), i
