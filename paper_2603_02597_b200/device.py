@@ -73,6 +73,7 @@ class _HostPool:
         self._free: dict[int, list[np.ndarray]] = {}
         self._keep = keep
         self._lock = threading.Lock()
+        self.pinned_max = 8 << 30  # larger result buffers are plain (pageable) host arrays
 
     def take(self, nbytes: int, lib, device: int) -> np.ndarray:
         cls = 1 << max(20, int(nbytes - 1).bit_length())
@@ -98,7 +99,7 @@ class _HostPool:
         return np.empty(cls, dtype=np.uint8)
 
     def put(self, buf: np.ndarray) -> None:
-        key = buf.size if buf.size <= _POOLED_MAX else -buf.size
+        key = buf.size if buf.size <= self.pinned_max else -buf.size
         with self._lock:
             lst = self._free.setdefault(key, [])
             if len(lst) < (self._keep if 0 < key <= (256 << 20) else 1):
@@ -109,7 +110,7 @@ class _HostPool:
 
 
 _RESULTS = _HostPool()
-_POOLED_MAX = 8 << 30  # result buffers above this are plain host arrays
+_POOLED_MAX = _RESULTS.pinned_max
 
 
 def pinned_empty(nbytes: int, device: int = 0) -> np.ndarray:
