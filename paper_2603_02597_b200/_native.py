@@ -37,8 +37,10 @@ class Stats(ctypes.Structure):
         "overflow", "well_formed")]
 
     def as_dict(self) -> dict:
-        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+        return {n: getattr(self, n) for n in _STAT_NAMES}
 
+
+_STAT_NAMES = tuple(n for n, _ in Stats._fields_)
 
 SIGNATURES = {
     "gpubpe_ctx_create": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _u64,

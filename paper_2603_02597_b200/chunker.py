@@ -117,13 +117,19 @@ class Tokenizer:
         """The DeviceEncoder for `device` (built once, then cached)."""
         from .device import DeviceEncoder, _require_cuda
 
-        _require_cuda()
-        import torch
+        if device is None:
+            try:
+                import torch
 
-        dev = torch.cuda.current_device() if device is None else int(device)
-        key = (dev, memo, strict)
+                device = torch.cuda.current_device()
+            except Exception:  # no CUDA: DeviceError below
+                _require_cuda()
+                raise
+        key = (int(device), memo, strict)
         enc = self._devices.get(key)
         if enc is None:
+            _require_cuda()
+            dev = int(device)
             left, right, rank, new = rule_arrays(self.table)
             vids, blob, offs = self._vocab_strings() if memo else (None, None, None)
             enc = DeviceEncoder(self._base_ids, left, right, rank, new, vids, blob, offs,
@@ -145,9 +151,13 @@ def pack_texts(texts) -> tuple[np.ndarray, np.ndarray]:
             parts.append(_as_bytes(text))
         except (TypeError, ValueError, UnicodeError) as exc:
             raise BatchError(i, str(exc)) from exc
-    offs = np.zeros(len(parts) + 1, dtype=np.int64)
-    if parts:
-        offs[1:] = np.cumsum([len(p) for p in parts])
+    n = len(parts)
+    offs = np.zeros(n + 1, dtype=np.int64)
+    if n == 1:
+        offs[1] = len(parts[0])
+        return np.frombuffer(parts[0], dtype=np.uint8), offs
+    if n:
+        np.cumsum(np.fromiter(map(len, parts), dtype=np.int64, count=n), out=offs[1:])
     data = np.frombuffer(b"".join(parts), dtype=np.uint8)
     return data, offs
 

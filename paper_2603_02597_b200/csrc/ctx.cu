@@ -910,7 +910,10 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     } else {  // pinned staging in 4 MiB pieces; staging of piece k+1 overlaps the DMA of piece k;
               // the doc offsets ride with the last piece (they follow the bytes in the layout)
         memcpy(pin + o_doffs, h_doc_offs, offs_b);
-        const size_t piece = 4u << 20;
+        // ~4 pieces (64 KiB .. 4 MiB) so the DMA starts after the first one is staged
+        const char *pe = getenv("GPUBPE_PIECE_KB");
+        const size_t piece = pe ? std::max<size_t>(4096, (size_t)atoll(pe) << 10)
+                                : std::min<size_t>(4u << 20, std::max<size_t>(64u << 10, ((n_bytes / 4) + 65535) & ~(size_t)65535));
         size_t lo = 0;
         for (; lo + piece < n_bytes; lo += piece) {
             copy_par(pin + o_in + lo, h_bytes + lo, piece);
