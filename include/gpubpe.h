@@ -56,6 +56,7 @@ typedef struct gpubpe_stats {
 /* Context flags */
 #define GPUBPE_F_NO_MEMO 1u      /* disable the vocab-string memo (evidence runs) */
 #define GPUBPE_F_STRICT 2u       /* force one-merge-per-pass even if well-formed */
+#define GPUBPE_F_HOST_TABLES 4u  /* build the junction bitmap with the host loops (parity checks) */
 
 /* Encode modes (gpubpe_set_mode) */
 #define GPUBPE_MODE_DEFAULT 0u     /* the reference's semantics: no pre-tokenization */
@@ -164,6 +165,20 @@ int gpubpe_set_mode(gpubpe_ctx *ctx, uint32_t mode);
  * the reference can span, so a document may be split there across GPUs
  * (multigpu.py). */
 int gpubpe_junction_bits(gpubpe_ctx *ctx, uint32_t *h_out);
+
+/* Device-side merges parsing; replaces the line loop
+ * of parse_merges (merge_table.py:88-116) with its vocabulary lookups
+ * (byte_codec.py:80-88).  The vocabulary is given as UTF-8 symbols in CSR form
+ * (sym_bytes, sym_offs[n_syms+1]) with their ids; line i of the merges text
+ * is text[line_start[i], line_end[i]) (line breaks and the optional "#"
+ * header removed by the caller).  For every line: out_status[i] = 0 and the
+ * ids of a, b and a+b in out_left/out_right/out_new, or 1 (not exactly two
+ * nonempty space-separated symbols: MalformedLine) or 2 (a symbol missing
+ * from the vocabulary: UnknownSymbol).  Ranks are the line indices. */
+int gpubpe_parse_merges(int device, const uint8_t *sym_bytes, const uint64_t *sym_offs,
+                        const uint32_t *sym_ids, uint64_t n_syms, const uint8_t *text, uint64_t text_len,
+                        const uint64_t *line_start, const uint64_t *line_end, uint64_t n_lines,
+                        uint32_t *out_left, uint32_t *out_right, uint32_t *out_new, uint8_t *out_status);
 
 /* Number of kernels one gpubpe_encode enqueues (launch accounting): 1, the
  * fused persistent k_encode. */

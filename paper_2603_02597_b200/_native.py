@@ -22,7 +22,7 @@ import os
 LIB_PATH = Path(__file__).resolve().parent / os.environ.get("GPUBPE_LIB", "libgpubpe.so")
 
 OK, EINVAL, ECUDA, ENOMEM, ETABLE, ERANGE = 0, 1, 2, 3, 4, 5
-F_NO_MEMO, F_STRICT = 1, 2
+F_NO_MEMO, F_STRICT, F_HOST_TABLES = 1, 2, 4
 MODE_DEFAULT, MODE_GPT2_REGEX = 0, 1
 
 # (name, restype, argtypes) for every entry point of include/gpubpe.h
@@ -57,6 +57,7 @@ SIGNATURES = {
     "gpubpe_set_vocab": (_int, [_vp, _vp, _vp, _vp, _u64]),
     "gpubpe_decode": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _u64, _vp, ctypes.POINTER(ctypes.c_uint64),
                              ctypes.POINTER(ctypes.c_uint64), _vp]),
+    "gpubpe_parse_merges": (_int, [_int, _vp, _vp, _vp, _u64, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "gpubpe_launches_per_encode": (_int, []),
     "gpubpe_lookup_pairs": (_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),
     "gpubpe_set_profiling": (_int, [_vp, _int]),

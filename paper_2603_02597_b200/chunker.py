@@ -26,7 +26,7 @@ import numpy as np
 from .byte_codec import ByteEncoder, Vocab, base_id_table, build_byte_encoder, decode_tokens, symbol_bytes
 from .engine import BlockConfig, PassCounters
 from .errors import BatchError, DeviceError, InvalidBudget, TokenizerError
-from .merge_table import PackedPairTable, build_table, parse_merges, rule_arrays
+from .merge_table import MergeRule, PackedPairTable, build_table, parse_merges, rule_arrays
 
 ENGINE_NAMES = ("sequential", "baseline", "optimized", "cuda")
 
@@ -59,20 +59,46 @@ class Tokenizer:
     """Vocabulary + merge table + config; device tables are built lazily,
     once per GPU, on first use."""
 
-    def __init__(self, vocab: Vocab, table: PackedPairTable, config: BlockConfig | None = None,
-                 encoder: ByteEncoder | None = None):
+    def __init__(self, vocab: Vocab, table: PackedPairTable | None, config: BlockConfig | None = None,
+                 encoder: ByteEncoder | None = None, *, rules=None):
         self.encoder = encoder if encoder is not None else build_byte_encoder()
         self.vocab = vocab
-        self.table = table
+        if table is None and rules is None:
+            raise ValueError("a Tokenizer needs a table (or the rule arrays it is built from)")
+        self._table = table
+        self._rules = rules  # (left, right, rank, new) uint32 in rank order, when parsed on the device
         self.config = config if config is not None else BlockConfig()
         self._base_ids = base_id_table(self.encoder, vocab)
         self._devices: dict = {}
 
+    @property
+    def table(self) -> PackedPairTable:
+        """The packed pair table (merge_table.build_table, the reference's slot
+        layout); built on first use when the merges were parsed on the device."""
+        if self._table is None:
+            left, right, rank, new = self._rules
+            self._table = build_table([MergeRule(int(a), int(b), int(k), int(c))
+                                       for a, b, k, c in zip(left.tolist(), right.tolist(), rank.tolist(),
+                                                             new.tolist())])
+        return self._table
+
+    @table.setter
+    def table(self, value: PackedPairTable) -> None:
+        self._table = value
+        self._rules = None
+
+    def rule_arrays(self):
+        """(left, right, rank, new) uint32 arrays in rank order."""
+        return self._rules if self._rules is not None else rule_arrays(self.table)
+
     @classmethod
     def from_files(cls, vocab_path, merges_path, config: BlockConfig | None = None) -> "Tokenizer":
         vocab = Vocab.from_file(vocab_path)
-        rules = parse_merges(Path(merges_path).read_bytes(), vocab)
-        return cls(vocab, build_table(rules), config)
+        text = Path(merges_path).read_bytes()
+        rules = _device_rules(text, vocab) if _device_parse_enabled() else None
+        if rules is None:
+            return cls(vocab, build_table(parse_merges(text, vocab)), config)
+        return cls(vocab, None, config, rules=rules)
 
     def encode(self, text: bytes) -> np.ndarray:
         """bytes -> base token ids, one per byte (no merges)."""
@@ -87,31 +113,52 @@ class Tokenizer:
         """Many id sequences -> their byte strings in one device call."""
         return self.device_encoder().decode_host(seqs)
 
+    def _symbol_bytes(self):
+        """(ids uint32[], blob uint8[], offs uint64[]) of every id whose symbol maps
+        to a nonempty byte string (symbol_bytes semantics), vectorised: all
+        symbols are translated at once through a code point -> byte table."""
+        cached = getattr(self, "_sym_cache", None)
+        if cached is not None:
+            return cached
+        items = list(self.vocab.id_to_symbol.items())
+        n = len(items)
+        ids = np.fromiter((k for k, _ in items), dtype=np.uint32, count=n)
+        syms = [v for _, v in items]
+        lens = np.fromiter(map(len, syms), dtype=np.int64, count=n)
+        cps = np.frombuffer("".join(syms).encode("utf-32-le"), dtype=np.uint32)
+        s2b = self.encoder.symbol_to_byte
+        top = max(map(ord, s2b)) + 1 if s2b else 1
+        lut = np.full(top, -1, dtype=np.int32)
+        for ch, byte in s2b.items():
+            lut[ord(ch)] = byte
+        val = np.where(cps < top, lut[np.minimum(cps, top - 1)], -1)
+        seg = np.repeat(np.arange(n), lens)  # symbol index of every character
+        bad = np.zeros(n, dtype=bool)
+        bad[seg[val < 0]] = True
+        keep = (lens > 0) & ~bad
+        blob = val[keep[seg]].astype(np.uint8) if cps.size else np.empty(0, np.uint8)
+        offs = np.zeros(int(keep.sum()) + 1, dtype=np.uint64)
+        np.cumsum(lens[keep], out=offs[1:])
+        self._sym_cache = (ids[keep], blob, offs)
+        return self._sym_cache
+
     def _decode_strings(self):
         """(ids, blob, offs) of every id whose symbol maps to bytes."""
-        ids, pieces = [], []
-        for tid, sym in self.vocab.id_to_symbol.items():
-            b = symbol_bytes(sym, self.encoder)
-            if b:
-                ids.append(tid)
-                pieces.append(b)
-        offs = np.zeros(len(pieces) + 1, dtype=np.uint64)
-        if pieces:
-            offs[1:] = np.cumsum([len(p) for p in pieces])
-        return np.array(ids, dtype=np.uint32), np.frombuffer(b"".join(pieces), dtype=np.uint8), offs
+        return self._symbol_bytes()
 
     def _vocab_strings(self):
-        ids, pieces = [], []
-        for tid, sym in self.vocab.id_to_symbol.items():
-            b = symbol_bytes(sym, self.encoder)
-            if b is not None and len(b) >= 2:
-                ids.append(tid)
-                pieces.append(b)
-        offs = np.zeros(len(pieces) + 1, dtype=np.uint64)
-        if pieces:
-            offs[1:] = np.cumsum([len(p) for p in pieces])
-        blob = np.frombuffer(b"".join(pieces), dtype=np.uint8)
-        return np.array(ids, dtype=np.uint32), blob, offs
+        """(ids, blob, offs) of the ids whose byte strings are >= 2 bytes (memo candidates)."""
+        ids, blob, offs = self._symbol_bytes()
+        lens = np.diff(offs)
+        sel = lens >= 2
+        if sel.all():
+            return ids, blob, offs
+        starts = offs[:-1][sel].astype(np.int64)
+        ln = lens[sel].astype(np.int64)
+        idx = np.repeat(starts - np.r_[0, np.cumsum(ln)[:-1]], ln) + np.arange(int(ln.sum()))
+        o2 = np.zeros(int(sel.sum()) + 1, dtype=np.uint64)
+        np.cumsum(ln, out=o2[1:].view(np.int64))
+        return ids[sel], blob[idx], o2
 
     def device_encoder(self, device: int | None = None, memo: bool = True, strict: bool = False):
         """The DeviceEncoder for `device` (built once, then cached)."""
@@ -130,13 +177,44 @@ class Tokenizer:
         if enc is None:
             _require_cuda()
             dev = int(device)
-            left, right, rank, new = rule_arrays(self.table)
+            left, right, rank, new = self.rule_arrays()
             vids, blob, offs = self._vocab_strings() if memo else (None, None, None)
             enc = DeviceEncoder(self._base_ids, left, right, rank, new, vids, blob, offs,
                                 device=dev, memo=memo, strict=strict)
             enc.set_vocab(*self._decode_strings())
             self._devices[key] = enc
         return enc
+
+
+def _device_parse_enabled() -> bool:
+    """Merges are parsed on the GPU when one is
+    present; GPUBPE_HOST_PARSE=1 forces the host parser."""
+    import os
+
+    if os.environ.get("GPUBPE_HOST_PARSE"):
+        return False
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover - torch is part of the image
+        return False
+
+
+def _device_rules(text: bytes, vocab: Vocab):
+    """Rule arrays from the device parser, or None when the host path must run
+    (it then raises the reference's exact error, or handles str.splitlines
+    breaks): a duplicated pair or the reserved key go to build_table."""
+    from .merge_table import EMPTY_KEY, parse_merges_device
+
+    rules = parse_merges_device(text, vocab)
+    if rules is None:
+        return None
+    left, right = rules[0].astype(np.uint64), rules[1].astype(np.uint64)
+    keys = (left << np.uint64(32)) | right
+    if (keys == np.uint64(EMPTY_KEY)).any() or np.unique(keys).size != keys.size:
+        return None
+    return rules
 
 
 def _as_bytes(text) -> bytes:

@@ -28,6 +28,9 @@ cudaError_t launch_encode(const EncodeParams &P, int grid, cudaStream_t s, cudaE
                           const cudaAccessPolicyWindow *win, bool coop);
 cudaError_t setup_kernels();
 cudaError_t tile_occupancy(int *blocks);
+cudaError_t build_junction_device(const uint32_t *h_base, const uint32_t *h_L, const uint32_t *h_R,
+                                  const uint32_t *h_NW, uint64_t n_rules, uint64_t n_ids, uint32_t *h_jbits,
+                                  int *h_rounds);
 cudaError_t launch_lookup(const DevTables &T, const uint32_t *l, const uint32_t *r,
                           unsigned long long n, uint32_t *nw, uint32_t *rank, cudaStream_t s);
 
@@ -161,6 +164,9 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
                        uint64_t chunk_budget, uint32_t *d_out_ids, int64_t *d_out_offs,
                        cudaStream_t s, bool *checked);
 
+// ctx_create phase timing (GPUBPE_HOSTTIME): stamp k at the start of phase k
+#define BUILD_STAMP(k) (build_t[k] = std::chrono::steady_clock::now())
+
 extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int device, const uint32_t *base_ids, const uint32_t *left,
                                  const uint32_t *right, const uint32_t *rank,
                                  const uint32_t *new_tok, uint64_t n_rules,
@@ -169,6 +175,8 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
                                  gpubpe_ctx **out) {
     if (!out) return GPUBPE_EINVAL;
     *out = nullptr;
+    std::chrono::steady_clock::time_point build_t[8];
+    BUILD_STAMP(7);
     gpubpe_ctx *ctx = new gpubpe_ctx();
     *out = ctx;  // on failure the caller reads the message, then destroys
     ctx->device = device;
@@ -183,9 +191,9 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
     {
         cudaError_t e = cudaSetDevice(device);
         if (e != cudaSuccess) return bail(fail(ctx, GPUBPE_ECUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e)));
-        cudaDeviceProp prop;
-        cudaGetDeviceProperties(&prop, device);
-        ctx->num_sms = prop.multiProcessorCount;
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        ctx->num_sms = sms;
         if ((e = setup_kernels()) != cudaSuccess)
             return bail(fail(ctx, GPUBPE_ECUDA, "kernel setup: %s", cudaGetErrorString(e)));
         // the per-lane engine keeps its token arrays on the thread stack
@@ -203,6 +211,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
         ctx->tile_blocks_per_sm = blocks;
     }
 
+    BUILD_STAMP(0);
     // ---- internal ids: used as-is when every id < 2^24, else densely remapped
     uint64_t max_id = 0;
     for (int b = 0; b < 256; ++b) max_id = std::max<uint64_t>(max_id, base_ids[b]);
@@ -236,6 +245,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
     if (n_ids >= (1ull << 24))
         return bail(fail(ctx, GPUBPE_EINVAL, "more than 2^24 distinct token ids (%llu)", (unsigned long long)n_ids));
 
+    BUILD_STAMP(1);
     // ---- pair table
     uint64_t cap = 2;
     while (cap < 2 * n_rules) cap <<= 1;
@@ -254,6 +264,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
             h = (h + 1) & (uint32_t)(cap - 1);
         }
     }
+    BUILD_STAMP(2);
     // ---- rl / rr and well-formedness
     std::vector<uint32_t> rl(n_ids, GPUBPE_INF), rr(n_ids, GPUBPE_INF);
     std::vector<int64_t> maxprod(n_ids, -1);
@@ -267,36 +278,46 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
         if (rank[i] >= 0x7FFFFFFFu) wf = false;
     for (uint64_t i = 0; i < n_rules && wf; ++i)
         if ((int64_t)rank[i] <= maxprod[L[i]] || (int64_t)rank[i] <= maxprod[R[i]]) wf = false;
-    // ---- junction bitmap: first/last covered byte sets to a fixpoint
-    std::vector<uint64_t> F(n_ids * 4, 0), B(n_ids * 4, 0);
-    for (int b = 0; b < 256; ++b) {
-        F[base[b] * 4 + (b >> 6)] |= 1ull << (b & 63);
-        B[base[b] * 4 + (b >> 6)] |= 1ull << (b & 63);
-    }
-    std::vector<uint64_t> order(n_rules);
-    for (uint64_t i = 0; i < n_rules; ++i) order[i] = i;
-    std::sort(order.begin(), order.end(), [&](uint64_t x, uint64_t y) { return rank[x] < rank[y]; });
-    for (bool changed = true; changed;) {
-        changed = false;
-        for (uint64_t oi : order) {
-            for (int w = 0; w < 4; ++w) {
-                uint64_t f = F[NW[oi] * 4 + w] | F[L[oi] * 4 + w];
-                uint64_t l = B[NW[oi] * 4 + w] | B[R[oi] * 4 + w];
-                if (f != F[NW[oi] * 4 + w] || l != B[NW[oi] * 4 + w]) changed = true;
-                F[NW[oi] * 4 + w] = f;
-                B[NW[oi] * 4 + w] = l;
+    BUILD_STAMP(3);
+    // ---- junction bitmap: first/last covered byte sets to a fixpoint; built on
+    //      the device (build.cu) unless GPUBPE_F_HOST_TABLES asks for the host loops
+    std::vector<uint32_t> jbits(2048);
+    if (!(flags & GPUBPE_F_HOST_TABLES)) {
+        int rounds = 0;
+        cudaError_t e = build_junction_device(base.data(), L.data(), R.data(), NW.data(), n_rules, n_ids,
+                                              jbits.data(), &rounds);
+        if (e != cudaSuccess)
+            return bail(fail(ctx, GPUBPE_ECUDA, "junction build: %s", cudaGetErrorString(e)));
+    } else {
+        std::vector<uint64_t> F(n_ids * 4, 0), B(n_ids * 4, 0);
+        for (int b = 0; b < 256; ++b) {
+            F[base[b] * 4 + (b >> 6)] |= 1ull << (b & 63);
+            B[base[b] * 4 + (b >> 6)] |= 1ull << (b & 63);
+        }
+        std::vector<uint64_t> order(n_rules);
+        for (uint64_t i = 0; i < n_rules; ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), [&](uint64_t x, uint64_t y) { return rank[x] < rank[y]; });
+        for (bool changed = true; changed;) {
+            changed = false;
+            for (uint64_t oi : order) {
+                for (int w = 0; w < 4; ++w) {
+                    uint64_t f = F[NW[oi] * 4 + w] | F[L[oi] * 4 + w];
+                    uint64_t l = B[NW[oi] * 4 + w] | B[R[oi] * 4 + w];
+                    if (f != F[NW[oi] * 4 + w] || l != B[NW[oi] * 4 + w]) changed = true;
+                    F[NW[oi] * 4 + w] = f;
+                    B[NW[oi] * 4 + w] = l;
+                }
             }
         }
-    }
-    std::vector<uint64_t> J(65536 / 64, 0);  // row x: 256 bits of y
-    for (uint64_t i = 0; i < n_rules; ++i) {
-        for (int x = 0; x < 256; ++x) {
-            if (!((B[L[i] * 4 + (x >> 6)] >> (x & 63)) & 1)) continue;
-            for (int w = 0; w < 4; ++w) J[x * 4 + w] |= F[R[i] * 4 + w];
+        std::vector<uint64_t> J(65536 / 64, 0);  // row x: 256 bits of y
+        for (uint64_t i = 0; i < n_rules; ++i) {
+            for (int x = 0; x < 256; ++x) {
+                if (!((B[L[i] * 4 + (x >> 6)] >> (x & 63)) & 1)) continue;
+                for (int w = 0; w < 4; ++w) J[x * 4 + w] |= F[R[i] * 4 + w];
+            }
         }
+        for (int k = 0; k < 2048; ++k) jbits[k] = (uint32_t)(J[k >> 1] >> (32 * (k & 1)));
     }
-    std::vector<uint32_t> jbits(2048);
-    for (int k = 0; k < 2048; ++k) jbits[k] = (uint32_t)(J[k >> 1] >> (32 * (k & 1)));
     ctx->h_jbits = jbits;
 
     // memo upper bounds (the memo is built after a verification encode)
@@ -352,6 +373,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
         memset(ctx->h_state, 0, sizeof(EncodeState));
     }
 
+    BUILD_STAMP(4);
     // ---- memo: vocab strings whose BPE (computed by this engine) is themselves
     if (!(flags & GPUBPE_F_NO_MEMO) && n_vocab && vocab_ids && vocab_bytes && vocab_offs) {
         std::vector<uint64_t> cand;
@@ -437,16 +459,18 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
             ctx->T.blob = d_blob;
         }
     }
+    BUILD_STAMP(5);
     // ---- keep the tables resident in L2 across unrelated traffic
     {
-        cudaDeviceProp prop;
-        cudaGetDeviceProperties(&prop, device);
-        size_t want = std::min<size_t>(ctx->tables_used, (size_t)prop.persistingL2CacheMaxSize);
+        int persist_max = 0, win_max = 0;
+        cudaDeviceGetAttribute(&persist_max, cudaDevAttrMaxPersistingL2CacheSize, device);
+        cudaDeviceGetAttribute(&win_max, cudaDevAttrMaxAccessPolicyWindowSize, device);
+        size_t want = std::min<size_t>(ctx->tables_used, (size_t)persist_max);
         size_t cur = 0;
         cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
         if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
         cudaGetLastError();
-        size_t win = std::min<size_t>(ctx->tables_used, (size_t)prop.accessPolicyMaxWindowSize);
+        size_t win = std::min<size_t>(ctx->tables_used, (size_t)win_max);
         if (want && win) {
             ctx->win.base_ptr = ctx->tables;
             ctx->win.num_bytes = win;
@@ -456,6 +480,13 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
         }
     }
     *out = ctx;
+    if (getenv("GPUBPE_HOSTTIME")) {
+        auto ms = [&](int a, int b) { return std::chrono::duration<double, std::milli>(build_t[b] - build_t[a]).count(); };
+        const auto end = std::chrono::steady_clock::now();
+        fprintf(stderr, "ctx_create: setup %.1f | intern %.1f | pairs %.1f | rl/rr %.1f | junction %.1f | memo %.1f | l2 %.1f ms\n",
+                ms(7, 0), ms(0, 1), ms(1, 2), ms(2, 3), ms(3, 4), ms(4, 5),
+                std::chrono::duration<double, std::milli>(end - build_t[5]).count());
+    }
     return GPUBPE_OK;
 }
 

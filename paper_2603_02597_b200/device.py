@@ -133,7 +133,7 @@ class DeviceEncoder:
 
     def __init__(self, base_ids, left, right, rank, new, vocab_ids=None, vocab_blob=None,
                  vocab_offs=None, device: int | None = None, memo: bool = True,
-                 strict: bool = False):
+                 strict: bool = False, host_tables: bool = False):
         _require_cuda()
         lib = _native.load()
         self.device = torch.cuda.current_device() if device is None else int(device)
@@ -146,7 +146,8 @@ class DeviceEncoder:
         vids = np.ascontiguousarray(vocab_ids, dtype=np.uint32)
         vblob = np.ascontiguousarray(vocab_blob, dtype=np.uint8)
         voffs = np.ascontiguousarray(vocab_offs, dtype=np.uint64)
-        flags = (0 if memo else _native.F_NO_MEMO) | (_native.F_STRICT if strict else 0)
+        flags = ((0 if memo else _native.F_NO_MEMO) | (_native.F_STRICT if strict else 0)
+                 | (_native.F_HOST_TABLES if host_tables else 0))
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             rc = lib.gpubpe_ctx_create(self.device, _ptr(base), *[_ptr(a) for a in arrs],

@@ -88,6 +88,71 @@ def parse_merges(merges_text, vocab: Vocab) -> list[MergeRule]:
     return rules
 
 
+# line breaks str.splitlines() honours besides "\n" (UTF-8): such texts take the host parser
+_OTHER_BREAKS = (b"\r", b"\x0b", b"\x0c", b"\x1c", b"\x1d", b"\x1e", b"\xc2\x85", b"\xe2\x80\xa8", b"\xe2\x80\xa9")
+
+
+def _symbol_csr(vocab: Vocab):
+    """UTF-8 of every vocabulary symbol as CSR (bytes, offsets) with the ids."""
+    syms = list(vocab.symbol_to_id)
+    n = len(syms)
+    ids = np.fromiter(vocab.symbol_to_id.values(), dtype=np.uint32, count=n)
+    cps = np.frombuffer("".join(syms).encode("utf-32-le", "surrogatepass"), dtype=np.uint32)
+    width = 1 + (cps >= 0x80).astype(np.int64) + (cps >= 0x800) + (cps >= 0x10000)
+    lens = np.fromiter(map(len, syms), dtype=np.int64, count=n)
+    offs = np.zeros(n + 1, dtype=np.uint64)
+    if cps.size:
+        seg_end = np.cumsum(lens)
+        csum = np.r_[0, np.cumsum(width)]
+        offs[1:] = csum[seg_end]
+    blob = np.frombuffer("".join(syms).encode("utf-8", "surrogatepass"), dtype=np.uint8)
+    return blob, offs, ids
+
+
+def parse_merges_device(merges_text, vocab: Vocab, device: int = 0):
+    """parse_merges on the GPU (build.cu): (left, right,
+    rank, new) uint32 arrays in rank order.  Any input the reference would
+    reject is re-parsed by parse_merges so that exactly its exception (type and
+    message) is raised; texts with line breaks other than "\n" also take the
+    host parser (str.splitlines semantics).  Returns None for those."""
+    import ctypes
+
+    from . import _native
+
+    if not isinstance(merges_text, (bytes, bytearray)):
+        return None  # str input: the host parser (exact str semantics)
+    text = bytes(merges_text)
+    text.decode("utf-8")  # the reference decodes first: UnicodeDecodeError as there
+    if any(b in text for b in _OTHER_BREAKS):
+        return None
+    arr = np.frombuffer(text, dtype=np.uint8)
+    nl = np.flatnonzero(arr == 10).astype(np.uint64)
+    starts = np.r_[np.uint64(0), nl + np.uint64(1)].astype(np.uint64)
+    ends = np.r_[nl, np.uint64(len(text))].astype(np.uint64)
+    if text.endswith(b"\n") or not text:  # splitlines: no empty last line
+        starts, ends = starts[:-1], ends[:-1]
+    if len(starts) and text[int(starts[0]):int(starts[0]) + 1] == b"#":
+        starts, ends = starts[1:], ends[1:]
+    n = len(starts)
+    left = np.empty(n, np.uint32)
+    right = np.empty(n, np.uint32)
+    new = np.empty(n, np.uint32)
+    status = np.zeros(n, np.uint8)
+    blob, offs, ids = _symbol_csr(vocab)
+    lib = _native.load()
+
+    def ptr(a):
+        return ctypes.c_void_p(a.ctypes.data) if a.size else None
+
+    rc = lib.gpubpe_parse_merges(int(device), ptr(blob), ptr(offs), ptr(ids), len(ids), ptr(arr), len(text),
+                                 ptr(starts), ptr(ends), n, ptr(left), ptr(right), ptr(new), ptr(status))
+    _native.check(rc, None, "gpubpe_parse_merges")
+    if status.any():
+        parse_merges(text, vocab)  # raises the reference's error for the first bad line
+        raise AssertionError("device merges parser rejected a line the host parser accepts")
+    return left, right, np.arange(n, dtype=np.uint32), new
+
+
 class PackedPairTable:
     """Open-addressing pair table with the reference's exact slot layout."""
 

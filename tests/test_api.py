@@ -175,3 +175,34 @@ def test_make_windows_token_mode_matches_reference_cpu(tokenizer):
         spec = bpe.SweepSpec(lengths=tuple(case["lengths"]), samples_per_length=case["samples"])
         got = bpe.make_windows(corpus, fx["stream"], spec, tokenizer=_HostDecoder(tokenizer), seed=case["seed"])
         assert {str(k): [w.hex() for w in v] for k, v in got.items()} == case["windows"]
+
+
+def _symbol_bytes_loop(tok, minlen):
+    from paper_2603_02597_b200.byte_codec import symbol_bytes
+
+    ids, pieces = [], []
+    for tid, sym in tok.vocab.id_to_symbol.items():
+        b = symbol_bytes(sym, tok.encoder)
+        if b is not None and len(b) >= minlen:
+            ids.append(tid)
+            pieces.append(b)
+    offs = np.zeros(len(pieces) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(p) for p in pieces])
+    return np.array(ids, np.uint32), np.frombuffer(b"".join(pieces), np.uint8), offs
+
+
+def test_vectorised_symbol_bytes_match_symbol_bytes(tokenizer):
+    """The device tables' vocab strings (memo candidates, decode LUT) equal
+    symbol_bytes applied symbol by symbol -- on GPT-2 and on a vocab with
+    empty symbols, non-byte characters and astral code points."""
+    enc = bpe.build_byte_encoder()
+    b2s = {b: s for s, b in enc.symbol_to_byte.items()}
+    base = {b2s[b]: b for b in range(256)}
+    odd = dict(base)
+    odd.update({"": 300, "a b": 301, b2s[104] + b2s[105]: 302, "\U0001F600": 303,
+                b2s[0] + "一": 304, b2s[255] * 5: 305, "x": 306 if "x" not in base else 307})
+    small = bpe.Tokenizer(bpe.Vocab(odd), bpe.build_table([]))
+    for tok in (tokenizer, small):
+        for got, minlen in ((tok._decode_strings(), 1), (tok._vocab_strings(), 2)):
+            want = _symbol_bytes_loop(tok, minlen)
+            assert all(np.array_equal(g, w) for g, w in zip(got, want))

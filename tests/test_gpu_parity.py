@@ -381,3 +381,71 @@ def test_streamed_host_encode_matches_device_encode(tokenizer, oracle, monkeypat
         want = oracle.encode_docs([docs[i] for i in sample], 8192, 8192)
         for i, w in zip(sample, want):
             assert np.array_equal(ids[oo[i]:oo[i + 1]], w), i
+
+
+def _parse_errors(fn, text, vocab):
+    try:
+        fn(text, vocab)
+    except Exception as exc:  # noqa: BLE001 - the exact type and message are compared
+        return type(exc), str(exc)
+    return None
+
+
+def test_device_merges_parse_matches_host(gpt2_paths):
+    """merges.txt parsed on the device gives the reference's rules,
+    and Tokenizer.from_files built from them has the reference's packed table."""
+    from pathlib import Path
+
+    from paper_2603_02597_b200.merge_table import parse_merges_device
+
+    vocab = bpe.Vocab.from_file(gpt2_paths[0])
+    text = Path(gpt2_paths[1]).read_bytes()
+    left, right, rank, new = parse_merges_device(text, vocab)
+    rules = bpe.parse_merges(text, vocab)
+    assert len(left) == len(rules) == 50000
+    assert left.tolist() == [r.left for r in rules] and right.tolist() == [r.right for r in rules]
+    assert new.tolist() == [r.new_token for r in rules] and rank.tolist() == [r.rank for r in rules]
+    tok = bpe.Tokenizer.from_files(*gpt2_paths)
+    assert tok._rules is not None  # took the device parser
+    ref = bpe.build_table(rules)
+    assert np.array_equal(tok.table.keys, ref.keys) and np.array_equal(tok.table.values, ref.values)
+
+
+def test_device_merges_parse_errors_match_host(gpt2_paths):
+    from paper_2603_02597_b200.merge_table import parse_merges_device
+
+    vocab = bpe.Vocab.from_file(gpt2_paths[0])
+    good = "#version: 0.2\nĠ t\nĠ a\nh e\n"
+    cases = [good, good.rstrip("\n"), "Ġ t\n", "Ġ t\n\nh e\n", "Ġ t x\n", "Ġt\n", " t\n", "Ġ \n",
+             "Ġ t\nzzz§ q\n", "Ġ t\nh e\n# comment later\n", "#only header\n", "", "\n", "Ġ t\r\nh e\r\n",
+             "Ġ t\x0bh e\n", "Ġ t\n" * 3]
+    for c in cases:
+        raw = c.encode("utf-8")
+        want = _parse_errors(bpe.parse_merges, raw, vocab)
+        got = _parse_errors(parse_merges_device, raw, vocab)
+        if want is not None:
+            assert got == want, (c, got, want)
+        else:
+            assert got is None, (c, got)
+            res = parse_merges_device(raw, vocab)
+            if res is not None:  # (None: line breaks only the host parser handles)
+                rules = bpe.parse_merges(raw, vocab)
+                assert res[0].tolist() == [r.left for r in rules], c
+                assert res[3].tolist() == [r.new_token for r in rules], c
+    bad_utf8 = b"\xff\xfe t\n"
+    assert _parse_errors(parse_merges_device, bad_utf8, vocab) == _parse_errors(bpe.parse_merges, bad_utf8, vocab)
+
+
+def test_device_junction_build_matches_host_loops(tokenizer, prose_samples):
+    from paper_2603_02597_b200.device import DeviceEncoder
+
+    left, right, rank, new = tokenizer.rule_arrays()
+    vids, blob, offs = tokenizer._vocab_strings()
+    dev = DeviceEncoder(tokenizer._base_ids, left, right, rank, new, vids, blob, offs, device=0)
+    host = DeviceEncoder(tokenizer._base_ids, left, right, rank, new, vids, blob, offs, device=0,
+                         host_tables=True)
+    assert np.array_equal(dev.junction_bits(), host.junction_bits())
+    data, doffs = bpe.pack_texts(prose_samples[:20])
+    a = dev.encode_packed_host(data, doffs, 8192, 8192)
+    b = host.encode_packed_host(data, doffs, 8192, 8192)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
