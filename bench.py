@@ -275,6 +275,7 @@ def run_corpus(args, rank, world, local, dist):
                        "semantics": "P-default", "l2": f"input {mb} MiB > L2 (not flushed)",
                        "parallelism": f"documents sharded x{world}"},
             "clocks": clocks.summary(), "gpu_launches": args.steps,
+            "roofline": corpus_roofline(args, offs, total_ids, ms / args.steps, world, local),
             "e2e": {"value": total_ids * e2e_steps / e2e_s, "unit": "tokens/s",
                     "h2d_bytes_per_step": int(offs[-1]) + 8 * len(offs),
                     "d2h_bytes_per_step": 4 * total_ids + 8 * len(offs),
@@ -285,6 +286,45 @@ def run_corpus(args, rank, world, local, dist):
     if dist:
         dist.destroy_process_group()
 
+
+
+def corpus_roofline(args, offs, total_ids, kernel_ms, world, device):
+    """HBM roofline of one corpus step (all ranks' bytes over the max-over-ranks
+    time, per GPU peak x world) and, for the captured workload, the issue roofline."""
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0)) * world
+    b_alg = int(offs[-1]) + 4 * total_ids + 16 * len(offs)
+    achieved = b_alg / (kernel_ms / 1e3) / 1e9
+    summ = {}
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        summ = json.loads(prof.read_text()).get(args.workload, {})
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": summ.get("traffic_bytes"), "kernel": "k_encode", "alg_bytes_per_launch": b_alg,
+            "kernel_ms": kernel_ms,
+            "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback") + f" x {world} GPU(s)",
+            "issue": issue_roofline(summ.get("warp_instructions"), kernel_ms, device) if world == 1 else None}
+
+
+def issue_roofline(warp_inst, kernel_ms, device):
+    """Warp instructions issued per second vs the SMs' issue peak (4 schedulers
+    per SM, one instruction per cycle each, at the maximum SM clock)."""
+    import torch
+
+    if not warp_inst or not kernel_ms:
+        return None
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        mhz = pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(device), pynvml.NVML_CLOCK_SM)
+    except Exception:
+        mhz = 1965
+    peak = sms * 4 * mhz * 1e6
+    achieved = warp_inst / (kernel_ms / 1e3)
+    return {"achieved": achieved, "peak": peak, "unit": "warp-instructions/s", "frac": achieved / peak,
+            "warp_instructions_per_launch": warp_inst, "source": "profiles/ncu_summary.json"}
 
 
 def main():
@@ -374,9 +414,12 @@ def main():
     # DRAM bytes of one k_encode launch on this workload, from the committed
     # `ncu --set full` capture (profiles/ncu_summary.json, tools/ncu_summary.py)
     traffic = None
+    warp_inst = None
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get(args.workload, {}).get("traffic_bytes")
+        summ = json.loads(prof.read_text()).get(args.workload, {})
+        traffic = summ.get("traffic_bytes")
+        warp_inst = summ.get("warp_instructions")
 
     # e2e through the public API: host bytes in, host ids out
     e2e = None
@@ -411,7 +454,10 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "k_encode",
                      "alg_bytes_per_launch": b_alg, "kernel_ms": statistics.mean(k_tile),
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)" if peaks else "fallback"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)" if peaks else "fallback",
+                     # the binding ceiling of this integer kernel: warp-instruction issue
+                     # (ncu smsp__inst_executed.sum per launch / the live kernel time)
+                     "issue": issue_roofline(warp_inst, statistics.mean(k_tile), local)},
         "kernel_ms": {"k_encode": statistics.mean(k_tile), "k_encode_p50": statistics.median(k_tile)},
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
