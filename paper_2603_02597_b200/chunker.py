@@ -223,12 +223,15 @@ def _as_bytes(text) -> bytes:
 
 def pack_texts(texts) -> tuple[np.ndarray, np.ndarray]:
     """list[str|bytes] -> (uint8 data, int64 offsets); BatchError(i) on a bad item."""
-    parts = []
-    for i, text in enumerate(texts):
-        try:
-            parts.append(_as_bytes(text))
-        except (TypeError, ValueError, UnicodeError) as exc:
-            raise BatchError(i, str(exc)) from exc
+    if type(texts) is list and all(type(t) is bytes for t in texts):
+        parts = texts  # already bytes: no per-item conversion
+    else:
+        parts = []
+        for i, text in enumerate(texts):
+            try:
+                parts.append(_as_bytes(text))
+            except (TypeError, ValueError, UnicodeError) as exc:
+                raise BatchError(i, str(exc)) from exc
     n = len(parts)
     offs = np.zeros(n + 1, dtype=np.int64)
     if n == 1:
@@ -273,7 +276,8 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
     except TokenizerError as exc:  # pragma: no cover - the device reports no per-input errors
         raise BatchError(0, str(exc)) from exc
     t2 = time.perf_counter()
-    token_ids = [ids[out_offs[i] : out_offs[i + 1]] for i in range(n_docs)]
+    o = out_offs.tolist()
+    token_ids = [ids[a:b] for a, b in zip(o, o[1:])]
     assemble_ms = (time.perf_counter() - t2) * 1000.0
     counters = PassCounters(passes=int(data.size) - int(ids.size))
     return BatchResult(token_ids, engine_ms, encode_ms, assemble_ms, counters, st)
