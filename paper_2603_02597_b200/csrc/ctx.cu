@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <cstdarg>
 #include <cstdio>
@@ -646,22 +648,92 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *
                        d_out_ids, d_out_offs, s, &checked);
 }
 
-// memcpy with up to 8 threads for large buffers (staging through pinned memory)
+// Host copies through pinned memory (staging, copy-out) on a small persistent
+// worker pool: the caller copies one chunk itself, workers the others.
+namespace {
+class CopyPool {
+  public:
+    static CopyPool &get() {
+        static CopyPool *p = new CopyPool();  // never destroyed: workers live for the process
+        return *p;
+    }
+    unsigned workers() const { return (unsigned)th_.size(); }
+    void copy(uint8_t *dst, const uint8_t *src, size_t n, unsigned parts) {
+        const size_t chunk = (n + parts - 1) / parts;
+        {
+            std::lock_guard<std::mutex> g(m_);
+            for (unsigned i = 1; i < parts; ++i) {
+                const size_t lo = i * chunk, hi = std::min(n, lo + chunk);
+                if (lo < hi) {
+                    jobs_.push_back({dst + lo, src + lo, hi - lo});
+                    ++pending_;
+                }
+            }
+        }
+        cv_.notify_all();
+        memcpy(dst, src, std::min(n, chunk));
+        for (;;) {  // help with what the workers have not picked up yet, then wait
+            Job j;
+            {
+                std::unique_lock<std::mutex> g(m_);
+                if (jobs_.empty()) {
+                    done_.wait(g, [&] { return pending_ == 0; });
+                    return;
+                }
+                j = jobs_.back();
+                jobs_.pop_back();
+            }
+            memcpy(j.d, j.s, j.n);
+            finish();
+        }
+    }
+
+  private:
+    struct Job {
+        uint8_t *d;
+        const uint8_t *s;
+        size_t n;
+    };
+    CopyPool() {
+        const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+        const unsigned nw = std::min(7u, hw - 1);
+        for (unsigned i = 0; i < nw; ++i) th_.emplace_back([this] { loop(); });
+        for (auto &t : th_) t.detach();
+    }
+    void finish() {
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_.notify_all();
+    }
+    void loop() {
+        for (;;) {
+            Job j;
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return !jobs_.empty(); });
+                j = jobs_.back();
+                jobs_.pop_back();
+            }
+            memcpy(j.d, j.s, j.n);
+            finish();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    std::vector<Job> jobs_;
+    size_t pending_ = 0;
+};
+}  // namespace
+
 static void copy_par(void *dst, const void *src, size_t n) {
-    const size_t per = 4u << 20;
+    const size_t per = 4u << 20;  // one chunk per 4 MiB beyond 8 MiB (below, a worker wake-up costs more)
     if (n <= 2 * per) {
         memcpy(dst, src, n);
         return;
     }
-    const unsigned nt = (unsigned)std::min<size_t>(8, (n + per - 1) / per);
-    std::vector<std::thread> th;
-    const size_t chunk = (n + nt - 1) / nt;
-    for (unsigned i = 1; i < nt; ++i) {
-        const size_t lo = i * chunk, hi = std::min(n, lo + chunk);
-        if (lo < hi) th.emplace_back([=] { memcpy((uint8_t *)dst + lo, (const uint8_t *)src + lo, hi - lo); });
-    }
-    memcpy(dst, src, std::min(n, chunk));
-    for (auto &t : th) t.join();
+    CopyPool &pool = CopyPool::get();
+    const unsigned parts = (unsigned)std::min<size_t>(pool.workers() + 1, (n + per - 1) / per);
+    pool.copy(static_cast<uint8_t *>(dst), static_cast<const uint8_t *>(src), n, parts);
 }
 
 static int ensure_pinned(gpubpe_ctx *ctx, size_t bytes) {
