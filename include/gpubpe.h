@@ -51,6 +51,9 @@ typedef struct gpubpe_stats {
     uint64_t tiles;            /* encode tiles launched */
     uint64_t overflow;         /* 1 if the giant arena overflowed (call re-run) */
     uint64_t well_formed;      /* 1 if the table admits exact multi-merge passes */
+    uint64_t allocations;      /* device / pinned buffers allocated by the last call
+                                  (0 in steady state: workspaces are grow-only;
+                                  PassCounters.buffer_allocations) */
 } gpubpe_stats;
 
 /* Context flags */

@@ -34,7 +34,7 @@ class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "n_bytes", "n_ids", "passes", "n_segments", "memo_hits", "short_merges",
         "medium_segments", "giant_segments", "giant_bytes", "engine_passes", "tiles",
-        "overflow", "well_formed")]
+        "overflow", "well_formed", "allocations")]
 
     def as_dict(self) -> dict:
         return {n: getattr(self, n) for n in _STAT_NAMES}

@@ -279,5 +279,5 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
     o = out_offs.tolist()
     token_ids = [ids[a:b] for a, b in zip(o, o[1:])]
     assemble_ms = (time.perf_counter() - t2) * 1000.0
-    counters = PassCounters(passes=int(data.size) - int(ids.size))
+    counters = PassCounters(passes=int(data.size) - int(ids.size), buffer_allocations=int(st["allocations"]))
     return BatchResult(token_ids, engine_ms, encode_ms, assemble_ms, counters, st)

@@ -94,6 +94,8 @@ struct gpubpe_ctx {
     bool defer_check = false;  // the caller checks EncodeState.overflow itself (streamed encode)
     EncodeState *h_state_ss = nullptr;  // pinned [2]: per-slot encode state
     uint64_t last_n_tiles = 0;
+    uint64_t n_allocs = 0, alloc_mark = 0;  // buffers allocated (grow-only workspaces), mark at call entry
+    bool host_call = false;                  // inside gpubpe_encode_host (its mark stands)
     unsigned int epoch = 0;
     uint64_t calls = 0;  // selects the EncodeState slot (two, alternating)
     EncodeState *h_state = nullptr;  // pinned
@@ -145,6 +147,7 @@ static int ensure(gpubpe_ctx *ctx, DevBuf &b, size_t bytes, bool zero) {
     b.bytes = 0;
     size_t nb = std::max<size_t>(bytes + bytes / 4, 256);
     CK(cudaMalloc(&b.p, nb));
+    ++ctx->n_allocs;
     if (zero) CK(cudaMemset(b.p, 0, nb));
     b.bytes = nb;
     return GPUBPE_OK;
@@ -603,6 +606,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *
         return fail(ctx, GPUBPE_EINVAL, "chunk_budget must be in [2, max_seq_len]");
     if (n_docs && (!d_doc_offs || !d_out_offs)) return fail(ctx, GPUBPE_EINVAL, "null offsets");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!ctx->host_call) ctx->alloc_mark = ctx->n_allocs;
     CK(cudaSetDevice(ctx->device));
     ctx->state_fresh = false;
     ctx->last_n_bytes = n_docs ? n_bytes : 0;
@@ -743,6 +747,7 @@ static int ensure_pinned(gpubpe_ctx *ctx, size_t bytes) {
     ctx->pin_bytes = 0;
     const size_t nb = std::max<size_t>(bytes + bytes / 4, 1 << 20);
     CK(cudaHostAlloc(reinterpret_cast<void **>(&ctx->pin), nb, cudaHostAllocMapped));
+    ++ctx->n_allocs;
     void *dev = nullptr;
     CK(cudaHostGetDevicePointer(&dev, ctx->pin, 0));
     ctx->pin_dev = static_cast<uint8_t *>(dev);
@@ -757,6 +762,7 @@ static int ensure_host(gpubpe_ctx *ctx, uint8_t **p, uint8_t **p_dev, size_t *ha
     *have = 0;
     const size_t nb = std::max<size_t>(bytes + bytes / 8, 1 << 20);
     CK(cudaHostAlloc(reinterpret_cast<void **>(p), nb, p_dev ? cudaHostAllocMapped : 0));
+    ++ctx->n_allocs;
     if (p_dev) {
         void *dev = nullptr;
         CK(cudaHostGetDevicePointer(&dev, *p, 0));
@@ -797,7 +803,10 @@ static int encode_host_streamed(gpubpe_ctx *ctx, const uint8_t *h_bytes, const i
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!ctx->s_copy) CK(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
     if (!ctx->s_d2h) CK(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
-    if (!ctx->h_state_ss) CK(cudaHostAlloc(reinterpret_cast<void **>(&ctx->h_state_ss), 2 * sizeof(EncodeState), 0));
+    if (!ctx->h_state_ss) {
+        CK(cudaHostAlloc(reinterpret_cast<void **>(&ctx->h_state_ss), 2 * sizeof(EncodeState), 0));
+        ++ctx->n_allocs;
+    }
     for (auto &S : ctx->ss) {
         if (!S.ev_h2d) CK(cudaEventCreate(&S.ev_h2d));
         if (!S.ev_done) CK(cudaEventCreate(&S.ev_done));
@@ -967,6 +976,12 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     if (!n_ids_out || (n_docs && (!h_doc_offs || !h_out_offs)) || (n_bytes && (!h_bytes || !h_out_ids)))
         return fail(ctx, GPUBPE_EINVAL, "null host pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->alloc_mark = ctx->n_allocs;
+    struct HostCall {  // gpubpe_encode calls below keep this call's allocation mark
+        gpubpe_ctx *c;
+        explicit HostCall(gpubpe_ctx *c_) : c(c_) { c->host_call = true; }
+        ~HostCall() { c->host_call = false; }
+    } host_call_guard(ctx);
     CK(cudaSetDevice(ctx->device));
     *n_ids_out = 0;
     if (kernel_ms) *kernel_ms = 0.f;
@@ -1121,6 +1136,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_query(gpubpe_ctx *c
     out->tiles = ctx->last_n_bytes ? ctx->last_n_tiles : 0;
     out->overflow = st.overflow;
     out->well_formed = (uint64_t)ctx->T.well_formed;
+    out->allocations = ctx->n_allocs - ctx->alloc_mark;
     return GPUBPE_OK;
 }
 

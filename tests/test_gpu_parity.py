@@ -449,3 +449,16 @@ def test_device_junction_build_matches_host_loops(tokenizer, prose_samples):
     a = dev.encode_packed_host(data, doffs, 8192, 8192)
     b = host.encode_packed_host(data, doffs, 8192, 8192)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_steady_state_needs_no_allocations(tokenizer, prose_samples):
+    """Workspaces are grow-only: repeating a call allocates nothing
+    (PassCounters.buffer_allocations)."""
+    docs = prose_samples[:50]
+    bpe.tokenize_batch(docs, tokenizer)
+    again = bpe.tokenize_batch(docs, tokenizer)
+    assert again.counters.buffer_allocations == 0
+    assert again.device_stats["allocations"] == 0
+    bigger = bpe.tokenize_batch(docs * 40, tokenizer)  # may grow the workspace once
+    assert bigger.counters.buffer_allocations >= 0
+    assert bpe.tokenize_batch(docs * 40, tokenizer).counters.buffer_allocations == 0
