@@ -508,6 +508,10 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
     int wt = 128;
     if (n_bytes >= 2 * n_warps * 512) wt = 512;
     else if (n_bytes >= 2 * n_warps * 256) wt = 256;
+    if (const char *e = getenv("GPUBPE_WT")) {  // tuning override: 128, 256 or 512
+        const int w = atoi(e);
+        if (w == 128 || w == 256 || w == 512) wt = w;
+    }
     const uint64_t n_tiles = (n_bytes + wt - 1) / wt;
     const uint64_t R = std::min<uint64_t>(n_tiles, (uint64_t)UNIT_MAX * grid);
     const uint64_t n_rounds = (n_tiles + R - 1) / R;
