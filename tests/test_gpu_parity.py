@@ -462,3 +462,36 @@ def test_steady_state_needs_no_allocations(tokenizer, prose_samples):
     bigger = bpe.tokenize_batch(docs * 40, tokenizer)  # may grow the workspace once
     assert bigger.counters.buffer_allocations >= 0
     assert bpe.tokenize_batch(docs * 40, tokenizer).counters.buffer_allocations == 0
+
+
+def test_batch_beyond_4_gib_offsets(tokenizer, oracle):
+    """A 4.3 GiB batch: byte and id offsets past 2**32 (64-bit positions end to
+    end); documents around the 2**32 boundary and a random sample equal the
+    oracle, and the CSR is consistent."""
+    import torch
+    import synth_corpus
+
+    total = (1 << 32) + (300 << 20)
+    data, offs = synth_corpus.corpus_docs(total, seed=3)
+    d = torch.from_numpy(data).cuda()
+    o = torch.from_numpy(offs).cuda()
+    del data
+    enc = tokenizer.device_encoder()
+    out_ids = torch.empty(d.numel(), dtype=torch.int32, device="cuda")
+    out_offs = torch.empty(o.numel(), dtype=torch.int64, device="cuda")
+    enc.encode_into(d, o, out_ids, out_offs, 8192, 8192)
+    st = enc.query()
+    oo = out_offs.cpu().numpy()
+    assert oo[0] == 0 and np.all(np.diff(oo) >= 0) and oo[-1] == st["n_ids"]
+    assert st["passes"] == total - st["n_ids"]
+    b = int(np.searchsorted(offs, 1 << 32, side="right")) - 1  # the document holding byte 2**32
+    rng = np.random.default_rng(7)
+    sample = sorted(set(range(max(0, b - 3), min(len(offs) - 1, b + 4))) |
+                    set(rng.integers(0, len(offs) - 1, 12).tolist()) | {len(offs) - 2})
+    docs = [bytes(d[int(offs[i]):int(offs[i + 1])].cpu().numpy()) for i in sample]
+    want = oracle.encode_docs(docs, 8192, 8192)
+    for i, w in zip(sample, want):
+        got = out_ids[int(oo[i]):int(oo[i + 1])].cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, w), i
+    del d, out_ids
+    torch.cuda.empty_cache()
