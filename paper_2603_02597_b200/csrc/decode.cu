@@ -10,9 +10,10 @@
 // k_decode: one launch, CTA tiles of TD ids (8 per thread, loaded as uint4 by
 // warp-contiguous 512-B rows), lengths from the LUT (L2-resident), warp and
 // block scans, a CTA-granular decoupled look-back for the tile's output
-// offset, the tile's bytes staged in shared memory and stored with coalesced
-// byte stores (tiles whose bytes exceed the stage write directly).  HBM-bound:
-// 4 B read per id + its bytes written.
+// offset, the tile's strings OR-ed into a zeroed shared-memory stage as
+// shifted 32-bit words (one 16-B load per string) and stored with 16-B stores
+// (tiles whose bytes exceed the stage write directly).  Bound: HBM (4 B read
+// per id + its bytes written) once the staging is a few instructions per id.
 #include <cuda_runtime.h>
 
 #include <cuda/atomic>
@@ -20,14 +21,18 @@
 #include "common.cuh"
 #include "decode.cuh"
 
+#ifndef GPUBPE_DEC_DT
+#define GPUBPE_DEC_DT 1024
+#endif
+
 namespace {
 
-constexpr int DT = 1024;             // threads per CTA
+constexpr int DT = GPUBPE_DEC_DT;      // threads per CTA
 constexpr int DPT = 8;               // ids per thread
 constexpr int KG = DPT / 4;          // 4-id groups per lane
 constexpr int ROW = 32 * DPT;        // ids per warp row
 constexpr int TD = DT * DPT;         // ids per tile
-constexpr int STAGE = 96 * 1024;     // staged output bytes per tile (+16 alignment slack)
+constexpr int STAGE = DT * 96;         // staged output bytes per tile (+16 alignment slack)
 
 struct DecSmem {
     uint32_t goff[TD / 4];           // output offset of each 4-id group inside the tile
@@ -53,7 +58,7 @@ __device__ __forceinline__ uint32_t info_of(const DecodeParams &P, uint32_t id) 
 
 }  // namespace
 
-__global__ void __launch_bounds__(DT, 1) k_decode(const __grid_constant__ DecodeParams P) {
+__global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant__ DecodeParams P) {
     extern __shared__ __align__(16) unsigned char dsm_raw[];
     DecSmem &S = *reinterpret_cast<DecSmem *>(dsm_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -63,6 +68,8 @@ __global__ void __launch_bounds__(DT, 1) k_decode(const __grid_constant__ Decode
         const unsigned long long t = S.base;
         __syncthreads();
         if (t >= P.n_tiles) break;
+        // the stage starts zeroed: strings are OR-ed into it (below)
+        for (int q = tid; q < (STAGE + 32) / 16; q += DT) reinterpret_cast<uint4 *>(S.stage)[q] = make_uint4(0, 0, 0, 0);
         const unsigned long long t0 = t * TD;
         // ---- ids: warp row w covers tile ids [w*ROW, (w+1)*ROW); lane l holds
         //      4-id groups g = k*32 + l (k < KG) of that row
@@ -178,15 +185,19 @@ __global__ void __launch_bounds__(DT, 1) k_decode(const __grid_constant__ Decode
                 const uint32_t inf = len[4 * k + j], l = inf & 0xFFu;
                 if (l) {
                     const uint4 *src = reinterpret_cast<const uint4 *>(P.blob) + (inf >> 8);
-                    if (staged) {  // shared-memory stores (the common case)
-                        uint8_t *dst = S.stage + shift + o;
+                    if (staged) {  // shared memory (the common case): the zero-padded
+                                   // 16-B chunk shifted to its byte offset and OR-ed
+                                   // word by word (neighbouring strings share edge words)
+                        uint32_t *sw = reinterpret_cast<uint32_t *>(S.stage);
                         for (uint32_t c = 0; c < l; c += 16) {
                             const uint4 v = __ldg(src + (c >> 4));
-                            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-                            const uint32_t m = min(16u, l - c);
-#pragma unroll
-                            for (uint32_t b = 0; b < 16; ++b)
-                                if (b < m) dst[c + b] = (uint8_t)(w[b >> 2] >> (8 * (b & 3)));
+                            const uint32_t p = shift + o + c, sh = 8 * (p & 3), wi = p >> 2;
+                            const uint32_t nw = ((p & 3) + min(16u, l - c) + 3) >> 2;  // words touched
+                            atomicOr(&sw[wi], v.x << sh);
+                            if (nw > 1) atomicOr(&sw[wi + 1], __funnelshift_l(v.x, v.y, sh));
+                            if (nw > 2) atomicOr(&sw[wi + 2], __funnelshift_l(v.y, v.z, sh));
+                            if (nw > 3) atomicOr(&sw[wi + 3], __funnelshift_l(v.z, v.w, sh));
+                            if (nw > 4) atomicOr(&sw[wi + 4], v.w >> (32 - sh));
                         }
                     } else if (fits) {  // tile larger than the stage: straight to global
                         uint8_t *dst = P.out + base + o;

@@ -92,7 +92,13 @@ def decode_row(name, enc, flush, peak, args):
     oo = torch.empty_like(ioffs)
     for _ in range(args.warmup):
         enc.decode_into(ids, ioffs, out, oo)
-    assert torch.equal(out[: data.size].cpu(), torch.from_numpy(data)), "decode round trip"
+    got = out[: data.size].cpu().numpy()
+    bad = np.flatnonzero(got != data)
+    if bad.size:
+        b = int(bad[0])
+        print(f"{name}: {bad.size} bytes differ, first at {b} of {data.size}: got {bytes(got[b-8:b+24])!r} "
+              f"want {bytes(data[b-8:b+24])!r}", flush=True)
+    assert not bad.size, "decode round trip"
     times = []
     prof = os.environ.get("GPUBPE_PROFILE_TIMED")
     if prof:
