@@ -62,3 +62,6 @@ for _ in range(100):
     raw_enq.append(time.perf_counter() - t0)
 torch.cuda.synchronize()
 print("enqueue C gpubpe_encode %6.1f us" % (1e6 * statistics.median(raw_enq)))
+pin = bpe.pinned_empty(n)
+pin[:] = data
+print("encode_packed_host (pinned input) %8.1f us" % t(lambda: enc.encode_packed_host(pin, offs, W, W)))

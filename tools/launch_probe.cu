@@ -12,7 +12,43 @@ __global__ void k_sync(int *ctr, int n) {  // one grid barrier
     }
     __syncthreads();
 }
+#include <chrono>
+static double host_us(void (*f)(), int k) {
+    for (int i = 0; i < 10; ++i) f();
+    cudaDeviceSynchronize();
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < k; ++i) f();
+    auto t1 = std::chrono::steady_clock::now();
+    cudaDeviceSynchronize();
+    return std::chrono::duration<double, std::micro>(t1 - t0).count() / k;
+}
+static int g_coop = 0, g_smem = 0;
+static void launch_one() {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(148); cfg.blockDim = dim3(1024); cfg.dynamicSmemBytes = g_smem;
+    cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeCooperative; at[0].val.cooperative = 1;
+    cfg.attrs = at; cfg.numAttrs = g_coop;
+    cudaLaunchKernelEx(&cfg, k_empty, (int *)nullptr);
+}
+static char *g_h, *g_d;
+static void memcpy_one() { cudaMemcpyAsync(g_d, g_h, 4096, cudaMemcpyHostToDevice, 0); }
+static cudaEvent_t g_ev;
+static void event_one() { cudaEventRecord(g_ev, 0); }
+static void attr_one() { cudaPointerAttributes pa; cudaPointerGetAttributes(&pa, g_h); }
+
 int main() {
+    cudaMallocHost(&g_h, 1 << 20); cudaMalloc(&g_d, 1 << 20); cudaEventCreate(&g_ev);
+    for (int smem : {0, 200 * 1024}) {
+        cudaFuncSetAttribute(k_empty, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        for (int coop : {0, 1}) {
+            g_coop = coop; g_smem = smem;
+            printf("host enqueue: launch smem %6d coop %d  %.2f us\n", smem, coop, host_us(launch_one, 200));
+        }
+    }
+    printf("host enqueue: cudaMemcpyAsync 4 KB pinned H2D %.2f us\n", host_us(memcpy_one, 200));
+    printf("host enqueue: cudaEventRecord %.2f us\n", host_us(event_one, 200));
+    printf("host: cudaPointerGetAttributes %.2f us\n", host_us(attr_one, 200));
+
     int *ctr; cudaMalloc(&ctr, 4);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     for (int smem : {0, 200 * 1024}) {
