@@ -38,6 +38,7 @@ struct CtaSmem {
     uint32_t base[256];
     EngineShared es;
     unsigned long long bcast[4];
+    unsigned long long red[NW][4];  // per-warp partial sums (no 64-bit shared atomics: CAS loops)
     PassCounters pc;
     unsigned long long tb[UNIT_MAX];  // phase B: tile output offsets inside the unit
     unsigned long long tw[UNIT_MAX];  // phase B: tile words
@@ -660,19 +661,15 @@ __device__ __noinline__ void place_range(const EncodeParams &P, CtaSmem &C, unsi
     // of all tiles before this range directly (L2 reads, no CTA waits on
     // another) while warp 0 scans the range.
     const bool direct = r == 0 && P.n_tiles <= P.round_tiles;
-    if (direct) {
-        if (tid == 0) C.bcast[1] = 0;
-        __syncthreads();
-        if (wid > 0) {
-            unsigned long long acc = 0;
-            for (unsigned long long t = (unsigned long long)(tid - 32); t < lo; t += NT - 32) {
-                const unsigned long long w = __ldcg(&P.tiles[t]);  // round 0: parity 0, t0 == 0
-                acc += TW_ENTRIES(w) + TW_EXTRA(w);
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
-            if (lane == 0 && acc) atomicAdd(&C.bcast[1], acc);
+    if (direct && wid > 0) {
+        unsigned long long acc = 0;
+        for (unsigned long long t = (unsigned long long)(tid - 32); t < lo; t += NT - 32) {
+            const unsigned long long w = __ldcg(&P.tiles[t]);  // round 0: parity 0, t0 == 0
+            acc += TW_ENTRIES(w) + TW_EXTRA(w);
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
+        if (lane == 0) C.red[wid][0] = acc;
     }
     if (wid == 0) {
         constexpr int PER = UNIT_MAX / 32;
@@ -712,7 +709,12 @@ __device__ __noinline__ void place_range(const EncodeParams &P, CtaSmem &C, unsi
         }
     }
     __syncthreads();
-    const unsigned long long base = direct ? C.bcast[1] : C.bcast[0];
+    unsigned long long base = C.bcast[0];
+    if (direct) {  // every warp sums the partials of warps 1..
+        base = lane > 0 && lane < NW ? C.red[lane][0] : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(FULL_MASK, base, o);
+    }
     if (tid == 0 && nt > 0 && hi == P.n_tiles) P.st->n_ids = base + C.bcast[2];
     for (int k = wid; k < nt; k += NW) place_tile(P, slots + (size_t)k * SLOT, C.tw[k], base + C.tb[k]);
     // CSR offsets of the documents starting in [lo, hi): tile-local -> global
@@ -778,18 +780,32 @@ __device__ void publish_counters(CtaSmem &C, WarpCtx &X, PassCounters *dst) {
         sm += __shfl_xor_sync(FULL_MASK, sm, o);
         ep += __shfl_xor_sync(FULL_MASK, ep, o);
     }
+    const int wid = threadIdx.x >> 5;
     if (lane == 0) {
-        atomicAdd(&C.pc.n_segments, seg);
-        atomicAdd(&C.pc.memo_hits, memo);
-        atomicAdd(&C.pc.short_merges, sm);
-        atomicAdd(&C.pc.engine_passes, ep);
+        C.red[wid][0] = seg;
+        C.red[wid][1] = memo;
+        C.red[wid][2] = sm;
+        C.red[wid][3] = ep;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned long long *s = &C.pc.n_segments;
-        unsigned long long *d = &dst->n_segments;
-        for (int i = 0; i < (int)(sizeof(PassCounters) / 8); ++i)
-            if (s[i]) atomicAdd(&d[i], s[i]);
+    if (wid == 0) {  // the CTA's sums, then one global add per counter
+        unsigned long long v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            v[q] = lane < NW ? C.red[lane][q] : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(FULL_MASK, v[q], o);
+        }
+        if (lane == 0) {
+            C.pc.n_segments += v[0];
+            C.pc.memo_hits += v[1];
+            C.pc.short_merges += v[2];
+            C.pc.engine_passes += v[3];
+            const unsigned long long *s = &C.pc.n_segments;
+            unsigned long long *d = &dst->n_segments;
+            for (int i = 0; i < (int)(sizeof(PassCounters) / 8); ++i)
+                if (s[i]) atomicAdd(&d[i], s[i]);
+        }
     }
 }
 
