@@ -391,7 +391,14 @@ __device__ __noinline__ void encode_tile(const EncodeParams &P, CtaSmem &C, Warp
                     const long long e = __ldg(&P.doc_offs[d + 1]);
                     if ((unsigned long long)(e - s) > P.max_seq_len) {
                         const long long cb = (long long)P.chunk_budget;
-                        long long k = s < a ? (a - s + cb - 1) / cb : 1;
+                        long long k = 1;
+                        if (s < a) {  // first chunk cut at or after a (64-bit division only when needed)
+                            const unsigned long long num = (unsigned long long)(a - s + cb - 1);
+                            if ((cb & (cb - 1)) == 0) k = (long long)(num >> (63 - __clzll(cb)));
+                            else if ((num >> 32) == 0 && ((unsigned long long)cb >> 32) == 0)
+                                k = (long long)((uint32_t)num / (uint32_t)cb);
+                            else k = (long long)(num / (unsigned long long)cb);
+                        }
                         if (k < 1) k = 1;
 #pragma unroll 1
                         for (long long c = s + k * cb; c < e && c < a + nst; c += cb)
@@ -742,7 +749,7 @@ __device__ __noinline__ void place_range(const EncodeParams &P, CtaSmem &C, unsi
                 const long long s = __ldg(&P.doc_offs[dd]);
                 if (s < (long long)hi * P.tile_bytes || hi == P.n_tiles) in = s >= blo;
                 if (in) {
-                    const long long t = min(s / P.tile_bytes, (long long)P.n_tiles - 1);
+                    const long long t = min(s >> (31 - __clz(P.tile_bytes)), (long long)P.n_tiles - 1);  // wt: 2^k
                     const int k = (int)(t - (long long)lo);
                     const uint32_t local = (uint32_t)__ldcg(&P.out_offs[dd]);
                     unsigned long long v = base + C.tb[k] + local;
