@@ -14,6 +14,16 @@ from .byte_codec import ByteEncoder, Vocab, base_id_table, build_byte_encoder, d
 from .chunker import ENGINE_NAMES, BatchResult, Chunk, Tokenizer, chunk_tokens, pack_texts, tokenize_batch
 from .engine import BlockConfig, PassCounters
 from .windows import DEFAULT_LENGTHS, SweepSpec, make_windows
+from .report import (
+    BenchRecord,
+    GoldenReport,
+    ProfileReport,
+    compare_golden,
+    emit_report,
+    load_golden_file,
+    profile_run,
+    run_sweep,
+)
 from .merge_table import (
     MergeRule,
     PackedPairTable,
@@ -36,7 +46,8 @@ def pinned_empty(nbytes: int, device: int = 0):
     return _pinned_empty(nbytes, device)
 
 __all__ = [
-    "BatchResult", "BlockConfig", "DEFAULT_LENGTHS", "SweepSpec", "make_windows", "ByteEncoder", "Chunk", "ENGINE_NAMES", "MergeRule",
+    "BatchResult", "BenchRecord", "GoldenReport", "ProfileReport", "compare_golden", "emit_report",
+    "load_golden_file", "profile_run", "run_sweep", "BlockConfig", "DEFAULT_LENGTHS", "SweepSpec", "make_windows", "ByteEncoder", "Chunk", "ENGINE_NAMES", "MergeRule",
     "PackedPairTable", "PassCounters", "Tokenizer", "TokenizerHandle", "Vocab", "base_id_table",
     "build_byte_encoder", "build_table", "chunk_tokens", "decode_tokens", "encode_bytes", "errors",
     "pack_key", "pack_texts", "pack_value", "pinned_empty", "parse_merges", "rule_arrays", "tokenize_batch",

@@ -206,3 +206,38 @@ def test_vectorised_symbol_bytes_match_symbol_bytes(tokenizer):
         for got, minlen in ((tok._decode_strings(), 1), (tok._vocab_strings(), 2)):
             want = _symbol_bytes_loop(tok, minlen)
             assert all(np.array_equal(g, w) for g, w in zip(got, want))
+
+
+def test_report_schema_matches_reference(tmp_path):
+    """emit_report / compare_golden / load_golden_file reproduce the reference's
+    output byte for byte (tests/golden/report.json, made by the reference itself:
+    tests/golden/make_report_golden.py)."""
+    import json
+    from pathlib import Path
+
+    from paper_2603_02597_b200 import report
+
+    fx = json.loads((Path(__file__).parent / "golden" / "report.json").read_text())
+    for case in fx["reports"]:
+        recs = [report.BenchRecord(*r) for r in fx["records"][case["set"]]]
+        assert report.emit_report(recs, case["fmt"], case["baseline"]) == case["text"], case
+    for i, g in enumerate(fx["golden_files"]):
+        p = tmp_path / f"g{i}.tokens"
+        p.write_text(g["body"])
+        assert report.load_golden_file(p) == g["loaded"]
+        r = report.compare_golden(g["tokens"], p)
+        assert (r.match, r.first_divergence, r.divergences) == (g["match"], g["first"], g["divergences"]), g
+    with pytest.raises(errors.EmptyRecords):
+        report.emit_report([], "csv")
+    with pytest.raises(ValueError):
+        report.emit_report([report.BenchRecord("a", 1, 1.0, 0.0, 1.0)], "xml")
+
+
+def test_golden_file_errors(tmp_path):
+    from paper_2603_02597_b200 import report
+
+    for body in ("[1, 2, true]", "[1, 2", "1\nx\n", '{"a": 1}'):
+        p = tmp_path / "g.tokens"
+        p.write_text(body)
+        with pytest.raises(errors.MalformedGoldenFile):
+            report.load_golden_file(p)

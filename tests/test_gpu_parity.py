@@ -495,3 +495,25 @@ def test_batch_beyond_4_gib_offsets(tokenizer, oracle):
         assert np.array_equal(got, w), i
     del d, out_ids
     torch.cuda.empty_cache()
+
+
+def test_run_sweep_and_profile_run_on_the_device(tokenizer, oracle, prose_samples, tmp_path):
+    """The reference's sweep methodology on the device engine:
+    windows cut by make_windows, goldens written from the oracle, every window
+    matches; the report renders; profile_run's splits and counters hold."""
+    corpus = b"\n".join(prose_samples[:30])
+    spec = bpe.SweepSpec(lengths=(64, 512, 2048), samples_per_length=3, warmup_runs=1, measured_runs=3)
+    windows = bpe.make_windows(corpus, None, spec, seed=5)
+    for length, cell in windows.items():
+        for k, ids in enumerate(oracle.encode_docs(cell, 8192, 8192)):
+            (tmp_path / f"len{length}_s{k:03d}.tokens").write_text("\n".join(map(str, ids.tolist())) + "\n")
+    recs = bpe.run_sweep(windows, ["cuda", "optimized"], spec, tokenizer, golden_dir=tmp_path)
+    assert len(recs) == 6
+    assert all(r.golden_matches == 3 and r.golden_divergences == 0 for r in recs)
+    assert all(r.mean_latency_ms > 0 and r.throughput_tokens_per_s > 0 for r in recs)
+    table = bpe.emit_report(recs, "table", baseline_engine="cuda")
+    assert "optimized speedup_vs_cuda" in table and len(table.splitlines()) == 2 + 3
+    prof = bpe.profile_run(prose_samples[:10], tokenizer)
+    assert prof.counters.passes == sum(map(len, prose_samples[:10])) - sum(
+        len(x) for x in bpe.tokenize_batch(prose_samples[:10], tokenizer).token_ids)
+    assert prof.end_to_end_ms >= prof.engine_ms >= 0 and abs(sum(prof.event_shares.values()) - 1.0) < 1e-9
