@@ -169,6 +169,16 @@ int gpubpe_set_mode(gpubpe_ctx *ctx, uint32_t mode);
  * (multigpu.py). */
 int gpubpe_junction_bits(gpubpe_ctx *ctx, uint32_t *h_out);
 
+/* Token-level merges (replaces sequential_bpe, engines.py:269-335, and the
+ * output of run_block_engine, engines.py:338-403): for each sequence s of
+ * device tokens d_tokens[h_offs[s] .. h_offs[s+1]) the greedy lowest-rank /
+ * leftmost BPE fixpoint is written to d_out at the same offset, its length in
+ * h_counts[s] (host).  Every token must be an id the merge table covers
+ * (< the context's id bound; GPUBPE_EINVAL names the sequence otherwise) and
+ * ids must be below 2^24.  Synchronous. */
+int gpubpe_merge_tokens(gpubpe_ctx *ctx, const uint32_t *d_tokens, const uint64_t *h_offs, uint64_t n_seqs,
+                        uint32_t *d_out, uint64_t *h_counts, void *stream);
+
 /* Device-side merges parsing; replaces the line loop
  * of parse_merges (merge_table.py:88-116) with its vocabulary lookups
  * (byte_codec.py:80-88).  The vocabulary is given as UTF-8 symbols in CSR form

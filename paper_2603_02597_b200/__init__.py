@@ -12,7 +12,7 @@ from . import errors
 from .bindings import TokenizerHandle
 from .byte_codec import ByteEncoder, Vocab, base_id_table, build_byte_encoder, decode_tokens, encode_bytes
 from .chunker import ENGINE_NAMES, BatchResult, Chunk, Tokenizer, chunk_tokens, pack_texts, tokenize_batch
-from .engine import BlockConfig, PassCounters
+from .engine import BlockConfig, PassCounters, run_block_engine, sequential_bpe, token_seq
 from .windows import DEFAULT_LENGTHS, SweepSpec, make_windows
 from .report import (
     BenchRecord,
@@ -51,5 +51,5 @@ __all__ = [
     "PackedPairTable", "PassCounters", "Tokenizer", "TokenizerHandle", "Vocab", "base_id_table",
     "build_byte_encoder", "build_table", "chunk_tokens", "decode_tokens", "encode_bytes", "errors",
     "pack_key", "pack_texts", "pack_value", "pinned_empty", "parse_merges", "rule_arrays", "tokenize_batch",
-    "unpack_value", "__version__",
+    "unpack_value", "run_block_engine", "sequential_bpe", "token_seq", "__version__",
 ]

@@ -57,6 +57,7 @@ SIGNATURES = {
     "gpubpe_set_vocab": (_int, [_vp, _vp, _vp, _vp, _u64]),
     "gpubpe_decode": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _u64, _vp, ctypes.POINTER(ctypes.c_uint64),
                              ctypes.POINTER(ctypes.c_uint64), _vp]),
+    "gpubpe_merge_tokens": (_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),
     "gpubpe_parse_merges": (_int, [_int, _vp, _vp, _vp, _u64, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "gpubpe_launches_per_encode": (_int, []),
     "gpubpe_lookup_pairs": (_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),

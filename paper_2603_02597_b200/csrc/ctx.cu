@@ -24,6 +24,7 @@
 #include "kernels.cuh"
 #include "decode.cuh"
 #include "pretok.cuh"
+#include "tokens.cuh"
 
 size_t tile_smem_bytes();
 cudaError_t launch_encode(const EncodeParams &P, int grid, cudaStream_t s, cudaEvent_t *ev,
@@ -94,6 +95,8 @@ struct gpubpe_ctx {
     bool defer_check = false;  // the caller checks EncodeState.overflow itself (streamed encode)
     EncodeState *h_state_ss = nullptr;  // pinned [2]: per-slot encode state
     uint64_t last_n_tiles = 0;
+    uint32_t n_ids = 0;             // internal ids the tables cover
+    DevBuf mt_offs, mt_counts;      // token-level merges (gpubpe_merge_tokens)
     uint64_t n_allocs = 0, alloc_mark = 0;  // buffers allocated (grow-only workspaces), mark at call entry
     bool host_call = false;                  // inside gpubpe_encode_host (its mark stands)
     unsigned int epoch = 0;
@@ -364,6 +367,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
     ctx->T.memo_mask = 0;
     ctx->T.blob = nullptr;
     ctx->T.well_formed = wf ? 1 : 0;
+    ctx->n_ids = (uint32_t)n_ids;
     ctx->T.ext_id = nullptr;
     if (!identity) {
         const uint32_t *d_ext;
@@ -1269,6 +1273,51 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_set_mode(gpubpe_ctx
     return GPUBPE_OK;
 }
 
+extern "C" __attribute__((visibility("default"))) int gpubpe_merge_tokens(gpubpe_ctx *ctx, const uint32_t *d_tokens,
+                                                                           const uint64_t *h_offs, uint64_t n_seqs,
+                                                                           uint32_t *d_out, uint64_t *h_counts,
+                                                                           void *stream) {
+    if (!ctx || (n_seqs && (!h_offs || !h_counts))) return GPUBPE_EINVAL;
+    if (ctx->T.ext_id) return fail(ctx, GPUBPE_EINVAL, "token-level merges need token ids below 2^24");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device));
+    if (n_seqs == 0) return GPUBPE_OK;
+    uint64_t max_len = 0;
+    for (uint64_t i = 0; i < n_seqs; ++i) {
+        if (h_offs[i + 1] < h_offs[i]) return fail(ctx, GPUBPE_EINVAL, "offsets decrease at %llu", (unsigned long long)i);
+        max_len = std::max<uint64_t>(max_len, h_offs[i + 1] - h_offs[i]);
+    }
+    if (max_len && (!d_tokens || !d_out)) return fail(ctx, GPUBPE_EINVAL, "null token pointer");
+    if (max_len >= (1ull << 31)) return fail(ctx, GPUBPE_EINVAL, "sequence too long for the CTA engine");
+    const uint64_t per_cta = (ENGINE_BYTES(max_len) + 15) / 16 * 4;  // words
+    uint64_t grid = std::min<uint64_t>(n_seqs, (uint64_t)ctx->num_sms * 2);
+    while (grid > 1 && grid * per_cta * 4 > (2ull << 30)) grid >>= 1;  // arena <= 2 GiB
+    int rc;
+    if ((rc = ensure(ctx, ctx->ws_arena, grid * per_cta * 4, false))) return rc;
+    if ((rc = ensure(ctx, ctx->mt_offs, (n_seqs + 1) * 8, false))) return rc;
+    if ((rc = ensure(ctx, ctx->mt_counts, n_seqs * 8, false))) return rc;
+    CK(cudaMemcpyAsync(ctx->mt_offs.p, h_offs, (n_seqs + 1) * 8, cudaMemcpyHostToDevice, s));
+    MergeParams Q{};
+    Q.T = ctx->T;
+    Q.tok = d_tokens;
+    Q.offs = static_cast<const unsigned long long *>(ctx->mt_offs.p);
+    Q.n_seqs = n_seqs;
+    Q.arena = static_cast<uint32_t *>(ctx->ws_arena.p);
+    Q.arena_words_per_cta = per_cta;
+    Q.out = d_out;
+    Q.counts = static_cast<unsigned long long *>(ctx->mt_counts.p);
+    Q.strict = ((ctx->flags & GPUBPE_F_STRICT) || !ctx->T.well_formed) ? 1 : 0;
+    Q.n_ids = ctx->n_ids;
+    CK(launch_merge_tokens(Q, (int)grid, s));
+    CK(cudaMemcpyAsync(h_counts, ctx->mt_counts.p, n_seqs * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (uint64_t i = 0; i < n_seqs; ++i)
+        if (h_counts[i] == ~0ull)
+            return fail(ctx, GPUBPE_EINVAL, "sequence %llu holds a token id the merge table does not cover",
+                        (unsigned long long)i);
+    return GPUBPE_OK;
+}
+
 extern "C" __attribute__((visibility("default"))) int gpubpe_junction_bits(gpubpe_ctx *ctx, uint32_t *h_out) {
     if (!ctx || !h_out) return GPUBPE_EINVAL;
     if (ctx->h_jbits.size() != 2048) return fail(ctx, GPUBPE_EINVAL, "context has no junction bitmap");
@@ -1328,7 +1377,7 @@ extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe
     if (ctx->h_state_ss) cudaFreeHost(ctx->h_state_ss);
     if (ctx->d_vinfo) cudaFree(ctx->d_vinfo);
     if (ctx->d_vblob) cudaFree(ctx->d_vblob);
-    for (DevBuf *b : {&ctx->dec_state, &ctx->dec_status, &ctx->pt_bits})
+    for (DevBuf *b : {&ctx->dec_state, &ctx->dec_status, &ctx->pt_bits, &ctx->mt_offs, &ctx->mt_counts})
         if (b->p) cudaFree(b->p);
     if (ctx->d_pt_classes) cudaFree(ctx->d_pt_classes);
     for (auto &e : ctx->io_ev)

@@ -517,3 +517,65 @@ def test_run_sweep_and_profile_run_on_the_device(tokenizer, oracle, prose_sample
     assert prof.counters.passes == sum(map(len, prose_samples[:10])) - sum(
         len(x) for x in bpe.tokenize_batch(prose_samples[:10], tokenizer).token_ids)
     assert prof.end_to_end_ms >= prof.engine_ms >= 0 and abs(sum(prof.event_shares.values()) - 1.0) < 1e-9
+
+
+def _tiny():
+    from types import SimpleNamespace
+
+    symbols = {"a": 5, "b": 9, "c": 13, "d": 21, "e": 34, "f": 55,
+               "ab": 100, "abc": 101, "cd": 103, "ef": 105, "bc": 107}
+    rules = bpe.parse_merges("a b\nab c\nc d\ne f\nb c\n", bpe.Vocab(symbols))
+    return SimpleNamespace(symbols=symbols, table=bpe.build_table(rules),
+                           encode=lambda text: [symbols[ch] for ch in text],
+                           pair_map={(r.left, r.right): (r.rank, r.new_token) for r in rules})
+
+
+def test_token_level_engines_known_answers():
+    """sequential_bpe / run_block_engine on token ids (engines.py:269-403) on the
+    device: the reference's known answers, traces and counters."""
+    tiny = _tiny()
+    assert bpe.sequential_bpe([], tiny.table)[0].tolist() == []
+    trace = []
+    out, c = bpe.sequential_bpe(tiny.encode("abcd"), tiny.table, trace=trace)
+    assert out.tolist() == [101, 21] and c.passes == 2 and trace == [0, 1]
+    assert (c.lookups, c.compaction_moves, c.buffer_allocations) == (3 + 1 + 1, 0, 0)
+    trace = []
+    out, _ = bpe.sequential_bpe(tiny.encode("abab"), tiny.table, trace=trace)
+    assert out.tolist() == [100, 100] and trace == [0, 0]
+    out, c = bpe.run_block_engine(tiny.encode("abcd"), tiny.table)
+    assert out.tolist() == [101, 21]
+    assert (c.passes, c.buffer_allocations, c.lookups, c.compaction_moves) == (2, 2, 6, 5)
+    with pytest.raises(bpe.errors.SequenceTooLong):
+        bpe.run_block_engine(list(range(10)), tiny.table, bpe.BlockConfig(max_seq_len=8))
+    with pytest.raises(ValueError):
+        bpe.run_block_engine([5, 9], tiny.table, variant="fast")
+
+
+def test_token_level_engines_match_greedy(tokenizer, oracle, oracle_tables):
+    """Random tiny texts against the naive greedy (trace and lookups included),
+    and GPT-2 prose / random bytes against the C oracle's sequential_bpe."""
+    import random as _r
+
+    from oracle.oracle import greedy_merge
+
+    tiny = _tiny()
+    rng = _r.Random(5)
+    for _ in range(200):
+        ids = tiny.encode("".join(rng.choice("abcdef") for _ in range(rng.randrange(0, 40))))
+        trace = []
+        out, c = bpe.sequential_bpe(ids, tiny.table, trace=trace)
+        assert out.tolist() == greedy_merge(ids, tiny.pair_map), ids
+        assert c.passes == len(ids) - len(out) and len(trace) == c.passes
+        assert trace == sorted(trace)
+    for doc in fixtures.prose_samples()[:5] + [bytes(rng.randrange(256) for _ in range(3000))]:
+        ids = tokenizer.encode(doc)
+        want, want_trace = oracle.sequential_bpe(ids, with_trace=True)
+        trace = []
+        out, c = bpe.sequential_bpe(ids, tokenizer.table, trace=trace)
+        assert np.array_equal(out, want)
+        assert trace == want_trace.tolist()
+        out2, c2 = bpe.run_block_engine(ids[:8192], tokenizer.table, tokenizer.config)
+        assert np.array_equal(out2, oracle.sequential_bpe(ids[:8192]))
+    # ids outside the table never merge and stay in place
+    out, _ = bpe.sequential_bpe([5, 9, 999999, 5, 9, 13], tiny.table)
+    assert out.tolist() == [100, 999999, 101]
