@@ -344,12 +344,18 @@ def main():
     import paper_2603_02597_b200 as bpe
     import fixtures
 
+    if os.environ.get("GPUBPE_BENCH_SHARE_GPU"):  # test only: several ranks on one GPU
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("GPUBPE_BENCH_BACKEND", "nccl")  # gloo: test of the rank logic only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     if args.workload.startswith("corpus"):
         run_corpus(args, rank, world, local, dist)
         return
