@@ -26,4 +26,6 @@ for W in ${WORKLOADS:-c1_131k corpus_256m}; do
 done
 GPUBPE_PROFILE_TIMED=1 timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_pretok -c 1 \
   -o gpurun_out/prof_${TAG}_pretok -f python tools/perf.py --only rx_corpus_256m --iters 1 --warmup 1 --no-flush > gpurun_out/ncu_${TAG}_pretok.log 2>&1
+GPUBPE_PROFILE_TIMED=1 timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_decode -c 1 \
+  -o gpurun_out/prof_${TAG}_decode_corpus_256m -f python tools/perf.py --only decode_corpus_256m --iters 1 --warmup 1 --no-flush > gpurun_out/ncu_${TAG}_decode.log 2>&1
 cat gpurun_out/perf_${TAG}.log; tail -3 gpurun_out/bench_${TAG}.log | cut -c1-600; tail -2 gpurun_out/bench_ref_${TAG}.log | cut -c1-400

@@ -23,6 +23,7 @@ KEYS = {
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "lts__t_bytes.sum": "l2_bytes",
     "launch__registers_per_thread": "registers",
     "launch__grid_size": "grid",
     "launch__block_size": "block",
