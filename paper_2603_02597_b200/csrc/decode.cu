@@ -130,10 +130,13 @@ __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant_
             }
             if (lane < DT / 32) S.wsum[lane] = x - v;  // exclusive warp offsets
             const uint32_t total = __shfl_sync(FULL_MASK, x, 31);
-            // decoupled look-back over tiles (value+flag+epoch in one word)
+            // the tile's output offset: precomputed (two-pass mode) or a decoupled
+            // look-back over tiles (value+flag+epoch in one word)
             const unsigned long long tag = (unsigned long long)P.epoch << 44;
             unsigned long long excl = 0;
-            if (t == 0) {
+            if (P.tile_base) {
+                excl = P.tile_base[t];
+            } else if (t == 0) {
                 if (lane == 0) st_rel(&P.status[0], tag | (2ull << 42) | total);
             } else {
                 if (lane == 0) st_rel(&P.status[t], tag | (1ull << 42) | total);
@@ -272,6 +275,81 @@ __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant_
         if (t + 1 == P.n_tiles && tid == 0) P.st->n_bytes = base + total;
         __syncthreads();
     }
+}
+
+// ---- two-pass mode: tile byte totals (one CTA per tile, every CTA at once),
+//      then one CTA scans them into tile offsets; k_decode then needs no look-back
+__global__ void __launch_bounds__(256) k_dec_tile_bytes(const __grid_constant__ DecodeParams P,
+                                                        unsigned long long *tile_bytes) {
+    __shared__ unsigned long long red[8];
+    const unsigned long long t = blockIdx.x, t0 = t * TD;
+    unsigned long long sum = 0;
+    for (unsigned long long i = t0 + threadIdx.x * 4; i < min(P.n_ids, t0 + TD); i += 256 * 4) {
+        uint32_t id[4];
+        if (P.aligned && i + 4 <= P.n_ids) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(P.ids + i));
+            id[0] = v.x; id[1] = v.y; id[2] = v.z; id[3] = v.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) id[j] = i + j < P.n_ids ? __ldg(&P.ids[i + j]) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (i + j >= P.n_ids) break;
+            const uint32_t inf = info_of(P, id[j]);
+            if (inf == GPUBPE_INF) atomicMin(&P.st->bad, i + j);
+            else sum += inf & 0xFFu;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL_MASK, sum, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < 8; ++w) s += red[w];
+        tile_bytes[t] = s;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_dec_scan(const unsigned long long *tile_bytes, unsigned long long n,
+                                                   unsigned long long *tile_base) {
+    __shared__ unsigned long long wsum[32];
+    const unsigned long long per = (n + 1023) / 1024, lo = min(n, threadIdx.x * per), hi = min(n, lo + per);
+    unsigned long long s = 0;
+    for (unsigned long long i = lo; i < hi; ++i) s += tile_bytes[i];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL_MASK, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned long long v = wsum[lane], y2 = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(FULL_MASK, y2, o);
+            if (lane >= o) y2 += y;
+        }
+        wsum[lane] = y2 - v;
+    }
+    __syncthreads();
+    unsigned long long run = wsum[wid] + x - s;
+    for (unsigned long long i = lo; i < hi; ++i) {
+        tile_base[i] = run;
+        run += tile_bytes[i];
+    }
+}
+
+cudaError_t launch_decode_offsets(const DecodeParams &P, unsigned long long *tile_bytes,
+                                  unsigned long long *tile_base, cudaStream_t s) {
+    if (P.n_tiles == 0) return cudaSuccess;
+    k_dec_tile_bytes<<<(unsigned int)P.n_tiles, 256, 0, s>>>(P, tile_bytes);
+    k_dec_scan<<<1, 1024, 0, s>>>(tile_bytes, P.n_tiles, tile_base);
+    return cudaGetLastError();
 }
 
 size_t decode_smem_bytes() { return sizeof(DecSmem); }

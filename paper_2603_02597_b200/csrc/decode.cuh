@@ -21,7 +21,8 @@ struct DecodeParams {
     unsigned long long out_cap;
     long long *out_offs;       // [n_seqs + 1] byte offsets
     DecodeState *st;
-    unsigned long long *status;  // [n_tiles] look-back words
+    unsigned long long *status;  // [n_tiles] look-back words (single-pass mode)
+    const unsigned long long *tile_base;  // [n_tiles] output offset of each tile (two-pass mode), or null
     unsigned long long n_tiles;
     unsigned int epoch;
     int aligned;               // ids pointer is 16-B aligned
@@ -33,4 +34,6 @@ int decode_tile_ids();
 cudaError_t setup_decode();
 cudaError_t decode_occupancy(int *blocks);
 cudaError_t launch_decode(const DecodeParams &P, int grid, cudaStream_t s);
+cudaError_t launch_decode_offsets(const DecodeParams &P, unsigned long long *tile_bytes,
+                                  unsigned long long *tile_base, cudaStream_t s);
 #endif

@@ -579,3 +579,23 @@ def test_token_level_engines_match_greedy(tokenizer, oracle, oracle_tables):
     # ids outside the table never merge and stay in place
     out, _ = bpe.sequential_bpe([5, 9, 999999, 5, 9, 13], tiny.table)
     assert out.tolist() == [100, 999999, 101]
+
+
+def test_decode_two_pass_large_batch(tokenizer):
+    """A batch of ~7.5 M ids decodes through the two-pass path (tile totals +
+    scan, no look-back): byte-exact round trip and offsets."""
+    import torch
+    import synth_corpus
+
+    data, offs = synth_corpus.corpus_docs(32 << 20, seed=1)
+    enc = tokenizer.device_encoder()
+    d = torch.from_numpy(data).cuda()
+    o = torch.from_numpy(offs).cuda()
+    ids, ioffs, _ = enc.encode_tensors(d, o, 8192, 8192)
+    assert ids.numel() > 4 * 148 * 8192
+    out = torch.empty(data.size + 64, dtype=torch.uint8, device="cuda")
+    oo = torch.empty_like(ioffs)
+    n = enc.decode_into(ids, ioffs, out, oo)
+    assert n == data.size
+    assert torch.equal(out[:data.size], d)
+    assert torch.equal(oo, o)
