@@ -22,7 +22,7 @@
 #include "decode.cuh"
 
 #ifndef GPUBPE_DEC_DT
-#define GPUBPE_DEC_DT 1024
+#define GPUBPE_DEC_DT 512
 #endif
 
 namespace {
