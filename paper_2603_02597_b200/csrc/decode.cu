@@ -38,6 +38,7 @@ struct DecSmem {
     uint32_t goff[TD / 4];           // output offset of each 4-id group inside the tile
     uint32_t wsum[DT / 32];
     unsigned long long base, need;
+    long long seq_cur;               // first sequence not before the previous tile (tiles of a CTA ascend)
     uint32_t total;
     __align__(16) uint8_t stage[STAGE + 32];
 };
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant_
     extern __shared__ __align__(16) unsigned char dsm_raw[];
     DecSmem &S = *reinterpret_cast<DecSmem *>(dsm_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) S.seq_cur = 0;
     for (;;) {
         if (tid == 0) S.base = atomicAdd(&P.st->tile_ctr, 1ull);
         __syncthreads();
@@ -216,11 +218,13 @@ __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant_
             }
         }
         __syncthreads();
-        if (staged && fits) {
+        // the last warp fixes the sequence offsets while the others store the stage
+        const int nstore = P.n_seqs ? DT - 32 : DT;
+        if (staged && fits && tid < nstore) {
             // chunk q of the stage covers global [(base & ~15) + 16q, +16)
             const uint32_t end = shift + total, nq = (end + 15) >> 4;
             uint8_t *gdst = P.out + (base & ~15ull);
-            for (uint32_t q = tid; q < nq; q += DT) {
+            for (uint32_t q = tid; q < nq; q += nstore) {
                 const uint32_t lo = q * 16, hi = lo + 16;
                 if (lo >= shift && hi <= end) {
                     reinterpret_cast<uint4 *>(gdst)[q] = reinterpret_cast<const uint4 *>(S.stage)[q];
@@ -230,9 +234,17 @@ __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant_
             }
         }
         // ---- byte offsets of the sequences that start in this tile
-        if (P.n_seqs && wid == 0) {
-            // first sequence with id_offs >= t0 (lower bound, 32-ary)
-            long long lo = 0, hi = (long long)P.n_seqs;
+        if (P.n_seqs && wid == DT / 32 - 1) {
+            // first sequence with id_offs >= t0: the 32 after the cursor first, else a
+            // 32-ary lower bound beyond them
+            long long lo = S.seq_cur, hi = (long long)P.n_seqs;
+            {
+                const long long idx = lo + lane;
+                const bool lt = idx < hi && (unsigned long long)__ldg(&P.id_offs[idx]) < t0;
+                const unsigned m = __ballot_sync(FULL_MASK, lt);
+                if (m != FULL_MASK) hi = lo = lo + __popc(m);
+                else lo += 32;
+            }
             while (hi > lo) {
                 const long long step = (hi - lo + 31) / 32;
                 const long long idx = lo + (long long)lane * step;
@@ -243,6 +255,7 @@ __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant_
                 lo = lo + (long long)l * step + 1;
                 hi = min(hi, lo - 1 + step);
             }
+            if (lane == 0) S.seq_cur = lo;
             const bool last_tile = t + 1 == P.n_tiles;
             for (long long d0 = lo;; d0 += 32) {
                 const long long d = d0 + lane;
