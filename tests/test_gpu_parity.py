@@ -599,3 +599,47 @@ def test_decode_two_pass_large_batch(tokenizer):
     assert n == data.size
     assert torch.equal(out[:data.size], d)
     assert torch.equal(oo, o)
+
+
+def test_integration_stub_binding(tokenizer, prose_samples):
+    """The ctypes binding INTEGRATION.md shows a lanebpe maintainer (host buffers,
+    no torch, no memo strings) gives the same ids as tokenize_batch."""
+    import ctypes
+
+    from paper_2603_02597_b200 import _native
+
+    lib = ctypes.CDLL(str(_native.LIB_PATH))
+    vp, u64 = ctypes.c_void_p, ctypes.c_uint64
+    lib.gpubpe_ctx_create.argtypes = [ctypes.c_int, vp, vp, vp, vp, vp, u64, vp, vp, vp, u64,
+                                      ctypes.c_uint32, ctypes.POINTER(vp)]
+    lib.gpubpe_encode_host.argtypes = [vp, vp, u64, vp, u64, u64, u64, vp, vp,
+                                       ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_float), vp]
+    lib.gpubpe_last_error.restype = ctypes.c_char_p
+    lib.gpubpe_ctx_destroy.argtypes = [vp]
+    keys, vals = tokenizer.table.keys, tokenizer.table.values
+    live = keys != np.uint64(2**64 - 1)
+    left = (keys[live] >> np.uint64(32)).astype(np.uint32)
+    right = (keys[live] & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    new = (vals[live] >> np.uint64(32)).astype(np.uint32)
+    rank = (vals[live] & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    base = np.ascontiguousarray(tokenizer._base_ids, np.uint32)
+    h = vp()
+    p = lambda a: a.ctypes.data  # noqa: E731
+    rc = lib.gpubpe_ctx_create(0, p(base), p(left), p(right), p(rank), p(new), len(left), None, None, None, 0, 0,
+                               ctypes.byref(h))
+    assert rc == 0, lib.gpubpe_last_error(h)
+    try:
+        texts = prose_samples[:20] + [b"", b"hello world"]
+        data = np.frombuffer(b"".join(texts), np.uint8)
+        offs = np.zeros(len(texts) + 1, np.int64)
+        offs[1:] = np.cumsum([len(x) for x in texts])
+        ids = np.empty(max(len(data), 1), np.uint32)
+        oo = np.empty(len(texts) + 1, np.int64)
+        n, ms = u64(), ctypes.c_float()
+        rc = lib.gpubpe_encode_host(h, p(data), len(data), p(offs), len(texts), 8192, 8192, p(ids), p(oo),
+                                    ctypes.byref(n), ctypes.byref(ms), None)
+        assert rc == 0, lib.gpubpe_last_error(h)
+        got = [ids[oo[i]:oo[i + 1]] for i in range(len(texts))]
+        assert_same(got, bpe.tokenize_batch(texts, tokenizer).token_ids, "stub")
+    finally:
+        lib.gpubpe_ctx_destroy(h)
