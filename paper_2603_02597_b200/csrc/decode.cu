@@ -296,22 +296,30 @@ __global__ void __launch_bounds__(256) k_dec_tile_bytes(const __grid_constant__ 
                                                         unsigned long long *tile_bytes) {
     __shared__ unsigned long long red[8];
     const unsigned long long t = blockIdx.x, t0 = t * TD;
+    constexpr int IT = TD / (256 * 4);  // 4-id groups per thread, all loads issued together
     unsigned long long sum = 0;
-    for (unsigned long long i = t0 + threadIdx.x * 4; i < min(P.n_ids, t0 + TD); i += 256 * 4) {
-        uint32_t id[4];
+    uint32_t id[IT][4];
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+        const unsigned long long i = t0 + (unsigned long long)k * 1024 + threadIdx.x * 4;
         if (P.aligned && i + 4 <= P.n_ids) {
             const uint4 v = __ldg(reinterpret_cast<const uint4 *>(P.ids + i));
-            id[0] = v.x; id[1] = v.y; id[2] = v.z; id[3] = v.w;
+            id[k][0] = v.x; id[k][1] = v.y; id[k][2] = v.z; id[k][3] = v.w;
         } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) id[j] = i + j < P.n_ids ? __ldg(&P.ids[i + j]) : 0u;
+            for (int j = 0; j < 4; ++j) id[k][j] = i + j < P.n_ids ? __ldg(&P.ids[i + j]) : 0u;
         }
+    }
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+        const unsigned long long i = t0 + (unsigned long long)k * 1024 + threadIdx.x * 4;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            if (i + j >= P.n_ids) break;
-            const uint32_t inf = info_of(P, id[j]);
-            if (inf == GPUBPE_INF) atomicMin(&P.st->bad, i + j);
-            else sum += inf & 0xFFu;
+            if (i + j < P.n_ids) {
+                const uint32_t inf = info_of(P, id[k][j]);
+                if (inf == GPUBPE_INF) atomicMin(&P.st->bad, i + j);
+                else sum += inf & 0xFFu;
+            }
         }
     }
 #pragma unroll
