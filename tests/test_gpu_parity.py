@@ -643,3 +643,32 @@ def test_integration_stub_binding(tokenizer, prose_samples):
         assert_same(got, bpe.tokenize_batch(texts, tokenizer).token_ids, "stub")
     finally:
         lib.gpubpe_ctx_destroy(h)
+
+
+def test_random_batches_random_configs_match_oracle(tokenizer, oracle):
+    """Fuzz: random batches (prose, random bytes, runs, empty documents) under
+    random chunking configs (tiny chunk budgets included) equal the oracle."""
+    import synth_corpus
+
+    rng = np.random.default_rng(2024)
+    prose = synth_corpus.english_bytes(1 << 20, 9)
+    for trial in range(25):
+        docs = []
+        for _ in range(int(rng.integers(1, 40))):
+            n = int(np.exp(rng.uniform(0, np.log(60000)))) if rng.random() > 0.1 else 0
+            kind = rng.integers(0, 4)
+            if kind == 0:
+                at = int(rng.integers(0, len(prose) - n - 1)) if n < len(prose) - 1 else 0
+                docs.append(prose[at:at + n])
+            elif kind == 1:
+                docs.append(rng.integers(0, 256, n, dtype=np.uint8).tobytes())
+            elif kind == 2:
+                docs.append(bytes([int(rng.choice(list(b"a1 \n.\x00")))]) * n)
+            else:
+                docs.append(bytes(rng.choice(list(b"ab cd\n12"), n).tolist()))
+        msl = int(rng.choice([2, 3, 17, 100, 1000, 8192, 1 << 40]))
+        cb = msl if msl >= 1 << 40 or rng.random() < 0.3 else int(rng.integers(2, msl + 1))
+        tok = with_config(tokenizer, msl, cb)
+        got = bpe.tokenize_batch(docs, tok).token_ids
+        want = oracle.encode_docs(docs, msl, cb)
+        assert_same(got, want, f"trial {trial} msl {msl} cb {cb}")
