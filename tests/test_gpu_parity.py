@@ -672,3 +672,38 @@ def test_random_batches_random_configs_match_oracle(tokenizer, oracle):
         got = bpe.tokenize_batch(docs, tok).token_ids
         want = oracle.encode_docs(docs, msl, cb)
         assert_same(got, want, f"trial {trial} msl {msl} cb {cb}")
+
+
+@pytest.mark.parametrize("well_formed", [True, False])
+def test_token_engine_random_tables_match_greedy(well_formed):
+    """The device engines on random merge tables (well-formed: multi-merge passes;
+    not: strict one-merge passes) equal the naive greedy on random sequences."""
+    import random as _r
+
+    from oracle.oracle import greedy_merge
+
+    rng = _r.Random(7 if well_formed else 8)
+    for trial in range(6):
+        k = rng.randrange(3, 8)
+        tokens = list(range(k))
+        rules, seen = [], set()
+        pending = []
+        for rank in range(rng.randrange(10, 60)):
+            a, b = rng.choice(tokens), rng.choice(tokens)
+            if (a, b) in seen:
+                continue
+            seen.add((a, b))
+            new = 100 + len(rules)
+            rules.append(bpe.MergeRule(a, b, len(rules), new))
+            tokens.append(new)
+        if not well_formed:  # ranks shuffled: rules may use tokens produced at higher ranks
+            ranks = list(range(len(rules)))
+            rng.shuffle(ranks)
+            rules = [bpe.MergeRule(r.left, r.right, ranks[i], r.new_token) for i, r in enumerate(rules)]
+        table = bpe.build_table(sorted(rules, key=lambda r: r.rank))
+        pair_map = {(r.left, r.right): (r.rank, r.new_token) for r in rules}
+        for _ in range(40):
+            ids = [rng.randrange(k) for _ in range(rng.randrange(0, 60))]
+            out, c = bpe.sequential_bpe(ids, table)
+            assert out.tolist() == greedy_merge(ids, pair_map), (trial, ids)
+            assert c.passes == len(ids) - len(out)
