@@ -707,3 +707,49 @@ def test_token_engine_random_tables_match_greedy(well_formed):
             out, c = bpe.sequential_bpe(ids, table)
             assert out.tolist() == greedy_merge(ids, pair_map), (trial, ids)
             assert c.passes == len(ids) - len(out)
+
+
+@pytest.mark.parametrize("well_formed", [True, False])
+def test_byte_level_random_tables_match_oracle(well_formed):
+    """k_encode (junction cuts, memo verification, warp / CTA / grid engines) with
+    random byte-level merge tables, well-formed or not, against the C oracle on
+    texts with long runs (deferred and giant segments)."""
+    import random as _r
+
+    from oracle.oracle import OracleEncoder
+
+    rng = _r.Random(21 if well_formed else 22)
+    enc = bpe.build_byte_encoder()
+    b2s = {b: s for s, b in enc.symbol_to_byte.items()}
+    symbols = {b2s[b]: b for b in range(256)}
+    alphabet = b"abc d\n1"
+    sym_of = {b: b2s[b] for b in range(256)}
+    ids = [b for b in alphabet]
+    rules, next_id = [], 256
+    for _ in range(120):
+        a, b = rng.choice(ids), rng.choice(ids)
+        s = sym_of[a] + sym_of[b]
+        if s in symbols or len(s) > 40:
+            continue
+        symbols[s] = next_id
+        sym_of[next_id] = s
+        rules.append(bpe.MergeRule(a, b, len(rules), next_id))
+        ids.append(next_id)
+        next_id += 1
+    if not well_formed:
+        ranks = list(range(len(rules)))
+        rng.shuffle(ranks)
+        rules = [bpe.MergeRule(r.left, r.right, ranks[i], r.new_token) for i, r in enumerate(rules)]
+        rules.sort(key=lambda r: r.rank)
+    tok = bpe.Tokenizer(bpe.Vocab(symbols), bpe.build_table(rules),
+                        bpe.BlockConfig(max_seq_len=1 << 40, chunk_budget=1 << 40))
+    left, right, rank, new = tok.rule_arrays()
+    orc = OracleEncoder(tok._base_ids, left, right, rank, new)
+    docs = []
+    for _ in range(60):
+        n = rng.choice([0, 1, 5, 50, 500, 5000, 20000])
+        docs.append(bytes(rng.choice(alphabet) for _ in range(n)))
+    docs += [b"a" * 30000, b"ab" * 9000, b"1" * 70000, b"abc d" * 3000]
+    got = bpe.tokenize_batch(docs, tok).token_ids
+    want = orc.encode_docs(docs, 1 << 40, 1 << 40)
+    assert_same(got, want, f"well_formed={well_formed}")
