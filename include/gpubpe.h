@@ -197,6 +197,14 @@ int gpubpe_parse_merges(int device, const uint8_t *sym_bytes, const uint64_t *sy
  * fused persistent k_encode. */
 int gpubpe_launches_per_encode(void);
 
+/* gpubpe_encode_host for a batch given as n_docs separate host buffers
+ * (h_ptrs[d], h_lens[d]): the documents are gathered (in parallel) straight
+ * into the pinned staging buffer -- one host copy instead of a join plus a
+ * staging copy.  Same outputs and errors as gpubpe_encode_host. */
+int gpubpe_encode_host_gather(gpubpe_ctx *ctx, const uint64_t *h_ptrs, const uint64_t *h_lens, uint64_t n_docs,
+                              uint64_t max_seq_len, uint64_t chunk_budget, uint32_t *h_out_ids,
+                              int64_t *h_out_offs, uint64_t *n_ids_out, float *kernel_ms, void *stream);
+
 /* Device-side probe of the packed pair table: for i < n, (d_left[i],
  * d_right[i]) -> d_new[i], d_rank[i] (0xFFFFFFFF rank on miss).  Replaces
  * PackedPairTable.lookup_pairs (merge_table.py:232-243); used by the table

@@ -48,6 +48,8 @@ SIGNATURES = {
     "gpubpe_encode": (_int, [_vp, _vp, _u64, _vp, _u64, _u64, _u64, _vp, _vp, _vp]),
     "gpubpe_encode_host": (_int, [_vp, _vp, _u64, _vp, _u64, _u64, _u64, _vp, _vp,
                                   ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_float), _vp]),
+    "gpubpe_encode_host_gather": (_int, [_vp, _vp, _vp, _u64, _u64, _u64, _vp, _vp,
+                                         ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_float), _vp]),
     "gpubpe_host_alloc": (_int, [_int, _u64, ctypes.POINTER(_vp)]),
     "gpubpe_host_free": (None, [_vp]),
     "gpubpe_query": (_int, [_vp, _vp, ctypes.POINTER(Stats)]),

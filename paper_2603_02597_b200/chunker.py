@@ -221,17 +221,22 @@ def _as_bytes(text) -> bytes:
     return text.encode("utf-8") if isinstance(text, str) else bytes(text)
 
 
+def _as_parts(texts) -> list:
+    """Every input as bytes (str UTF-8 encoded); BatchError(i) on a bad item."""
+    if type(texts) is list and all(type(t) is bytes for t in texts):
+        return texts  # already bytes: no per-item conversion
+    parts = []
+    for i, text in enumerate(texts):
+        try:
+            parts.append(_as_bytes(text))
+        except (TypeError, ValueError, UnicodeError) as exc:
+            raise BatchError(i, str(exc)) from exc
+    return parts
+
+
 def pack_texts(texts) -> tuple[np.ndarray, np.ndarray]:
     """list[str|bytes] -> (uint8 data, int64 offsets); BatchError(i) on a bad item."""
-    if type(texts) is list and all(type(t) is bytes for t in texts):
-        parts = texts  # already bytes: no per-item conversion
-    else:
-        parts = []
-        for i, text in enumerate(texts):
-            try:
-                parts.append(_as_bytes(text))
-            except (TypeError, ValueError, UnicodeError) as exc:
-                raise BatchError(i, str(exc)) from exc
+    parts = _as_parts(texts)
     n = len(parts)
     offs = np.zeros(n + 1, dtype=np.int64)
     if n == 1:
@@ -259,18 +264,22 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
         raise ValueError(f"unknown pretokenize {pretokenize!r}, expected None or 'gpt2'")
     cfg = tokenizer.config
     t0 = time.perf_counter()
-    data, offs = pack_texts(texts)
+    parts = _as_parts(texts)
     encode_ms = (time.perf_counter() - t0) * 1000.0
-    n_docs = len(offs) - 1
+    n_docs = len(parts)
     if n_docs == 0:
         return BatchResult([], 0.0, encode_ms, 0.0, PassCounters())
     try:
         enc = tokenizer.device_encoder()
         from ._native import MODE_DEFAULT, MODE_GPT2_REGEX
 
-        ids, out_offs, st, engine_ms = enc.encode_packed_host(
-            data, offs, cfg.max_seq_len, cfg.chunk_budget,
-            MODE_GPT2_REGEX if pretokenize == "gpt2" else MODE_DEFAULT)
+        mode = MODE_GPT2_REGEX if pretokenize == "gpt2" else MODE_DEFAULT
+        if n_docs == 1:  # one buffer: staged piecewise, overlapping its DMA
+            data = np.frombuffer(parts[0], dtype=np.uint8)
+            ids, out_offs, st, engine_ms = enc.encode_packed_host(
+                data, np.array([0, data.size], np.int64), cfg.max_seq_len, cfg.chunk_budget, mode)
+        else:  # many: gathered natively into pinned memory, no join here
+            ids, out_offs, st, engine_ms = enc.encode_list_host(parts, cfg.max_seq_len, cfg.chunk_budget, mode)
     except DeviceError:
         raise
     except TokenizerError as exc:  # pragma: no cover - the device reports no per-input errors
@@ -279,5 +288,5 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
     o = out_offs.tolist()
     token_ids = [ids[a:b] for a, b in zip(o, o[1:])]
     assemble_ms = (time.perf_counter() - t2) * 1000.0
-    counters = PassCounters(passes=int(data.size) - int(ids.size), buffer_allocations=int(st["allocations"]))
+    counters = PassCounters(passes=int(st["n_bytes"]) - int(ids.size), buffer_allocations=int(st["allocations"]))
     return BatchResult(token_ids, engine_ms, encode_ms, assemble_ms, counters, st)

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <cstdarg>
@@ -670,42 +671,35 @@ class CopyPool {
         return *p;
     }
     unsigned workers() const { return (unsigned)th_.size(); }
-    void copy(uint8_t *dst, const uint8_t *src, size_t n, unsigned parts) {
-        const size_t chunk = (n + parts - 1) / parts;
+    // Runs part(0) .. part(parts - 1): the caller takes part 0 and whatever the
+    // workers have not picked up when it is done, then waits for the rest.
+    void run(unsigned parts, const std::function<void(unsigned)> &part) {
         {
             std::lock_guard<std::mutex> g(m_);
             for (unsigned i = 1; i < parts; ++i) {
-                const size_t lo = i * chunk, hi = std::min(n, lo + chunk);
-                if (lo < hi) {
-                    jobs_.push_back({dst + lo, src + lo, hi - lo});
-                    ++pending_;
-                }
+                jobs_.push_back([&part, i] { part(i); });
+                ++pending_;
             }
         }
         cv_.notify_all();
-        memcpy(dst, src, std::min(n, chunk));
-        for (;;) {  // help with what the workers have not picked up yet, then wait
-            Job j;
+        part(0);
+        for (;;) {
+            std::function<void()> j;
             {
                 std::unique_lock<std::mutex> g(m_);
                 if (jobs_.empty()) {
                     done_.wait(g, [&] { return pending_ == 0; });
                     return;
                 }
-                j = jobs_.back();
+                j = std::move(jobs_.back());
                 jobs_.pop_back();
             }
-            memcpy(j.d, j.s, j.n);
+            j();
             finish();
         }
     }
 
   private:
-    struct Job {
-        uint8_t *d;
-        const uint8_t *s;
-        size_t n;
-    };
     CopyPool() {
         const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
         const unsigned nw = std::min(7u, hw - 1);
@@ -718,21 +712,21 @@ class CopyPool {
     }
     void loop() {
         for (;;) {
-            Job j;
+            std::function<void()> j;
             {
                 std::unique_lock<std::mutex> g(m_);
                 cv_.wait(g, [&] { return !jobs_.empty(); });
-                j = jobs_.back();
+                j = std::move(jobs_.back());
                 jobs_.pop_back();
             }
-            memcpy(j.d, j.s, j.n);
+            j();
             finish();
         }
     }
     std::vector<std::thread> th_;
     std::mutex m_;
     std::condition_variable cv_, done_;
-    std::vector<Job> jobs_;
+    std::vector<std::function<void()>> jobs_;
     size_t pending_ = 0;
 };
 }  // namespace
@@ -745,7 +739,34 @@ static void copy_par(void *dst, const void *src, size_t n) {
     }
     CopyPool &pool = CopyPool::get();
     const unsigned parts = (unsigned)std::min<size_t>(pool.workers() + 1, (n + per - 1) / per);
-    pool.copy(static_cast<uint8_t *>(dst), static_cast<const uint8_t *>(src), n, parts);
+    const size_t chunk = (n + parts - 1) / parts;
+    pool.run(parts, [&](unsigned i) {
+        const size_t lo = i * chunk, hi = std::min(n, lo + chunk);
+        if (lo < hi) memcpy(static_cast<uint8_t *>(dst) + lo, static_cast<const uint8_t *>(src) + lo, hi - lo);
+    });
+}
+
+// Gather documents (ptrs[d], lens[d]) back to back into dst (offs = their
+// prefix sums): byte ranges split across the copy pool above 8 MiB.
+static void gather_par(uint8_t *dst, const uint64_t *ptrs, const uint64_t *lens, const int64_t *offs,
+                       uint64_t n_docs) {
+    const uint64_t n = (uint64_t)offs[n_docs];
+    auto range = [&](uint64_t lo, uint64_t hi) {  // copy bytes [lo, hi) of the packed batch
+        uint64_t d = (uint64_t)(std::upper_bound(offs, offs + n_docs + 1, (int64_t)lo) - offs) - 1;
+        for (; d < n_docs && (uint64_t)offs[d] < hi; ++d) {
+            const uint64_t a = std::max<uint64_t>(lo, offs[d]), b = std::min<uint64_t>(hi, offs[d + 1]);
+            if (a < b) memcpy(dst + a, reinterpret_cast<const uint8_t *>(ptrs[d]) + (a - offs[d]), b - a);
+        }
+    };
+    const size_t per = 4u << 20;
+    if (n <= 2 * per) {
+        range(0, n);
+        return;
+    }
+    CopyPool &pool = CopyPool::get();
+    const unsigned parts = (unsigned)std::min<size_t>(pool.workers() + 1, (n + per - 1) / per);
+    const uint64_t chunk = (n + parts - 1) / parts;
+    pool.run(parts, [&](unsigned i) { range(std::min(n, i * chunk), std::min(n, (i + 1) * chunk)); });
 }
 
 static int ensure_pinned(gpubpe_ctx *ctx, size_t bytes) {
@@ -976,6 +997,15 @@ static int encode_host_streamed(gpubpe_ctx *ctx, const uint8_t *h_bytes, const i
     return GPUBPE_OK;
 }
 
+// Copies bytes [lo, hi) of the batch to dst (gather entry point: documents
+// in separate buffers); null for a contiguous h_bytes.
+using StageFn = std::function<void(uint8_t *dst, uint64_t lo, uint64_t hi)>;
+
+static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const StageFn *stage, uint64_t n_bytes,
+                            const int64_t *h_doc_offs, uint64_t n_docs, uint64_t max_seq_len, uint64_t chunk_budget,
+                            uint32_t *h_out_ids, int64_t *h_out_offs, uint64_t *n_ids_out, float *kernel_ms,
+                            void *stream);
+
 extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     gpubpe_ctx *ctx, const uint8_t *h_bytes, uint64_t n_bytes, const int64_t *h_doc_offs, uint64_t n_docs,
     uint64_t max_seq_len, uint64_t chunk_budget, uint32_t *h_out_ids, int64_t *h_out_offs,
@@ -983,6 +1013,14 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     if (!ctx) return GPUBPE_EINVAL;
     if (!n_ids_out || (n_docs && (!h_doc_offs || !h_out_offs)) || (n_bytes && (!h_bytes || !h_out_ids)))
         return fail(ctx, GPUBPE_EINVAL, "null host pointer");
+    return encode_host_core(ctx, h_bytes, nullptr, n_bytes, h_doc_offs, n_docs, max_seq_len, chunk_budget, h_out_ids,
+                            h_out_offs, n_ids_out, kernel_ms, stream);
+}
+
+static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const StageFn *stage, uint64_t n_bytes,
+                            const int64_t *h_doc_offs, uint64_t n_docs, uint64_t max_seq_len, uint64_t chunk_budget,
+                            uint32_t *h_out_ids, int64_t *h_out_offs, uint64_t *n_ids_out, float *kernel_ms,
+                            void *stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->alloc_mark = ctx->n_allocs;
     struct HostCall {  // gpubpe_encode calls below keep this call's allocation mark
@@ -998,14 +1036,15 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
         const char *env = getenv("GPUBPE_STREAM_MB");
         const long long part_mb = env ? atoll(env) : 32;
         const uint64_t part = (uint64_t)std::max(part_mb, 0ll) << 20;
-        if (part && n_bytes > 2 * part && n_docs > 1)
+        if (part && n_bytes > 2 * part && n_docs > 1 && !stage)
             return encode_host_streamed(ctx, h_bytes, h_doc_offs, n_docs, max_seq_len, chunk_budget, h_out_ids,
                                         h_out_offs, n_ids_out, kernel_ms, stream, part);
     }
     static const bool htime = getenv("GPUBPE_HOSTTIME") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto t_a = now();
-    static const int mode = getenv("GPUBPE_HOSTMODE") ? atoi(getenv("GPUBPE_HOSTMODE")) : 3;
+    static const int env_mode = getenv("GPUBPE_HOSTMODE") ? atoi(getenv("GPUBPE_HOSTMODE")) : 3;
+    const int mode = stage ? 3 : env_mode;  // gathered batches always stage through pinned pieces
     int rc;
     const size_t offs_b = (n_docs + 1) * 8;
     const size_t o_in = 0;
@@ -1029,7 +1068,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     } else if (mode == 2) {  // pageable copies straight from the caller's buffers
         CK(cudaMemcpyAsync(dv + o_doffs, h_doc_offs, offs_b, cudaMemcpyHostToDevice, s));
         if (n_bytes) CK(cudaMemcpyAsync(dv + o_in, h_bytes, n_bytes, cudaMemcpyHostToDevice, s));
-    } else if (n_bytes && mapped_alias(h_bytes)) {  // caller bytes already pinned: no staging copy
+    } else if (n_bytes && !stage && mapped_alias(h_bytes)) {  // caller bytes already pinned: no staging copy
         memcpy(pin + o_doffs, h_doc_offs, offs_b);
         CK(cudaMemcpyAsync(dv + o_in, h_bytes, n_bytes, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(dv + o_doffs, pin + o_doffs, offs_b, cudaMemcpyHostToDevice, s));
@@ -1042,10 +1081,12 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
                                 : std::min<size_t>(4u << 20, std::max<size_t>(64u << 10, ((n_bytes / 4) + 65535) & ~(size_t)65535));
         size_t lo = 0;
         for (; lo + piece < n_bytes; lo += piece) {
-            copy_par(pin + o_in + lo, h_bytes + lo, piece);
+            if (stage) (*stage)(pin + o_in + lo, lo, lo + piece);
+            else copy_par(pin + o_in + lo, h_bytes + lo, piece);
             CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, piece, cudaMemcpyHostToDevice, s));
         }
-        copy_par(pin + o_in + lo, h_bytes + lo, n_bytes - lo);
+        if (stage) (*stage)(pin + o_in + lo, lo, n_bytes);
+        else copy_par(pin + o_in + lo, h_bytes + lo, n_bytes - lo);
         CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, o_doffs + offs_b - lo, cudaMemcpyHostToDevice, s));
     }
     auto t_b = now();
@@ -1098,6 +1139,41 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
                 us(t_a, t_b), us(t_b, t_c), us(t_c, t_d), us(t_d, t_e));
     }
     return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host_gather(
+    gpubpe_ctx *ctx, const uint64_t *h_ptrs, const uint64_t *h_lens, uint64_t n_docs, uint64_t max_seq_len,
+    uint64_t chunk_budget, uint32_t *h_out_ids, int64_t *h_out_offs, uint64_t *n_ids_out, float *kernel_ms,
+    void *stream) {
+    if (!ctx) return GPUBPE_EINVAL;
+    if (!n_ids_out || (n_docs && (!h_ptrs || !h_lens || !h_out_offs)))
+        return fail(ctx, GPUBPE_EINVAL, "null host pointer");
+    std::vector<int64_t> offs(n_docs + 1, 0);
+    for (uint64_t d = 0; d < n_docs; ++d) {
+        if (h_lens[d] && !h_ptrs[d]) return fail(ctx, GPUBPE_EINVAL, "document %llu: null pointer", (unsigned long long)d);
+        offs[d + 1] = offs[d] + (int64_t)h_lens[d];
+    }
+    const uint64_t n = (uint64_t)offs[n_docs];
+    const char *env = getenv("GPUBPE_STREAM_MB");
+    const uint64_t part = (uint64_t)std::max(env ? atoll(env) : 32ll, 0ll) << 20;
+    if (n == 0 || (part && n > 2 * part && n_docs > 1)) {  // (large batches: contiguous copy, then streamed)
+        std::vector<uint8_t> buf(std::max<uint64_t>(n, 1));
+        gather_par(buf.data(), h_ptrs, h_lens, offs.data(), n_docs);
+        return gpubpe_encode_host(ctx, buf.data(), n, offs.data(), n_docs, max_seq_len, chunk_budget, h_out_ids,
+                                  h_out_offs, n_ids_out, kernel_ms, stream);
+    }
+    // stage the pieces straight from the documents into pinned memory (each piece
+    // DMA'd while the next one is gathered): one host copy, no join
+    const StageFn stage = [&](uint8_t *dst, uint64_t lo, uint64_t hi) {
+        uint64_t d = (uint64_t)(std::upper_bound(offs.begin(), offs.end(), (int64_t)lo) - offs.begin()) - 1;
+        for (; d < n_docs && (uint64_t)offs[d] < hi; ++d) {
+            const uint64_t a = std::max<uint64_t>(lo, offs[d]), b = std::min<uint64_t>(hi, offs[d + 1]);
+            if (a < b) memcpy(dst + (a - lo), reinterpret_cast<const uint8_t *>(h_ptrs[d]) + (a - offs[d]), b - a);
+        }
+    };
+    if (!h_out_ids) return fail(ctx, GPUBPE_EINVAL, "null host pointer");
+    return encode_host_core(ctx, nullptr, &stage, n, offs.data(), n_docs, max_seq_len, chunk_budget, h_out_ids,
+                            h_out_offs, n_ids_out, kernel_ms, stream);
 }
 
 extern "C" __attribute__((visibility("default"))) int gpubpe_host_alloc(int device, uint64_t bytes, void **out) {

@@ -111,6 +111,9 @@ class _HostPool:
 
 _RESULTS = _HostPool()
 _POOLED_MAX = _RESULTS.pinned_max
+# address of a bytes object's data relative to id() (CPython layout, measured once)
+_BYTES_PROBE = b"\x00gpubpe"
+_BYTES_DATA = ctypes.cast(ctypes.c_char_p(_BYTES_PROBE), ctypes.c_void_p).value - id(_BYTES_PROBE)
 
 
 def pinned_empty(nbytes: int, device: int = 0) -> np.ndarray:
@@ -319,6 +322,38 @@ class DeviceEncoder:
             _native.check(self._lib.gpubpe_set_pretok(self._h, _ptr(cls), N_CPS), self._h, "set_pretok")
             self._pretok = True
         _native.check(self._lib.gpubpe_set_mode(self._h, int(mode)), self._h, "set_mode")
+
+    def encode_list_host(self, parts: list, max_seq_len: int, chunk_budget: int, mode: int = 0):
+        """A batch of separate `bytes` documents -> host CSR (ids, offs, stats,
+        engine_ms), gathered straight into the pinned staging buffer by the
+        native side (gpubpe_encode_host_gather): no join on the Python side."""
+        n_docs = len(parts)
+        if not all(type(p) is bytes for p in parts):
+            raise TypeError("encode_list_host takes a list of bytes")
+        ptrs = np.fromiter(map(id, parts), dtype=np.uint64, count=n_docs) + np.uint64(_BYTES_DATA)
+        lens = np.fromiter(map(len, parts), dtype=np.uint64, count=n_docs)
+        n = int(lens.sum())
+        pinned = 4 * n <= _POOLED_MAX
+        buf = (_RESULTS.take(4 * max(n, 1), self._lib, self.device) if pinned
+               else _RESULTS.take_pageable(4 * max(n, 1)))
+        ids = buf.view(np.uint32)
+        out_offs = np.zeros(n_docs + 1, dtype=np.int64)
+        n_ids = ctypes.c_uint64(0)
+        ms = ctypes.c_float(0.0)
+        with self._lock, torch.cuda.device(self.device):
+            if mode != _native.MODE_DEFAULT:
+                self.set_mode(mode)
+            s = torch.cuda.current_stream(self.device)
+            try:
+                rc = self._lib.gpubpe_encode_host_gather(self._h, _ptr(ptrs), _ptr(lens), n_docs, int(max_seq_len),
+                                                         int(chunk_budget), _ptr(ids), _ptr(out_offs),
+                                                         ctypes.byref(n_ids), ctypes.byref(ms), s.cuda_stream)
+            finally:
+                if mode != _native.MODE_DEFAULT:
+                    self.set_mode(_native.MODE_DEFAULT)
+            _native.check(rc, self._h, "gpubpe_encode_host_gather")
+            st = self.query(s)
+        return _RESULTS.array(buf, np.uint32, n_ids.value), out_offs, st, float(ms.value)
 
     def encode_packed_host(self, data: np.ndarray, offs: np.ndarray, max_seq_len: int,
                            chunk_budget: int, mode: int = 0):

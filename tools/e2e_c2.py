@@ -30,3 +30,7 @@ def split2():
     return [ids[a:b] for a, b in zip(o, o[1:])]
 print("split (tolist)      %7.3f ms" % t(split2))
 print("join                %7.3f ms" % t(lambda: b"".join(docs)))
+print("encode_list_host    %7.3f ms" % t(lambda: enc.encode_list_host(docs, 8192, 8192)))
+import os
+os.environ["GPUBPE_HOSTTIME"] = "1"
+enc.encode_list_host(docs, 8192, 8192)
