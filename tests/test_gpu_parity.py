@@ -753,3 +753,28 @@ def test_byte_level_random_tables_match_oracle(well_formed):
     got = bpe.tokenize_batch(docs, tok).token_ids
     want = orc.encode_docs(docs, 1 << 40, 1 << 40)
     assert_same(got, want, f"well_formed={well_formed}")
+
+
+def test_tokenize_batch_gather_paths(tokenizer, monkeypatch):
+    """Multi-document batches go through gpubpe_encode_host_gather: piecewise
+    staging straight from the documents (small batches) and the contiguous
+    copy into the streamed pipeline (large ones, here above 2 x 1 MiB)."""
+    import synth_corpus
+
+    rng = np.random.default_rng(5)
+    pool = synth_corpus.english_bytes(4 << 20, 6)
+    docs = []
+    for k in range(300):
+        n = int(rng.choice([0, 3, 700, 9000, 40000]))
+        at = int(rng.integers(0, len(pool) - n - 1))
+        docs.append(pool[at:at + n])
+    docs.append(pool[: 2 << 20])  # one document larger than a streamed part
+    data, offs = bpe.pack_texts(docs)
+    enc = tokenizer.device_encoder()
+    ref_ids, ref_offs, _, _ = enc.encode_packed_host(data, offs, 8192, 8192)
+    want = [ref_ids[ref_offs[i]:ref_offs[i + 1]].copy() for i in range(len(docs))]
+    for stream_mb in ("0", "1"):
+        monkeypatch.setenv("GPUBPE_STREAM_MB", stream_mb)
+        res = bpe.tokenize_batch(docs, tokenizer)
+        assert_same(res.token_ids, want, f"stream {stream_mb}")
+        assert res.counters.passes == len(data) - sum(len(x) for x in want)
