@@ -44,7 +44,10 @@ constexpr int NT = NW * 32;     // threads per CTA
 constexpr int SHORT_MAX = 32;   // longest segment encoded inside the tile loop
 constexpr int GIANT_MIN = 4097; // deferred segments this long are encoded by the whole grid (else a warp)
 constexpr int SLOT = WT + SHORT_MAX;  // scratch entries per tile (ids of segments starting in it)
-constexpr int UNIT_MAX = 512;   // tiles per CTA per round in phase B
+#ifndef GPUBPE_UNIT_MAX
+#define GPUBPE_UNIT_MAX 512
+#endif
+constexpr int UNIT_MAX = GPUBPE_UNIT_MAX;   // tiles per CTA per round in phase B
 constexpr unsigned int MARK = 0x80000000u;  // scratch entry: deferred record index follows
 
 // tile word: bits 0-15 entries, bit 16 has deferred markers, bits 17.. extra ids
