@@ -724,8 +724,14 @@ __device__ __noinline__ void place_range(const EncodeParams &P, CtaSmem &C, unsi
     }
     if (tid == 0 && nt > 0 && hi == P.n_tiles) P.st->n_ids = base + C.bcast[2];
     for (int k = wid; k < nt; k += NW) place_tile(P, slots + (size_t)k * SLOT, C.tw[k], base + C.tb[k]);
-    // CSR offsets of the documents starting in [lo, hi): tile-local -> global
-    if (wid == 0 && nt > 0 && (P.n_docs > 1 || lo == 0 || hi == P.n_tiles)) {
+    // CSR offsets of the documents starting in [lo, hi): tile-local -> global.
+    // One document: its offsets are 0 and the id total, no look-ups needed.
+    if (P.n_docs == 1) {
+        if (tid == 0 && nt > 0) {
+            if (lo == 0) P.out_offs[0] = 0;
+            if (hi == P.n_tiles) P.out_offs[1] = (long long)(base + C.bcast[2]);
+        }
+    } else if (wid == 0 && nt > 0) {
         const long long blo = (long long)lo * P.tile_bytes;
         long long d = 0;
         if (blo > 0) {  // first document with offs >= blo (lower bound)
