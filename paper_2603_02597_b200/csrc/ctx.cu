@@ -644,6 +644,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *
         Q.n_cps = ctx->pt_n_cps;
         memcpy(Q.ascii, ctx->pt_ascii, 128);
         Q.ascii_std = 1;
+        Q.paths = getenv("GPUBPE_PRETOK_PATHS") ? (uint32_t)atoi(getenv("GPUBPE_PRETOK_PATHS")) : 7u;  // (tests)
         for (int c = 0; c < 128; ++c) {
             const uint8_t want = ((c | 32) >= 'a' && (c | 32) <= 'z') ? 1 : (c >= '0' && c <= '9') ? 2
                                  : ((c >= 9 && c <= 13) || c == ' ') ? 3 : 0;

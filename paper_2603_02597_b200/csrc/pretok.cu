@@ -96,10 +96,14 @@ __device__ __forceinline__ unsigned long long eq_mask(const unsigned long long (
     return m;
 }
 
-// Token-start bits of the 32 positions j in [8, 40) of a window whose bytes
-// are ASCII on E (bit j: byte j exists in the word's document).
+// Token-start bits of the 32 positions j in [8, 40) of the window (bit j:
+// byte 32w - 8 + j), E = bytes of the word's document.  The class masks hold,
+// at every byte, the class of the code point containing it; LEAD marks code
+// point starts and NNS, at a start, "the next code point exists and is not
+// \s".  For ASCII every byte is a code point (LEAD = E, NNS = (E & ~S) >> 1).
 __device__ __forceinline__ uint32_t rules_bitparallel(const unsigned long long (&win)[6], const Masks &M0,
-                                                      unsigned long long E) {
+                                                      unsigned long long E, unsigned long long LEAD,
+                                                      unsigned long long NNS) {
     const unsigned long long L = M0.L & E, N = M0.N & E, S = M0.S & E, SP = M0.SP & E, AP = M0.AP & E;
     unsigned long long C2 = 0, C3 = 0;  // contractions starting at j: 's 'd 'm 't / 'll 've 're
     if (AP) {
@@ -116,11 +120,68 @@ __device__ __forceinline__ uint32_t rules_bitparallel(const unsigned long long (
     const unsigned long long C = C2 | C3;
     const unsigned long long B =
         ~(E << 1)                                                    // text start
-        | (S & (~(S << 1) | ((E & ~S) >> 1)))                        // whitespace run start / last char of a run
+        | (S & (~(S << 1) | NNS))                                    // whitespace run start / last char of a run
         | (~S & (S << 1) & ~(SP << 1))                               // after \s other than ' '
         | (~S & ~(S << 1) & ~((C << 1) | (C3 << 2)) &                // not inside a contraction:
            ((C2 << 2) | (C3 << 3) | (L ^ (L << 1)) | (N ^ (N << 1))));  // after one, or a class change
-    return (uint32_t)((B & E) >> 8);
+    return (uint32_t)((B & E & LEAD) >> 8);
+}
+
+// bytes j .. j + 3 of the window (little endian), 0 <= j < 44
+__device__ __forceinline__ uint32_t win_bytes4(const unsigned long long (&win)[6], int j) {
+    unsigned long long lo = 0, hi = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        if (k == (j >> 3)) lo = win[k];
+        if (k == (j >> 3) + 1) hi = win[k];
+    }
+    const int sh = 8 * (j & 7);
+    return (uint32_t)(sh ? (lo >> sh) | (hi << (64 - sh)) : lo);
+}
+
+// Masks of a window with non-ASCII bytes (the scalar path's code point rules:
+// a byte that is not 10xxxxxx starts a code point, as does the document's
+// first byte; a sequence whose continuation run does not match its lead byte
+// is one "other" code point).  Returns false when a continuation run longer
+// than 3 bytes (a code point the window cannot hold) calls for the scalar path.
+__device__ __forceinline__ bool unicode_masks(const PretokParams &Q, const unsigned long long (&win)[6], Masks &M,
+                                              unsigned long long E, int jlo, unsigned long long &LEAD,
+                                              unsigned long long &NNS) {
+    unsigned long long CONT = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) CONT |= (unsigned long long)movemask8(win[k] & ~(win[k] << 1) & K80) << (8 * k);
+    const unsigned long long start = jlo >= 0 ? (1ull << jlo) : 0ull;  // the document's first byte
+    LEAD = (~CONT | start) & E;
+    const unsigned long long CE = CONT & E & ~start;  // continuation bytes joined to the preceding start
+    if (CE & (CE << 1) & (CE << 2) & (CE << 3)) return false;
+    // non-ASCII starts below 44 (the next code point of byte 39's) get their class from the table
+    for (unsigned long long nl = LEAD & M.NA & ((1ull << 44) - 1); nl; nl &= nl - 1) {
+        const int j = __ffsll((long long)nl) - 1;
+        const uint32_t x = win_bytes4(win, j), b0 = x & 0xFFu;
+        const int need = b0 >= 0xF0u ? 3 : b0 >= 0xE0u ? 2 : b0 >= 0xC0u ? 1 : -1;
+        const unsigned long long after = CE >> (j + 1);
+        const int run = (after & 1) ? ((after & 2) ? ((after & 4) ? 3 : 2) : 1) : 0;
+        uint8_t c = C_O;
+        if (need > 0 && run == need && b0 < 0xF8u) {
+            uint32_t cp = b0 & (0x3Fu >> need);
+            for (int k = 1; k <= need; ++k) cp = (cp << 6) | ((x >> (8 * k)) & 0x3Fu);
+            c = cp_class(Q, cp);
+        }
+        const unsigned long long bit = 1ull << j;
+        if (c == C_L) M.L |= bit;
+        else if (c == C_N) M.N |= bit;
+        else if (c == C_S) M.S |= bit;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {  // every byte of a code point carries its class
+        M.L |= (M.L << 1) & CE;
+        M.N |= (M.N << 1) & CE;
+        M.S |= (M.S << 1) & CE;
+    }
+    NNS = (LEAD & ~M.S) >> 1;  // at a code point's last byte: the next one exists and is not \s
+#pragma unroll
+    for (int k = 0; k < 3; ++k) NNS |= (NNS >> 1) & (CE >> 1);  // ... carried back to its start
+    return true;
 }
 
 // SWAR forms on 4 bytes: 0x80 in each byte whose value is in [lo, hi]
@@ -227,7 +288,7 @@ __global__ void __launch_bounds__(PT, 4) k_pretok(const __grid_constant__ Pretok
     while (__ldg(&Q.doc_offs[d + 1]) <= p0) ++d;
     if (Q.ascii_std) {
         const long long ds = __ldg(&Q.doc_offs[d]), de = __ldg(&Q.doc_offs[d + 1]);
-        if (ds <= p0 - 4 && de >= p0 + 36) {
+        if ((Q.paths & 1) && ds <= p0 - 4 && de >= p0 + 36) {
             uint32_t x[10], hb = 0, ap = 0;
 #pragma unroll
             for (int i = 0; i < 10; ++i) {
@@ -251,8 +312,22 @@ __global__ void __launch_bounds__(PT, 4) k_pretok(const __grid_constant__ Pretok
             const long long jlo = max(0ll, s0 - (p0 - 8)), jhi = min(48ll, s1 - (p0 - 8));
             if (jhi > jlo) {
                 const unsigned long long E = ((1ull << jhi) - 1) & ~((1ull << jlo) - 1);
-                if (M.NA & E) { ok = false; break; }
-                bits |= rules_bitparallel(win, M, E);
+                if (M.NA & E) {
+                    // non-ASCII bytes in this document's part of the window
+                    Masks MU = M;
+                    unsigned long long LEAD, NNS;
+                    const int start = s0 >= p0 - 8 ? (int)jlo : -1;  // document start inside the window
+                    if (!(Q.paths & 4) || !unicode_masks(Q, win, MU, E, start, LEAD, NNS)) {
+                        ok = false;
+                        break;
+                    }
+                    bits |= rules_bitparallel(win, MU, E, LEAD, NNS);
+                } else if (Q.paths & 2) {
+                    bits |= rules_bitparallel(win, M, E, E, (E & ~M.S) >> 1);
+                } else {
+                    ok = false;
+                    break;
+                }
             }
             if (s1 >= p1) break;
         }

@@ -778,3 +778,33 @@ def test_tokenize_batch_gather_paths(tokenizer, monkeypatch):
         res = bpe.tokenize_batch(docs, tokenizer)
         assert_same(res.token_ids, want, f"stream {stream_mb}")
         assert res.counters.passes == len(data) - sum(len(x) for x in want)
+
+
+def test_regex_mode_fast_paths_equal_scalar_path(tokenizer, monkeypatch):
+    """k_pretok's bit-parallel paths (SWAR, ASCII masks, Unicode masks) mark
+    exactly the scalar code point path's pre-token starts, on valid and invalid
+    UTF-8, runs of continuation bytes and documents starting mid-window."""
+    import random as _r
+
+    rng = _r.Random(31)
+    pieces = ["漢字", "テキスト", "мир ", "café", "😀", " \u3000", "\u00a0x", "'s", "'ll", " 1234", "a", " ",
+              "\n", "ß", "\t", "Ü", "\u2028", " \u3000\u3000 "]
+    docs = []
+    for k in range(400):
+        n = rng.choice([0, 1, 3, 9, 33, 70, 200, 900])
+        txt = "".join(rng.choice(pieces) for _ in range(n)).encode()
+        if k % 5 == 0 and txt:  # invalid UTF-8: cut sequences, stray continuation runs, bad leads
+            b = bytearray(txt)
+            for _ in range(rng.randrange(1, 4)):
+                b.insert(rng.randrange(len(b) + 1), rng.choice([0x80, 0xBF, 0xC3, 0xE6, 0xF0, 0xF8, 0xFF]))
+            if rng.random() < 0.3:
+                b[rng.randrange(len(b) + 1):0] = bytes([0x80] * rng.randrange(1, 8))
+            txt = bytes(b)
+        docs.append(txt)
+    tok = with_config(tokenizer, 1 << 40, 1 << 40)
+    monkeypatch.setenv("GPUBPE_PRETOK_PATHS", "0")
+    want = bpe.tokenize_batch(docs, tok, pretokenize="gpt2").token_ids
+    for paths in ("7", "6", "4", "2"):
+        monkeypatch.setenv("GPUBPE_PRETOK_PATHS", paths)
+        got = bpe.tokenize_batch(docs, tok, pretokenize="gpt2").token_ids
+        assert_same(got, want, f"paths {paths}")
