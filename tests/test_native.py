@@ -54,3 +54,16 @@ def test_device_api_refuses_without_cuda(tokenizer):
         pytest.skip("CUDA present")
     with pytest.raises(DeviceError):
         bpe.tokenize_batch([b"hello"], tokenizer)
+
+
+def test_signatures_match_header_arity():
+    """Every ctypes signature in _native.py has as many arguments as the
+    prototype in include/gpubpe.h."""
+    from paper_2603_02597_b200 import _native
+
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    protos = dict(re.findall(r"\b(gpubpe_[a-z_]+)\s*\(([^;{]*?)\)\s*;", text))
+    assert set(protos) == set(_native.SIGNATURES)
+    for name, args in protos.items():
+        n = 0 if args.strip() in ("", "void") else args.count(",") + 1
+        assert len(_native.SIGNATURES[name][1]) == n, name
