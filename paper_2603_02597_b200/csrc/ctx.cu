@@ -598,7 +598,7 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         CK(cudaMemcpyAsync(ctx->h_state, P.st, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (!ctx->h_state->overflow) return GPUBPE_OK;
-        const uint64_t nd = ctx->h_state->n_def;
+        const uint64_t nd = ctx->h_state->bar >> 32;
         if (nd > rec_cap && (rc = ensure(ctx, ctx->ws_recs, nd * sizeof(DefRec), false))) return rc;
         const uint64_t used = ctx->h_state->arena_used * 4;
         if (used > ctx->ws_arena.bytes && (rc = ensure(ctx, ctx->ws_arena, used, false))) return rc;
@@ -891,7 +891,7 @@ static int encode_host_streamed(gpubpe_ctx *ctx, const uint8_t *h_bytes, const i
             int rc2;
             ctx->defer_check = false;
             tiles -= ctx->last_n_tiles;
-            if ((rc2 = ensure(ctx, ctx->ws_recs, o.n_def * sizeof(DefRec), false)) ||
+            if ((rc2 = ensure(ctx, ctx->ws_recs, (o.bar >> 32) * sizeof(DefRec), false)) ||
                 (rc2 = ensure(ctx, ctx->ws_arena, o.arena_used * 4, false)) || (rc2 = encode_part(i))) {
                 ctx->defer_check = true;
                 return rc2;

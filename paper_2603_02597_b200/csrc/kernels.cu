@@ -441,7 +441,7 @@ __device__ __noinline__ void encode_tile(const EncodeParams &P, CtaSmem &C, Warp
         const int e = next_cut(S.cm, p + 1, p + SHORT_MAX);
         ++c_seg;
         if (e < 0) {  // longer than SHORT_MAX: deferred to the CTA engine
-            const unsigned long long r = atomicAdd(&P.st->n_def, 1ull);
+            const unsigned long long r = atomicAdd(&P.st->bar, 1ull << 32) >> 32;
             if (r < P.rec_cap) P.recs[r].start = (unsigned long long)(a + p);
             S.sid[SI(p)] = 0xFF000000u;
             S.sid[SI(p + 1)] = (uint32_t)r;
@@ -770,14 +770,18 @@ __device__ __noinline__ void place_range(const EncodeParams &P, CtaSmem &C, unsi
 }
 
 // All CTAs (co-resident: cooperative launch).  k = 1, 2, ... per use.
-__device__ void grid_sync(EncodeState *st, unsigned int k) {
+// Grid barrier k (1, 2, ...).  *defs (shared memory, optional) receives the
+// deferred-segment count, final once every CTA has arrived.
+__device__ void grid_sync(EncodeState *st, unsigned int k, unsigned long long *defs = nullptr) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        atomicAdd(&st->bar, 1u);
-        const unsigned int target = k * gridDim.x;
-        while (ld_relaxed_u32(&st->bar) < target) __nanosleep(128);
+        atomicAdd(&st->bar, 1ull);
+        const unsigned long long target = (unsigned long long)k * gridDim.x;
+        unsigned long long w;
+        while (((w = ld_relaxed(&st->bar)) & 0xFFFFFFFFull) < target) __nanosleep(128);
         __threadfence();  // acquire side of the barrier, once
+        if (defs) *defs = w >> 32;
     }
     __syncthreads();
 }
@@ -1186,11 +1190,9 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
         if (P.dbg_phase_a_only) return;
         if (blockIdx.x == 0 && tid == 0) st->actr[par ^ 1] = 0;
         if (P.dbg && tid == 0 && r == 0) P.dbg[4 * blockIdx.x + 1] = gtimer();
-        grid_sync(st, ++nbar);
+        grid_sync(st, ++nbar, &C.bcast[3]);
         if (P.dbg && tid == 0 && r == 0) P.dbg[4 * blockIdx.x + 2] = gtimer();
-        // ---- rare: deferred segments recorded in this round
-        if (tid == 0) C.bcast[3] = __ldcg(&st->n_def);
-        __syncthreads();
+        // ---- rare: deferred segments recorded in this round (count read with the barrier)
         const unsigned long long D = C.bcast[3];
         if (D > d_done) {
             if (D > P.rec_cap) {

@@ -71,9 +71,10 @@ struct PassCounters {
 struct EncodeState {
     unsigned long long actr[2];      // phase-A tile counters by round parity
     unsigned long long pad0[14];
-    unsigned int bar;                // grid barrier arrivals
-    unsigned int pad1[31];
-    unsigned long long n_def;        // deferred segments recorded
+    unsigned long long bar;          // low 32 bits: grid barrier arrivals; high 32 bits: deferred
+                                     // segments recorded (read with the barrier, no extra round trip)
+    unsigned long long pad1[15];
+    unsigned long long n_def_unused; // (layout)
     unsigned long long rec_ctr;      // deferred records taken by warps (medium pass)
     unsigned long long rec_ctr2;     // deferred records scanned by CTAs (giant pass)
     unsigned long long arena_used;   // u32 words requested from the arena
