@@ -1174,11 +1174,18 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
     const unsigned long long G = gridDim.x;
     for (unsigned long long r = 0, t0 = 0; t0 < P.n_tiles; ++r, t0 += R) {
         const unsigned long long t1 = min(P.n_tiles, t0 + R), par = r & 1;
-        // ---- phase A: encode tiles of the round into their slots
-        for (;;) {
+        // ---- phase A: encode tiles of the round into their slots.  At most one
+        //      tile per warp: tile = warp rank, interleaved across the SMs (no claim
+        //      atomics); otherwise tiles are claimed from the round's counter.
+        const bool one_each = t1 - t0 <= G * NW;
+        for (unsigned long long k = 0;; ++k) {
             unsigned long long t = 0;
-            if (lane == 0) t = t0 + atomicAdd(&st->actr[par], 1ull);
-            t = __shfl_sync(FULL_MASK, t, 0);
+            if (one_each) {
+                t = k ? t1 : t0 + (unsigned long long)wid * G + blockIdx.x;
+            } else {
+                if (lane == 0) t = t0 + atomicAdd(&st->actr[par], 1ull);
+                t = __shfl_sync(FULL_MASK, t, 0);
+            }
             if (t >= t1) break;
             const unsigned long long g0 = P.dbg ? gtimer() : 0;
             encode_tile(P, C, S, t, par * R + (t - t0), X);
