@@ -1152,6 +1152,10 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
 
 // ------------------------------------------------------------------ kernel
 
+// kOneEach: the batch has at most one tile per warp (one round; tiles assigned
+// statically).  A separate instantiation keeps the general kernel's code (and
+// register allocation) exactly as tuned for many tiles per warp.
+template <bool kOneEach>
 __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ EncodeParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CtaSmem &C = *reinterpret_cast<CtaSmem *>(smem_raw);
@@ -1177,21 +1181,28 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
         // ---- phase A: encode tiles of the round into their slots.  At most one
         //      tile per warp: tile = warp rank, interleaved across the SMs (no claim
         //      atomics); otherwise tiles are claimed from the round's counter.
-        const bool one_each = t1 - t0 <= G * NW;
-        for (unsigned long long k = 0;; ++k) {
-            unsigned long long t = 0;
-            if (one_each) {
-                t = k ? t1 : t0 + (unsigned long long)wid * G + blockIdx.x;
-            } else {
+        if constexpr (kOneEach) {
+            const unsigned long long t = t0 + (unsigned long long)wid * G + blockIdx.x;
+            if (t < t1) {
+                const unsigned long long g0 = P.dbg ? gtimer() : 0;
+                encode_tile(P, C, S, t, par * R + (t - t0), X);
+                if (P.dbg && lane == 0 && t < 4096) {
+                    P.dbg[1024 + 2 * t] = g0;
+                    P.dbg[1024 + 2 * t + 1] = gtimer();
+                }
+            }
+        } else {
+            for (;;) {
+                unsigned long long t = 0;
                 if (lane == 0) t = t0 + atomicAdd(&st->actr[par], 1ull);
                 t = __shfl_sync(FULL_MASK, t, 0);
-            }
-            if (t >= t1) break;
-            const unsigned long long g0 = P.dbg ? gtimer() : 0;
-            encode_tile(P, C, S, t, par * R + (t - t0), X);
-            if (P.dbg && lane == 0 && t < 4096) {
-                P.dbg[1024 + 2 * t] = g0;
-                P.dbg[1024 + 2 * t + 1] = gtimer();
+                if (t >= t1) break;
+                const unsigned long long g0 = P.dbg ? gtimer() : 0;
+                encode_tile(P, C, S, t, par * R + (t - t0), X);
+                if (P.dbg && lane == 0 && t < 4096) {
+                    P.dbg[1024 + 2 * t] = g0;
+                    P.dbg[1024 + 2 * t + 1] = gtimer();
+                }
             }
         }
         if (P.dbg_phase_a_only) return;
@@ -1278,18 +1289,26 @@ cudaError_t launch_encode(const EncodeParams &P, int grid, cudaStream_t s, cudaE
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_encode, P);
+    const bool one_each = P.n_tiles <= (unsigned long long)grid * NW;  // one round, <= 1 tile per warp
+    cudaError_t e = one_each ? cudaLaunchKernelEx(&cfg, k_encode<true>, P) : cudaLaunchKernelEx(&cfg, k_encode<false>, P);
     if (ev) cudaEventRecord(ev[1], s);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t setup_kernels() {
-    return cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_encode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(CtaSmem));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_encode<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(CtaSmem));
 }
 
 cudaError_t tile_occupancy(int *blocks) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_encode, NT, sizeof(CtaSmem));
+    int b1 = 0, b2 = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_encode<true>, NT, sizeof(CtaSmem));
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_encode<false>, NT, sizeof(CtaSmem));
+    *blocks = std::min(b1, b2);
+    return e;
 }
 
 cudaError_t launch_lookup(const DevTables &T, const uint32_t *l, const uint32_t *r,
