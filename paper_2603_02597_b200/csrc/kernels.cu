@@ -1230,6 +1230,9 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
         // ---- phase B: place this CTA's contiguous range of the round's tiles
         const unsigned long long q = (t1 - t0 + G - 1) / G;
         const unsigned long long lo = min(t1, t0 + blockIdx.x * q), hi = min(t1, lo + q);
+        // one round only: the counters are final here; publishing them before the
+        // placement takes their atomics off the kernel's tail
+        if constexpr (kOneEach) publish_counters(C, X, &st->c);
         place_range(P, C, r, t0, lo, hi);
         if (ng) {  // giants' ids: one grid-wide copy once their destinations are placed
             grid_sync(st, ++nbar);
@@ -1247,7 +1250,7 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
             ng = 0;
         }
     }
-    publish_counters(C, X, &st->c);
+    if constexpr (!kOneEach) publish_counters(C, X, &st->c);
     if (P.dbg && tid == 0) P.dbg[4 * blockIdx.x + 3] = gtimer();
 }
 
