@@ -113,6 +113,15 @@ class Tokenizer:
         """Many id sequences -> their byte strings in one device call."""
         return self.device_encoder().decode_host(seqs)
 
+    def encode_batch_tensors(self, data, doc_offs):
+        """Tensor-native batch encode: a packed batch
+        already on the GPU -- data uint8[n], doc_offs int64[n_docs + 1] (cuda
+        tensors) -> (ids int32[n_ids], offsets int64[n_docs + 1]) on the same
+        device, under this tokenizer's BlockConfig.  One launch, one sync."""
+        ids, offs, _ = self.device_encoder(data.device.index).encode_tensors(
+            data, doc_offs, self.config.max_seq_len, self.config.chunk_budget)
+        return ids, offs
+
     def _symbol_bytes(self):
         """(ids uint32[], blob uint8[], offs uint64[]) of every id whose symbol maps
         to a nonempty byte string (symbol_bytes semantics), vectorised: all

@@ -808,3 +808,14 @@ def test_regex_mode_fast_paths_equal_scalar_path(tokenizer, monkeypatch):
         monkeypatch.setenv("GPUBPE_PRETOK_PATHS", paths)
         got = bpe.tokenize_batch(docs, tok, pretokenize="gpt2").token_ids
         assert_same(got, want, f"paths {paths}")
+
+
+def test_encode_batch_tensors(tokenizer, prose_samples):
+    import torch
+
+    data, offs = bpe.pack_texts(prose_samples[:12])
+    ids, oo = tokenizer.encode_batch_tensors(torch.from_numpy(data.copy()).cuda(), torch.from_numpy(offs).cuda())
+    assert ids.is_cuda and ids.dtype == torch.int32 and oo.dtype == torch.int64
+    h, ho = ids.cpu().numpy().view(np.uint32), oo.cpu().numpy()
+    gold = fixtures.golden_prose()[:12]
+    assert [h[ho[i]:ho[i + 1]].tolist() for i in range(12)] == [g.tolist() for g in gold]
