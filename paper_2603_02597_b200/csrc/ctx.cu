@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <functional>
@@ -732,6 +733,82 @@ class CopyPool {
 };
 }  // namespace
 
+// Staging helpers for the latency path: a few workers that are woken when a
+// host call begins and spin for work only while one is active, so the
+// piecewise staging copies of a ~0.5 MiB batch split across cores without a
+// thread wake-up per copy (and without spinning between calls).
+namespace {
+class StagePool {
+  public:
+    static StagePool &get() {
+        static StagePool *p = new StagePool();  // never destroyed: workers live for the process
+        return *p;
+    }
+    void begin() {
+        if (active_.fetch_add(1) == 0) {
+            std::lock_guard<std::mutex> g(m_);
+            cv_.notify_all();
+        }
+    }
+    void end() { active_.fetch_sub(1); }
+    // memcpy split in (workers + 1) parts; the caller takes part 0
+    void copy(uint8_t *dst, const uint8_t *src, size_t n) {
+        const unsigned parts = (unsigned)th_.size() + 1;
+        const size_t chunk = ((n + parts - 1) / parts + 63) & ~(size_t)63;
+        std::lock_guard<std::mutex> call(call_);  // one staged copy at a time
+        dst_ = dst;
+        src_ = src;
+        n_ = n;
+        chunk_ = chunk;
+        left_.store((int)parts - 1, std::memory_order_relaxed);
+        next_.store(1, std::memory_order_release);
+        gen_.fetch_add(1, std::memory_order_release);
+        memcpy(dst, src, std::min(n, chunk));
+        for (unsigned i; (i = next_.fetch_add(1)) < parts;) run(i);  // parts nobody took yet
+        while (left_.load(std::memory_order_acquire) > 0) {
+        }
+    }
+
+  private:
+    StagePool() {
+        const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+        const unsigned nw = std::min(3u, hw / 4);
+        for (unsigned i = 0; i < nw; ++i) th_.emplace_back([this] { loop(); });
+        for (auto &t : th_) t.detach();
+    }
+    void run(unsigned i) {
+        const size_t lo = std::min(n_, i * chunk_), hi = std::min(n_, lo + chunk_);
+        if (lo < hi) memcpy(dst_ + lo, src_ + lo, hi - lo);
+        left_.fetch_sub(1, std::memory_order_acq_rel);
+    }
+    void loop() {
+        unsigned long long seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return active_.load() > 0; });
+            }
+            while (active_.load(std::memory_order_acquire) > 0) {  // spin only inside a host call
+                const unsigned long long gen = gen_.load(std::memory_order_acquire);
+                if (gen == seen) continue;
+                seen = gen;
+                const unsigned parts = (unsigned)th_.size() + 1;
+                for (unsigned i; (i = next_.fetch_add(1)) < parts;) run(i);
+            }
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_, call_;
+    std::condition_variable cv_;
+    std::atomic<int> active_{0}, left_{0};
+    std::atomic<unsigned> next_{0};
+    std::atomic<unsigned long long> gen_{0};
+    uint8_t *dst_ = nullptr;
+    const uint8_t *src_ = nullptr;
+    size_t n_ = 0, chunk_ = 0;
+};
+}  // namespace
+
 static void copy_par(void *dst, const void *src, size_t n) {
     const size_t per = 4u << 20;  // one chunk per 4 MiB beyond 8 MiB (below, a worker wake-up costs more)
     if (n <= 2 * per) {
@@ -1022,6 +1099,16 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
                             const int64_t *h_doc_offs, uint64_t n_docs, uint64_t max_seq_len, uint64_t chunk_budget,
                             uint32_t *h_out_ids, int64_t *h_out_offs, uint64_t *n_ids_out, float *kernel_ms,
                             void *stream) {
+    // wake the staging helpers now, so they are spinning when the pieces are ready
+    struct StageCall {
+        bool on;
+        explicit StageCall(bool b) : on(b) {
+            if (on) StagePool::get().begin();
+        }
+        ~StageCall() {
+            if (on) StagePool::get().end();
+        }
+    } stage_call(!stage && n_bytes >= (512u << 10) && n_bytes <= (16u << 20) && !getenv("GPUBPE_NO_STAGE_POOL"));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->alloc_mark = ctx->n_allocs;
     struct HostCall {  // gpubpe_encode calls below keep this call's allocation mark
@@ -1080,14 +1167,20 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         const char *pe = getenv("GPUBPE_PIECE_KB");
         const size_t piece = pe ? std::max<size_t>(4096, (size_t)atoll(pe) << 10)
                                 : std::min<size_t>(4u << 20, std::max<size_t>(64u << 10, ((n_bytes / 4) + 65535) & ~(size_t)65535));
+        // pieces of 128 KiB .. 4 MiB: split across the staging helpers
+        const bool helpers = !stage && piece >= (128u << 10) && piece <= (4u << 20) && !getenv("GPUBPE_NO_STAGE_POOL");
+        auto copy_piece = [&](uint8_t *dst, const uint8_t *src, size_t len) {
+            if (helpers) StagePool::get().copy(dst, src, len);
+            else copy_par(dst, src, len);
+        };
         size_t lo = 0;
         for (; lo + piece < n_bytes; lo += piece) {
             if (stage) (*stage)(pin + o_in + lo, lo, lo + piece);
-            else copy_par(pin + o_in + lo, h_bytes + lo, piece);
+            else copy_piece(pin + o_in + lo, h_bytes + lo, piece);
             CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, piece, cudaMemcpyHostToDevice, s));
         }
         if (stage) (*stage)(pin + o_in + lo, lo, n_bytes);
-        else copy_par(pin + o_in + lo, h_bytes + lo, n_bytes - lo);
+        else copy_piece(pin + o_in + lo, h_bytes + lo, n_bytes - lo);
         CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, o_doffs + offs_b - lo, cudaMemcpyHostToDevice, s));
     }
     auto t_b = now();
