@@ -63,6 +63,8 @@ struct gpubpe_ctx {
     // decode (ids -> bytes): per-id LUT + byte blob, workspace
     uint32_t *d_vinfo = nullptr;
     uint8_t *d_vblob = nullptr;
+    uint4 *d_vrec = nullptr;
+    uint8_t *d_vlen = nullptr;
     uint32_t n_vocab_dec = 0;
     DevBuf dec_state, dec_status, dec_tiles;  // dec_tiles: tile byte totals + offsets (two-pass)
     // GPT-2 regex pre-tokenization (optional mode)
@@ -73,7 +75,7 @@ struct gpubpe_ctx {
     DevBuf pt_bits;
     const uint32_t *cur_pretok = nullptr;  // bits for the encode being launched
     unsigned int dec_epoch = 0;
-    int dec_grid = 0;
+    int dec_grid = 0, dec_rows_grid = 0;
     // workspace
     DevBuf ws_state, ws_status, ws_recs, ws_scratch, ws_tiles, ws_arena, ws_gscr, ws_glist;
     // host-buffer entry point: pinned (device-mapped) staging + device copy
@@ -1341,6 +1343,26 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_set_vocab(gpubpe_ct
     }
     blob.resize(blob.size() + 16, 0);
     const uint64_t blob_b = blob.size();
+    // per id: a 16-B record (length byte, then the string if it fits, else its
+    // blob chunk) and a 1-byte length table (the two-pass decode's first pass)
+    std::vector<uint8_t> vrec(vinfo.size() * 16, 0), vlen(vinfo.size(), 0);
+    for (size_t i = 0; i < vinfo.size(); ++i) {
+        if (vinfo[i] == GPUBPE_INF) continue;
+        const uint32_t len = vinfo[i] & 0xFFu, chunk = vinfo[i] >> 8;
+        uint8_t *r = &vrec[16 * i];
+        r[0] = (uint8_t)len;
+        if (len <= 15) memcpy(r + 1, &blob[16ull * chunk], len);
+        else memcpy(r + 4, &chunk, 4);
+        vlen[i] = (uint8_t)len;
+    }
+    if (ctx->d_vrec) cudaFree(ctx->d_vrec);
+    if (ctx->d_vlen) cudaFree(ctx->d_vlen);
+    ctx->d_vrec = nullptr;
+    ctx->d_vlen = nullptr;
+    CK(cudaMalloc(&ctx->d_vrec, vrec.size()));
+    CK(cudaMemcpy(ctx->d_vrec, vrec.data(), vrec.size(), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&ctx->d_vlen, vlen.size()));
+    CK(cudaMemcpy(ctx->d_vlen, vlen.data(), vlen.size(), cudaMemcpyHostToDevice));
     if (ctx->d_vinfo) cudaFree(ctx->d_vinfo);
     if (ctx->d_vblob) cudaFree(ctx->d_vblob);
     ctx->d_vinfo = nullptr;
@@ -1354,6 +1376,8 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_set_vocab(gpubpe_ct
     int blocks = 0;
     CK(decode_occupancy(&blocks));
     ctx->dec_grid = ctx->num_sms * std::max(1, blocks);
+    CK(decode_rows_occupancy(&blocks));
+    ctx->dec_rows_grid = ctx->num_sms * std::max(1, blocks);
     return GPUBPE_OK;
 }
 
@@ -1388,6 +1412,8 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *
     DecodeParams P{};
     P.vinfo = ctx->d_vinfo;
     P.blob = ctx->d_vblob;
+    P.vrec = ctx->d_vrec;
+    P.vlen = ctx->d_vlen;
     P.n_vocab = ctx->n_vocab_dec;
     P.ids = d_ids;
     P.n_ids = n_ids;
@@ -1405,13 +1431,18 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *
     // many tiles per CTA: two passes (tile totals + scan, then no look-back) are ~5%
     // faster; a few tiles per CTA: the single pass saves two launches
     if (n_tiles >= 4 * (uint64_t)ctx->dec_grid && !getenv("GPUBPE_DEC_LOOKBACK")) {
-        if ((rc = ensure(ctx, ctx->dec_tiles, n_tiles * 16, false))) return rc;
+        if ((rc = ensure(ctx, ctx->dec_tiles, n_tiles * 16 + n_tiles * 4 * (decode_tile_ids() / 128), false)))
+            return rc;
         unsigned long long *tb = static_cast<unsigned long long *>(ctx->dec_tiles.p);
+        const bool rows = !getenv("GPUBPE_DEC_TILES");
+        P.row_bytes = rows ? reinterpret_cast<uint32_t *>(tb + 2 * n_tiles) : nullptr;
         CK(launch_decode_offsets(P, tb, tb + n_tiles, s));
         P.tile_base = tb + n_tiles;
+        if (rows) CK(launch_decode_rows(P, ctx->dec_rows_grid, s));
+        else CK(launch_decode(P, (int)std::min<uint64_t>(n_tiles, (uint64_t)ctx->dec_grid), s));
+    } else {
+        CK(launch_decode(P, (int)std::min<uint64_t>(n_tiles, (uint64_t)ctx->dec_grid), s));
     }
-    const int grid = (int)std::min<uint64_t>(n_tiles, (uint64_t)ctx->dec_grid);
-    CK(launch_decode(P, grid, s));
     DecodeState h;
     CK(cudaMemcpyAsync(ctx->h_state, d_st, sizeof h, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1556,6 +1587,8 @@ extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe
     if (ctx->h_state_ss) cudaFreeHost(ctx->h_state_ss);
     if (ctx->d_vinfo) cudaFree(ctx->d_vinfo);
     if (ctx->d_vblob) cudaFree(ctx->d_vblob);
+    if (ctx->d_vrec) cudaFree(ctx->d_vrec);
+    if (ctx->d_vlen) cudaFree(ctx->d_vlen);
     for (DevBuf *b : {&ctx->dec_state, &ctx->dec_status, &ctx->dec_tiles, &ctx->pt_bits, &ctx->mt_offs, &ctx->mt_counts})
         if (b->p) cudaFree(b->p);
     if (ctx->d_pt_classes) cudaFree(ctx->d_pt_classes);

@@ -290,14 +290,224 @@ __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant_
     }
 }
 
+// ---- two-pass mode, second pass: every warp decodes a contiguous range of
+//      128-id rows on its own (no CTA barriers).  The row's output offset is the
+//      tile's (scanned) plus the bytes of the rows before it in the tile (both
+//      from the first pass); lane l holds the row's ids [4l, 4l + 4) and fetches
+//      one 16-B record per id -- length and, for strings of up to 15 bytes (all
+//      but a few hundred GPT-2 symbols), the string itself -- so an id costs one
+//      gather.  The next row's ids are loaded while this one is placed; strings
+//      are OR-ed into a warp-private shared-memory stage and stored with 16-B
+//      stores (partial edge chunks word/byte-wise: the neighbouring rows belong to
+//      other warps).
+namespace {
+constexpr int RW = 8;                 // warps per CTA
+constexpr int RDPT = 4;              // ids per lane
+constexpr int RROW = 32 * RDPT;      // ids per row
+constexpr int RPT = TD / RROW;       // rows per tile (first-pass row totals)
+constexpr int STW = 1024;            // staged bytes per warp (8 per id; larger rows go straight to global)
+constexpr int SOFF = 16;             // stage origin (records are placed one byte early)
+static_assert(RPT == 32 && TD == 1024 * 4, "row layout matches k_dec_tile_bytes");
+
+__device__ __forceinline__ uint4 load_ids4(const DecodeParams &P, unsigned long long r, int lane) {
+    const unsigned long long i = r * RROW + (unsigned long long)lane * RDPT;
+    if (P.aligned && i + RDPT <= P.n_ids) return __ldg(reinterpret_cast<const uint4 *>(P.ids + i));
+    uint4 v;
+    v.x = i < P.n_ids ? __ldg(&P.ids[i]) : 0u;
+    v.y = i + 1 < P.n_ids ? __ldg(&P.ids[i + 1]) : 0u;
+    v.z = i + 2 < P.n_ids ? __ldg(&P.ids[i + 2]) : 0u;
+    v.w = i + 3 < P.n_ids ? __ldg(&P.ids[i + 3]) : 0u;
+    return v;
+}
+
+__device__ __forceinline__ uint32_t comp(const uint4 &v, int j) {
+    return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+
+// OR 16 bytes (v) into the stage at byte position p, touching only the words
+// that hold bytes [p, p + n)
+__device__ __forceinline__ void or16(uint32_t *sw, uint32_t p, const uint4 &v, uint32_t n) {
+    const uint32_t sh = 8 * (p & 3), wi = p >> 2, nw = ((p & 3) + n + 3) >> 2;
+    atomicOr(&sw[wi], v.x << sh);
+    if (nw > 1) atomicOr(&sw[wi + 1], __funnelshift_l(v.x, v.y, sh));
+    if (nw > 2) atomicOr(&sw[wi + 2], __funnelshift_l(v.y, v.z, sh));
+    if (nw > 3) atomicOr(&sw[wi + 3], __funnelshift_l(v.z, v.w, sh));
+    if (nw > 4) atomicOr(&sw[wi + 4], v.w >> (32 - sh));
+}
+
+// first index in [lo, hi) whose offset is >= key (offsets ascend), 32-ary
+__device__ __forceinline__ long long warp_lower_bound(const long long *a, long long lo, long long hi,
+                                                      unsigned long long key, int lane) {
+    while (hi > lo) {
+        const long long step = (hi - lo + 31) / 32;
+        const long long idx = lo + (long long)lane * step;
+        const bool lt = idx < hi && (unsigned long long)__ldg(&a[idx]) < key;
+        const unsigned m = __ballot_sync(FULL_MASK, lt);
+        if (!m) break;
+        const int l = 31 - __clz(m);
+        lo = lo + (long long)l * step + 1;
+        hi = min(hi, lo - 1 + step);
+    }
+    return lo;
+}
+}  // namespace
+
+struct RowSmem {
+    __align__(16) uint8_t stage[RW][SOFF + STW + 48];
+};
+
+#ifndef GPUBPE_DEC_MINB
+#define GPUBPE_DEC_MINB 4
+#endif
+__global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const __grid_constant__ DecodeParams P) {
+    extern __shared__ __align__(16) unsigned char rsm_raw[];
+    RowSmem &S = *reinterpret_cast<RowSmem *>(rsm_raw);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint8_t *stage = S.stage[wid];
+    uint32_t *sw = reinterpret_cast<uint32_t *>(stage);
+    for (int q = lane; q < (SOFF + STW + 48) / 16; q += 32) reinterpret_cast<uint4 *>(stage)[q] = make_uint4(0, 0, 0, 0);
+    const unsigned long long n_rows = (P.n_ids + RROW - 1) / RROW;
+    const unsigned long long gw = (unsigned long long)blockIdx.x * RW + wid, GW = (unsigned long long)gridDim.x * RW;
+    const unsigned long long q0 = n_rows / GW, rem = n_rows % GW;
+    const unsigned long long r0 = gw * q0 + min(gw, rem), r1 = r0 + q0 + (gw < rem ? 1 : 0);
+    if (r0 >= r1) return;
+    long long cur = P.n_seqs ? warp_lower_bound(P.id_offs, 0, (long long)P.n_seqs + 1, r0 * RROW, lane) : 0;
+    uint4 idv = load_ids4(P, r0, lane);
+    __syncwarp();
+    for (unsigned long long r = r0; r < r1; ++r) {
+        uint4 nidv = make_uint4(0, 0, 0, 0);
+        if (r + 1 < r1) nidv = load_ids4(P, r + 1, lane);
+        const unsigned long long t = r / RPT;
+        const uint32_t rr = (uint32_t)(r % RPT);
+        uint32_t pb = lane < (int)rr ? __ldg(&P.row_bytes[t * RPT + lane]) : 0u;
+        const unsigned long long tb = __ldg(&P.tile_base[t]);
+        const unsigned long long i0 = r * RROW + (unsigned long long)lane * RDPT;
+        uint4 rec[RDPT];
+        uint32_t sum = 0;
+#pragma unroll
+        for (int j = 0; j < RDPT; ++j) {
+            const uint32_t id = comp(idv, j);
+            rec[j] = make_uint4(0, 0, 0, 0);  // unknown ids: length 0 (the first pass reported them)
+            if (i0 + j < P.n_ids) {
+                if (id < P.n_vocab) rec[j] = __ldg(&P.vrec[id]);
+            }
+            sum += rec[j].x & 0xFFu;
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL_MASK, x, o);
+            if (lane >= o) x += y;
+        }
+        const uint32_t excl = x - sum, total = __shfl_sync(FULL_MASK, x, 31);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pb += __shfl_xor_sync(FULL_MASK, pb, o);
+        const unsigned long long base = tb + pb;
+        const bool fits = base + total <= P.out_cap;
+        if (!fits && lane == 0) atomicMax(&P.st->need, base + total);
+        const uint32_t shift = (uint32_t)(base & 15);
+        const bool staged = shift + total <= STW;
+        if (staged) {
+            uint32_t o = SOFF + shift + excl;
+#pragma unroll
+            for (int j = 0; j < RDPT; ++j) {
+                const uint32_t l = rec[j].x & 0xFFu;
+                if (l && l <= 15) {
+                    uint4 v = rec[j];
+                    v.x &= ~0xFFu;  // the length byte lands (as zero) just before the string
+                    or16(sw, o - 1, v, l + 1);
+                } else if (l) {
+                    const uint4 *src = reinterpret_cast<const uint4 *>(P.blob) + rec[j].y;
+                    for (uint32_t c = 0; c < l; c += 16) or16(sw, o + c, __ldg(src + (c >> 4)), min(16u, l - c));
+                }
+                o += l;
+            }
+        } else if (fits) {  // more than the stage holds: straight to global, byte by byte
+            uint32_t o = excl;
+#pragma unroll
+            for (int j = 0; j < RDPT; ++j) {
+                const uint32_t l = rec[j].x & 0xFFu;
+                uint8_t *dst = P.out + base + o;
+                if (l <= 15) {
+                    for (uint32_t b = 0; b < l; ++b) dst[b] = (uint8_t)(comp(rec[j], (b + 1) >> 2) >> (8 * ((b + 1) & 3)));
+                } else {
+                    const uint8_t *src = P.blob + 16ull * rec[j].y;
+                    for (uint32_t b = 0; b < l; ++b) dst[b] = __ldg(src + b);
+                }
+                o += l;
+            }
+        }
+        __syncwarp();
+        const uint32_t end = shift + total, nq = (end + 15) >> 4;
+        if (staged && fits) {
+            uint8_t *gdst = P.out + (base & ~15ull);
+            const uint8_t *sb = stage + SOFF;
+            for (uint32_t q = lane; q < nq; q += 32) {
+                const uint32_t lo = q * 16, hi = lo + 16;
+                if (lo >= shift && hi <= end) {
+                    reinterpret_cast<uint4 *>(gdst)[q] = reinterpret_cast<const uint4 *>(sb)[q];
+                } else {  // an edge chunk shared with a neighbouring row: bytes, then words, then bytes
+                    uint32_t b = max(lo, shift);
+                    const uint32_t e = min(hi, end);
+                    for (; b < e && (b & 3); ++b) gdst[b] = sb[b];
+                    for (; b + 4 <= e; b += 4)
+                        *reinterpret_cast<uint32_t *>(gdst + b) = *reinterpret_cast<const uint32_t *>(sb + b);
+                    for (; b < e; ++b) gdst[b] = sb[b];
+                }
+            }
+        }
+        if (P.n_seqs) {  // byte offsets of the sequences that start in this row
+            const unsigned long long rowlo = r * RROW, rowhi = rowlo + RROW;
+            const bool last = r + 1 == n_rows;
+            for (;;) {
+                const long long d = cur + lane;
+                unsigned long long s = ~0ull;
+                bool in = false;
+                if (d <= (long long)P.n_seqs) {
+                    s = (unsigned long long)__ldg(&P.id_offs[d]);
+                    in = s < rowhi || last;
+                }
+                const unsigned long long q = in && s < P.n_ids ? s - rowlo : 0;
+                const int src = (int)(q / RDPT) & 31, jj = (int)(q % RDPT);
+                uint32_t pre = excl, pick = 0;
+#pragma unroll
+                for (int j = 0; j < RDPT; ++j) {
+                    const uint32_t v = __shfl_sync(FULL_MASK, pre, src);
+                    if (j == jj) pick = v;
+                    pre += rec[j].x & 0xFFu;
+                }
+                if (in) P.out_offs[d] = (long long)(s >= P.n_ids ? base + total : base + pick);
+                const unsigned m = __ballot_sync(FULL_MASK, in);
+                cur += __popc(m);
+                if (m != FULL_MASK) break;
+            }
+        }
+        if (r + 1 == n_rows && lane == 0) P.st->n_bytes = base + total;
+        __syncwarp();
+        if (staged)
+            for (uint32_t q = lane; q <= nq; q += 32) reinterpret_cast<uint4 *>(stage + SOFF)[q] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        idv = nidv;
+    }
+}
+
+cudaError_t decode_rows_occupancy(int *blocks) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_decode_rows, RW * 32, sizeof(RowSmem));
+}
+
+cudaError_t launch_decode_rows(const DecodeParams &P, int grid, cudaStream_t s) {
+    k_decode_rows<<<grid, RW * 32, sizeof(RowSmem), s>>>(P);
+    return cudaGetLastError();
+}
+
 // ---- two-pass mode: tile byte totals (one CTA per tile, every CTA at once),
 //      then one CTA scans them into tile offsets; k_decode then needs no look-back
 __global__ void __launch_bounds__(256) k_dec_tile_bytes(const __grid_constant__ DecodeParams P,
                                                         unsigned long long *tile_bytes) {
-    __shared__ unsigned long long red[8];
-    const unsigned long long t = blockIdx.x, t0 = t * TD;
     constexpr int IT = TD / (256 * 4);  // 4-id groups per thread, all loads issued together
-    unsigned long long sum = 0;
+    __shared__ uint32_t red[8];
+    const unsigned long long t = blockIdx.x, t0 = t * TD;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t id[IT][4];
 #pragma unroll
     for (int k = 0; k < IT; ++k) {
@@ -310,21 +520,27 @@ __global__ void __launch_bounds__(256) k_dec_tile_bytes(const __grid_constant__ 
             for (int j = 0; j < 4; ++j) id[k][j] = i + j < P.n_ids ? __ldg(&P.ids[i + j]) : 0u;
         }
     }
+    // lengths from the 1-byte table (128 ids per L1 line: the frequent low ids share lines)
+    uint32_t tot = 0;
 #pragma unroll
     for (int k = 0; k < IT; ++k) {
         const unsigned long long i = t0 + (unsigned long long)k * 1024 + threadIdx.x * 4;
+        uint32_t sk = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (i + j < P.n_ids) {
-                const uint32_t inf = info_of(P, id[k][j]);
-                if (inf == GPUBPE_INF) atomicMin(&P.st->bad, i + j);
-                else sum += inf & 0xFFu;
+                const uint32_t l = id[k][j] < P.n_vocab ? __ldg(&P.vlen[id[k][j]]) : 0u;
+                if (l == 0) atomicMin(&P.st->bad, i + j);
+                sk += l;
             }
         }
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL_MASK, sum, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+        for (int o = 16; o > 0; o >>= 1) sk += __shfl_xor_sync(FULL_MASK, sk, o);
+        // warp w at k covers ids [k*1024 + w*128, +128): row 8k + w of the tile
+        if (P.row_bytes && lane == 0) P.row_bytes[t * (TD / 128) + 8 * k + wid] = sk;
+        tot += sk;
+    }
+    if (lane == 0) red[wid] = tot;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long s = 0;
@@ -377,7 +593,9 @@ size_t decode_smem_bytes() { return sizeof(DecSmem); }
 int decode_tile_ids() { return TD; }
 
 cudaError_t setup_decode() {
-    return cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem));
+    cudaError_t e = cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_decode_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
 }
 
 cudaError_t decode_occupancy(int *blocks) {

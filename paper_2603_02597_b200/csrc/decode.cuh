@@ -12,6 +12,9 @@ struct DecodeState {
 struct DecodeParams {
     const uint32_t *vinfo;  // per id: blob offset << 8 | length, INF if not decodable
     const uint8_t *blob;
+    const uint4 *vrec;      // per id: 16-B record, byte 0 = length; length <= 15: the string in
+                            // bytes 1..15, else .y = its blob chunk (offset / 16); zero if unknown
+    const uint8_t *vlen;    // per id: length, 0 if not decodable
     uint32_t n_vocab;       // ids >= n_vocab are unknown
     const uint32_t *ids;
     unsigned long long n_ids;
@@ -23,6 +26,7 @@ struct DecodeParams {
     DecodeState *st;
     unsigned long long *status;  // [n_tiles] look-back words (single-pass mode)
     const unsigned long long *tile_base;  // [n_tiles] output offset of each tile (two-pass mode), or null
+    uint32_t *row_bytes;       // [n_tiles * 32] bytes of each 128-id row (two-pass mode), or null
     unsigned long long n_tiles;
     unsigned int epoch;
     int aligned;               // ids pointer is 16-B aligned
@@ -34,6 +38,8 @@ int decode_tile_ids();
 cudaError_t setup_decode();
 cudaError_t decode_occupancy(int *blocks);
 cudaError_t launch_decode(const DecodeParams &P, int grid, cudaStream_t s);
+cudaError_t decode_rows_occupancy(int *blocks);
+cudaError_t launch_decode_rows(const DecodeParams &P, int grid, cudaStream_t s);
 cudaError_t launch_decode_offsets(const DecodeParams &P, unsigned long long *tile_bytes,
                                   unsigned long long *tile_base, cudaStream_t s);
 #endif

@@ -601,6 +601,84 @@ def test_decode_two_pass_large_batch(tokenizer):
     assert torch.equal(oo, o)
 
 
+def _host_decode(tokenizer, ids, offs):
+    """numpy restatement of decode_tokens over a CSR batch (bytes, byte offsets)."""
+    sid, blob, soff = tokenizer._symbol_bytes()
+    n = int(max(sid.max(), ids.max())) + 1
+    lens = np.zeros(n, np.int64)
+    start = np.zeros(n, np.int64)
+    lens[sid] = np.diff(soff.astype(np.int64))
+    start[sid] = soff[:-1].astype(np.int64)
+    L = lens[ids]
+    ends = np.cumsum(L)
+    total = int(ends[-1]) if L.size else 0
+    gather = np.repeat(start[ids] - (ends - L), L) + np.arange(total)
+    cum = np.concatenate([[0], ends])
+    return blob[gather], cum[offs]
+
+
+def test_decode_rows_edge_cases(tokenizer):
+    """The two-pass decode (first pass: tile and 256-id row totals; second: one
+    warp per row range) on ~6 M ids: empty and one-id sequences, sequences that
+    start exactly at row boundaries, more than 32 sequences starting in one row,
+    rows of long tokens that exceed the warp's stage, an unaligned id pointer, a
+    batch length that is not a multiple of 256; same bytes and offsets as the
+    host restatement and as the CTA-tile kernel (GPUBPE_DEC_TILES)."""
+    import os
+
+    import torch
+
+    sid, _, soff = tokenizer._symbol_bytes()
+    rng = np.random.default_rng(11)
+    n = 6_000_003
+    ids = sid[rng.integers(0, sid.size, n + 1)].astype(np.uint32)
+    lens = np.diff(soff.astype(np.int64))
+    longest = sid[np.argsort(lens)[-64:]]
+    ids[1_000_000:1_004_096] = longest[rng.integers(0, 64, 4096)]  # rows > 2 KiB of output
+    cuts = [0]
+    i = 0
+    while i < n:
+        k = int(rng.choice([0, 0, 1, 2, 3, 7, 256, 300, 5000]))
+        if rng.random() < 0.02:
+            k = 256 - (i % 256)  # next sequence starts on a row boundary
+        i = min(n, i + k)
+        cuts.append(i)
+    cuts += [n, n]  # trailing empty sequences
+    cuts += list(range(2_000_000, 2_004_000, 2)) + [2_000_512] * 40  # dense starts, empty runs
+    offs = np.sort(np.asarray(cuts, np.int64))
+    assert np.any(np.diff(np.searchsorted(offs, np.arange(0, n, 256))) > 40)  # >32 starts in a row
+    enc = tokenizer.device_encoder()
+    full = torch.from_numpy(ids.view(np.int32)).cuda()
+    d_ids = full[1:]  # 4-byte offset: unaligned id loads
+    want_bytes, want_offs = _host_decode(tokenizer, ids[1:], offs)
+    o = torch.from_numpy(offs).cuda()
+    results = []
+    for tiles in (False, True):
+        if tiles:
+            os.environ["GPUBPE_DEC_TILES"] = "1"
+        try:
+            out = torch.empty(want_bytes.size + 64, dtype=torch.uint8, device="cuda")
+            oo = torch.empty_like(o)
+            nb = enc.decode_into(d_ids, o, out, oo)
+        finally:
+            os.environ.pop("GPUBPE_DEC_TILES", None)
+        assert nb == want_bytes.size
+        assert np.array_equal(out[:nb].cpu().numpy(), want_bytes)
+        assert np.array_equal(oo.cpu().numpy(), want_offs)
+        results.append(out[:nb])
+    assert torch.equal(results[0], results[1])
+    # an unknown id deep inside the batch is reported by its index
+    bad = full.clone()
+    bad[3_333_334] = 60000
+    with pytest.raises(bpe.errors.UnknownTokenId):
+        enc.decode_into(bad[1:], o, torch.empty(want_bytes.size + 64, dtype=torch.uint8, device="cuda"),
+                        torch.empty_like(o))
+    # too small an output buffer: ValueError, nothing written past it
+    with pytest.raises(ValueError):
+        enc.decode_into(d_ids, o, torch.empty(want_bytes.size // 2, dtype=torch.uint8, device="cuda"),
+                        torch.empty_like(o))
+
+
 def test_integration_stub_binding(tokenizer, prose_samples):
     """The ctypes binding INTEGRATION.md shows a lanebpe maintainer (host buffers,
     no torch, no memo strings) gives the same ids as tokenize_batch."""
