@@ -373,6 +373,10 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
     if (r0 >= r1) return;
     long long cur = P.n_seqs ? warp_lower_bound(P.id_offs, 0, (long long)P.n_seqs + 1, r0 * RROW, lane) : 0;
     uint4 idv = load_ids4(P, r0, lane);
+    // carry_lo >= 0: stage chunk 0 holds the previous row's last, partial 16-B chunk,
+    // whose bytes from carry_lo on are ours (the warp's rows are contiguous, so only
+    // the range's first and last chunks are shared with other warps)
+    int carry_lo = -1;
     __syncwarp();
     for (unsigned long long r = r0; r < r1; ++r) {
         uint4 nidv = make_uint4(0, 0, 0, 0);
@@ -407,6 +411,15 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
         if (!fits && lane == 0) atomicMax(&P.st->need, base + total);
         const uint32_t shift = (uint32_t)(base & 15);
         const bool staged = shift + total <= STW;
+        if (carry_lo >= 0 && !(staged && fits)) {  // this row is not staged: flush the carried chunk
+            uint8_t *gdst = P.out + (base & ~15ull);
+            for (uint32_t b = carry_lo + lane; b < shift; b += 32) gdst[b] = stage[SOFF + b];
+            __syncwarp();
+            if (lane == 0) reinterpret_cast<uint4 *>(stage + SOFF)[0] = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+            carry_lo = -1;
+        }
+        const uint32_t own_lo = carry_lo >= 0 ? (uint32_t)carry_lo : shift;
         if (staged) {
             uint32_t o = SOFF + shift + excl;
 #pragma unroll
@@ -439,15 +452,17 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
         }
         __syncwarp();
         const uint32_t end = shift + total, nq = (end + 15) >> 4;
+        const bool keep_tail = staged && fits && r + 1 < r1 && (end & 15);
         if (staged && fits) {
             uint8_t *gdst = P.out + (base & ~15ull);
             const uint8_t *sb = stage + SOFF;
-            for (uint32_t q = lane; q < nq; q += 32) {
+            const uint32_t nst = keep_tail ? nq - 1 : nq;  // the partial tail chunk moves on
+            for (uint32_t q = lane; q < nst; q += 32) {
                 const uint32_t lo = q * 16, hi = lo + 16;
-                if (lo >= shift && hi <= end) {
+                if (lo >= own_lo && hi <= end) {
                     reinterpret_cast<uint4 *>(gdst)[q] = reinterpret_cast<const uint4 *>(sb)[q];
-                } else {  // an edge chunk shared with a neighbouring row: bytes, then words, then bytes
-                    uint32_t b = max(lo, shift);
+                } else {  // a chunk shared with another warp's row: bytes, then words, then bytes
+                    uint32_t b = max(lo, own_lo);
                     const uint32_t e = min(hi, end);
                     for (; b < e && (b & 3); ++b) gdst[b] = sb[b];
                     for (; b + 4 <= e; b += 4)
@@ -484,8 +499,18 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
         }
         if (r + 1 == n_rows && lane == 0) P.st->n_bytes = base + total;
         __syncwarp();
+        uint4 tail = make_uint4(0, 0, 0, 0);
+        if (keep_tail) tail = reinterpret_cast<const uint4 *>(stage + SOFF)[nq - 1];
+        __syncwarp();
         if (staged)
             for (uint32_t q = lane; q <= nq; q += 32) reinterpret_cast<uint4 *>(stage + SOFF)[q] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        if (keep_tail) {
+            if (lane == 0) reinterpret_cast<uint4 *>(stage + SOFF)[0] = tail;
+            carry_lo = nq == 1 ? (int)own_lo : 0;
+        } else {
+            carry_lo = -1;
+        }
         __syncwarp();
         idv = nidv;
     }

@@ -24,7 +24,7 @@ ROOT = Path(__file__).resolve().parent.parent
 LIB = ROOT / "paper_2603_02597_b200" / "libgpubpe.so"
 
 
-def line_map(kernel: str, lib: Path = LIB) -> dict[int, tuple[str, int]]:
+def line_map(kernel: str, lib: Path = LIB, template: str = "") -> dict[int, tuple[str, int]]:
     tmp = Path(tempfile.mkdtemp())
     subprocess.run(["cuobjdump", "-xelf", "all", str(Path(lib).resolve())], cwd=tmp, check=True,
                    capture_output=True)
@@ -34,7 +34,10 @@ def line_map(kernel: str, lib: Path = LIB) -> dict[int, tuple[str, int]]:
         inside, cur = False, None
         for ln in txt.splitlines():
             if ln.startswith(".text."):
-                inside = kernel in ln
+                # exact kernel (k_decode must not match k_decode_rows) and, for a
+                # template, the instantiation the report profiled
+                inside = re.search(r"_Z\d+" + re.escape(kernel) + r"(?![A-Za-z_])", ln) is not None and (
+                    not template or template in ln)
                 continue
             if not inside:
                 continue
@@ -67,7 +70,12 @@ def main():
                                      "Instructions Executed")}
     body = [r for r in rows[hdr_i + 1:] if len(r) == len(hdr)]
     base = int(body[0][ci["Address"]], 16)
-    lm = line_map(args.kernel, Path(args.lib))
+    # which template instantiation the report holds (k_encode<true> / <false>)
+    names = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv", "--metrics", "launch__grid_size"],
+                           capture_output=True, text=True).stdout
+    template = ("ILb1E" if ("<true>" in names or "<1>" in names) else
+                "ILb0E" if ("<false>" in names or "<0>" in names) else "")
+    lm = line_map(args.kernel, Path(args.lib), template)
     reason_cols = [n for n in hdr if n.startswith("stall_") and "Not Issued" not in n]
     reasons = defaultdict(lambda: defaultdict(int))
     samples, insts = defaultdict(int), defaultdict(int)

@@ -8,7 +8,7 @@ for W in c1_131k corpus_256m; do
   python tools/ncu_lines.py gpurun_out/prof_${TAG}_$W.ncu-rep --kernel k_encode --top 40 --lib gpurun_out/lib_${TAG}.so > profiles/${TAG}_${W}_lines.txt 2>&1
 done
 python tools/ncu_lines.py gpurun_out/prof_${TAG}_pretok.ncu-rep --kernel k_pretok --top 30 --lib gpurun_out/lib_${TAG}.so > profiles/${TAG}_pretok_lines.txt 2>&1
-[ -f gpurun_out/prof_${TAG}_decode_corpus_256m.ncu-rep ] && python tools/ncu_lines.py gpurun_out/prof_${TAG}_decode_corpus_256m.ncu-rep --kernel k_decode --top 30 --lib gpurun_out/lib_${TAG}.so > profiles/${TAG}_decode_lines.txt 2>&1
+[ -f gpurun_out/prof_${TAG}_decode_corpus_256m.ncu-rep ] && python tools/ncu_lines.py gpurun_out/prof_${TAG}_decode_corpus_256m.ncu-rep --kernel k_decode_rows --top 30 --lib gpurun_out/lib_${TAG}.so > profiles/${TAG}_decode_lines.txt 2>&1
 grep -h "^{" gpurun_out/bench_${TAG}.log > profiles/${TAG}_bench.jsonl
 grep -h "^{" gpurun_out/bench_ref_${TAG}.log > profiles/${TAG}_bench_reference.jsonl
 grep -h "^{" gpurun_out/bench_corpus_${TAG}.log gpurun_out/bench_c4_${TAG}.log > profiles/${TAG}_bench_corpus.jsonl

@@ -36,3 +36,6 @@ for mode in (0, 1):
     e1.record(); e1.synchronize()
     print("mode %d: %.1f us per 16 MiB batch" % (mode, e0.elapsed_time(e1) * 100))
 enc.set_mode(0)
+enc.encode_into(d, o, out, oo, 1 << 40, 1 << 40)
+st = enc.query()
+print("stats:", {k: st[k] for k in ("n_bytes", "n_ids", "n_segments", "memo_hits", "medium_segments", "giant_segments", "engine_passes", "tiles")})
