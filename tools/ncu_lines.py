@@ -36,7 +36,7 @@ def line_map(kernel: str, lib: Path = LIB, template: str = "") -> dict[int, tupl
             if ln.startswith(".text."):
                 # exact kernel (k_decode must not match k_decode_rows) and, for a
                 # template, the instantiation the report profiled
-                inside = re.search(r"_Z\d+" + re.escape(kernel) + r"(?![A-Za-z_])", ln) is not None and (
+                inside = re.search(r"_Z\d+" + re.escape(kernel) + r"(?![a-z_])", ln) is not None and (
                     not template or template in ln)
                 continue
             if not inside:
