@@ -1406,9 +1406,14 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *
         CK(cudaMemsetAsync(ctx->dec_status.p, 0, ctx->dec_status.bytes, s));
         ctx->dec_epoch = 1;
     }
-    DecodeState init{0, 0, 0, ~0ull};
+    // the state goes down and comes back through the pinned state buffer (a pageable
+    // source would make the first copy a staged, host-blocking one)
+    static_assert(sizeof(EncodeState) >= 2 * sizeof(DecodeState), "pinned state buffer too small");
+    DecodeState *hs = reinterpret_cast<DecodeState *>(ctx->h_state);
+    ctx->state_fresh = false;
+    hs[0] = DecodeState{0, 0, 0, ~0ull};
     DecodeState *d_st = static_cast<DecodeState *>(ctx->dec_state.p);
-    CK(cudaMemcpyAsync(d_st, &init, sizeof init, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_st, &hs[0], sizeof(DecodeState), cudaMemcpyHostToDevice, s));
     DecodeParams P{};
     P.vinfo = ctx->d_vinfo;
     P.blob = ctx->d_vblob;
@@ -1428,9 +1433,12 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *
     P.epoch = ctx->dec_epoch;
     P.aligned = (reinterpret_cast<uintptr_t>(d_ids) & 15) == 0;
     P.tile_base = nullptr;
-    // many tiles per CTA: two passes (tile totals + scan, then no look-back) are ~5%
-    // faster; a few tiles per CTA: the single pass saves two launches
-    if (n_tiles >= 4 * (uint64_t)ctx->dec_grid && !getenv("GPUBPE_DEC_LOOKBACK")) {
+    const char *tp_env = getenv("GPUBPE_DEC_TWOPASS_MIN");  // tiles (tuning)
+    // two passes (tile totals + scan, then the warp-per-row kernel) from ~1.25 tiles per
+    // CTA of the one-pass kernel: measured crossover between 1 M ids (256 tiles: one pass
+    // 46 us, two 54 us) and 2.1 M ids (515 tiles: 62 vs 57 us)
+    const uint64_t tp_min = tp_env ? strtoull(tp_env, nullptr, 10) : (5 * (uint64_t)ctx->dec_grid) / 4;
+    if (n_tiles >= tp_min && !getenv("GPUBPE_DEC_LOOKBACK")) {
         if ((rc = ensure(ctx, ctx->dec_tiles, n_tiles * 16 + n_tiles * 4 * (decode_tile_ids() / 128), false)))
             return rc;
         unsigned long long *tb = static_cast<unsigned long long *>(ctx->dec_tiles.p);
@@ -1444,9 +1452,9 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *
         CK(launch_decode(P, (int)std::min<uint64_t>(n_tiles, (uint64_t)ctx->dec_grid), s));
     }
     DecodeState h;
-    CK(cudaMemcpyAsync(ctx->h_state, d_st, sizeof h, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs[1], d_st, sizeof h, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    memcpy(&h, ctx->h_state, sizeof h);
+    memcpy(&h, &hs[1], sizeof h);
     ctx->state_fresh = false;
     if (h.bad != ~0ull) {
         *bad_index = h.bad;

@@ -623,7 +623,8 @@ def test_decode_rows_edge_cases(tokenizer):
     start exactly at row boundaries, more than 32 sequences starting in one row,
     rows of long tokens that exceed the warp's stage, an unaligned id pointer, a
     batch length that is not a multiple of 256; same bytes and offsets as the
-    host restatement and as the CTA-tile kernel (GPUBPE_DEC_TILES)."""
+    host restatement and as the CTA-tile kernel (GPUBPE_DEC_TILES) and the one-pass
+    look-back kernel (GPUBPE_DEC_LOOKBACK)."""
     import os
 
     import torch
@@ -653,20 +654,21 @@ def test_decode_rows_edge_cases(tokenizer):
     want_bytes, want_offs = _host_decode(tokenizer, ids[1:], offs)
     o = torch.from_numpy(offs).cuda()
     results = []
-    for tiles in (False, True):
-        if tiles:
-            os.environ["GPUBPE_DEC_TILES"] = "1"
+    for knob in (None, "GPUBPE_DEC_TILES", "GPUBPE_DEC_LOOKBACK"):  # rows / CTA tiles / one pass
+        if knob:
+            os.environ[knob] = "1"
         try:
             out = torch.empty(want_bytes.size + 64, dtype=torch.uint8, device="cuda")
             oo = torch.empty_like(o)
             nb = enc.decode_into(d_ids, o, out, oo)
         finally:
-            os.environ.pop("GPUBPE_DEC_TILES", None)
+            if knob:
+                os.environ.pop(knob)
         assert nb == want_bytes.size
         assert np.array_equal(out[:nb].cpu().numpy(), want_bytes)
         assert np.array_equal(oo.cpu().numpy(), want_offs)
         results.append(out[:nb])
-    assert torch.equal(results[0], results[1])
+    assert torch.equal(results[0], results[1]) and torch.equal(results[0], results[2])
     # an unknown id deep inside the batch is reported by its index
     bad = full.clone()
     bad[3_333_334] = 60000
