@@ -469,6 +469,9 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
                         *reinterpret_cast<uint32_t *>(gdst + b) = *reinterpret_cast<const uint32_t *>(sb + b);
                     for (; b < e; ++b) gdst[b] = sb[b];
                 }
+                // the lane that stored the chunk clears it (bytes past `end` are never set:
+                // records and blob strings are zero-padded)
+                reinterpret_cast<uint4 *>(stage + SOFF)[q] = make_uint4(0, 0, 0, 0);
             }
         }
         if (P.n_seqs) {  // byte offsets of the sequences that start in this row
@@ -499,14 +502,15 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
         }
         if (r + 1 == n_rows && lane == 0) P.st->n_bytes = base + total;
         __syncwarp();
-        uint4 tail = make_uint4(0, 0, 0, 0);
-        if (keep_tail) tail = reinterpret_cast<const uint4 *>(stage + SOFF)[nq - 1];
-        __syncwarp();
-        if (staged)
-            for (uint32_t q = lane; q <= nq; q += 32) reinterpret_cast<uint4 *>(stage + SOFF)[q] = make_uint4(0, 0, 0, 0);
-        __syncwarp();
-        if (keep_tail) {
-            if (lane == 0) reinterpret_cast<uint4 *>(stage + SOFF)[0] = tail;
+        if (staged && !fits)  // staged but not stored (the call fails with the size needed)
+            for (uint32_t q = lane; q < nq; q += 32) reinterpret_cast<uint4 *>(stage + SOFF)[q] = make_uint4(0, 0, 0, 0);
+        if (keep_tail) {  // lane 0 moves the unstored tail chunk to the front
+            if (lane == 0) {
+                uint4 *c = reinterpret_cast<uint4 *>(stage + SOFF);
+                const uint4 tail = c[nq - 1];
+                c[nq - 1] = make_uint4(0, 0, 0, 0);
+                c[0] = tail;
+            }
             carry_lo = nq == 1 ? (int)own_lo : 0;
         } else {
             carry_lo = -1;
