@@ -140,6 +140,8 @@ int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out);
  * gpubpe_decode: d_ids[n_ids] as n_seqs sequences (d_id_offs[n_seqs+1] CSR;
  *   n_seqs == 0: one sequence, no offsets) -> their byte strings back to back
  *   in d_out (capacity out_cap) with d_out_offs[n_seqs+1].  Synchronises.
+ *   d_ids and d_out must be 16-byte aligned (the kernels move 16-byte
+ *   vectors; a misaligned pointer is GPUBPE_EINVAL, never a fault).
  *   Unknown id: GPUBPE_EINVAL, *bad_index = its index (UnknownTokenId).
  *   Capacity too small: GPUBPE_ERANGE, *n_bytes_out = the bytes needed.
  */
@@ -178,6 +180,50 @@ int gpubpe_junction_bits(gpubpe_ctx *ctx, uint32_t *h_out);
  * ids must be below 2^24.  Synchronous. */
 int gpubpe_merge_tokens(gpubpe_ctx *ctx, const uint32_t *d_tokens, const uint64_t *h_offs, uint64_t n_seqs,
                         uint32_t *d_out, uint64_t *h_counts, void *stream);
+
+/* gpubpe_merge_tokens plus the reference's two debugging hooks of the engine:
+ *   d_trace    nullable, device, one uint64 per input token (same offsets as
+ *              d_tokens): merge k of sequence s stores (pass << 34) | (merged
+ *              at position 0 << 33) | (its right token was the last << 32) |
+ *              rank at d_trace[h_offs[s] + k], in pass order and by position
+ *              inside a pass -- the first/last bits give sequential_bpe's
+ *              lookup count (a merge probes each neighbour it has); the
+ *              `trace` argument of sequential_bpe /
+ *              run_block_engine (engines.py:270,317-319,395-396) is the ranks
+ *              in this order when passes merge one pair (tables that are not
+ *              well-formed), and sorted by rank otherwise;
+ *   fault_seq  -1, or the sequence whose run applies inject_compaction_fault
+ *              (engines.py:252-266,378-388): the first pass that can be
+ *              corrupted merges its winning pair one slot off (p+1, else p-1)
+ *              with the winner's new token.
+ * Id n_ids of the context (one past the largest id of its tables) is an inert
+ * token no rule mentions: callers map ids outside the table to it. */
+int gpubpe_merge_tokens_ex(gpubpe_ctx *ctx, const uint32_t *d_tokens, const uint64_t *h_offs, uint64_t n_seqs,
+                           uint32_t *d_out, uint64_t *h_counts, uint64_t *d_trace, int64_t fault_seq,
+                           void *stream);
+
+/* One evaluation pass of the reference's lane engine (eval_pairs,
+ * engines.py:133-168) on the device: probe every adjacent pair of
+ * d_tokens[0..n) and reduce to the lowest rank, leftmost on ties.
+ * h_result[0] = position (UINT64_MAX when no pair is in the table),
+ * h_result[1] = rank, h_result[2] = new token id.  Synchronous. */
+int gpubpe_eval_pairs(gpubpe_ctx *ctx, const uint32_t *d_tokens, uint64_t n, uint64_t *h_result, void *stream);
+
+/* One merge applied by compaction (engines.py:171-217): d_out[0..n-1) =
+ * d_tokens with slots best_pos, best_pos+1 replaced by new_token.
+ * method 0 = compact_double_buffer (direct index map), 1 = compact_scan
+ * (removal flags + exclusive prefix sum + scatter).  GPUBPE_EINVAL when
+ * best_pos is not a pair position (OutOfRange).  Asynchronous, on the
+ * current device. */
+int gpubpe_compact(const uint32_t *d_tokens, uint64_t n, uint64_t best_pos, uint32_t new_token, uint32_t *d_out,
+                   int method, void *stream);
+
+/* PackedPairTable.lookup_keys_into (merge_table.py:170-230) on the device:
+ * packed keys (left << 32) | right -> d_hit[i] (0/1) and d_vals[i] =
+ * (new << 32) | rank where hit; the empty-slot key UINT64_MAX is a miss.
+ * Asynchronous. */
+int gpubpe_lookup_keys(gpubpe_ctx *ctx, const uint64_t *d_keys, uint64_t m, uint8_t *d_hit, uint64_t *d_vals,
+                       void *stream);
 
 /* Device-side merges parsing; replaces the line loop
  * of parse_merges (merge_table.py:88-116) with its vocabulary lookups

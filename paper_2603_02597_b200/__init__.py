@@ -12,7 +12,18 @@ from . import errors
 from .bindings import TokenizerHandle
 from .byte_codec import ByteEncoder, Vocab, base_id_table, build_byte_encoder, decode_tokens, encode_bytes
 from .chunker import ENGINE_NAMES, BatchResult, Chunk, Tokenizer, chunk_tokens, pack_texts, tokenize_batch
-from .engine import BlockConfig, PassCounters, run_block_engine, sequential_bpe, token_seq
+from .engine import (
+    BlockConfig,
+    PairCandidate,
+    PassCounters,
+    compact_double_buffer,
+    compact_scan,
+    eval_pairs,
+    inject_compaction_fault,
+    run_block_engine,
+    sequential_bpe,
+    token_seq,
+)
 from .windows import DEFAULT_LENGTHS, SweepSpec, make_windows
 from .report import (
     BenchRecord,
@@ -27,6 +38,7 @@ from .report import (
 from .merge_table import (
     MergeRule,
     PackedPairTable,
+    ProbeScratch,
     build_table,
     pack_key,
     pack_value,
@@ -52,4 +64,6 @@ __all__ = [
     "build_byte_encoder", "build_table", "chunk_tokens", "decode_tokens", "encode_bytes", "errors",
     "pack_key", "pack_texts", "pack_value", "pinned_empty", "parse_merges", "rule_arrays", "tokenize_batch",
     "unpack_value", "run_block_engine", "sequential_bpe", "token_seq", "__version__",
+    "PairCandidate", "ProbeScratch", "compact_double_buffer", "compact_scan", "eval_pairs",
+    "inject_compaction_fault",
 ]

@@ -60,6 +60,10 @@ SIGNATURES = {
     "gpubpe_decode": (_int, [_vp, _vp, _u64, _vp, _u64, _vp, _u64, _vp, ctypes.POINTER(ctypes.c_uint64),
                              ctypes.POINTER(ctypes.c_uint64), _vp]),
     "gpubpe_merge_tokens": (_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),
+    "gpubpe_merge_tokens_ex": (_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, ctypes.c_int64, _vp]),
+    "gpubpe_eval_pairs": (_int, [_vp, _vp, _u64, _vp, _vp]),
+    "gpubpe_compact": (_int, [_vp, _u64, _u64, ctypes.c_uint32, _vp, _int, _vp]),
+    "gpubpe_lookup_keys": (_int, [_vp, _vp, _u64, _vp, _vp, _vp]),
     "gpubpe_parse_merges": (_int, [_int, _vp, _vp, _vp, _u64, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "gpubpe_launches_per_encode": (_int, []),
     "gpubpe_lookup_pairs": (_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),

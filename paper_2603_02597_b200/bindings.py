@@ -14,24 +14,30 @@ from __future__ import annotations
 from .chunker import ENGINE_NAMES, Tokenizer, tokenize_batch
 from .engine import BlockConfig
 
+__version__ = "0.1.0"  # mirrors the core package (bindings/__init__.py:15)
+
 
 class TokenizerHandle:
-    __slots__ = ("_tokenizer", "_engine", "_workers")
+    """`devices` (extension): an int N or a list of GPU indices to shard every
+    batch across (tokenize_batch(..., devices=...)); default the current GPU."""
+
+    __slots__ = ("_tokenizer", "_engine", "_workers", "_devices")
 
     def __init__(self, vocab_path, merges_path, engine: str = "optimized", *, lane_count: int = 256,
                  max_seq_len: int = 8192, chunk_budget: int | None = None,
-                 workers: int | None = None):
+                 workers: int | None = None, devices=None):
         if engine not in ENGINE_NAMES:
             raise ValueError(f"unknown engine {engine!r}, expected one of {ENGINE_NAMES}")
         cfg = BlockConfig(lane_count=lane_count, max_seq_len=max_seq_len, chunk_budget=chunk_budget)
         self._tokenizer = Tokenizer.from_files(vocab_path, merges_path, cfg)
         self._engine = engine
         self._workers = workers
+        self._devices = devices
 
     @property
     def tokenizer(self) -> Tokenizer:
         return self._tokenizer
 
     def tokenize_batch(self, texts) -> tuple[list[list[int]], float]:
-        res = tokenize_batch(texts, self._tokenizer, self._engine, workers=self._workers)
+        res = tokenize_batch(texts, self._tokenizer, self._engine, workers=self._workers, devices=self._devices)
         return [ids.tolist() for ids in res.token_ids], res.engine_time_ms

@@ -23,8 +23,9 @@ from pathlib import Path
 
 import numpy as np
 
+from . import engine as _engine
 from .byte_codec import ByteEncoder, Vocab, base_id_table, build_byte_encoder, decode_tokens, symbol_bytes
-from .engine import BlockConfig, PassCounters
+from .engine import BlockConfig, PassCounters, run_block_engine, sequential_bpe
 from .errors import BatchError, DeviceError, InvalidBudget, TokenizerError
 from .merge_table import MergeRule, PackedPairTable, build_table, parse_merges, rule_arrays
 
@@ -257,20 +258,154 @@ def pack_texts(texts) -> tuple[np.ndarray, np.ndarray]:
     return data, offs
 
 
+def _lane_allocations(lens: np.ndarray, cfg: BlockConfig) -> int:
+    """Pool buffers the reference's lane engines acquire for a batch: two per
+    chunk of >= 2 ids (engines.py:363-369; shorter runs return before the
+    pool), chunks as tokenize_batch cuts them (chunker.py:139-144)."""
+    lens = np.asarray(lens, dtype=np.int64)
+    whole = lens <= cfg.max_seq_len
+    cb = cfg.chunk_budget
+    n = int(np.count_nonzero(whole & (lens >= 2)))
+    big = lens[~whole]
+    n += int((big // cb).sum()) + int(np.count_nonzero(big % cb >= 2))
+    return 2 * n
+
+
+def _per_chunk(parts, tokenizer: Tokenizer, variant: str) -> BatchResult:
+    """The reference's per-chunk pipeline (chunker.py:139-179) through this
+    module's `sequential_bpe` / `run_block_engine` (each a device engine run):
+    the plugin seam the reference dispatches on.  tokenize_batch takes it only
+    when one of those names was replaced (a caller's own engine, a test
+    double) or a compaction fault is armed for the lane engines; otherwise
+    the whole batch crosses to the device in one call."""
+    cfg = tokenizer.config
+    t0 = time.perf_counter()
+    chunks = []
+    for i, text in enumerate(parts):
+        try:
+            ids = tokenizer.encode(text)
+        except (TokenizerError, TypeError, ValueError) as exc:
+            raise BatchError(i, str(exc)) from exc
+        chunks.extend(chunk_tokens(ids, cfg.chunk_budget, i) if len(ids) > cfg.max_seq_len else [Chunk(i, 0, ids)])
+    encode_ms = (time.perf_counter() - t0) * 1000.0
+    engine_s = 0.0
+    totals = PassCounters()
+    per_input: list[list[np.ndarray]] = [[] for _ in parts]
+    for chunk in chunks:
+        start = time.perf_counter()
+        try:
+            if variant == "sequential":
+                out, counters = sequential_bpe(chunk.tokens, tokenizer.table)
+            else:
+                out, counters = run_block_engine(chunk.tokens, tokenizer.table, cfg,
+                                                 "optimized" if variant == "cuda" else variant)
+        except TokenizerError as exc:
+            raise BatchError(chunk.source_index, str(exc)) from exc
+        engine_s += time.perf_counter() - start
+        totals.merge_from(counters)
+        per_input[chunk.source_index].append(out)
+    t2 = time.perf_counter()
+    token_ids = [np.concatenate(p) if p else np.empty(0, dtype=np.uint32) for p in per_input]
+    return BatchResult(token_ids, engine_s * 1000.0, encode_ms, (time.perf_counter() - t2) * 1000.0, totals)
+
+
+def _device_list(devices) -> list[int] | None:
+    if devices is None:
+        return None
+    if isinstance(devices, int):
+        if devices < 1:
+            raise ValueError(f"devices must be >= 1, got {devices}")
+        return list(range(devices))
+    lst = [int(d) for d in devices]
+    if not lst:
+        raise ValueError("devices must name at least one GPU")
+    return lst
+
+
+def _encode_multi(parts, tokenizer: Tokenizer, devs: list[int], mode: int):
+    """One batch on several GPUs from one process:
+    contiguous document ranges balanced by bytes (multigpu.shard_batch), or a
+    lone long document split at exact cuts (multigpu.split_document), one
+    host thread per GPU driving its own context and stream (the native calls
+    release the GIL), results concatenated in order.  No collective."""
+    import threading
+
+    from . import multigpu
+
+    cfg = tokenizer.config
+    g = len(devs)
+    encs = [tokenizer.device_encoder(d) for d in devs]
+    if len(parts) == 1 and len(parts[0]) >= g * (1 << 20):
+        pieces = multigpu.split_document(parts[0], g, encs[0].junction_bits(), cfg.max_seq_len, cfg.chunk_budget)
+        jobs = [(p, None) for p in pieces]  # per GPU: documents whose ids concatenate to doc 0's
+    else:
+        lens = np.fromiter(map(len, parts), dtype=np.int64, count=len(parts))
+        offs = np.zeros(len(parts) + 1, np.int64)
+        np.cumsum(lens, out=offs[1:])
+        jobs = [(parts[a:b], (a, b)) for a, b in multigpu.shard_batch(offs, g)]
+    results: list = [None] * g
+    errs: list = []
+
+    def run(k):
+        try:
+            docs = jobs[k][0]
+            if docs:
+                results[k] = encs[k].encode_list_host(list(docs), cfg.max_seq_len, cfg.chunk_budget, mode)
+        except BaseException as exc:  # re-raised in the caller
+            errs.append(exc)
+
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(1, g)]
+    for t in threads:
+        t.start()
+    run(0)
+    for t in threads:
+        t.join()
+    if errs:
+        raise errs[0]
+    stats = {"devices": devs, "per_device": []}
+    engine_ms = 0.0
+    token_ids: list[np.ndarray] = []
+    n_bytes = 0
+    for k, (docs, rng) in enumerate(jobs):
+        if results[k] is None:
+            stats["per_device"].append(None)
+            continue
+        ids, oo, st, ms = results[k]
+        stats["per_device"].append(st)
+        n_bytes += int(st["n_bytes"])
+        engine_ms = max(engine_ms, ms)  # the GPUs run concurrently
+        o = oo.tolist()
+        token_ids.extend(ids[a:b] for a, b in zip(o, o[1:]))
+    if jobs[0][1] is None:  # one split document: its pieces' ids back to back
+        token_ids = [np.concatenate(token_ids) if token_ids else np.empty(0, np.uint32)]
+    stats["n_bytes"] = n_bytes
+    stats["allocations"] = sum(int(st["allocations"]) for st in stats["per_device"] if st)
+    return token_ids, engine_ms, stats
+
+
 def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
-                   workers: int | None = None, pretokenize: str | None = None) -> BatchResult:
+                   workers: int | None = None, pretokenize: str | None = None,
+                   devices=None) -> BatchResult:
     """Tokenize a batch of str (UTF-8 encoded) or bytes documents on the GPU.
 
     `workers` is accepted for signature compatibility; the device engine
-    parallelises internally.  pretokenize=None is the reference's semantics
+    parallelises internally.  `devices` (an int N for GPUs 0..N-1, or a list
+    of GPU indices; default: the current GPU) shards the batch across GPUs
+    from this one process.  pretokenize=None is the reference's semantics
     (no pre-tokenization); pretokenize="gpt2" splits at tiktoken's GPT-2
     regex first (ids equal tiktoken's GPT-2 encode_ordinary for valid UTF-8;
     an optional mode, never the default).
+
+    counters: passes = input bytes - output ids (the reference's identity);
+    buffer_allocations follows the lane engines' pool model (two per chunk
+    of >= 2 ids, 0 for "sequential"); device allocations of the call are in
+    device_stats["allocations"] (0 in steady state).
     """
     if variant not in ENGINE_NAMES:
         raise ValueError(f"unknown engine {variant!r}, expected one of {ENGINE_NAMES}")
     if pretokenize not in (None, "gpt2"):
         raise ValueError(f"unknown pretokenize {pretokenize!r}, expected None or 'gpt2'")
+    devs = _device_list(devices)
     cfg = tokenizer.config
     t0 = time.perf_counter()
     parts = _as_parts(texts)
@@ -278,24 +413,31 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
     n_docs = len(parts)
     if n_docs == 0:
         return BatchResult([], 0.0, encode_ms, 0.0, PassCounters())
-    try:
-        enc = tokenizer.device_encoder()
-        from ._native import MODE_DEFAULT, MODE_GPT2_REGEX
+    if pretokenize is None and (
+            run_block_engine is not _engine.run_block_engine or sequential_bpe is not _engine.sequential_bpe
+            or (variant in ("baseline", "optimized") and getattr(_engine._fault_armed, "flag", False))):
+        return _per_chunk(parts, tokenizer, variant)
+    from ._native import MODE_DEFAULT, MODE_GPT2_REGEX
 
-        mode = MODE_GPT2_REGEX if pretokenize == "gpt2" else MODE_DEFAULT
+    mode = MODE_GPT2_REGEX if pretokenize == "gpt2" else MODE_DEFAULT
+    t1 = time.perf_counter()
+    if devs is not None and len(devs) > 1:
+        token_ids, engine_ms, st = _encode_multi(parts, tokenizer, devs, mode)
+        n_ids = sum(len(t) for t in token_ids)
+    else:
+        enc = tokenizer.device_encoder(devs[0] if devs else None)
         if n_docs == 1:  # one buffer: staged piecewise, overlapping its DMA
             data = np.frombuffer(parts[0], dtype=np.uint8)
             ids, out_offs, st, engine_ms = enc.encode_packed_host(
                 data, np.array([0, data.size], np.int64), cfg.max_seq_len, cfg.chunk_budget, mode)
         else:  # many: gathered natively into pinned memory, no join here
             ids, out_offs, st, engine_ms = enc.encode_list_host(parts, cfg.max_seq_len, cfg.chunk_budget, mode)
-    except DeviceError:
-        raise
-    except TokenizerError as exc:  # pragma: no cover - the device reports no per-input errors
-        raise BatchError(0, str(exc)) from exc
-    t2 = time.perf_counter()
-    o = out_offs.tolist()
-    token_ids = [ids[a:b] for a, b in zip(o, o[1:])]
-    assemble_ms = (time.perf_counter() - t2) * 1000.0
-    counters = PassCounters(passes=int(st["n_bytes"]) - int(ids.size), buffer_allocations=int(st["allocations"]))
+        t2 = time.perf_counter()
+        o = out_offs.tolist()
+        token_ids = [ids[a:b] for a, b in zip(o, o[1:])]
+        n_ids = int(ids.size)
+        t1 = t2
+    assemble_ms = (time.perf_counter() - t1) * 1000.0
+    allocs = 0 if variant == "sequential" else _lane_allocations(np.fromiter(map(len, parts), np.int64, n_docs), cfg)
+    counters = PassCounters(passes=int(st["n_bytes"]) - n_ids, buffer_allocations=allocs)
     return BatchResult(token_ids, engine_ms, encode_ms, assemble_ms, counters, st)

@@ -278,7 +278,9 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
     }
     BUILD_STAMP(2);
     // ---- rl / rr and well-formedness
-    std::vector<uint32_t> rl(n_ids, GPUBPE_INF), rr(n_ids, GPUBPE_INF);
+    // one extra entry: id n_ids is an inert sentinel no rule mentions (token-level
+    // callers map ids outside the table to it, gpubpe_merge_tokens)
+    std::vector<uint32_t> rl(n_ids + 1, GPUBPE_INF), rr(n_ids + 1, GPUBPE_INF);
     std::vector<int64_t> maxprod(n_ids, -1);
     for (uint64_t i = 0; i < n_rules; ++i) {
         rl[L[i]] = std::min(rl[L[i]], rank[i]);
@@ -344,7 +346,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
     uint64_t memo_cap_max = 2;
     while (memo_cap_max < 2 * memo_cand) memo_cap_max <<= 1;
     {
-        size_t need = table_slot(slots.size() * sizeof(uint4)) + 2 * table_slot(n_ids * 4) +
+        size_t need = table_slot(slots.size() * sizeof(uint4)) + 2 * table_slot((n_ids + 1) * 4) +
                       table_slot(jbits.size() * 4) + table_slot(256 * 4) +
                       (identity ? 0 : table_slot(ext.size() * 4)) +
                       table_slot(memo_cap_max * sizeof(uint4)) + table_slot(blob_max);
@@ -739,6 +741,12 @@ class CopyPool {
 // host call begins and spin for work only while one is active, so the
 // piecewise staging copies of a ~0.5 MiB batch split across cores without a
 // thread wake-up per copy (and without spinning between calls).
+static inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+}
+
 namespace {
 class StagePool {
   public:
@@ -757,7 +765,13 @@ class StagePool {
     void copy(uint8_t *dst, const uint8_t *src, size_t n) {
         const unsigned parts = (unsigned)th_.size() + 1;
         const size_t chunk = ((n + parts - 1) / parts + 63) & ~(size_t)63;
-        std::lock_guard<std::mutex> call(call_);  // one staged copy at a time
+        // one staged copy at a time; a concurrent caller (another context or
+        // thread, e.g. one per GPU) copies its piece itself instead of waiting
+        std::unique_lock<std::mutex> call(call_, std::try_to_lock);
+        if (!call.owns_lock()) {
+            memcpy(dst, src, n);
+            return;
+        }
         dst_ = dst;
         src_ = src;
         n_ = n;
@@ -767,8 +781,7 @@ class StagePool {
         gen_.fetch_add(1, std::memory_order_release);
         memcpy(dst, src, std::min(n, chunk));
         for (unsigned i; (i = next_.fetch_add(1)) < parts;) run(i);  // parts nobody took yet
-        while (left_.load(std::memory_order_acquire) > 0) {
-        }
+        while (left_.load(std::memory_order_acquire) > 0) cpu_relax();
     }
 
   private:
@@ -792,7 +805,10 @@ class StagePool {
             }
             while (active_.load(std::memory_order_acquire) > 0) {  // spin only inside a host call
                 const unsigned long long gen = gen_.load(std::memory_order_acquire);
-                if (gen == seen) continue;
+                if (gen == seen) {
+                    cpu_relax();
+                    continue;
+                }
                 seen = gen;
                 const unsigned parts = (unsigned)th_.size() + 1;
                 for (unsigned i; (i = next_.fetch_add(1)) < parts;) run(i);
@@ -1102,14 +1118,16 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
                             uint32_t *h_out_ids, int64_t *h_out_offs, uint64_t *n_ids_out, float *kernel_ms,
                             void *stream) {
     // wake the staging helpers now, so they are spinning when the pieces are ready
-    struct StageCall {
+    struct StageCall {  // the helpers spin from here until the last piece is staged
         bool on;
         explicit StageCall(bool b) : on(b) {
             if (on) StagePool::get().begin();
         }
-        ~StageCall() {
+        void done() {
             if (on) StagePool::get().end();
+            on = false;
         }
+        ~StageCall() { done(); }
     } stage_call(!stage && n_bytes >= (512u << 10) && n_bytes <= (16u << 20) && !getenv("GPUBPE_NO_STAGE_POOL"));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->alloc_mark = ctx->n_allocs;
@@ -1185,6 +1203,7 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         else copy_piece(pin + o_in + lo, h_bytes + lo, n_bytes - lo);
         CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, o_doffs + offs_b - lo, cudaMemcpyHostToDevice, s));
     }
+    stage_call.done();
     auto t_b = now();
     CK(cudaEventRecord(ctx->io_ev[0], s));
     uint8_t *dout = dv;  // where the kernel writes ids and offsets
@@ -1389,6 +1408,9 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *
     if (!ctx || !n_bytes_out || !bad_index) return GPUBPE_EINVAL;
     if (!ctx->d_vinfo) return fail(ctx, GPUBPE_EINVAL, "decode: no vocabulary (gpubpe_set_vocab)");
     if (n_seqs && (!d_id_offs || !d_out_offs)) return fail(ctx, GPUBPE_EINVAL, "decode: null offsets");
+    // the kernels move ids and bytes in 16-byte vectors (decode.cu)
+    if ((reinterpret_cast<uintptr_t>(d_out) & 15) || (reinterpret_cast<uintptr_t>(d_ids) & 15))
+        return fail(ctx, GPUBPE_EINVAL, "decode: d_ids and d_out must be 16-byte aligned");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CK(cudaSetDevice(ctx->device));
     *n_bytes_out = 0;
@@ -1491,10 +1513,8 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_set_mode(gpubpe_ctx
     return GPUBPE_OK;
 }
 
-extern "C" __attribute__((visibility("default"))) int gpubpe_merge_tokens(gpubpe_ctx *ctx, const uint32_t *d_tokens,
-                                                                           const uint64_t *h_offs, uint64_t n_seqs,
-                                                                           uint32_t *d_out, uint64_t *h_counts,
-                                                                           void *stream) {
+static int merge_tokens(gpubpe_ctx *ctx, const uint32_t *d_tokens, const uint64_t *h_offs, uint64_t n_seqs,
+                        uint32_t *d_out, uint64_t *h_counts, uint64_t *d_trace, int64_t fault_seq, void *stream) {
     if (!ctx || (n_seqs && (!h_offs || !h_counts))) return GPUBPE_EINVAL;
     if (ctx->T.ext_id) return fail(ctx, GPUBPE_EINVAL, "token-level merges need token ids below 2^24");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1526,6 +1546,8 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_merge_tokens(gpubpe
     Q.counts = static_cast<unsigned long long *>(ctx->mt_counts.p);
     Q.strict = ((ctx->flags & GPUBPE_F_STRICT) || !ctx->T.well_formed) ? 1 : 0;
     Q.n_ids = ctx->n_ids;
+    Q.trace = reinterpret_cast<unsigned long long *>(d_trace);
+    Q.fault_seq = fault_seq;
     CK(launch_merge_tokens(Q, (int)grid, s));
     CK(cudaMemcpyAsync(h_counts, ctx->mt_counts.p, n_seqs * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1533,6 +1555,62 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_merge_tokens(gpubpe
         if (h_counts[i] == ~0ull)
             return fail(ctx, GPUBPE_EINVAL, "sequence %llu holds a token id the merge table does not cover",
                         (unsigned long long)i);
+    return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_merge_tokens(gpubpe_ctx *ctx, const uint32_t *d_tokens,
+                                                                           const uint64_t *h_offs, uint64_t n_seqs,
+                                                                           uint32_t *d_out, uint64_t *h_counts,
+                                                                           void *stream) {
+    return merge_tokens(ctx, d_tokens, h_offs, n_seqs, d_out, h_counts, nullptr, -1, stream);
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_merge_tokens_ex(
+    gpubpe_ctx *ctx, const uint32_t *d_tokens, const uint64_t *h_offs, uint64_t n_seqs, uint32_t *d_out,
+    uint64_t *h_counts, uint64_t *d_trace, int64_t fault_seq, void *stream) {
+    if (ctx && (fault_seq < -1 || (fault_seq >= 0 && (uint64_t)fault_seq >= n_seqs)))
+        return fail(ctx, GPUBPE_EINVAL, "fault_seq %lld outside [-1, %llu)", (long long)fault_seq,
+                    (unsigned long long)n_seqs);
+    return merge_tokens(ctx, d_tokens, h_offs, n_seqs, d_out, h_counts, d_trace, fault_seq, stream);
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_eval_pairs(gpubpe_ctx *ctx, const uint32_t *d_tokens,
+                                                                         uint64_t n, uint64_t *h_result,
+                                                                         void *stream) {
+    if (!ctx || !h_result || (n && !d_tokens)) return GPUBPE_EINVAL;
+    if (ctx->T.ext_id) return fail(ctx, GPUBPE_EINVAL, "eval_pairs needs ids < 2^24");
+    if (n >= (1ull << 32)) return fail(ctx, GPUBPE_EINVAL, "sequence too long for eval_pairs");
+    h_result[0] = ~0ull;
+    if (n < 2) return GPUBPE_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device));
+    int rc;
+    if ((rc = ensure(ctx, ctx->mt_counts, 3 * 8, false))) return rc;
+    unsigned long long *d_res = static_cast<unsigned long long *>(ctx->mt_counts.p);
+    CK(launch_eval_pairs(ctx->T, d_tokens, n, d_res, s));
+    CK(cudaMemcpyAsync(h_result, d_res, 3 * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return GPUBPE_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_compact(const uint32_t *d_tokens, uint64_t n,
+                                                                      uint64_t best_pos, uint32_t new_token,
+                                                                      uint32_t *d_out, int method, void *stream) {
+    if (n < 2 || best_pos >= n - 1 || !d_tokens || !d_out || (method != 0 && method != 1)) return GPUBPE_EINVAL;
+    return launch_compact(d_tokens, n, best_pos, new_token, d_out, method, static_cast<cudaStream_t>(stream)) ==
+                   cudaSuccess
+               ? GPUBPE_OK
+               : GPUBPE_ECUDA;
+}
+
+extern "C" __attribute__((visibility("default"))) int gpubpe_lookup_keys(gpubpe_ctx *ctx, const uint64_t *d_keys,
+                                                                          uint64_t m, uint8_t *d_hit, uint64_t *d_vals,
+                                                                          void *stream) {
+    if (!ctx || (m && (!d_keys || !d_hit || !d_vals))) return GPUBPE_EINVAL;
+    if (ctx->T.ext_id) return fail(ctx, GPUBPE_EINVAL, "lookup_keys needs ids < 2^24");
+    CK(cudaSetDevice(ctx->device));
+    CK(launch_lookup_keys(ctx->T, reinterpret_cast<const unsigned long long *>(d_keys), m, d_hit,
+                          reinterpret_cast<unsigned long long *>(d_vals), static_cast<cudaStream_t>(stream)));
     return GPUBPE_OK;
 }
 

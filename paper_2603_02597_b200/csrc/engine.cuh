@@ -187,13 +187,31 @@ struct WarpGroup {
     }
 };
 
+// Token-level extras (tokens.cu only; EXT = false compiles them out):
+//   trace  nullable; merge k of the run (in pass order, by position inside a
+//          pass) stores (pass << 34) | (at the sequence start << 33) | (its right
+//          token last << 32) | rank at trace[k] -- the reference's
+//          merge-rank trace (engines.py:270,317-319) is this list in order when
+//          passes merge one pair (strict mode), and sorted by rank otherwise
+//          (a well-formed table merges in non-decreasing rank order);
+//   fault  the reference's inject_compaction_fault (engines.py:252-266,
+//          378-388): the first pass that can be corrupted merges the single
+//          global-min pair ONE SLOT OFF (p+1, else p-1) with p's new token.
+struct EngineExt {
+    unsigned long long *trace;
+    bool fault;
+};
+
 // Runs the engine on M.tok[0..n).  Returns the output length; *out points at
 // the buffer holding the result.  Every thread of the group must call.
-template <class G>
+template <class G, bool EXT = false>
 static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_t n, bool strict, const G &g,
-                                        uint32_t *passes_out, const uint32_t **out) {
+                                        uint32_t *passes_out, const uint32_t **out,
+                                        EngineExt ext = EngineExt{nullptr, false}) {
     const uint32_t nt = g.size(), me = g.rank();
     uint32_t passes = 0;
+    const uint32_t n0 = n;
+    bool fault = EXT && ext.fault;
     for (uint32_t b = 0; b < n; b += nt) {
         uint32_t i = b + me;
         if (i + 1 < n) {
@@ -220,7 +238,12 @@ static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_
         const uint32_t rmin = (uint32_t)(kmin >> 32);
         const uint32_t pmin = (uint32_t)kmin;
         // 2. selection
-        if (strict) {
+        bool corrupt = false;
+        if (EXT && fault) {  // uniform across the group
+            corrupt = pmin + 1 < n - 1 || pmin > 0;
+            fault = !corrupt;
+        }
+        if (strict || corrupt) {
             for (uint32_t b = 0; b < n; b += nt) {
                 uint32_t i = b + me;
                 if (i < n) M.sel[i] = (i == pmin);
@@ -243,6 +266,15 @@ static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_
             }
         }
         g.sync();
+        if (EXT && corrupt) {
+            if (me == 0) {
+                const uint32_t q = pmin + 1 < n - 1 ? pmin + 1 : pmin - 1;
+                M.sel[pmin] = 0;
+                M.sel[q] = 1;
+                M.pr[q] = make_uint2(rmin, M.pr[pmin].y);
+            }
+            g.sync();
+        }
         // 3. apply + compact
         uint32_t carry = 0;
         for (uint32_t b = 0; b < n; b += nt) {
@@ -254,6 +286,11 @@ static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_
             if (keep) {
                 bool sj = M.sel[j];
                 uint2 pj = (j + 1 < n) ? M.pr[j] : make_uint2(GPUBPE_INF, 0);
+                // merges before j in this pass = tokens removed before j = j - pos
+                if (EXT && sj && ext.trace)
+                    ext.trace[(n0 - n) + (j - pos)] = ((unsigned long long)passes << 34) |
+                                                      ((unsigned long long)(j == 0) << 33) |
+                                                      ((unsigned long long)(j + 2 == n) << 32) | pj.x;
                 uint32_t t = sj ? pj.y : M.tok[j];
                 M.tok2[pos] = t;
                 uint32_t jn = sj ? j + 2 : j + 1;

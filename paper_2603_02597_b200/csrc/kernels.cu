@@ -38,6 +38,7 @@ struct CtaSmem {
     uint32_t base[256];
     EngineShared es;
     unsigned long long bcast[4];
+    unsigned long long seen[2];     // ndef[] by parity as of this CTA's last read (thread 0)
     unsigned long long red[NW][4];  // per-warp partial sums (no 64-bit shared atomics: CAS loops)
     PassCounters pc;
     unsigned long long tb[UNIT_MAX];  // phase B: tile output offsets inside the unit
@@ -442,6 +443,7 @@ __device__ __noinline__ void encode_tile(const EncodeParams &P, CtaSmem &C, Warp
         ++c_seg;
         if (e < 0) {  // longer than SHORT_MAX: deferred to the CTA engine
             const unsigned long long r = atomicAdd(&P.st->bar, 1ull << 32) >> 32;
+            atomicAdd(&P.st->ndef[slot >= P.round_tiles], 1ull);
             if (r < P.rec_cap) P.recs[r].start = (unsigned long long)(a + p);
             S.sid[SI(p)] = 0xFF000000u;
             S.sid[SI(p + 1)] = (uint32_t)r;
@@ -1168,6 +1170,7 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
     for (int k = tid; k < 2048; k += NT) C.jb[k] = __ldg(&P.T.jbits[k]);
     for (int k = tid; k < 256; k += NT) C.base[k] = __ldg(&P.T.base[k]);
     if (tid < (int)(sizeof(PassCounters) / 8)) (&C.pc.n_segments)[tid] = 0;
+    if (tid < 2) C.seen[tid] = 0;
     __syncthreads();
     if (P.dbg && tid == 0) P.dbg[4 * blockIdx.x] = gtimer();
     WarpSmem &S = C.w[wid];
@@ -1210,8 +1213,20 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
         if (P.dbg && tid == 0 && r == 0) P.dbg[4 * blockIdx.x + 1] = gtimer();
         grid_sync(st, ++nbar, &C.bcast[3]);
         if (P.dbg && tid == 0 && r == 0) P.dbg[4 * blockIdx.x + 2] = gtimer();
-        // ---- rare: deferred segments recorded in this round (count read with the barrier)
-        const unsigned long long D = C.bcast[3];
+        // ---- rare: deferred segments recorded in this round (count read with the barrier).
+        //      When another round follows, a CTA that already left this barrier may append
+        //      next-round records before a slower CTA polls, so the total comes from the
+        //      per-parity counters instead (this round's parity is stable until the next
+        //      barrier; the other one was read last round): every CTA sees the same D.
+        unsigned long long D = C.bcast[3];
+        if (!kOneEach && t1 < P.n_tiles) {  // (kOneEach: one round only)
+            if (tid == 0) {
+                C.seen[par] = ld_relaxed(&st->ndef[par]);
+                C.bcast[3] = C.seen[0] + C.seen[1];
+            }
+            __syncthreads();
+            D = C.bcast[3];
+        }
         if (D > d_done) {
             if (D > P.rec_cap) {
                 if (blockIdx.x == 0 && tid == 0) atomicExch(&st->overflow, 1ull);

@@ -74,13 +74,14 @@ struct EncodeState {
     unsigned long long bar;          // low 32 bits: grid barrier arrivals; high 32 bits: deferred
                                      // segments recorded (read with the barrier, no extra round trip)
     unsigned long long pad1[15];
-    unsigned long long n_def_unused; // (layout)
+    unsigned long long ndef[2];      // deferred segments recorded, by round parity (multi-round
+                                     // calls: a round's count independent of the next round's)
     unsigned long long rec_ctr;      // deferred records taken by warps (medium pass)
     unsigned long long rec_ctr2;     // deferred records scanned by CTAs (giant pass)
     unsigned long long arena_used;   // u32 words requested from the arena
     unsigned long long overflow;     // arena or record list overflowed: host re-runs
     unsigned long long n_ids;
-    unsigned long long pad2[3];
+    unsigned long long pad2[2];
     PassCounters c;
 };
 

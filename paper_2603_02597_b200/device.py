@@ -165,7 +165,7 @@ class DeviceEncoder:
             _native.check(rc, None, f"gpubpe_ctx_create: {msg}")
         self._h = h
         self._lib = lib
-        self._lock = threading.Lock()
+        self._lock = threading.RLock()  # decode_host -> decode_into re-enters
         self._pinned: dict[str, torch.Tensor] = {}
 
     def close(self) -> None:
@@ -217,15 +217,23 @@ class DeviceEncoder:
     def decode_into(self, ids: "torch.Tensor", id_offs, out: "torch.Tensor", out_offs, stream=None) -> int:
         """Device CSR of ids -> device CSR of bytes; returns the bytes written.
         id_offs/out_offs: int64 [n_seqs+1] tensors, or None for one sequence.
-        Raises UnknownTokenId, or ValueError when `out` is too small."""
+        Raises UnknownTokenId, or ValueError when `out` is too small or a
+        tensor has the wrong dtype / layout / device (ids int32 or uint32,
+        out uint8, offsets int64; ids and out 16-byte aligned)."""
         n = ids.numel()
         n_seqs = 0 if id_offs is None else id_offs.numel() - 1
+        checks = [(ids, (torch.int32, torch.uint32)), (out, (torch.uint8,))]
+        if n_seqs:
+            checks += [(id_offs, (torch.int64,)), (out_offs, (torch.int64,))]
+        for t, dts in checks:
+            if t.dtype not in dts or not t.is_cuda or not t.is_contiguous() or t.device.index != self.device:
+                raise ValueError(f"expected contiguous {dts} on cuda:{self.device}, got {t.dtype} {t.device}")
+        if ids.data_ptr() % 16 or out.data_ptr() % 16:
+            raise ValueError("decode_into: ids and out must be 16-byte aligned")
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         nb, bad = ctypes.c_uint64(0), ctypes.c_uint64(0)
-        rc = self._lib.gpubpe_decode(self._h, ids.data_ptr(), n, id_offs.data_ptr() if n_seqs else None,
-                                     n_seqs, out.data_ptr(), out.numel(),
-                                     out_offs.data_ptr() if n_seqs else None, ctypes.byref(nb),
-                                     ctypes.byref(bad), s.cuda_stream)
+        with self._lock:
+            rc = self._decode_call(ids, n, id_offs, n_seqs, out, out_offs, nb, bad, s)
         if rc == _native.EINVAL and bad.value != (1 << 64) - 1:
             raise UnknownTokenId(f"id {int(ids[bad.value].item()) & 0xFFFFFFFF} at index {bad.value} "
                                  "not in vocabulary")
@@ -233,6 +241,12 @@ class DeviceEncoder:
             raise ValueError(f"decode output needs {nb.value} bytes, capacity {out.numel()}")
         _native.check(rc, self._h, "gpubpe_decode")
         return int(nb.value)
+
+    def _decode_call(self, ids, n, id_offs, n_seqs, out, out_offs, nb, bad, s):
+        return self._lib.gpubpe_decode(self._h, ids.data_ptr(), n, id_offs.data_ptr() if n_seqs else None,
+                                     n_seqs, out.data_ptr(), out.numel(),
+                                     out_offs.data_ptr() if n_seqs else None, ctypes.byref(nb),
+                                     ctypes.byref(bad), s.cuda_stream)
 
     def decode_host(self, seqs) -> list[bytes]:
         """list of id sequences -> list of byte strings, decoded on the device."""

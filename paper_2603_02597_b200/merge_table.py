@@ -43,6 +43,7 @@ def unpack_value(value: int) -> tuple[int, int]:
 
 
 def fmix64(x: int) -> int:
+    """murmur3 fmix64 (merge_table.py:49-57), the table's slot hash."""
     x &= U64_MASK
     x = ((x ^ (x >> 33)) * _M1) & U64_MASK
     x = ((x ^ (x >> 33)) * _M2) & U64_MASK
@@ -51,13 +52,28 @@ def fmix64(x: int) -> int:
 
 def fmix64_array(x: np.ndarray) -> np.ndarray:
     x = np.asarray(x, dtype=np.uint64).copy()
-    with np.errstate(over="ignore"):
-        x ^= x >> np.uint64(33)
-        x *= np.uint64(_M1)
-        x ^= x >> np.uint64(33)
-        x *= np.uint64(_M2)
-        x ^= x >> np.uint64(33)
+    _mix64_inplace(x, np.empty_like(x))
     return x
+
+
+def _mix64_inplace(x: np.ndarray, tmp: np.ndarray) -> None:
+    """fmix64 of a uint64 array in place, with caller scratch (merge_table.py:68-77)."""
+    np.right_shift(x, np.uint64(33), out=tmp)
+    np.bitwise_xor(x, tmp, out=x)
+    np.multiply(x, np.uint64(_M1), out=x)
+    np.right_shift(x, np.uint64(33), out=tmp)
+    np.bitwise_xor(x, tmp, out=x)
+    np.multiply(x, np.uint64(_M2), out=x)
+    np.right_shift(x, np.uint64(33), out=tmp)
+    np.bitwise_xor(x, tmp, out=x)
+
+
+# the reference's private names for the same functions (merge_table.py:49-66)
+_mix64 = fmix64
+
+
+def _mix64_np(x: np.ndarray) -> np.ndarray:
+    return fmix64_array(x)
 
 
 @dataclass(frozen=True)
@@ -153,8 +169,29 @@ def parse_merges_device(merges_text, vocab: Vocab, device: int = 0):
     return left, right, np.arange(n, dtype=np.uint32), new
 
 
+class ProbeScratch:
+    """Reusable result buffers for repeated vectorised probes up to a fixed
+    width (merge_table.py:119-137).  lookup_keys_into returns views of
+    `hit` / `vals`; the other fields keep the reference's layout."""
+
+    __slots__ = ("width", "idx", "tmp", "slots", "vals", "hit", "aux", "res")
+
+    def __init__(self, width: int):
+        self.width = width
+        self.idx = np.empty(width, dtype=np.uint64)
+        self.tmp = np.empty(width, dtype=np.uint64)
+        self.slots = np.empty(width, dtype=np.uint64)
+        self.vals = np.empty(width, dtype=np.uint64)
+        self.hit = np.empty(width, dtype=bool)
+        self.aux = np.empty(width, dtype=bool)
+        self.res = np.empty(width, dtype=bool)
+
+
 class PackedPairTable:
-    """Open-addressing pair table with the reference's exact slot layout."""
+    """Open-addressing pair table with the reference's exact slot layout.
+    `lookup` is the scalar host probe (construction / tests); the vectorised
+    probes `lookup_keys_into` / `lookup_pairs` run on the device against the
+    table's device context (engine._table_device, k_lookup_keys)."""
 
     __slots__ = ("keys", "values", "capacity", "count", "_mask")
 
@@ -178,22 +215,30 @@ class PackedPairTable:
                 return None
             i = (i + 1) & self._mask
 
+    def lookup_keys_into(self, probe_keys: np.ndarray, scratch: ProbeScratch):
+        """Probe many packed keys at once (merge_table.py:170-230) on the device.
+        Returns views (hit, values) of width len(probe_keys) into scratch;
+        values are meaningful only where hit is True, and both views are
+        overwritten by the next call.  The empty-slot key is always a miss."""
+        from .engine import _table_device
+
+        m = len(probe_keys)
+        hit = scratch.hit[:m]
+        vals = scratch.vals[:m]
+        if m == 0:
+            return hit, vals
+        h, v = _table_device(self).lookup_keys(probe_keys)
+        hit[:] = h
+        vals[:] = v
+        return hit, vals
+
     def lookup_pairs(self, left: np.ndarray, right: np.ndarray):
-        """Vectorised probe: (found bool[], new_tokens u64[], ranks u64[])."""
-        key = (np.asarray(left, np.uint64) << np.uint64(32)) | np.asarray(right, np.uint64)
-        n = len(key)
-        found = np.zeros(n, dtype=bool)
-        vals = np.zeros(n, dtype=np.uint64)
-        idx = fmix64_array(key) & np.uint64(self._mask)
-        live = np.nonzero(key != np.uint64(EMPTY_KEY))[0]
-        while len(live):
-            slot = self.keys[idx[live]]
-            hit = slot == key[live]
-            found[live[hit]] = True
-            vals[live[hit]] = self.values[idx[live[hit]]]
-            live = live[~hit & (slot != np.uint64(EMPTY_KEY))]
-            idx[live] = (idx[live] + np.uint64(1)) & np.uint64(self._mask)
-        return found, vals >> np.uint64(32), vals & np.uint64(U32_MASK)
+        """Vectorised probe (merge_table.py:232-243), on the device:
+        (found bool[], new_tokens u64[], ranks u64[])."""
+        n = len(left)
+        keys = (np.asarray(left).astype(np.uint64) << np.uint64(32)) | np.asarray(right).astype(np.uint64)
+        hit, vals = self.lookup_keys_into(keys, ProbeScratch(n))
+        return hit, vals >> np.uint64(32), vals & np.uint64(U32_MASK)
 
 
 def build_table(rules) -> PackedPairTable:

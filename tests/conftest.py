@@ -44,3 +44,7 @@ def tokenizer(gpt2_paths):
 @pytest.fixture(scope="session")
 def prose_samples():
     return fixtures.prose_samples()
+
+
+# the vendored reference suite runs in its own pytest process (test_ref_suite.py)
+collect_ignore = ["ref_suite"]

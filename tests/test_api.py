@@ -50,8 +50,8 @@ def test_table_lookups_and_rule_recovery(tokenizer, oracle_tables):
     left, right, rank, new = bpe.rule_arrays(t)
     assert np.array_equal(left, oracle_tables.left) and np.array_equal(right, oracle_tables.right)
     assert np.array_equal(rank, oracle_tables.rank) and np.array_equal(new, oracle_tables.new)
-    found, nw, rk = t.lookup_pairs(left[:1000], right[:1000])
-    assert found.all() and np.array_equal(rk, rank[:1000])
+    hits = [t.lookup(int(a), int(b)) for a, b in zip(left[:1000].tolist(), right[:1000].tolist())]
+    assert [h[1] for h in hits] == rank[:1000].tolist() and [h[0] for h in hits] == new[:1000].tolist()
 
 
 def test_parse_merges_errors():

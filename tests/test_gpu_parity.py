@@ -211,8 +211,8 @@ def test_device_csr_api(tokenizer, prose_samples):
     h = ids.cpu().numpy().view(np.uint32)
     for i in range(10):
         assert np.array_equal(h[oo[i]:oo[i + 1]], gold[i])
-    assert st["passes"] == 0 or True
-    assert st["n_ids"] == len(h)
+    assert st["n_bytes"] == len(data) and st["n_ids"] == len(h)
+    assert st["passes"] == st["n_bytes"] - st["n_ids"] == sum(len(d) for d in prose_samples[:10]) - len(h)
 
 
 def test_device_junction_bits_match_rules_and_split_exactly(tokenizer, oracle, oracle_tables):
@@ -452,16 +452,14 @@ def test_device_junction_build_matches_host_loops(tokenizer, prose_samples):
 
 
 def test_steady_state_needs_no_allocations(tokenizer, prose_samples):
-    """Workspaces are grow-only: repeating a call allocates nothing
-    (PassCounters.buffer_allocations)."""
+    """Workspaces are grow-only: repeating a call allocates nothing on the
+    device (device_stats["allocations"])."""
     docs = prose_samples[:50]
     bpe.tokenize_batch(docs, tokenizer)
     again = bpe.tokenize_batch(docs, tokenizer)
-    assert again.counters.buffer_allocations == 0
     assert again.device_stats["allocations"] == 0
-    bigger = bpe.tokenize_batch(docs * 40, tokenizer)  # may grow the workspace once
-    assert bigger.counters.buffer_allocations >= 0
-    assert bpe.tokenize_batch(docs * 40, tokenizer).counters.buffer_allocations == 0
+    bpe.tokenize_batch(docs * 40, tokenizer)  # may grow the workspace once
+    assert bpe.tokenize_batch(docs * 40, tokenizer).device_stats["allocations"] == 0
 
 
 def test_batch_beyond_4_gib_offsets(tokenizer, oracle):

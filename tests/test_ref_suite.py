@@ -1,0 +1,73 @@
+"""The reference's OWN test suite (lanebpe pkg/tests + pkg/bindings/tests)
+run against this package, as the drop-in proof of the boundary.
+
+tests/ref_suite/sync.py copies the suite from /root/reference (in the build
+container) into tests/ref_suite/_vendor/ (git-ignored test infrastructure;
+it travels to the GPU box with the working tree).  The `lanebpe` and
+`lanebpe_bindings` alias packages in tests/ref_suite/shim/ point the suite's
+imports at this package, so every engine call in it runs on the device.
+
+Every reference test must pass except the documented list below.  The run is
+a separate pytest process; its junit report is parsed here.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+import xml.etree.ElementTree as ET
+from pathlib import Path
+
+import pytest
+
+HERE = Path(__file__).resolve().parent
+SUITE = HERE / "ref_suite"
+VENDOR = SUITE / "_vendor"
+ROOT = HERE.parent
+
+# reference test -> why it cannot pass against this package
+EXPECTED_FAIL = {
+    # the lanebpe CLI (cli.py: tokenize / verify / bench / profile) is out of scope
+    "tests.test_cli": "CLI out of scope (every test drives lanebpe.cli.main)",
+    "tests.test_acceptance::test_report_schema_and_performance": "drives `lanebpe bench` through the CLI",
+    "bindings.tests.test_bindings::test_cli_parity_on_shared_fixture": "runs `python -m lanebpe.cli tokenize`",
+}
+
+
+def _expected(classname: str, name: str) -> bool:
+    return classname in EXPECTED_FAIL or f"{classname}::{name.split('[')[0]}" in EXPECTED_FAIL
+
+
+def run_suite(junit: Path, extra=()) -> dict:
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([str(SUITE / "shim"), str(ROOT), env.get("PYTHONPATH", "")])
+    env["PYTHONDONTWRITEBYTECODE"] = "1"
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-p", "ref_suite_plugin",
+           "--rootdir", str(VENDOR), "-o", "testpaths=", f"--junitxml={junit}",
+           str(VENDOR / "tests"), str(VENDOR / "bindings" / "tests"), *extra]
+    proc = subprocess.run(cmd, cwd=VENDOR, env=env, capture_output=True, text=True, timeout=1500)
+    root = ET.parse(junit).getroot()
+    out = {"passed": [], "failed": [], "skipped": [], "log": proc.stdout[-4000:] + proc.stderr[-2000:]}
+    for case in root.iter("testcase"):
+        key = (case.get("classname", ""), case.get("name", ""))
+        if case.find("failure") is not None or case.find("error") is not None:
+            out["failed"].append(key)
+        elif case.find("skipped") is not None:
+            out["skipped"].append(key)
+        else:
+            out["passed"].append(key)
+    return out
+
+
+@pytest.mark.gpu
+def test_reference_suite_passes_against_this_package(tmp_path):
+    if not (VENDOR / "tests" / "conftest.py").exists():
+        pytest.skip("reference suite not vendored (python tests/ref_suite/sync.py in the build container)")
+    res = run_suite(tmp_path / "ref.xml")
+    unexpected = [f"{c}::{n}" for c, n in res["failed"] if not _expected(c, n)]
+    summary = (f"reference suite: {len(res['passed'])} passed, {len(res['failed'])} failed "
+               f"({len(res['failed']) - len(unexpected)} documented), {len(res['skipped'])} skipped")
+    print(summary)
+    assert not unexpected, summary + "\nunexpected failures:\n" + "\n".join(unexpected) + "\n" + res["log"]
+    assert len(res["passed"]) >= 150, summary  # the suite has ~170 tests; most must run and pass

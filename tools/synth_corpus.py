@@ -154,6 +154,49 @@ def workload_doc(name: str) -> tuple[bytes, int]:
     return english_bytes(spec["n_bytes"], spec["seed"]), spec["tokens_whole"]
 
 
+def _corpus_layout(total_bytes: int, seed: int, min_doc: int, max_doc: int, pool_bytes: int):
+    """(pool, sizes, starts, offs) of the corpus: document i is
+    pool[starts[i] : starts[i] + sizes[i]], packed at offs[i]."""
+    rng = np.random.default_rng(seed + 7919)
+    pool = np.frombuffer(english_bytes(min(pool_bytes, max(total_bytes, max_doc) + max_doc), seed),
+                         dtype=np.uint8)
+    # sizes drawn one uniform per document until the total is reached (vectorised:
+    # a generous draw to find the count, then exactly that many from a fresh
+    # generator, so the stream position of the start draws below is unchanged)
+    lo, hi = np.log(min_doc), np.log(max_doc)
+    guess = int(total_bytes / np.exp((lo + hi) / 2) * 1.5) + 64
+    while True:
+        s = np.exp(np.random.default_rng(seed + 7919).uniform(lo, hi, size=guess)).astype(np.int64)
+        c = np.cumsum(s)
+        k = int(np.searchsorted(c, total_bytes, side="left")) + 1  # documents needed
+        if k <= guess or total_bytes <= 0:
+            break
+        guess *= 2
+    if total_bytes <= 0:
+        k = 0
+    rng.uniform(lo, hi, size=k)  # advance past the size draws
+    sizes = s[:k].copy()
+    if k:
+        sizes[-1] = total_bytes - (int(c[k - 2]) if k > 1 else 0)
+    offs = np.zeros(len(sizes) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(sizes)
+    starts = rng.integers(0, len(pool) - max_doc, size=len(sizes))
+    return pool, sizes, starts, offs
+
+
+def _fill(pool, sizes, starts, docs) -> tuple[np.ndarray, np.ndarray]:
+    """Pack the documents `docs` (indices, in order) -> (uint8 data, int64 offsets)."""
+    docs = np.asarray(docs, dtype=np.int64)
+    offs = np.zeros(len(docs) + 1, dtype=np.int64)
+    if len(docs):
+        np.cumsum(sizes[docs], out=offs[1:])
+    data = np.empty(int(offs[-1]), dtype=np.uint8)
+    for k, i in enumerate(docs.tolist()):
+        st = int(starts[i])
+        data[offs[k] : offs[k + 1]] = pool[st : st + int(sizes[i])]
+    return data, offs
+
+
 def corpus_docs(total_bytes: int, seed: int = 0, min_doc: int = 1024, max_doc: int = 65536,
                 pool_bytes: int = 64 << 20) -> tuple[np.ndarray, np.ndarray]:
     """Packed corpus of documents with log-uniform sizes in [min_doc, max_doc].
@@ -161,21 +204,31 @@ def corpus_docs(total_bytes: int, seed: int = 0, min_doc: int = 1024, max_doc: i
     Documents are slices of a pool of generated prose (so 10 GB does not need
     10 GB of generation).  Returns (uint8 data, int64 offsets).
     """
-    rng = np.random.default_rng(seed + 7919)
-    pool = np.frombuffer(english_bytes(min(pool_bytes, max(total_bytes, max_doc) + max_doc), seed),
-                         dtype=np.uint8)
-    sizes = []
-    acc = 0
-    while acc < total_bytes:
-        s = int(np.exp(rng.uniform(np.log(min_doc), np.log(max_doc))))
-        s = min(s, total_bytes - acc)
-        sizes.append(s)
-        acc += s
-    sizes = np.array(sizes, dtype=np.int64)
-    offs = np.zeros(len(sizes) + 1, dtype=np.int64)
-    offs[1:] = np.cumsum(sizes)
-    starts = rng.integers(0, len(pool) - max_doc, size=len(sizes))
-    data = np.empty(int(offs[-1]), dtype=np.uint8)
-    for i, (s, st) in enumerate(zip(sizes, starts)):
-        data[offs[i] : offs[i + 1]] = pool[st : st + s]
-    return data, offs
+    pool, sizes, starts, offs = _corpus_layout(total_bytes, seed, min_doc, max_doc, pool_bytes)
+    return _fill(pool, sizes, starts, np.arange(len(sizes)))
+
+
+def corpus_layout_offsets(total_bytes: int, seed: int = 0, min_doc: int = 1024, max_doc: int = 65536,
+                          pool_bytes: int = 64 << 20) -> np.ndarray:
+    """The corpus's document offsets only (no data)."""
+    return _corpus_layout(total_bytes, seed, min_doc, max_doc, pool_bytes)[3]
+
+
+def corpus_range(total_bytes: int, d0: int, d1: int, seed: int = 0, min_doc: int = 1024,
+                 max_doc: int = 65536, pool_bytes: int = 64 << 20) -> tuple[np.ndarray, np.ndarray]:
+    """Documents [d0, d1) of corpus_docs(total_bytes, seed) -- one rank's shard,
+    generated without the rest of the corpus.  Returns (data, offsets from 0)."""
+    pool, sizes, starts, _ = _corpus_layout(total_bytes, seed, min_doc, max_doc, pool_bytes)
+    return _fill(pool, sizes, starts, np.arange(d0, d1))
+
+
+def corpus_sample(total_bytes: int, frac: float, sample_seed: int, seed: int = 0, min_doc: int = 1024,
+                  max_doc: int = 65536, pool_bytes: int = 64 << 20):
+    """A seeded sample of about `frac` of the corpus's documents:
+    (document indices, data, offsets) -- the documents are byte-identical to
+    those of corpus_docs(total_bytes, seed)."""
+    pool, sizes, starts, _ = _corpus_layout(total_bytes, seed, min_doc, max_doc, pool_bytes)
+    rng = np.random.default_rng(sample_seed)
+    pick = np.flatnonzero(rng.random(len(sizes)) < frac)
+    data, offs = _fill(pool, sizes, starts, pick)
+    return pick, data, offs
