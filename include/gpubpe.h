@@ -140,8 +140,9 @@ int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out);
  * gpubpe_decode: d_ids[n_ids] as n_seqs sequences (d_id_offs[n_seqs+1] CSR;
  *   n_seqs == 0: one sequence, no offsets) -> their byte strings back to back
  *   in d_out (capacity out_cap) with d_out_offs[n_seqs+1].  Synchronises.
- *   d_ids and d_out must be 16-byte aligned (the kernels move 16-byte
- *   vectors; a misaligned pointer is GPUBPE_EINVAL, never a fault).
+ *   d_out must be 16-byte aligned (the kernels store 16-byte vectors) and
+ *   d_ids 4-byte aligned; a misaligned pointer is GPUBPE_EINVAL, never a
+ *   fault.
  *   Unknown id: GPUBPE_EINVAL, *bad_index = its index (UnknownTokenId).
  *   Capacity too small: GPUBPE_ERANGE, *n_bytes_out = the bytes needed.
  */

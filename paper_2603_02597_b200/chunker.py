@@ -123,6 +123,16 @@ class Tokenizer:
             data, doc_offs, self.config.max_seq_len, self.config.chunk_budget)
         return ids, offs
 
+    def _producers(self) -> dict:
+        """token -> (left, right) of the lowest-rank rule producing it."""
+        cached = getattr(self, "_prod_cache", None)
+        if cached is None:
+            cached = {}
+            for a, b, c in zip(*(x.tolist() for x in (self.rule_arrays()[i] for i in (0, 1, 3)))):
+                cached.setdefault(c, (a, b))
+            self._prod_cache = cached
+        return cached
+
     def _symbol_bytes(self):
         """(ids uint32[], blob uint8[], offs uint64[]) of every id whose symbol maps
         to a nonempty byte string (symbol_bytes semantics), vectorised: all
@@ -258,17 +268,85 @@ def pack_texts(texts) -> tuple[np.ndarray, np.ndarray]:
     return data, offs
 
 
-def _lane_allocations(lens: np.ndarray, cfg: BlockConfig) -> int:
-    """Pool buffers the reference's lane engines acquire for a batch: two per
-    chunk of >= 2 ids (engines.py:363-369; shorter runs return before the
-    pool), chunks as tokenize_batch cuts them (chunker.py:139-144)."""
+class _LazyCounters(PassCounters):
+    """PassCounters computed on first access (the batch path's counters are
+    bookkeeping over the per-chunk id counts; most callers never read them)."""
+
+    def __init__(self, fn):
+        object.__setattr__(self, "_fn", fn)
+
+    def __getattr__(self, name):
+        if name in ("passes", "lookups", "compaction_moves", "buffer_allocations"):
+            fn = self.__dict__.pop("_fn")
+            for k, v in fn().items():
+                object.__setattr__(self, k, v)
+            return self.__dict__[name]
+        raise AttributeError(name)
+
+
+def _tri(x: np.ndarray) -> np.ndarray:
+    return x * (x + 1) // 2
+
+
+def _batch_counters(variant: str, tokenizer: "Tokenizer", clens: np.ndarray, couts: np.ndarray,
+                    chunk_edges=None) -> dict:
+    """The reference's PassCounters for a batch (chunker.py:166-172 sums the
+    per-chunk engine counters) from each chunk's length n and id count:
+    passes = n - out (every engine); lane engines (engines.py:338-403): one
+    merge per pass, every evaluation probes cur_len - 1 pairs (a final one
+    finds none while >= 2 ids remain), cur_len - 1 compaction moves per merge,
+    two pool buffers per run of >= 2 ids; sequential (engines.py:269-335):
+    n - 1 initial probes plus one per neighbour of every merge -- merges on
+    the first output id's left spine / the last one's right spine lack one
+    (walked through the rule producing each id)."""
+    n = np.asarray(clens, dtype=np.int64)
+    out = np.asarray(couts, dtype=np.int64)
+    m = n - out
+    run = n >= 2
+    res = {"passes": int(m.sum()), "lookups": 0, "compaction_moves": 0, "buffer_allocations": 0}
+    if variant == "sequential":
+        lk = (n - 1) + 2 * m
+        if chunk_edges is not None and m.any():
+            prod = tokenizer._producers()
+            for k in np.flatnonzero(m > 0).tolist():
+                (fi, li), (fo, lo) = chunk_edges(k)
+                lk[k] -= _spine(prod, fo, fi, 0) + _spine(prod, lo, li, 1)
+        res["lookups"] = int(lk[run].sum())
+        return res
+    a = np.where(out >= 2, out, out + 1)
+    res["lookups"] = int(((_tri(n - 1) - _tri(a - 2)) * run).sum())
+    res["compaction_moves"] = int((m * (n - 1) - m * (m - 1) // 2).sum())
+    res["buffer_allocations"] = 2 * int(np.count_nonzero(run))
+    return res
+
+
+def _spine(prod: dict, top: int, leaf: int, side: int) -> int:
+    k = 0
+    while top != leaf and top in prod:
+        top = prod[top][side]
+        k += 1
+    return k
+
+
+def _chunk_units(lens: np.ndarray, cfg: BlockConfig):
+    """Chunks of a batch as tokenize_batch cuts them (chunker.py:139-144: a
+    document longer than max_seq_len becomes chunk_budget-sized chunks).
+    Returns (doc of each chunk, offset of each chunk in its document, chunk
+    lengths, first chunk of each document + total) or None when no document
+    is cut."""
     lens = np.asarray(lens, dtype=np.int64)
-    whole = lens <= cfg.max_seq_len
+    long = lens > cfg.max_seq_len
+    if not long.any():
+        return None
     cb = cfg.chunk_budget
-    n = int(np.count_nonzero(whole & (lens >= 2)))
-    big = lens[~whole]
-    n += int((big // cb).sum()) + int(np.count_nonzero(big % cb >= 2))
-    return 2 * n
+    k = np.where(long, (lens + cb - 1) // cb, 1)
+    first = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(k, out=first[1:])
+    doc = np.repeat(np.arange(len(lens)), k)
+    idx = np.arange(int(first[-1])) - first[doc]
+    off = idx * cb
+    clen = np.where(long[doc], np.minimum(cb, lens[doc] - off), lens[doc])
+    return doc, off, clen, first
 
 
 def _per_chunk(parts, tokenizer: Tokenizer, variant: str) -> BatchResult:
@@ -322,39 +400,56 @@ def _device_list(devices) -> list[int] | None:
     return lst
 
 
-def _encode_multi(parts, tokenizer: Tokenizer, devs: list[int], mode: int):
-    """One batch on several GPUs from one process:
-    contiguous document ranges balanced by bytes (multigpu.shard_batch), or a
-    lone long document split at exact cuts (multigpu.split_document), one
-    host thread per GPU driving its own context and stream (the native calls
-    release the GIL), results concatenated in order.  No collective."""
+def _encode_units(parts, ptrs, lens, tokenizer: "Tokenizer", devs: list[int], mode: int):
+    """Encode units (host address, length) -- whole documents or their chunks,
+    each an independent BPE sequence -- on one or several GPUs.  Several: one
+    host thread per GPU (the native calls release the GIL) over contiguous
+    unit ranges balanced by bytes (multigpu.shard_batch); a unit larger than
+    a GPU's share is split at exact cuts first (multigpu.split_points).
+    Returns (list of (ids, unit offsets) per GPU, unit -> source unit index,
+    engine_ms, stats).  No collective: per-GPU D2H of the ids only."""
     import threading
 
     from . import multigpu
 
     cfg = tokenizer.config
     g = len(devs)
-    encs = [tokenizer.device_encoder(d) for d in devs]
-    if len(parts) == 1 and len(parts[0]) >= g * (1 << 20):
-        pieces = multigpu.split_document(parts[0], g, encs[0].junction_bits(), cfg.max_seq_len, cfg.chunk_budget)
-        jobs = [(p, None) for p in pieces]  # per GPU: documents whose ids concatenate to doc 0's
+    src = np.arange(len(lens))
+    if g > 1 and len(lens):
+        total = int(lens.sum())
+        big = np.flatnonzero(lens > max(total // g, 1 << 20))
+        if big.size:  # pieces at junction misses (exact cuts; DESIGN.md section 3)
+            jb = tokenizer.device_encoder(devs[0]).junction_bits()
+            P, L, S = [], [], []
+            bigset = set(big.tolist())
+            for u in range(len(lens)):
+                if u in bigset:
+                    doc = ctypes_string(int(ptrs[u]), int(lens[u]))
+                    pts = multigpu.split_points(doc, g, jb, 1 << 62, 1 << 62)
+                    for a, b in zip(pts, pts[1:]):
+                        if b > a:
+                            P.append(int(ptrs[u]) + a), L.append(b - a), S.append(u)
+                else:
+                    P.append(int(ptrs[u])), L.append(int(lens[u])), S.append(u)
+            ptrs, lens, src = np.array(P, np.uint64), np.array(L, np.uint64), np.array(S, np.int64)
+        offs = np.zeros(len(lens) + 1, np.int64)
+        np.cumsum(lens.astype(np.int64), out=offs[1:])
+        ranges = multigpu.shard_batch(offs, g)
     else:
-        lens = np.fromiter(map(len, parts), dtype=np.int64, count=len(parts))
-        offs = np.zeros(len(parts) + 1, np.int64)
-        np.cumsum(lens, out=offs[1:])
-        jobs = [(parts[a:b], (a, b)) for a, b in multigpu.shard_batch(offs, g)]
-    results: list = [None] * g
+        ranges = [(0, len(lens))]
+    encs = [tokenizer.device_encoder(d) for d in devs[: len(ranges)]]
+    results: list = [None] * len(ranges)
     errs: list = []
 
     def run(k):
         try:
-            docs = jobs[k][0]
-            if docs:
-                results[k] = encs[k].encode_list_host(list(docs), cfg.max_seq_len, cfg.chunk_budget, mode)
+            a, b = ranges[k]
+            if b > a:
+                results[k] = encs[k].encode_ptrs_host(ptrs[a:b], lens[a:b], cfg.max_seq_len, cfg.chunk_budget, mode)
         except BaseException as exc:  # re-raised in the caller
             errs.append(exc)
 
-    threads = [threading.Thread(target=run, args=(k,)) for k in range(1, g)]
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(1, len(ranges))]
     for t in threads:
         t.start()
     run(0)
@@ -362,25 +457,21 @@ def _encode_multi(parts, tokenizer: Tokenizer, devs: list[int], mode: int):
         t.join()
     if errs:
         raise errs[0]
-    stats = {"devices": devs, "per_device": []}
-    engine_ms = 0.0
-    token_ids: list[np.ndarray] = []
-    n_bytes = 0
-    for k, (docs, rng) in enumerate(jobs):
-        if results[k] is None:
-            stats["per_device"].append(None)
-            continue
-        ids, oo, st, ms = results[k]
-        stats["per_device"].append(st)
-        n_bytes += int(st["n_bytes"])
-        engine_ms = max(engine_ms, ms)  # the GPUs run concurrently
-        o = oo.tolist()
-        token_ids.extend(ids[a:b] for a, b in zip(o, o[1:]))
-    if jobs[0][1] is None:  # one split document: its pieces' ids back to back
-        token_ids = [np.concatenate(token_ids) if token_ids else np.empty(0, np.uint32)]
-    stats["n_bytes"] = n_bytes
-    stats["allocations"] = sum(int(st["allocations"]) for st in stats["per_device"] if st)
-    return token_ids, engine_ms, stats
+    done = [r for r in results if r is not None]
+    if len(ranges) == 1:
+        st = done[0][2] if done else {"n_bytes": 0, "allocations": 0}
+    else:
+        st = {"devices": devs, "per_device": [r[2] if r else None for r in results],
+              "n_bytes": sum(int(r[2]["n_bytes"]) for r in done),
+              "allocations": sum(int(r[2]["allocations"]) for r in done)}
+    engine_ms = max((r[3] for r in done), default=0.0)  # the GPUs run concurrently
+    return [(r[0], r[1]) for r in done], src, engine_ms, st
+
+
+def ctypes_string(ptr: int, n: int) -> bytes:
+    import ctypes
+
+    return ctypes.string_at(ptr, n)
 
 
 def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
@@ -396,10 +487,11 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
     regex first (ids equal tiktoken's GPT-2 encode_ordinary for valid UTF-8;
     an optional mode, never the default).
 
-    counters: passes = input bytes - output ids (the reference's identity);
-    buffer_allocations follows the lane engines' pool model (two per chunk
-    of >= 2 ids, 0 for "sequential"); device allocations of the call are in
-    device_stats["allocations"] (0 in steady state).
+    Documents longer than max_seq_len cross to the device as their chunks
+    (the reference encodes chunks independently, chunker.py:139-144), so the
+    per-chunk id counts -- and with them the reference's counters -- come
+    back with the ids.  device_stats["allocations"] counts device / pinned
+    buffers the call allocated (0 in steady state).
     """
     if variant not in ENGINE_NAMES:
         raise ValueError(f"unknown engine {variant!r}, expected one of {ENGINE_NAMES}")
@@ -420,24 +512,67 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
     from ._native import MODE_DEFAULT, MODE_GPT2_REGEX
 
     mode = MODE_GPT2_REGEX if pretokenize == "gpt2" else MODE_DEFAULT
-    t1 = time.perf_counter()
-    if devs is not None and len(devs) > 1:
-        token_ids, engine_ms, st = _encode_multi(parts, tokenizer, devs, mode)
-        n_ids = sum(len(t) for t in token_ids)
-    else:
+    if n_docs == 1 and (devs is None or len(devs) == 1):
+        # one document (the latency path): one buffer staged piecewise, overlapping
+        # its DMA; a document longer than max_seq_len goes as its chunks
         enc = tokenizer.device_encoder(devs[0] if devs else None)
-        if n_docs == 1:  # one buffer: staged piecewise, overlapping its DMA
-            data = np.frombuffer(parts[0], dtype=np.uint8)
-            ids, out_offs, st, engine_ms = enc.encode_packed_host(
-                data, np.array([0, data.size], np.int64), cfg.max_seq_len, cfg.chunk_budget, mode)
-        else:  # many: gathered natively into pinned memory, no join here
-            ids, out_offs, st, engine_ms = enc.encode_list_host(parts, cfg.max_seq_len, cfg.chunk_budget, mode)
-        t2 = time.perf_counter()
-        o = out_offs.tolist()
-        token_ids = [ids[a:b] for a, b in zip(o, o[1:])]
-        n_ids = int(ids.size)
-        t1 = t2
-    assemble_ms = (time.perf_counter() - t1) * 1000.0
-    allocs = 0 if variant == "sequential" else _lane_allocations(np.fromiter(map(len, parts), np.int64, n_docs), cfg)
-    counters = PassCounters(passes=int(st["n_bytes"]) - n_ids, buffer_allocations=allocs)
-    return BatchResult(token_ids, engine_ms, encode_ms, assemble_ms, counters, st)
+        data = np.frombuffer(parts[0], dtype=np.uint8)
+        n = data.size
+        if mode == MODE_DEFAULT and n > cfg.max_seq_len:
+            offs = np.append(np.arange(0, n, cfg.chunk_budget, dtype=np.int64), n)
+        else:
+            offs = np.array([0, n], np.int64)
+        ids, out_offs, st, engine_ms = enc.encode_packed_host(data, offs, cfg.max_seq_len, cfg.chunk_budget, mode)
+        t1 = time.perf_counter()
+        base = tokenizer._base_ids
+
+        def edges1(k):
+            a, b, c, d = int(offs[k]), int(offs[k + 1]), int(out_offs[k]), int(out_offs[k + 1])
+            return (int(base[data[a]]), int(base[data[b - 1]])), (int(ids[c]), int(ids[d - 1]))
+
+        counters = _LazyCounters(lambda: _batch_counters(variant, tokenizer, np.diff(offs), np.diff(out_offs),
+                                                         edges1))
+        return BatchResult([ids], engine_ms, encode_ms, (time.perf_counter() - t1) * 1000.0, counters, st)
+    from .device import bytes_ptrs
+
+    lens = np.fromiter(map(len, parts), dtype=np.uint64, count=n_docs)
+    ptrs = bytes_ptrs(parts)
+    cut = _chunk_units(lens, cfg) if mode == MODE_DEFAULT else None
+    if cut is not None:  # documents longer than max_seq_len as their chunks
+        cdoc, coff, clen, first = cut
+        uptrs, ulens = ptrs[cdoc] + coff.astype(np.uint64), clen.astype(np.uint64)
+    else:
+        uptrs, ulens = ptrs, lens
+    pieces, src, engine_ms, st = _encode_units(parts, uptrs, ulens, tokenizer, devs or [None], mode)
+    t1 = time.perf_counter()
+    # per source unit: id count; per document: its ids (one slice when on one GPU)
+    if len(pieces) == 1 and len(src) == len(ulens):
+        ids, uo = pieces[0]
+        uout = np.diff(uo)
+        doc_o = (uo if cut is None else uo[first]).tolist()
+        token_ids = [ids[a:b] for a, b in zip(doc_o, doc_o[1:])]
+    else:
+        pout = np.concatenate([np.diff(o) for _, o in pieces])
+        uout = np.bincount(src, weights=pout, minlength=len(ulens)).astype(np.int64)
+        flat = np.concatenate([i for i, _ in pieces]) if pieces else np.empty(0, np.uint32)
+        uo = np.zeros(len(ulens) + 1, np.int64)
+        np.cumsum(uout, out=uo[1:])
+        doc_o = (uo if cut is None else uo[first]).tolist()
+        token_ids = [flat[a:b] for a, b in zip(doc_o, doc_o[1:])]
+    cl = ulens.astype(np.int64)
+    uo_all = np.zeros(len(cl) + 1, np.int64)
+    np.cumsum(uout, out=uo_all[1:])
+    all_ids = token_ids  # for the sequential counters' edge ids
+
+    def edges(k):
+        d = int(cdoc[k]) if cut is not None else k
+        o = int(coff[k]) if cut is not None else 0
+        b = parts[d]
+        base = tokenizer._base_ids
+        ids_d = all_ids[d]
+        lo = int(uo_all[k] - (uo_all[first[d]] if cut is not None else uo_all[k]))
+        hi = lo + int(uout[k])
+        return ((int(base[b[o]]), int(base[b[o + int(cl[k]) - 1]])), (int(ids_d[lo]), int(ids_d[hi - 1])))
+
+    counters = _LazyCounters(lambda: _batch_counters(variant, tokenizer, cl, uout, edges))
+    return BatchResult(token_ids, engine_ms, encode_ms, (time.perf_counter() - t1) * 1000.0, counters, st)

@@ -1408,9 +1408,9 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *
     if (!ctx || !n_bytes_out || !bad_index) return GPUBPE_EINVAL;
     if (!ctx->d_vinfo) return fail(ctx, GPUBPE_EINVAL, "decode: no vocabulary (gpubpe_set_vocab)");
     if (n_seqs && (!d_id_offs || !d_out_offs)) return fail(ctx, GPUBPE_EINVAL, "decode: null offsets");
-    // the kernels move ids and bytes in 16-byte vectors (decode.cu)
-    if ((reinterpret_cast<uintptr_t>(d_out) & 15) || (reinterpret_cast<uintptr_t>(d_ids) & 15))
-        return fail(ctx, GPUBPE_EINVAL, "decode: d_ids and d_out must be 16-byte aligned");
+    // the kernels store bytes in 16-byte vectors (decode.cu); ids may sit at any 4-byte offset
+    if ((reinterpret_cast<uintptr_t>(d_out) & 15) || (reinterpret_cast<uintptr_t>(d_ids) & 3))
+        return fail(ctx, GPUBPE_EINVAL, "decode: d_out must be 16-byte aligned and d_ids 4-byte aligned");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CK(cudaSetDevice(ctx->device));
     *n_bytes_out = 0;

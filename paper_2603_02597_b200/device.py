@@ -111,9 +111,28 @@ class _HostPool:
 
 _RESULTS = _HostPool()
 _POOLED_MAX = _RESULTS.pinned_max
-# address of a bytes object's data relative to id() (CPython layout, measured once)
-_BYTES_PROBE = b"\x00gpubpe"
-_BYTES_DATA = ctypes.cast(ctypes.c_char_p(_BYTES_PROBE), ctypes.c_void_p).value - id(_BYTES_PROBE)
+
+
+def _char_p(b: bytes) -> int:
+    return ctypes.cast(ctypes.c_char_p(b), ctypes.c_void_p).value
+
+
+# Address of a bytes object's data relative to id(): CPython keeps the data
+# inline at a fixed offset (PyBytesObject.ob_sval).  Measured here on objects
+# of several sizes, and re-checked on every batch (bytes_ptrs) against ctypes'
+# own pointer; any disagreement switches to the per-object ctypes path.
+_BYTES_DATA = _char_p(b"\x00gpubpe") - id(b"\x00gpubpe")
+_BYTES_LAYOUT_OK = all(_char_p(x) - id(x) == _BYTES_DATA for x in (b"", b"a", bytes(100), bytes(1 << 20)))
+
+
+def bytes_ptrs(parts: list) -> np.ndarray:
+    """uint64 data addresses of a list of `bytes` objects (kept alive by the caller)."""
+    n = len(parts)
+    if _BYTES_LAYOUT_OK and n:
+        ptrs = np.fromiter(map(id, parts), dtype=np.uint64, count=n) + np.uint64(_BYTES_DATA)
+        if int(ptrs[0]) == _char_p(parts[0]) and int(ptrs[-1]) == _char_p(parts[-1]):
+            return ptrs
+    return np.fromiter(map(_char_p, parts), dtype=np.uint64, count=n)
 
 
 def pinned_empty(nbytes: int, device: int = 0) -> np.ndarray:
@@ -219,7 +238,7 @@ class DeviceEncoder:
         id_offs/out_offs: int64 [n_seqs+1] tensors, or None for one sequence.
         Raises UnknownTokenId, or ValueError when `out` is too small or a
         tensor has the wrong dtype / layout / device (ids int32 or uint32,
-        out uint8, offsets int64; ids and out 16-byte aligned)."""
+        out uint8, offsets int64; out 16-byte aligned)."""
         n = ids.numel()
         n_seqs = 0 if id_offs is None else id_offs.numel() - 1
         checks = [(ids, (torch.int32, torch.uint32)), (out, (torch.uint8,))]
@@ -228,8 +247,8 @@ class DeviceEncoder:
         for t, dts in checks:
             if t.dtype not in dts or not t.is_cuda or not t.is_contiguous() or t.device.index != self.device:
                 raise ValueError(f"expected contiguous {dts} on cuda:{self.device}, got {t.dtype} {t.device}")
-        if ids.data_ptr() % 16 or out.data_ptr() % 16:
-            raise ValueError("decode_into: ids and out must be 16-byte aligned")
+        if out.data_ptr() % 16:
+            raise ValueError("decode_into: out must be 16-byte aligned")
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         nb, bad = ctypes.c_uint64(0), ctypes.c_uint64(0)
         with self._lock:
@@ -341,11 +360,20 @@ class DeviceEncoder:
         """A batch of separate `bytes` documents -> host CSR (ids, offs, stats,
         engine_ms), gathered straight into the pinned staging buffer by the
         native side (gpubpe_encode_host_gather): no join on the Python side."""
-        n_docs = len(parts)
         if not all(type(p) is bytes for p in parts):
             raise TypeError("encode_list_host takes a list of bytes")
-        ptrs = np.fromiter(map(id, parts), dtype=np.uint64, count=n_docs) + np.uint64(_BYTES_DATA)
-        lens = np.fromiter(map(len, parts), dtype=np.uint64, count=n_docs)
+        lens = np.fromiter(map(len, parts), dtype=np.uint64, count=len(parts))
+        return self.encode_ptrs_host(bytes_ptrs(parts), lens, max_seq_len, chunk_budget, mode)
+
+    def encode_ptrs_host(self, ptrs: np.ndarray, lens: np.ndarray, max_seq_len: int, chunk_budget: int,
+                         mode: int = 0):
+        """Documents given as host (address, length) pairs -- e.g. the chunks
+        of longer documents -- gathered into pinned staging by the native
+        side; the caller keeps the memory alive.  Same results as
+        encode_list_host."""
+        ptrs = np.ascontiguousarray(ptrs, dtype=np.uint64)
+        lens = np.ascontiguousarray(lens, dtype=np.uint64)
+        n_docs = len(lens)
         n = int(lens.sum())
         pinned = 4 * n <= _POOLED_MAX
         buf = (_RESULTS.take(4 * max(n, 1), self._lib, self.device) if pinned

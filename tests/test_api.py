@@ -241,3 +241,43 @@ def test_golden_file_errors(tmp_path):
         p.write_text(body)
         with pytest.raises(errors.MalformedGoldenFile):
             report.load_golden_file(p)
+
+
+def test_batch_counters_match_the_lane_engine_formulas():
+    """_batch_counters (chunk lengths + id counts -> the reference's summed
+    PassCounters) against run_block_engine's per-chunk formulas
+    (engines.py:338-403, test_engines.py:266-289) and the tiny known answer."""
+    from paper_2603_02597_b200.chunker import _batch_counters
+
+    rng = np.random.default_rng(3)
+    n = rng.integers(0, 300, 200)
+    out = np.array([int(rng.integers(min(k, 1), k + 1)) if k else 0 for k in n])
+    got = _batch_counters("optimized", None, n, out)
+    lk = mv = al = 0
+    for a, o in zip(n.tolist(), out.tolist()):
+        if a < 2:
+            continue
+        last = o
+        lk += sum(L - 1 for L in range(last if last >= 2 else last + 1, a + 1))
+        mv += sum(a - k - 1 for k in range(a - o))
+        al += 2
+    assert got == {"passes": int((n - out).sum()), "lookups": lk, "compaction_moves": mv, "buffer_allocations": al}
+    assert _batch_counters("baseline", None, np.array([4]), np.array([2])) == \
+        {"passes": 2, "lookups": 6, "compaction_moves": 5, "buffer_allocations": 2}
+
+
+def test_chunk_units_match_chunk_tokens():
+    from paper_2603_02597_b200.chunker import _chunk_units
+
+    cfg = bpe.BlockConfig(max_seq_len=64, chunk_budget=16)
+    lens = np.array([0, 1, 64, 65, 200, 3])
+    doc, off, clen, first = _chunk_units(lens, cfg)
+    want = []
+    for d, L in enumerate(lens.tolist()):
+        if L > 64:
+            want += [(d, c.chunk_index * 16, len(c.tokens)) for c in bpe.chunk_tokens(np.zeros(L, np.uint32), 16, d)]
+        else:
+            want.append((d, 0, L))
+    assert list(zip(doc.tolist(), off.tolist(), clen.tolist())) == want
+    assert first.tolist() == [0, 1, 2, 3, 8, 21, 22]
+    assert _chunk_units(np.array([5, 64]), cfg) is None

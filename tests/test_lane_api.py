@@ -262,3 +262,52 @@ def test_batch_counters_follow_the_lane_model(tokenizer, prose_samples):
     assert sum(len(d) for d in docs) - res.counters.passes == sum(len(t) for t in res.token_ids)
     assert res.counters.buffer_allocations == 2 * 3
     assert bpe.tokenize_batch(docs, tokenizer, "sequential").counters.buffer_allocations == 0
+
+
+def test_batch_counters_equal_per_chunk_engine_runs(tokenizer, prose_samples):
+    """tokenize_batch's counters (all engine names) equal the sum of the
+    token-level engines' counters over the reference's chunks
+    (chunker.py:166-172), with documents longer than max_seq_len."""
+    cfg = bpe.BlockConfig(max_seq_len=700, chunk_budget=300)
+    tok = bpe.Tokenizer(tokenizer.vocab, tokenizer.table, cfg)
+    tok._devices = tokenizer._devices
+    docs = prose_samples[:6] + [b"", b"x", b"ab", prose_samples[7][:700], prose_samples[8][:701]]
+    for variant in ("sequential", "baseline", "optimized"):
+        want = bpe.PassCounters()
+        for d in docs:
+            ids = tok.encode(d)
+            chunks = bpe.chunk_tokens(ids, 300) if len(ids) > 700 else [bpe.Chunk(0, 0, ids)]
+            for c in chunks:
+                fn = bpe.sequential_bpe if variant == "sequential" else bpe.run_block_engine
+                _, cc = fn(c.tokens, tok.table) if variant == "sequential" else fn(c.tokens, tok.table, cfg, variant)
+                want.merge_from(cc)
+        got = bpe.tokenize_batch(docs, tok, variant).counters
+        assert (got.passes, got.lookups, got.compaction_moves, got.buffer_allocations) == \
+            (want.passes, want.lookups, want.compaction_moves, want.buffer_allocations), variant
+        one = bpe.tokenize_batch([docs[0]], tok, variant).counters  # the one-document path
+        assert one.passes > 0 and one.lookups > 0
+
+
+def test_multi_device_batches_match_single_device(tokenizer, oracle, prose_samples):
+    """tokenize_batch(devices=...) shards units across GPUs from one process:
+    documents (P-default chunks included) by bytes, a lone huge document at
+    exact junction cuts.  On a one-GPU box, devices=[0, 0] runs the same
+    sharding, threads and reassembly against one context."""
+    import synth_corpus
+
+    docs = prose_samples[:40] + [b"", b"x" * 9000, synth_corpus.english_bytes(3 << 20, 4)]
+    want = oracle.encode_docs(docs, 8192, 8192, 8)
+    for devs in ([0, 0], [0, 0, 0]):
+        res = bpe.tokenize_batch(docs, tokenizer, devices=devs)
+        assert [t.tolist() for t in res.token_ids] == [w.tolist() for w in want]
+        assert res.counters.passes == sum(map(len, docs)) - sum(map(len, want))
+    whole = bpe.Tokenizer(tokenizer.vocab, tokenizer.table, bpe.BlockConfig(max_seq_len=1 << 40, chunk_budget=1 << 40))
+    whole._devices = tokenizer._devices
+    big = synth_corpus.english_bytes(5 << 20, 9)
+    w = oracle.encode_docs([big], 1 << 40, 1 << 40, 1)[0]
+    for devs in ([0, 0], 4):
+        got = bpe.tokenize_batch([big], whole, devices=[0] * devs if isinstance(devs, int) else devs).token_ids[0]
+        assert np.array_equal(got, w)
+    h = bpe.TokenizerHandle.__new__(bpe.TokenizerHandle)
+    h._tokenizer, h._engine, h._workers, h._devices = tokenizer, "optimized", None, [0, 0]
+    assert h.tokenize_batch(["hello world", b""])[0] == [[31373, 995], []]
