@@ -1,11 +1,16 @@
-"""bench.py's reference arm on CPU: the JSON line carries the driver's keys
-(the GPU arm is exercised on the B200 box)."""
+"""bench.py's contract: the reference arm's JSON line on CPU (the driver's
+keys), and on the GPU box `python bench.py --gpus 2` without torchrun --
+it spawns the ranks itself (sharing the one GPU over gloo when the box has
+fewer GPUs than ranks), rank 0 prints one line with n_gpus = 2 and the corpus
+leg sharded across both ranks, with the reference arm's config keys."""
 
 import json
 import os
 import subprocess
 import sys
 from pathlib import Path
+
+import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
 
@@ -37,3 +42,30 @@ def test_reference_arm_other_ranks_exit_quietly():
              {"RANK": "1", "LOCAL_RANK": "1", "WORLD_SIZE": "2"})
     assert r.returncode == 0, r.stderr[-2000:]
     assert not [l for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+def _line(out: str) -> dict:
+    lines = [l for l in out.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out[-3000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+def test_bench_gpus_2_spawns_ranks_and_shards_the_corpus():
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "20", "--warmup", "3",
+           "--corpus-mb", "64", "--cpu-seconds", "1"]
+    proc = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert proc.returncode == 0, proc.stderr[-3000:]
+    line = _line(proc.stdout)
+    assert line["n_gpus"] == 2 and line["steps"] == 20 and line["value"] > 0
+    assert line["e2e"]["value"] > 0 and line["roofline"]["frac"] > 0
+    c = line["corpus"]
+    assert c["n_gpus"] == 2 and c["scaling"] == "strong" and c["config"]["workload"] == "corpus_64m"
+    assert c["e2e"]["value"] > 0 and c["roofline"]["peak"] == 2 * line["roofline"]["peak"]
+    ref = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "2",
+                          "--warmup", "1"], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert ref.returncode == 0, ref.stderr[-3000:]
+    rline = _line(ref.stdout)
+    assert rline["impl"] == "reference" and set(rline["config"]) == set(line["config"])
+    assert {k: v for k, v in rline["config"].items() if k != "parallelism"} == \
+        {k: v for k, v in line["config"].items() if k != "parallelism"}

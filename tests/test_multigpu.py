@@ -77,17 +77,30 @@ def test_split_points_are_exact(oracle, oracle_tables, msl, cb):
             assert np.array_equal(got, want), (world, pts)
 
 
-def _worker(rank, world, port, docs, msl, cb, q):
+def _worker(rank, world, port, docs, msl, cb, q, device=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from oracle.oracle import OracleEncoder, load_tables
-
-    orc = OracleEncoder.from_tables(load_tables(*fixtures.gpt2_paths()))
     data, offs = pack_texts(docs)
+    if device:  # the CUDA engine of this rank's GPU (ranks share GPUs round-robin on a small box)
+        import torch
 
-    def encode(d, o):  # stands in for DeviceEncoder.encode_packed_host on this rank's GPU
-        ids, oo, _ = orc.encode_packed(d, o, msl, cb, 1)
-        return ids, oo
+        import paper_2603_02597_b200 as bpe
+
+        gpu = rank % torch.cuda.device_count()
+        torch.cuda.set_device(gpu)
+        enc = bpe.Tokenizer.from_files(*fixtures.gpt2_paths()).device_encoder(gpu)
+
+        def encode(d, o):
+            ids, oo, _, _ = enc.encode_packed_host(d, o, msl, cb)
+            return np.array(ids), oo
+    else:
+        from oracle.oracle import OracleEncoder, load_tables
+
+        orc = OracleEncoder.from_tables(load_tables(*fixtures.gpt2_paths()))
+
+        def encode(d, o):  # stands in for DeviceEncoder.encode_packed_host on this rank's GPU
+            ids, oo, _ = orc.encode_packed(d, o, msl, cb, 1)
+            return ids, oo
 
     res = multigpu.encode_sharded(data, offs, encode, rank, world)
     if rank == 0:
@@ -95,13 +108,16 @@ def _worker(rank, world, port, docs, msl, cb, q):
     dist.destroy_process_group()
 
 
-def test_gloo_world2_sharded_encode_matches_single(oracle):
-    docs = fixtures.prose_samples()[:30] + [b"", b"hello world", b" between"]
+@pytest.mark.parametrize("device", [False, pytest.param(True, marks=pytest.mark.gpu)])
+def test_gloo_world2_sharded_encode_matches_single(oracle, device):
+    """world 2 over gloo: the per-rank engine is the C oracle on CPU, or the
+    CUDA engine (DeviceEncoder) when a GPU is present (-m gpu)."""
+    docs = fixtures.prose_samples()[:30] + [b"", b"hello world", b" between", b"x" * 20000]
     msl, cb = 8192, 8192
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + random.Random(os.getpid()).randrange(2000)
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, docs, msl, cb, q)) for r in range(2)]
+    port = 29500 + random.Random(os.getpid() + device).randrange(2000)
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, docs, msl, cb, q, device)) for r in range(2)]
     for p in ps:
         p.start()
     ids, offs = q.get(timeout=240)

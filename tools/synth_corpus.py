@@ -232,3 +232,20 @@ def corpus_sample(total_bytes: int, frac: float, sample_seed: int, seed: int = 0
     pick = np.flatnonzero(rng.random(len(sizes)) < frac)
     data, offs = _fill(pool, sizes, starts, pick)
     return pick, data, offs
+
+
+def corpus_shard(total_bytes: int, rank: int, world: int, seed: int = 0):
+    """Rank `rank`'s contiguous, byte-balanced document range of
+    corpus_docs(total_bytes, seed) (the same split as multigpu.shard_batch),
+    generated without the other ranks' documents.  Returns (data, offsets
+    from 0, (d0, d1), total documents)."""
+    pool, sizes, starts, offs = _corpus_layout(total_bytes, seed, 1024, 65536, 64 << 20)
+    n_docs = len(sizes)
+    bounds = [0]
+    for r in range(1, world):
+        d = int(np.searchsorted(offs[:n_docs], int(offs[-1]) * r // world, side="left"))
+        bounds.append(max(bounds[-1], min(d, n_docs)))
+    bounds.append(n_docs)
+    d0, d1 = bounds[rank], bounds[rank + 1]
+    data, o = _fill(pool, sizes, starts, np.arange(d0, d1))
+    return data, o, (d0, d1), n_docs
