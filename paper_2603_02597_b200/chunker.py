@@ -272,16 +272,18 @@ class _LazyCounters(PassCounters):
     """PassCounters computed on first access (the batch path's counters are
     bookkeeping over the per-chunk id counts; most callers never read them)."""
 
+    _FIELDS = ("passes", "lookups", "compaction_moves", "buffer_allocations")
+
     def __init__(self, fn):
         object.__setattr__(self, "_fn", fn)
 
-    def __getattr__(self, name):
-        if name in ("passes", "lookups", "compaction_moves", "buffer_allocations"):
-            fn = self.__dict__.pop("_fn")
-            for k, v in fn().items():
-                object.__setattr__(self, k, v)
-            return self.__dict__[name]
-        raise AttributeError(name)
+    def __getattribute__(self, name):
+        if name in _LazyCounters._FIELDS:
+            d = object.__getattribute__(self, "__dict__")
+            fn = d.pop("_fn", None)
+            if fn is not None:
+                d.update(fn())
+        return object.__getattribute__(self, name)
 
 
 def _tri(x: np.ndarray) -> np.ndarray:

@@ -281,3 +281,20 @@ def test_chunk_units_match_chunk_tokens():
     assert list(zip(doc.tolist(), off.tolist(), clen.tolist())) == want
     assert first.tolist() == [0, 1, 2, 3, 8, 21, 22]
     assert _chunk_units(np.array([5, 64]), cfg) is None
+
+
+def test_lazy_counters_compute_once_on_first_read():
+    from paper_2603_02597_b200.chunker import _LazyCounters
+
+    calls = []
+
+    def fn():
+        calls.append(1)
+        return {"passes": 3, "lookups": 4, "compaction_moves": 5, "buffer_allocations": 6}
+
+    c = _LazyCounters(fn)
+    assert not calls
+    assert (c.passes, c.lookups, c.compaction_moves, c.buffer_allocations) == (3, 4, 5, 6)
+    total = bpe.PassCounters()
+    total.merge_from(c)
+    assert total == bpe.PassCounters(3, 4, 5, 6) and c == bpe.PassCounters(3, 4, 5, 6) and len(calls) == 1
