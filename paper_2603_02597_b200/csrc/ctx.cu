@@ -1406,6 +1406,8 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *
                                                                       int64_t *d_out_offs, uint64_t *n_bytes_out,
                                                                       uint64_t *bad_index, void *stream) {
     if (!ctx || !n_bytes_out || !bad_index) return GPUBPE_EINVAL;
+    *n_bytes_out = 0;
+    *bad_index = ~0ull;  // set before any argument check: EINVAL with an index means an unknown id
     if (!ctx->d_vinfo) return fail(ctx, GPUBPE_EINVAL, "decode: no vocabulary (gpubpe_set_vocab)");
     if (n_seqs && (!d_id_offs || !d_out_offs)) return fail(ctx, GPUBPE_EINVAL, "decode: null offsets");
     // the kernels store bytes in 16-byte vectors (decode.cu); ids may sit at any 4-byte offset
