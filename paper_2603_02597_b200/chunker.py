@@ -535,10 +535,9 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
         counters = _LazyCounters(lambda: _batch_counters(variant, tokenizer, np.diff(offs), np.diff(out_offs),
                                                          edges1))
         return BatchResult([ids], engine_ms, encode_ms, (time.perf_counter() - t1) * 1000.0, counters, st)
-    from .device import bytes_ptrs
+    from .device import bytes_ptrs_lens
 
-    lens = np.fromiter(map(len, parts), dtype=np.uint64, count=n_docs)
-    ptrs = bytes_ptrs(parts)
+    ptrs, lens = bytes_ptrs_lens(parts)
     cut = _chunk_units(lens, cfg) if mode == MODE_DEFAULT else None
     if cut is not None:  # documents longer than max_seq_len as their chunks
         cdoc, coff, clen, first = cut

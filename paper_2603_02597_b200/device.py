@@ -113,26 +113,28 @@ _RESULTS = _HostPool()
 _POOLED_MAX = _RESULTS.pinned_max
 
 
-def _char_p(b: bytes) -> int:
-    return ctypes.cast(ctypes.c_char_p(b), ctypes.c_void_p).value
+def _hostlist():
+    try:
+        from . import _hostlist as hl  # csrc/hostlist.c, built in-tree with libgpubpe.so
+    except ImportError as exc:
+        raise DeviceError(f"host helper _hostlist not built ({exc}); run make -C csrc") from exc
+    return hl
 
 
-# Address of a bytes object's data relative to id(): CPython keeps the data
-# inline at a fixed offset (PyBytesObject.ob_sval).  Measured here on objects
-# of several sizes, and re-checked on every batch (bytes_ptrs) against ctypes'
-# own pointer; any disagreement switches to the per-object ctypes path.
-_BYTES_DATA = _char_p(b"\x00gpubpe") - id(b"\x00gpubpe")
-_BYTES_LAYOUT_OK = all(_char_p(x) - id(x) == _BYTES_DATA for x in (b"", b"a", bytes(100), bytes(1 << 20)))
+def bytes_ptrs_lens(parts: list) -> tuple[np.ndarray, np.ndarray]:
+    """uint64 data addresses and lengths of a list of `bytes` objects (kept
+    alive by the caller), read through the CPython C API in one call."""
+    n = len(parts)
+    ptrs = np.empty(n, dtype=np.uint64)
+    lens = np.empty(n, dtype=np.uint64)
+    if n:
+        _hostlist().ptrs_lens(parts if type(parts) is list else list(parts), ptrs.ctypes.data, lens.ctypes.data)
+    return ptrs, lens
 
 
 def bytes_ptrs(parts: list) -> np.ndarray:
     """uint64 data addresses of a list of `bytes` objects (kept alive by the caller)."""
-    n = len(parts)
-    if _BYTES_LAYOUT_OK and n:
-        ptrs = np.fromiter(map(id, parts), dtype=np.uint64, count=n) + np.uint64(_BYTES_DATA)
-        if int(ptrs[0]) == _char_p(parts[0]) and int(ptrs[-1]) == _char_p(parts[-1]):
-            return ptrs
-    return np.fromiter(map(_char_p, parts), dtype=np.uint64, count=n)
+    return bytes_ptrs_lens(parts)[0]
 
 
 def pinned_empty(nbytes: int, device: int = 0) -> np.ndarray:
@@ -360,10 +362,8 @@ class DeviceEncoder:
         """A batch of separate `bytes` documents -> host CSR (ids, offs, stats,
         engine_ms), gathered straight into the pinned staging buffer by the
         native side (gpubpe_encode_host_gather): no join on the Python side."""
-        if not all(type(p) is bytes for p in parts):
-            raise TypeError("encode_list_host takes a list of bytes")
-        lens = np.fromiter(map(len, parts), dtype=np.uint64, count=len(parts))
-        return self.encode_ptrs_host(bytes_ptrs(parts), lens, max_seq_len, chunk_budget, mode)
+        ptrs, lens = bytes_ptrs_lens(parts)  # TypeError unless every item is bytes
+        return self.encode_ptrs_host(ptrs, lens, max_seq_len, chunk_budget, mode)
 
     def encode_ptrs_host(self, ptrs: np.ndarray, lens: np.ndarray, max_seq_len: int, chunk_budget: int,
                          mode: int = 0):

@@ -67,3 +67,20 @@ def test_signatures_match_header_arity():
     for name, args in protos.items():
         n = 0 if args.strip() in ("", "void") else args.count(",") + 1
         assert len(_native.SIGNATURES[name][1]) == n, name
+
+
+def test_hostlist_reads_bytes_addresses_through_the_c_api():
+    """device.bytes_ptrs_lens (csrc/hostlist.c): data addresses and lengths of a
+    list of bytes via PyBytes_AS_STRING; anything but bytes is a TypeError."""
+    from paper_2603_02597_b200.device import bytes_ptrs_lens
+
+    parts = [b"hello", b"", bytes(range(256)) * 40, b"\xff\x00x"]
+    ptrs, lens = bytes_ptrs_lens(parts)
+    assert lens.tolist() == [len(p) for p in parts]
+    for p, a, n in zip(parts, ptrs, lens):
+        assert ctypes.string_at(int(a), int(n)) == p
+    with pytest.raises(TypeError):
+        bytes_ptrs_lens([b"a", "str"])
+    with pytest.raises(TypeError):
+        bytes_ptrs_lens([bytearray(b"a")])
+    assert [x.size for x in bytes_ptrs_lens([])] == [0, 0]

@@ -16,6 +16,9 @@ out = torch.empty(len(data), dtype=torch.int32, device="cuda"); oo = torch.empty
 enc.set_profiling(True)
 for i in range(4):
     os.environ["GPUBPE_DEBUG_OUT"] = "/tmp/dbg.bin" if i == 3 else ""
+    if os.environ.get("FLUSH") and i == 3:
+        torch.empty(256 << 20, dtype=torch.uint8, device="cuda").fill_(1)
+        torch.cuda.synchronize()
     enc.encode_into(d, o, out, oo, 1 << 40, 1 << 40)
     torch.cuda.synchronize()
 print("kernel (events) %.1f us" % (1000 * enc.kernel_ms()))

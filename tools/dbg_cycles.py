@@ -16,6 +16,9 @@ d = torch.from_numpy(data.copy()).cuda(); o = torch.from_numpy(offs).cuda()
 out = torch.empty(len(data), dtype=torch.int32, device="cuda"); oo = torch.empty(len(offs), dtype=torch.int64, device="cuda")
 for i in range(3):
     os.environ["GPUBPE_DEBUG_OUT"] = "/tmp/dbg.bin" if i == 2 else ""
+    if os.environ.get("FLUSH") and i == 2:
+        torch.empty(256 << 20, dtype=torch.uint8, device="cuda").fill_(1)
+        torch.cuda.synchronize()
     enc.encode_into(d, o, out, oo, 1 << 40, 1 << 40)
     torch.cuda.synchronize()
 h = np.fromfile("/tmp/dbg.bin", dtype=np.uint64).astype(np.int64)

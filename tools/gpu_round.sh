@@ -11,6 +11,7 @@ tail -2 gpurun_out/pytest_${TAG}.log
 timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke_${TAG}.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_${TAG}.log
 tail -1 gpurun_out/smoke_${TAG}.log
 timeout 900 python bench.py > gpurun_out/bench_${TAG}.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_${TAG}.log
+timeout 600 python bench.py --gpus 2 --steps 200 --warmup 5 --corpus-mb 1024 > gpurun_out/bench_g2_${TAG}.log 2>&1; echo "g2 rc=$?" >> gpurun_out/bench_g2_${TAG}.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${TAG}.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref_${TAG}.log
 timeout 600 python bench.py --workload corpus_256m --steps 5 --warmup 3 > gpurun_out/bench_corpus_${TAG}.log 2>&1; echo "corpus rc=$?" >> gpurun_out/bench_corpus_${TAG}.log
 timeout 900 python bench.py --workload corpus_10240m --steps 3 --warmup 3 > gpurun_out/bench_c4_${TAG}.log 2>&1; echo "c4 rc=$?" >> gpurun_out/bench_c4_${TAG}.log
