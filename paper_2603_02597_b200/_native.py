@@ -42,6 +42,11 @@ class Stats(ctypes.Structure):
 
 _STAT_NAMES = tuple(n for n, _ in Stats._fields_)
 
+
+def stats_dict(values) -> dict:
+    """gpubpe_stats fields (a tuple in header order) as the device_stats dict."""
+    return dict(zip(_STAT_NAMES, values))
+
 SIGNATURES = {
     "gpubpe_ctx_create": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _u64,
                                  ctypes.c_uint32, ctypes.POINTER(_vp)]),

@@ -518,22 +518,29 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
         # one document (the latency path): one buffer staged piecewise, overlapping
         # its DMA; a document longer than max_seq_len goes as its chunks
         enc = tokenizer.device_encoder(devs[0] if devs else None)
-        data = np.frombuffer(parts[0], dtype=np.uint8)
-        n = data.size
-        if mode == MODE_DEFAULT and n > cfg.max_seq_len:
-            offs = np.append(np.arange(0, n, cfg.chunk_budget, dtype=np.int64), n)
+        doc = parts[0]
+        n = len(doc)
+        if mode == MODE_DEFAULT:  # one C call: chunk offsets, encode, counters
+            ids, out_offs, st, engine_ms = enc.encode_bytes_host(doc, cfg.max_seq_len, cfg.chunk_budget)
         else:
-            offs = np.array([0, n], np.int64)
-        ids, out_offs, st, engine_ms = enc.encode_packed_host(data, offs, cfg.max_seq_len, cfg.chunk_budget, mode)
+            ids, out_offs, st, engine_ms = enc.encode_packed_host(np.frombuffer(doc, dtype=np.uint8),
+                                                                  np.array([0, n], np.int64),
+                                                                  cfg.max_seq_len, cfg.chunk_budget, mode)
         t1 = time.perf_counter()
-        base = tokenizer._base_ids
+        chunked = mode == MODE_DEFAULT and n > cfg.max_seq_len
 
-        def edges1(k):
-            a, b, c, d = int(offs[k]), int(offs[k + 1]), int(out_offs[k]), int(out_offs[k + 1])
-            return (int(base[data[a]]), int(base[data[b - 1]])), (int(ids[c]), int(ids[d - 1]))
+        def counters1():  # (on first read) the chunk offsets the device encoded, then the counters
+            offs = (np.append(np.arange(0, n, cfg.chunk_budget, dtype=np.int64), n) if chunked
+                    else np.array([0, n], np.int64))
+            base, data = tokenizer._base_ids, np.frombuffer(doc, dtype=np.uint8)
 
-        counters = _LazyCounters(lambda: _batch_counters(variant, tokenizer, np.diff(offs), np.diff(out_offs),
-                                                         edges1))
+            def edges1(k):
+                a, b, c, d = int(offs[k]), int(offs[k + 1]), int(out_offs[k]), int(out_offs[k + 1])
+                return (int(base[data[a]]), int(base[data[b - 1]])), (int(ids[c]), int(ids[d - 1]))
+
+            return _batch_counters(variant, tokenizer, np.diff(offs), np.diff(out_offs), edges1)
+
+        counters = _LazyCounters(counters1)
         return BatchResult([ids], engine_ms, encode_ms, (time.perf_counter() - t1) * 1000.0, counters, st)
     from .device import bytes_ptrs_lens
 

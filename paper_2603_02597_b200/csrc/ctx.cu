@@ -97,6 +97,17 @@ struct gpubpe_ctx {
     } ss[2];
     cudaStream_t s_copy = nullptr, s_d2h = nullptr;
     bool defer_check = false;  // the caller checks EncodeState.overflow itself (streamed encode)
+    // overlapped host encode: the kernel is enqueued before the input pieces;
+    // each piece's arrival word is DMA'd (s_copy) after it
+    unsigned int *d_arrive = nullptr;  // [ARRIVE_MAX] device words
+    unsigned int *h_tag = nullptr;     // pinned source of the words' value
+    unsigned int arrive_tag = 0;
+    const unsigned int *cur_arrive = nullptr;  // for the encode being launched
+    uint64_t cur_piece = 0;
+    unsigned long long *dbg_buf = nullptr;  // GPUBPE_DEBUG & 8 timestamps
+    std::chrono::steady_clock::time_point t_call;  // GPUBPE_HOSTTIME: gpubpe_encode entry
+    int tl_n = 0;                                  // GPUBPE_HOSTTIME=2: piece events of this call
+    cudaEvent_t *tl_ev = nullptr;
     EncodeState *h_state_ss = nullptr;  // pinned [2]: per-slot encode state
     uint64_t last_n_tiles = 0;
     uint32_t n_ids = 0;             // internal ids the tables cover
@@ -505,6 +516,20 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
     return GPUBPE_OK;
 }
 
+// Debug timestamps of the last encode (GPUBPE_DEBUG & 8) to GPUBPE_DEBUG_OUT.
+static void dump_debug(gpubpe_ctx *ctx, cudaStream_t s) {
+    const char *path = getenv("GPUBPE_DEBUG_OUT");
+    if (!path || !*path || !ctx->dbg_buf) return;
+    std::vector<unsigned long long> h(40960);
+    cudaMemcpyAsync(h.data(), ctx->dbg_buf, h.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    FILE *f = fopen(path, "wb");
+    if (f) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+    }
+}
+
 static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes,
                        const int64_t *d_doc_offs, uint64_t n_docs, uint64_t max_seq_len,
                        uint64_t chunk_budget, uint32_t *d_out_ids, int64_t *d_out_offs,
@@ -572,32 +597,34 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.aligned = (reinterpret_cast<uintptr_t>(d_bytes) & 15) == 0;
         P.tile_bytes = wt;
         P.pretok = ctx->cur_pretok;
+        P.arrive = ctx->cur_arrive;
+        P.piece = ctx->cur_piece ? ctx->cur_piece : 1;
+        P.arrive_tag = ctx->arrive_tag;
         P.gscr = static_cast<unsigned long long *>(ctx->ws_gscr.p);
         P.glist = static_cast<uint32_t *>(ctx->ws_glist.p);
         ctx->last_n_tiles = n_tiles;
         // debug knobs (tuning only) never apply to the memo verification encode
         const int dbg = (ctx->T.memo && getenv("GPUBPE_DEBUG")) ? atoi(getenv("GPUBPE_DEBUG")) : 0;
         P.dbg_phase_a_only = (dbg & 16) ? 1 : (dbg & 32) ? 2 : 0;
-        static unsigned long long *dbuf = nullptr;
         if (dbg & 8) {
-            if (!dbuf) cudaMalloc(&dbuf, 40960 * 8);
-            cudaMemsetAsync(dbuf, 0, 40960 * 8, s);
-            P.dbg = dbuf;
+            if (!ctx->dbg_buf) cudaMalloc(&ctx->dbg_buf, 40960 * 8);
+            cudaMemsetAsync(ctx->dbg_buf, 0, 40960 * 8, s);
+            P.dbg = ctx->dbg_buf;
         }
+        static const bool htime_l = getenv("GPUBPE_HOSTTIME") != nullptr;
+        const auto tl0 = std::chrono::steady_clock::now();
         cudaError_t e = launch_encode(P, grid, s, ctx->profiling ? ctx->ev : nullptr, (dbg & 4) ? nullptr : &ctx->win, !(dbg & 2));
+        if (htime_l)
+            fprintf(stderr, "encode_impl: setup %.1f | launch %.1f us\n",
+                    std::chrono::duration<double, std::micro>(tl0 - ctx->t_call).count(),
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tl0).count());
         ctx->timed = ctx->profiling;
         if (e != cudaSuccess) return fail(ctx, GPUBPE_ECUDA, "encode launch: %s", cudaGetErrorString(e));
         // Overflow is impossible when every deferred segment fits the record
         // list and the arena (ENGINE_BYTES(len) rounded to 16 B per segment);
         // otherwise check after the call and re-run with larger buffers.
         const uint64_t arena_need = 26 * n_bytes + 96 * def_max;
-        if ((dbg & 8) && getenv("GPUBPE_DEBUG_OUT")) {
-            std::vector<unsigned long long> h(40960);
-            cudaMemcpyAsync(h.data(), dbuf, h.size() * 8, cudaMemcpyDeviceToHost, s);
-            cudaStreamSynchronize(s);
-            FILE *f = fopen(getenv("GPUBPE_DEBUG_OUT"), "wb");
-            if (f) { fwrite(h.data(), 8, h.size(), f); fclose(f); }
-        }
+        if ((dbg & 8) && !P.arrive) dump_debug(ctx, s);  // (overlapped calls: after their pieces)
         if (ctx->defer_check || (def_max <= rec_cap && arena_need <= ctx->ws_arena.bytes)) return GPUBPE_OK;
         *checked = true;
         CK(cudaMemcpyAsync(ctx->h_state, P.st, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
@@ -616,6 +643,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *
                              uint64_t chunk_budget, uint32_t *d_out_ids, int64_t *d_out_offs,
                              void *stream) {
     if (!ctx) return GPUBPE_EINVAL;
+    ctx->t_call = std::chrono::steady_clock::now();
     if (chunk_budget < 2 || chunk_budget > max_seq_len)
         return fail(ctx, GPUBPE_EINVAL, "chunk_budget must be in [2, max_seq_len]");
     if (n_docs && (!d_doc_offs || !d_out_offs)) return fail(ctx, GPUBPE_EINVAL, "null offsets");
@@ -748,6 +776,10 @@ static inline void cpu_relax() {
 }
 
 namespace {
+// Jobs: a buffer split in parts (at most 40).  One 64-bit word holds the job
+// id, its part count and the claimed parts, so a claim (CAS) can only succeed
+// on the job it read, and a job's buffers are only rewritten once all its
+// parts are done (left_ == 0) -- no part is ever run with another job's buffers.
 class StagePool {
   public:
     static StagePool &get() {
@@ -761,40 +793,81 @@ class StagePool {
         }
     }
     void end() { active_.fetch_sub(1); }
-    // memcpy split in (workers + 1) parts; the caller takes part 0
+    // memcpy split in (workers + 1) parts, the caller working too
     void copy(uint8_t *dst, const uint8_t *src, size_t n) {
         const unsigned parts = (unsigned)th_.size() + 1;
         const size_t chunk = ((n + parts - 1) / parts + 63) & ~(size_t)63;
-        // one staged copy at a time; a concurrent caller (another context or
+        // one staged job at a time; a concurrent caller (another context or
         // thread, e.g. one per GPU) copies its piece itself instead of waiting
         std::unique_lock<std::mutex> call(call_, std::try_to_lock);
         if (!call.owns_lock()) {
             memcpy(dst, src, n);
             return;
         }
-        dst_ = dst;
-        src_ = src;
-        n_ = n;
-        chunk_ = chunk;
-        left_.store((int)parts - 1, std::memory_order_relaxed);
-        next_.store(1, std::memory_order_release);
-        gen_.fetch_add(1, std::memory_order_release);
-        memcpy(dst, src, std::min(n, chunk));
-        for (unsigned i; (i = next_.fetch_add(1)) < parts;) run(i);  // parts nobody took yet
+        post(dst, src, n, chunk, parts);
+        while (claim_and_run()) {
+        }
         while (left_.load(std::memory_order_acquire) > 0) cpu_relax();
+    }
+    // Background staging in pieces of `piece` bytes: the helpers take pieces
+    // in order while the caller does other work (the kernel launch); the
+    // caller then waits for each piece (wait_piece, taking unclaimed ones
+    // itself) and releases the pool (finish_pieces).  false: the pool is busy.
+    bool start_pieces(uint8_t *dst, const uint8_t *src, size_t n, size_t piece) {
+        const size_t parts = (n + piece - 1) / piece;
+        if (parts > MAXP) return false;
+        std::unique_lock<std::mutex> call(call_, std::try_to_lock);
+        if (!call.owns_lock()) return false;
+        held_ = std::move(call);
+        post(dst, src, n, piece, (unsigned)parts);
+        return true;
+    }
+    void wait_piece(unsigned k) {
+        while (!((done_.load(std::memory_order_acquire) >> k) & 1ull))
+            if (!claim_and_run()) cpu_relax();
+    }
+    void finish_pieces() {
+        while (left_.load(std::memory_order_acquire) > 0) cpu_relax();
+        held_ = std::unique_lock<std::mutex>();
     }
 
   private:
+    static constexpr unsigned MAXP = 40;
+    static constexpr unsigned long long BITS = (1ull << MAXP) - 1;
     StagePool() {
         const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
         const unsigned nw = std::min(3u, hw / 4);
         for (unsigned i = 0; i < nw; ++i) th_.emplace_back([this] { loop(); });
         for (auto &t : th_) t.detach();
     }
-    void run(unsigned i) {
-        const size_t lo = std::min(n_, i * chunk_), hi = std::min(n_, lo + chunk_);
-        if (lo < hi) memcpy(dst_ + lo, src_ + lo, hi - lo);
-        left_.fetch_sub(1, std::memory_order_acq_rel);
+    void post(uint8_t *dst, const uint8_t *src, size_t n, size_t chunk, unsigned parts) {
+        dst_ = dst;
+        src_ = src;
+        n_ = n;
+        chunk_ = chunk;
+        done_.store(0, std::memory_order_relaxed);
+        left_.store((int)parts, std::memory_order_relaxed);
+        job_ = (job_ + 1) & 0xFFFF;
+        word_.store(((unsigned long long)job_ << 48) | ((unsigned long long)parts << 40), std::memory_order_release);
+        gen_.fetch_add(1, std::memory_order_release);
+    }
+    // Claim and copy one part of the posted job; false when none is left.
+    bool claim_and_run() {
+        unsigned long long w = word_.load(std::memory_order_acquire);
+        for (;;) {
+            const unsigned parts = (unsigned)((w >> 40) & 0xFF);
+            const unsigned long long free = ~w & BITS & ((1ull << parts) - 1);
+            if (!free) return false;
+            const unsigned i = (unsigned)__builtin_ctzll(free);
+            if (word_.compare_exchange_weak(w, w | (1ull << i), std::memory_order_acq_rel,
+                                            std::memory_order_acquire)) {
+                const size_t lo = std::min(n_, i * chunk_), hi = std::min(n_, lo + chunk_);
+                if (lo < hi) memcpy(dst_ + lo, src_ + lo, hi - lo);
+                done_.fetch_or(1ull << i, std::memory_order_acq_rel);
+                left_.fetch_sub(1, std::memory_order_acq_rel);
+                return true;
+            }
+        }
     }
     void loop() {
         unsigned long long seen = 0;
@@ -810,8 +883,8 @@ class StagePool {
                     continue;
                 }
                 seen = gen;
-                const unsigned parts = (unsigned)th_.size() + 1;
-                for (unsigned i; (i = next_.fetch_add(1)) < parts;) run(i);
+                while (claim_and_run()) {
+                }
             }
         }
     }
@@ -819,11 +892,12 @@ class StagePool {
     std::mutex m_, call_;
     std::condition_variable cv_;
     std::atomic<int> active_{0}, left_{0};
-    std::atomic<unsigned> next_{0};
-    std::atomic<unsigned long long> gen_{0};
+    std::atomic<unsigned long long> word_{0}, done_{0}, gen_{0};
+    unsigned job_ = 0;
     uint8_t *dst_ = nullptr;
     const uint8_t *src_ = nullptr;
     size_t n_ = 0, chunk_ = 0;
+    std::unique_lock<std::mutex> held_;
 };
 }  // namespace
 
@@ -1102,11 +1176,23 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
                             uint32_t *h_out_ids, int64_t *h_out_offs, uint64_t *n_ids_out, float *kernel_ms,
                             void *stream);
 
+// The caller thread's current device is restored on return (the host entry
+// points select the context's device themselves; callers need no device guard).
+struct DeviceRestore {
+    int prev = -1;
+    DeviceRestore() { cudaGetDevice(&prev); }
+    ~DeviceRestore() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
 extern "C" __attribute__((visibility("default"))) int gpubpe_encode_host(
     gpubpe_ctx *ctx, const uint8_t *h_bytes, uint64_t n_bytes, const int64_t *h_doc_offs, uint64_t n_docs,
     uint64_t max_seq_len, uint64_t chunk_budget, uint32_t *h_out_ids, int64_t *h_out_offs,
     uint64_t *n_ids_out, float *kernel_ms, void *stream) {
     if (!ctx) return GPUBPE_EINVAL;
+    DeviceRestore restore_device;
     if (!n_ids_out || (n_docs && (!h_doc_offs || !h_out_offs)) || (n_bytes && (!h_bytes || !h_out_ids)))
         return fail(ctx, GPUBPE_EINVAL, "null host pointer");
     return encode_host_core(ctx, h_bytes, nullptr, n_bytes, h_doc_offs, n_docs, max_seq_len, chunk_budget, h_out_ids,
@@ -1128,7 +1214,7 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
             on = false;
         }
         ~StageCall() { done(); }
-    } stage_call(!stage && n_bytes >= (512u << 10) && n_bytes <= (16u << 20) && !getenv("GPUBPE_NO_STAGE_POOL"));
+    } stage_call(!stage && n_bytes >= (128u << 10) && n_bytes <= (16u << 20) && !getenv("GPUBPE_NO_STAGE_POOL"));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->alloc_mark = ctx->n_allocs;
     struct HostCall {  // gpubpe_encode calls below keep this call's allocation mark
@@ -1169,6 +1255,21 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         if ((rc = ensure(ctx, ctx->io_dev, need, false))) return rc;
         dv = static_cast<uint8_t *>(ctx->io_dev.p);
     }
+    uint8_t *dout = mode == 3 ? ctx->pin_dev : dv;  // where the kernel writes ids and offsets (mode 3:
+                                                    // mapped pinned memory, the stores overlap the kernel)
+    // A caller buffer that is itself pinned and device-mapped (gpubpe_host_alloc)
+    // receives the ids directly: no copy-out at all.
+    uint32_t *d_ids_direct = (mode == 3 && n_bytes) ? static_cast<uint32_t *>(mapped_alias(h_out_ids)) : nullptr;
+    // overlapped launch (one pageable buffer of 128 KiB .. 16 MiB, default mode):
+    // ~4 pieces, the kernel enqueued before them
+    static const bool no_overlap = getenv("GPUBPE_NO_OVERLAP") != nullptr;
+    // (every H2D copy costs ~7 us of setup on this PCIe 5 link, measured by
+    // tools/overlap_probe.cu: one piece unless GPUBPE_OV_PIECES says otherwise)
+    static const int ov_pieces = getenv("GPUBPE_OV_PIECES") ? std::max(1, atoi(getenv("GPUBPE_OV_PIECES"))) : 1;
+    const size_t ov_piece = std::max<size_t>(32u << 10, ((n_bytes / ov_pieces) + 4095) & ~(size_t)4095);
+    const bool overlap = !no_overlap && mode == 3 && !stage && ctx->mode == GPUBPE_MODE_DEFAULT &&
+                         n_bytes >= (128u << 10) && n_bytes <= (16u << 20) &&
+                         (n_bytes + ov_piece - 1) / ov_piece <= (size_t)ARRIVE_MAX && !mapped_alias(h_bytes);
     if (mode == 1) {  // zero-copy: the kernel reads and writes mapped host memory
         copy_par(pin + o_in, h_bytes, n_bytes);
         memcpy(pin + o_doffs, h_doc_offs, offs_b);
@@ -1176,6 +1277,44 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
     } else if (mode == 2) {  // pageable copies straight from the caller's buffers
         CK(cudaMemcpyAsync(dv + o_doffs, h_doc_offs, offs_b, cudaMemcpyHostToDevice, s));
         if (n_bytes) CK(cudaMemcpyAsync(dv + o_in, h_bytes, n_bytes, cudaMemcpyHostToDevice, s));
+    } else if (overlap) {
+        // overlapped: the input (one piece: every H2D copy costs ~7 us of setup
+        // here) is staged by the helpers and DMA'd on s_copy, followed by its
+        // arrival word; the kernel is enqueued right after on the caller's
+        // stream, so its launch and prologue run while the DMA is in flight and
+        // its tiles wait for the word.  The document offsets go first.
+        if (!ctx->d_arrive) {
+            CK(cudaMalloc(&ctx->d_arrive, ARRIVE_MAX * ARRIVE_STRIDE * sizeof(unsigned int)));
+            CK(cudaMemset(ctx->d_arrive, 0, ARRIVE_MAX * ARRIVE_STRIDE * sizeof(unsigned int)));
+            CK(cudaHostAlloc(reinterpret_cast<void **>(&ctx->h_tag), 64, 0));
+            ctx->n_allocs += 2;
+        }
+        if (!ctx->s_copy) CK(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
+        if (++ctx->arrive_tag == 0) ctx->arrive_tag = 1;  // (words start at 0)
+        *ctx->h_tag = ctx->arrive_tag;
+        memcpy(pin + o_doffs, h_doc_offs, offs_b);
+        CK(cudaMemcpyAsync(dv + o_doffs, pin + o_doffs, offs_b, cudaMemcpyHostToDevice, ctx->s_copy));
+        const unsigned n_pieces = (unsigned)((n_bytes + ov_piece - 1) / ov_piece);
+        for (unsigned k = 0; k < n_pieces; ++k) {
+            const size_t lo = (size_t)k * ov_piece, len = std::min<size_t>(ov_piece, n_bytes - lo);
+            StagePool::get().copy(pin + o_in + lo, h_bytes + lo, len);
+            CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, len, cudaMemcpyHostToDevice, ctx->s_copy));
+            CK(cudaMemcpyAsync(ctx->d_arrive + ARRIVE_STRIDE * k, ctx->h_tag, sizeof(unsigned int),
+                               cudaMemcpyHostToDevice, ctx->s_copy));
+        }
+        CK(cudaEventRecord(ctx->io_ev[0], s));
+        ctx->cur_arrive = ctx->d_arrive;
+        ctx->cur_piece = ov_piece;
+        const bool dc = ctx->defer_check;
+        ctx->defer_check = true;  // the overflow check waits for the final synchronisation
+        rc = gpubpe_encode(ctx, dv + o_in, n_bytes, reinterpret_cast<const int64_t *>(dv + o_doffs), n_docs,
+                           max_seq_len, chunk_budget,
+                           d_ids_direct ? d_ids_direct : reinterpret_cast<uint32_t *>(dout + o_ids),
+                           reinterpret_cast<int64_t *>(dout + o_ooffs), stream);
+        ctx->defer_check = dc;
+        ctx->cur_arrive = nullptr;
+        ctx->cur_piece = 0;
+        if (rc) return rc;
     } else if (n_bytes && !stage && mapped_alias(h_bytes)) {  // caller bytes already pinned: no staging copy
         memcpy(pin + o_doffs, h_doc_offs, offs_b);
         CK(cudaMemcpyAsync(dv + o_in, h_bytes, n_bytes, cudaMemcpyHostToDevice, s));
@@ -1194,28 +1333,37 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
             else copy_par(dst, src, len);
         };
         size_t lo = 0;
+        static const bool tl = getenv("GPUBPE_HOSTTIME") && atoi(getenv("GPUBPE_HOSTTIME")) == 2;
+        static cudaEvent_t tev[10];
+        int ntev = 0;
+        if (tl && !tev[0])
+            for (auto &e : tev) cudaEventCreate(&e);
+        if (tl) cudaEventRecord(tev[ntev++], s);
         for (; lo + piece < n_bytes; lo += piece) {
             if (stage) (*stage)(pin + o_in + lo, lo, lo + piece);
             else copy_piece(pin + o_in + lo, h_bytes + lo, piece);
             CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, piece, cudaMemcpyHostToDevice, s));
+            if (tl && ntev < 8) cudaEventRecord(tev[ntev++], s);
         }
         if (stage) (*stage)(pin + o_in + lo, lo, n_bytes);
         else copy_piece(pin + o_in + lo, h_bytes + lo, n_bytes - lo);
         CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, o_doffs + offs_b - lo, cudaMemcpyHostToDevice, s));
+        if (tl) {  // GPU timeline of the pieces (GPUBPE_HOSTTIME=2): printed after the kernel
+            cudaEventRecord(tev[ntev++], s);
+            ctx->tl_n = ntev;
+            ctx->tl_ev = tev;
+        }
     }
     stage_call.done();
     auto t_b = now();
-    CK(cudaEventRecord(ctx->io_ev[0], s));
-    uint8_t *dout = dv;  // where the kernel writes ids and offsets
-    if (mode == 3) dout = ctx->pin_dev;  // outputs straight into mapped pinned memory (stores overlap the kernel)
-    // A caller buffer that is itself pinned and device-mapped (gpubpe_host_alloc)
-    // receives the ids directly: no copy-out at all.
-    uint32_t *d_ids_direct = (mode == 3 && n_bytes) ? static_cast<uint32_t *>(mapped_alias(h_out_ids)) : nullptr;
-    rc = gpubpe_encode(ctx, dv + o_in, n_bytes, reinterpret_cast<const int64_t *>(dv + o_doffs), n_docs,
-                       max_seq_len, chunk_budget,
-                       d_ids_direct ? d_ids_direct : reinterpret_cast<uint32_t *>(dout + o_ids),
-                       reinterpret_cast<int64_t *>(dout + o_ooffs), stream);
-    if (rc) return rc;
+    if (!overlap) {
+        CK(cudaEventRecord(ctx->io_ev[0], s));
+        rc = gpubpe_encode(ctx, dv + o_in, n_bytes, reinterpret_cast<const int64_t *>(dv + o_doffs), n_docs,
+                           max_seq_len, chunk_budget,
+                           d_ids_direct ? d_ids_direct : reinterpret_cast<uint32_t *>(dout + o_ids),
+                           reinterpret_cast<int64_t *>(dout + o_ooffs), stream);
+        if (rc) return rc;
+    }
     CK(cudaEventRecord(ctx->io_ev[1], s));
     if (mode != 1 && mode != 3) CK(cudaMemcpyAsync(pin + o_ooffs, dv + o_ooffs, offs_b, cudaMemcpyDeviceToHost, s));
     if (n_bytes) {  // the counters come back in the same sync (none needed by gpubpe_query)
@@ -1225,7 +1373,33 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
     auto t_c = now();
     CK(cudaStreamSynchronize(s));
     auto t_d = now();
+    if (ctx->tl_n) {
+        float ms;
+        fprintf(stderr, "timeline (us from the first piece's enqueue):");
+        for (int k = 1; k < ctx->tl_n; ++k) {
+            cudaEventElapsedTime(&ms, ctx->tl_ev[0], ctx->tl_ev[k]);
+            fprintf(stderr, " piece%d %.1f", k - 1, ms * 1e3);
+        }
+        cudaEventElapsedTime(&ms, ctx->tl_ev[0], ctx->io_ev[0]);
+        fprintf(stderr, " | kernel enqueued-point %.1f", ms * 1e3);
+        cudaEventElapsedTime(&ms, ctx->tl_ev[0], ctx->io_ev[1]);
+        fprintf(stderr, " | kernel end %.1f\n", ms * 1e3);
+        ctx->tl_n = 0;
+    }
     ctx->state_fresh = n_bytes != 0;
+    if (overlap && ctx->dbg_buf && getenv("GPUBPE_DEBUG")) dump_debug(ctx, s);
+    if (overlap && ctx->h_state->overflow) {
+        // deferred-segment buffers too small (checked here, not at the launch):
+        // the input is on the device now; re-run the plain path, which grows them
+        rc = gpubpe_encode(ctx, dv + o_in, n_bytes, reinterpret_cast<const int64_t *>(dv + o_doffs), n_docs,
+                           max_seq_len, chunk_budget,
+                           d_ids_direct ? d_ids_direct : reinterpret_cast<uint32_t *>(dout + o_ids),
+                           reinterpret_cast<int64_t *>(dout + o_ooffs), stream);
+        if (rc) return rc;
+        const EncodeState *last = static_cast<const EncodeState *>(ctx->ws_state.p) + ((ctx->calls - 1) & 1);
+        CK(cudaMemcpyAsync(ctx->h_state, last, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
     const int64_t *p_oo = reinterpret_cast<const int64_t *>(pin + o_ooffs);
     const uint64_t total = n_bytes ? (uint64_t)p_oo[n_docs] : 0;
     if (total > n_bytes)

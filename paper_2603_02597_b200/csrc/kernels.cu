@@ -39,6 +39,7 @@ struct CtaSmem {
     EngineShared es;
     unsigned long long bcast[4];
     unsigned long long seen[2];     // ndef[] by parity as of this CTA's last read (thread 0)
+    uint32_t arrived, poll_lock;    // overlapped host calls: pieces seen arrived; poller lock
     unsigned long long red[NW][4];  // per-warp partial sums (no 64-bit shared atomics: CAS loops)
     PassCounters pc;
     unsigned long long tb[UNIT_MAX];  // phase B: tile output offsets inside the unit
@@ -66,6 +67,10 @@ __device__ __forceinline__ unsigned long long ld_relaxed(unsigned long long *w) 
 __device__ __forceinline__ unsigned int ld_relaxed_u32(unsigned int *w) {
     cuda::atomic_ref<unsigned int, cuda::thread_scope_device> r(*w);
     return r.load(cuda::memory_order_relaxed);
+}
+
+__device__ __forceinline__ void red_release_add(unsigned long long *w, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(w), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -300,8 +305,8 @@ __device__ __forceinline__ void l2_discard(const void *p) {
 // kernels.cuh, phase A).  The segments starting in the tile are gathered
 // into a position-ordered list and dealt round-robin to the lanes, so every
 // lane handles ~1/32 of them (a warp's latency is its slowest lane's chain).
-__device__ __noinline__ void encode_tile(const EncodeParams &P, CtaSmem &C, WarpSmem &S, unsigned long long t,
-                                         unsigned long long slot, WarpCtx &X) {
+__device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, WarpSmem &S, unsigned long long t,
+                                             unsigned long long slot, WarpCtx &X) {
     const int lane = threadIdx.x & 31;
     const DevTables &T = P.T;
     const int wt = P.tile_bytes;
@@ -314,6 +319,35 @@ __device__ __noinline__ void encode_tile(const EncodeParams &P, CtaSmem &C, Warp
     uint32_t *sb = S.u.a.sbw;
     uint32_t c_seg = 0, c_memo = 0, c_miss = 0, c_pass = 0;
 
+    // ---- 0. overlapped host call: wait until the pieces holding bytes
+    //         [a - 1, a + nst) have arrived (their words are DMA'd after them;
+    //         no SM reads a piece before its word, so no stale line can exist)
+    //         One global poller per CTA at a time (a shared-memory lock); the
+    //         other warps watch the CTA's arrived mask in shared memory.
+    if (P.arrive) {
+        if (lane == 0) {
+            const uint32_t k0 = (uint32_t)((unsigned long long)(a > 0 ? a - 1 : 0) / P.piece);
+            const uint32_t k1 = (uint32_t)((unsigned long long)(a + nst - 1) / P.piece);
+            const uint32_t need = (k1 >= 31 ? 0xFFFFFFFFu : ((2u << k1) - 1)) & ~((1u << k0) - 1);
+            volatile uint32_t *arrived = &C.arrived;
+            while ((*arrived & need) != need) {
+                if (atomicCAS(&C.poll_lock, 0u, 1u) == 0u) {
+                    uint32_t m = *arrived;
+                    for (uint32_t k = k0; k <= k1; ++k)
+                        if (!((m >> k) & 1u) &&
+                            ld_relaxed_u32(const_cast<unsigned int *>(&P.arrive[ARRIVE_STRIDE * k])) == P.arrive_tag)
+                            m |= 1u << k;
+                    atomicOr(&C.arrived, m);
+                    atomicExch(&C.poll_lock, 0u);
+                    if ((m & need) == need) break;
+                }
+                __nanosleep(256);
+            }
+        }
+        if (P.dbg && lane == 0) atomicMax(&P.dbg[36864 + 4 * blockIdx.x + 3], gtimer());
+        __syncwarp();
+        asm volatile("" ::: "memory");
+    }
     // ---- 1. stage the tile and its halo (16-B loads, both rounds in flight)
     if (P.aligned && nst == ld) {
         const uint4 *src = reinterpret_cast<const uint4 *>(P.bytes + a);
@@ -590,6 +624,7 @@ __device__ __noinline__ void encode_tile(const EncodeParams &P, CtaSmem &C, Warp
     X.memo_hits += c_memo;
     X.short_merges += c_miss;
     if (lane == 0) X.engine_passes += c_pass;
+    return total | (S.n_def << 16);
 }
 
 // ------------------------------------------------------------------ phase B
@@ -655,6 +690,55 @@ __device__ void place_tile(const EncodeParams &P, const uint32_t *src, unsigned 
     // markers are re-read by the document fix-up)
     if (!TW_HASDEF(w))
         for (uint32_t k = lane; k < (n * 4 + 127) / 128; k += 32) l2_discard(src + 32 * k);
+}
+
+// CSR offsets of the documents starting in tiles [lo, hi) (C.tw / C.tb hold
+// their words and in-range offsets): tile-local -> global.
+__device__ __forceinline__ void fix_doc_offsets(const EncodeParams &P, CtaSmem &C, unsigned long long lo,
+                                                unsigned long long hi, int nt, unsigned long long base,
+                                                const uint32_t *slots) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // One document: its offsets are 0 and the id total, no look-ups needed.
+    if (P.n_docs == 1) {
+        if (tid == 0 && nt > 0) {
+            if (lo == 0) P.out_offs[0] = 0;
+            if (hi == P.n_tiles) P.out_offs[1] = (long long)(base + C.bcast[2]);
+        }
+    } else if (wid == 0 && nt > 0) {
+        const long long blo = (long long)lo * P.tile_bytes;
+        long long d = 0;
+        if (blo > 0) {  // first document with offs >= blo (lower bound)
+            long long lo_d = 0, hi_d = (long long)P.n_docs;  // answer in [lo_d, hi_d]
+            while (hi_d > lo_d) {
+                const long long step = (hi_d - lo_d + 31) / 32;
+                const long long idx = lo_d + (long long)lane * step;
+                const bool lt = idx < hi_d && __ldg(&P.doc_offs[idx]) < blo;
+                const unsigned m = __ballot_sync(FULL_MASK, lt);
+                if (!m) { hi_d = lo_d; break; }
+                const int l = 31 - __clz(m);
+                lo_d = lo_d + (long long)l * step + 1;
+                hi_d = min(hi_d, lo_d - 1 + step);
+            }
+            d = lo_d;
+        }
+        for (long long d0 = d;; d0 += 32) {
+            const long long dd = d0 + lane;
+            bool in = false;
+            if (dd <= (long long)P.n_docs) {
+                const long long s = __ldg(&P.doc_offs[dd]);
+                if (s < (long long)hi * P.tile_bytes || hi == P.n_tiles) in = s >= blo;
+                if (in) {
+                    const long long t = min(s >> (31 - __clz(P.tile_bytes)), (long long)P.n_tiles - 1);  // wt: 2^k
+                    const int k = (int)(t - (long long)lo);
+                    const uint32_t local = (uint32_t)__ldcg(&P.out_offs[dd]);
+                    unsigned long long v = base + C.tb[k] + local;
+                    if (TW_HASDEF(C.tw[k])) v += marker_extra(P, slots + (size_t)k * SLOT, local);
+                    P.out_offs[dd] = (long long)v;
+                }
+            }
+            if (__ballot_sync(FULL_MASK, in) != FULL_MASK) break;
+        }
+    }
 }
 
 // CTA: place the tiles [lo, hi) of round r (unit u = r * grid + blockIdx.x).
@@ -725,49 +809,10 @@ __device__ __noinline__ void place_range(const EncodeParams &P, CtaSmem &C, unsi
         for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(FULL_MASK, base, o);
     }
     if (tid == 0 && nt > 0 && hi == P.n_tiles) P.st->n_ids = base + C.bcast[2];
+    if (P.dbg && tid == 0 && r == 0) P.dbg[36864 + 4 * blockIdx.x + 1] = gtimer();
     for (int k = wid; k < nt; k += NW) place_tile(P, slots + (size_t)k * SLOT, C.tw[k], base + C.tb[k]);
-    // CSR offsets of the documents starting in [lo, hi): tile-local -> global.
-    // One document: its offsets are 0 and the id total, no look-ups needed.
-    if (P.n_docs == 1) {
-        if (tid == 0 && nt > 0) {
-            if (lo == 0) P.out_offs[0] = 0;
-            if (hi == P.n_tiles) P.out_offs[1] = (long long)(base + C.bcast[2]);
-        }
-    } else if (wid == 0 && nt > 0) {
-        const long long blo = (long long)lo * P.tile_bytes;
-        long long d = 0;
-        if (blo > 0) {  // first document with offs >= blo (lower bound)
-            long long lo_d = 0, hi_d = (long long)P.n_docs;  // answer in [lo_d, hi_d]
-            while (hi_d > lo_d) {
-                const long long step = (hi_d - lo_d + 31) / 32;
-                const long long idx = lo_d + (long long)lane * step;
-                const bool lt = idx < hi_d && __ldg(&P.doc_offs[idx]) < blo;
-                const unsigned m = __ballot_sync(FULL_MASK, lt);
-                if (!m) { hi_d = lo_d; break; }
-                const int l = 31 - __clz(m);
-                lo_d = lo_d + (long long)l * step + 1;
-                hi_d = min(hi_d, lo_d - 1 + step);
-            }
-            d = lo_d;
-        }
-        for (long long d0 = d;; d0 += 32) {
-            const long long dd = d0 + lane;
-            bool in = false;
-            if (dd <= (long long)P.n_docs) {
-                const long long s = __ldg(&P.doc_offs[dd]);
-                if (s < (long long)hi * P.tile_bytes || hi == P.n_tiles) in = s >= blo;
-                if (in) {
-                    const long long t = min(s >> (31 - __clz(P.tile_bytes)), (long long)P.n_tiles - 1);  // wt: 2^k
-                    const int k = (int)(t - (long long)lo);
-                    const uint32_t local = (uint32_t)__ldcg(&P.out_offs[dd]);
-                    unsigned long long v = base + C.tb[k] + local;
-                    if (TW_HASDEF(C.tw[k])) v += marker_extra(P, slots + (size_t)k * SLOT, local);
-                    P.out_offs[dd] = (long long)v;
-                }
-            }
-            if (__ballot_sync(FULL_MASK, in) != FULL_MASK) break;
-        }
-    }
+    if (P.dbg && lane == 0 && r == 0) atomicMax(&P.dbg[36864 + 4 * blockIdx.x + 2], gtimer());
+    fix_doc_offsets(P, C, lo, hi, nt, base, slots);
     __syncthreads();
 }
 
@@ -788,8 +833,95 @@ __device__ void grid_sync(EncodeState *st, unsigned int k, unsigned long long *d
     __syncthreads();
 }
 
-// Sum the warps' counters into the CTA, then into the call's global set.
-__device__ void publish_counters(CtaSmem &C, WarpCtx &X, PassCounters *dst) {
+// One-round calls: wait until every tile of the call is done -- per placement
+// range one word (tiles done << 40 | entries), one release add per tile --
+// then C.bcast[0] = the entries of the ranges before this CTA's and
+// C.bcast[3] = the deferred segments recorded (final once every tile is done).
+// This replaces the grid barrier and the prefix over every tile word.
+__device__ void complete_one_round(const EncodeParams &P, CtaSmem &C, unsigned long long q) {
+    if ((threadIdx.x >> 5) == 0) {
+        const int lane = threadIdx.x & 31;
+        const unsigned long long G = gridDim.x, n = P.n_tiles;
+        unsigned long long before;
+        for (;;) {
+            bool ok = true;
+            before = 0;
+#pragma unroll
+            for (int k = 0; k < RNG_MAX / 32; ++k) {
+                const unsigned long long j = (unsigned long long)(lane + 32 * k);
+                if (j < G) {
+                    const unsigned long long v = ld_relaxed(&P.st->rng[j]);
+                    const unsigned long long l = j * q, h = min(n, l + q);
+                    ok &= (v >> 40) == (h > l ? h - l : 0ull);
+                    if (j < blockIdx.x) before += v & ((1ull << 40) - 1);
+                }
+            }
+            if (__all_sync(FULL_MASK, ok)) break;
+            __nanosleep(32);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(FULL_MASK, before, o);
+        if (lane == 0) {
+            __threadfence();  // acquire: the tiles' slots, words and records
+            C.bcast[0] = before;
+            C.bcast[3] = ld_relaxed(&P.st->ndef[0]);
+        }
+    }
+    __syncthreads();
+}
+
+// One-round calls without deferred segments: CTA c places its range [lo, hi)
+// of at most NW tiles.  Every warp loads the range's tile words (one per lane)
+// and, speculatively and in the same round trip, the first entries of its own
+// tile's slot; base = entries of the ranges before (complete_one_round).
+__device__ __noinline__ void place_range_one(const EncodeParams &P, CtaSmem &C, unsigned long long lo,
+                                             unsigned long long hi, unsigned long long base) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int nt = (int)(hi - lo);
+    const uint32_t *slots = P.scratch + lo * SLOT;  // round 0: parity 0, t0 = 0
+    const uint32_t *src = slots + (size_t)wid * SLOT;
+    constexpr int PRE = 5;  // entries per lane fetched before the count is known (wt 128: <= 160)
+    uint32_t pre[PRE];
+    const unsigned long long w = lane < nt ? __ldcg(&P.tiles[lo + lane]) : 0ull;
+    if (wid < nt) {
+#pragma unroll
+        for (int j = 0; j < PRE; ++j) pre[j] = __ldcg(&src[lane + 32 * j]);
+    }
+    const uint32_t e = TW_ENTRIES(w);
+    uint32_t incl = e;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL_MASK, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - e;
+    if (wid == 0) {
+        C.tw[lane] = w;
+        C.tb[lane] = excl;
+        if (lane == 31) C.bcast[2] = incl;
+    }
+    if (wid < nt) {
+        const uint32_t n = __shfl_sync(FULL_MASK, e, wid);
+        const uint32_t off = __shfl_sync(FULL_MASK, excl, wid);
+        uint32_t *dst = P.out_ids + base + off;
+#pragma unroll
+        for (int j = 0; j < PRE; ++j) {
+            const uint32_t k = lane + 32 * j;
+            if (k < n) dst[k] = out_id(P.T, pre[j]);
+        }
+        for (uint32_t k = lane + 32 * PRE; k < n; k += 32) dst[k] = out_id(P.T, __ldcg(&src[k]));
+        if (P.dbg && lane == 0) atomicMax(&P.dbg[36864 + 4 * blockIdx.x + 0], gtimer());
+        __syncwarp();
+        for (uint32_t k = lane; k < (n * 4 + 127) / 128; k += 32) l2_discard(src + 32 * k);
+        if (P.dbg && lane == 0) atomicMax(&P.dbg[36864 + 4 * blockIdx.x + 2], gtimer());
+    }
+    __syncthreads();
+    if (tid == 0 && hi == P.n_tiles) P.st->n_ids = base + C.bcast[2];
+    fix_doc_offsets(P, C, lo, hi, nt, base, slots);
+}
+
+// Warp: its lanes' counters summed into C.red[wid] (part 1 of publish_counters).
+__device__ __forceinline__ void warp_counters(CtaSmem &C, const WarpCtx &X) {
     const int lane = threadIdx.x & 31;
     unsigned long long seg = X.n_segments, memo = X.memo_hits, sm = X.short_merges, ep = X.engine_passes;
 #pragma unroll
@@ -806,26 +938,36 @@ __device__ void publish_counters(CtaSmem &C, WarpCtx &X, PassCounters *dst) {
         C.red[wid][2] = sm;
         C.red[wid][3] = ep;
     }
-    __syncthreads();
-    if (wid == 0) {  // the CTA's sums, then one global add per counter
-        unsigned long long v[4];
+}
+
+// One warp, after a CTA barrier that follows every warp's warp_counters: the
+// CTA's sums, then one global add per counter (part 2).
+__device__ __forceinline__ void cta_counters(CtaSmem &C, PassCounters *dst) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long v[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            v[q] = lane < NW ? C.red[lane][q] : 0ull;
+    for (int q = 0; q < 4; ++q) {
+        v[q] = lane < NW ? C.red[lane][q] : 0ull;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(FULL_MASK, v[q], o);
-        }
-        if (lane == 0) {
-            C.pc.n_segments += v[0];
-            C.pc.memo_hits += v[1];
-            C.pc.short_merges += v[2];
-            C.pc.engine_passes += v[3];
-            const unsigned long long *s = &C.pc.n_segments;
-            unsigned long long *d = &dst->n_segments;
-            for (int i = 0; i < (int)(sizeof(PassCounters) / 8); ++i)
-                if (s[i]) atomicAdd(&d[i], s[i]);
-        }
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(FULL_MASK, v[q], o);
     }
+    if (lane == 0) {
+        C.pc.n_segments += v[0];
+        C.pc.memo_hits += v[1];
+        C.pc.short_merges += v[2];
+        C.pc.engine_passes += v[3];
+        const unsigned long long *s = &C.pc.n_segments;
+        unsigned long long *d = &dst->n_segments;
+        for (int i = 0; i < (int)(sizeof(PassCounters) / 8); ++i)
+            if (s[i]) atomicAdd(&d[i], s[i]);
+    }
+}
+
+// Sum the warps' counters into the CTA, then into the call's global set.
+__device__ void publish_counters(CtaSmem &C, WarpCtx &X, PassCounters *dst) {
+    warp_counters(C, X);
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0) cta_counters(C, dst);
 }
 
 #define REC_GIANT 0xFFFFFFFFu  // record marked by the warp pass: a whole-grid job
@@ -1163,14 +1305,27 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
     CtaSmem &C = *reinterpret_cast<CtaSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     EncodeState *st = P.st;
-    if (blockIdx.x == 0 && tid == 0) {
-        *P.st_next = EncodeState{};
-        P.gscr[4] = 0;  // giants of the round (appended after the round's first grid barrier)
+    if (blockIdx.x == 0) {
+        unsigned long long *z = reinterpret_cast<unsigned long long *>(P.st_next);
+        for (int k = tid; k < (int)(sizeof(EncodeState) / 8); k += NT) z[k] = 0;
+        if (tid == 0) P.gscr[4] = 0;  // giants of the round (appended after the round's first grid barrier)
+    }
+    if (kOneEach && !P.arrive) {  // this warp's tile bytes on their way to L2 while the bitmap loads
+        const unsigned long long t = (unsigned long long)wid * gridDim.x + blockIdx.x;
+        const int lane_ = tid & 31;
+        if (t < P.n_tiles && lane_ * 128 < P.tile_bytes + HALO) {
+            const unsigned long long at = t * (unsigned long long)P.tile_bytes + (unsigned long long)lane_ * 128;
+            if (at < P.n_bytes) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.bytes + at));
+        }
     }
     for (int k = tid; k < 2048; k += NT) C.jb[k] = __ldg(&P.T.jbits[k]);
     for (int k = tid; k < 256; k += NT) C.base[k] = __ldg(&P.T.base[k]);
     if (tid < (int)(sizeof(PassCounters) / 8)) (&C.pc.n_segments)[tid] = 0;
     if (tid < 2) C.seen[tid] = 0;
+    if (tid == 0) {
+        C.arrived = 0;
+        C.poll_lock = 0;
+    }
     __syncthreads();
     if (P.dbg && tid == 0) P.dbg[4 * blockIdx.x] = gtimer();
     WarpSmem &S = C.w[wid];
@@ -1185,14 +1340,38 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
         //      tile per warp: tile = warp rank, interleaved across the SMs (no claim
         //      atomics); otherwise tiles are claimed from the round's counter.
         if constexpr (kOneEach) {
+            // placement ranges of q tiles; a finished tile adds itself to its range's word
+            const bool fast = G <= (unsigned long long)RNG_MAX;
+            const unsigned long long q = (P.n_tiles + G - 1) / G;
             const unsigned long long t = t0 + (unsigned long long)wid * G + blockIdx.x;
             if (t < t1) {
                 const unsigned long long g0 = P.dbg ? gtimer() : 0;
-                encode_tile(P, C, S, t, par * R + (t - t0), X);
+                const uint32_t tw = encode_tile(P, C, S, t, par * R + (t - t0), X);
+                if (fast) {
+                    __syncwarp();
+                    // release (orders the warp's slot, tile word, document offsets and
+                    // records before the add; no L1 invalidation, unlike __threadfence)
+                    if (lane == 0) red_release_add(&st->rng[t / q], (1ull << 40) | TW_ENTRIES(tw));
+                }
                 if (P.dbg && lane == 0 && t < 4096) {
                     P.dbg[1024 + 2 * t] = g0;
                     P.dbg[1024 + 2 * t + 1] = gtimer();
                 }
+            }
+            if (P.dbg_phase_a_only) return;
+            if (fast) {
+                warp_counters(C, X);  // final: summed by warp 1 after the completion barrier
+                complete_one_round(P, C, q);
+                if (P.dbg && tid == 0) P.dbg[4 * blockIdx.x + 2] = gtimer();
+                if (C.bcast[3] == 0) {  // no deferred segments: place and finish
+                    if (wid == 1) cta_counters(C, &st->c);
+                    const unsigned long long lo = min(t1, blockIdx.x * q), hi = min(t1, lo + q);
+                    if (P.dbg && tid == 0) P.dbg[36864 + 4 * blockIdx.x + 1] = gtimer();
+                    if (hi > lo) place_range_one(P, C, lo, hi, C.bcast[0]);
+                    if (P.dbg && tid == 0) P.dbg[4 * blockIdx.x + 3] = gtimer();
+                    return;
+                }
+                // deferred segments: the general path below (every CTA read the same count)
             }
         } else {
             for (;;) {
@@ -1248,6 +1427,7 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
         // one round only: the counters are final here; publishing them before the
         // placement takes their atomics off the kernel's tail
         if constexpr (kOneEach) publish_counters(C, X, &st->c);
+        if (P.dbg && tid == 0 && r == 0) P.dbg[36864 + 4 * blockIdx.x] = gtimer();
         place_range(P, C, r, t0, lo, hi);
         if (ng) {  // giants' ids: one grid-wide copy once their destinations are placed
             grid_sync(st, ++nbar);

@@ -49,6 +49,10 @@ constexpr int SLOT = WT + SHORT_MAX;  // scratch entries per tile (ids of segmen
 #endif
 constexpr int UNIT_MAX = GPUBPE_UNIT_MAX;   // tiles per CTA per round in phase B
 constexpr unsigned int MARK = 0x80000000u;  // scratch entry: deferred record index follows
+constexpr int ARRIVE_MAX = 32;      // pieces of an overlapped host call (arrival words)
+constexpr int ARRIVE_STRIDE = 32;   // u32 words between arrival words (one 128-B line each)
+constexpr int RNG_MAX = 192;                // grids up to this many CTAs complete one-round calls
+                                            // through per-range words instead of a grid barrier
 
 // tile word: bits 0-15 entries, bit 16 has deferred markers, bits 17.. extra ids
 // of the deferred segments beyond their one marker entry
@@ -83,6 +87,7 @@ struct EncodeState {
     unsigned long long n_ids;
     unsigned long long pad2[2];
     PassCounters c;
+    unsigned long long rng[RNG_MAX];  // one-round calls: per placement range, tiles done << 40 | entries
 };
 
 struct DefRec {
@@ -119,6 +124,10 @@ struct EncodeParams {
     unsigned long long *gscr;    // grid-engine scratch: [0..7] scalars, [8..8+2*grid) per-CTA
     uint32_t *glist;             // [rec_cap] giant record indices of the round (count in gscr[4])
     const uint32_t *pretok;      // GPT-2 regex token-start bits (pretok.cu), null in the default mode
+    const unsigned int *arrive;  // overlapped host calls: per-piece arrival words (DMA'd after each
+                                 // piece of the input), else null -- a tile waits for its pieces
+    unsigned long long piece;    // bytes per piece
+    unsigned int arrive_tag;     // value of an arrived piece's word in this call
     unsigned long long *dbg;     // debug timestamps (GPUBPE_DEBUG & 8), else null
     int dbg_phase_a_only;        // GPUBPE_DEBUG & 16: profile phase A alone (output invalid)
 };

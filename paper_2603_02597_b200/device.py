@@ -397,6 +397,29 @@ class DeviceEncoder:
             st = self.query(s)
         return _RESULTS.array(buf, np.uint32, n_ids.value), out_offs, st, float(ms.value)
 
+    def encode_bytes_host(self, doc: bytes, max_seq_len: int, chunk_budget: int):
+        """One document (`bytes`) -> (ids uint32[], offs int64[units + 1], stats,
+        engine_ms), default mode: the latency path as one C call
+        (csrc/hostlist.c encode_one: the document's own buffer, its chunk
+        offsets when len > max_seq_len, gpubpe_encode_host with the GIL
+        released, gpubpe_query).  The current CUDA stream of this device."""
+        n = len(doc)
+        units = 1 if n <= max_seq_len else -(-n // int(chunk_budget))
+        buf = (_RESULTS.take(4 * max(n, 1), self._lib, self.device) if 4 * n <= _POOLED_MAX
+               else _RESULTS.take_pageable(4 * max(n, 1)))
+        out_offs = np.empty(units + 1, dtype=np.int64)
+        hl = _hostlist()
+        if not getattr(hl, "_bound", False):
+            hl.bind(ctypes.cast(self._lib.gpubpe_encode_host, ctypes.c_void_p).value,
+                    ctypes.cast(self._lib.gpubpe_query, ctypes.c_void_p).value)
+            hl._bound = True
+        with self._lock:
+            rc, n_ids, ms, st = hl.encode_one(self._h.value, doc, int(max_seq_len), int(chunk_budget),
+                                              buf.ctypes.data, out_offs.ctypes.data, units,
+                                              torch._C._cuda_getCurrentRawStream(self.device))
+        _native.check(rc, self._h, "gpubpe_encode_host")
+        return (_RESULTS.array(buf, np.uint32, n_ids), out_offs, _native.stats_dict(st), ms)
+
     def encode_packed_host(self, data: np.ndarray, offs: np.ndarray, max_seq_len: int,
                            chunk_budget: int, mode: int = 0):
         """Host CSR in -> host CSR out through gpubpe_encode_host (pinned

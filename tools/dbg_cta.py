@@ -28,3 +28,14 @@ t0 = cta[:, 0].min()
 for k, n in enumerate(["prologue done", "phase A done (warp 0)", "barrier exit", "kernel end"]):
     v = (cta[:, k] - t0) / 1e3
     print("%-24s min %6.1f p50 %6.1f max %6.1f us" % (n, v.min(), np.median(v), v.max()))
+pl = h[36864:36864 + 4 * 148].reshape(148, 4)
+for k, n in enumerate(["ids stored (last warp)", "placement base known", "slots discarded (last)"]):
+    v = (pl[:, k] - t0) / 1e3
+    print("%-24s min %6.1f p50 %6.1f max %6.1f us" % (n, v.min(), np.median(v), v.max()))
+te = h[1024:1024 + 2 * 4096].reshape(4096, 2)
+te = te[te[:, 1] > 0]
+if len(te):
+    v = (te[:, 1] - t0) / 1e3
+    print("%-24s min %6.1f p50 %6.1f max %6.1f us (%d tiles)" % ("tile end", v.min(), np.median(v), v.max(), len(te)))
+    v = (te[:, 0] - t0) / 1e3
+    print("%-24s min %6.1f p50 %6.1f max %6.1f us" % ("tile start", v.min(), np.median(v), v.max()))

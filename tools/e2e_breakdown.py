@@ -30,6 +30,11 @@ def craw():
     enc._lib.gpubpe_encode_host(enc._h, data.ctypes.data, n, offs.ctypes.data, 1, W, W, ids.ctypes.data,
                                 oo.ctypes.data, ctypes.byref(nid), ctypes.byref(ms), s.cuda_stream)
 print("pack_texts          %8.1f us" % t(lambda: pack_texts([doc])))
+ids_pin = bpe.pinned_empty(4 * n).view(np.uint32)
+def craw_pinned():
+    enc._lib.gpubpe_encode_host(enc._h, data.ctypes.data, n, offs.ctypes.data, 1, W, W, ids_pin.ctypes.data,
+                                oo.ctypes.data, ctypes.byref(nid), ctypes.byref(ms), s.cuda_stream)
+print("C encode_host, pinned ids %6.1f us" % t(craw_pinned))
 print("C encode_host       %8.1f us  (kernel %.1f us)" % (t(craw), ms.value * 1000))
 print("encode_packed_host  %8.1f us" % t(lambda: enc.encode_packed_host(data, offs, W, W)))
 print("tokenize_batch      %8.1f us" % t(lambda: bpe.tokenize_batch([doc], tok)))

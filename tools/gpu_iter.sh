@@ -9,3 +9,12 @@ timeout 1200 python -m pytest tests -q -m gpu --timeout 300 ${PYTEST_ARGS:--x} >
 tail -15 gpurun_out/pytest_${TAG}.log
 timeout 600 python tools/perf.py --iters 20 ${PERF_ARGS} --json gpurun_out/perf_${TAG}.json > gpurun_out/perf_${TAG}.log 2>&1; echo "perf rc=$?" >> gpurun_out/perf_${TAG}.log
 cat gpurun_out/perf_${TAG}.log
+if [ -n "$DIAG" ]; then
+  for W in $DIAG; do echo "== $W (L2 flushed)"; FLUSH=1 timeout 120 python tools/dbg_cta.py $W 2>&1 | tail -10; done > gpurun_out/diag_${TAG}.txt 2>&1
+  cat gpurun_out/diag_${TAG}.txt
+fi
+if [ -n "$CYCLES" ]; then
+  make -s -C paper_2603_02597_b200/csrc stamps > /dev/null 2>&1 || echo "stamps build failed"
+  for W in $CYCLES; do echo "== $W tile steps (stamps build, L2 flushed)"; FLUSH=1 timeout 120 python tools/dbg_cycles.py $W 2>&1 | tail -16; done > gpurun_out/cycles_${TAG}.txt 2>&1
+  cat gpurun_out/cycles_${TAG}.txt
+fi
