@@ -809,27 +809,6 @@ class StagePool {
         }
         while (left_.load(std::memory_order_acquire) > 0) cpu_relax();
     }
-    // Background staging in pieces of `piece` bytes: the helpers take pieces
-    // in order while the caller does other work (the kernel launch); the
-    // caller then waits for each piece (wait_piece, taking unclaimed ones
-    // itself) and releases the pool (finish_pieces).  false: the pool is busy.
-    bool start_pieces(uint8_t *dst, const uint8_t *src, size_t n, size_t piece) {
-        const size_t parts = (n + piece - 1) / piece;
-        if (parts > MAXP) return false;
-        std::unique_lock<std::mutex> call(call_, std::try_to_lock);
-        if (!call.owns_lock()) return false;
-        held_ = std::move(call);
-        post(dst, src, n, piece, (unsigned)parts);
-        return true;
-    }
-    void wait_piece(unsigned k) {
-        while (!((done_.load(std::memory_order_acquire) >> k) & 1ull))
-            if (!claim_and_run()) cpu_relax();
-    }
-    void finish_pieces() {
-        while (left_.load(std::memory_order_acquire) > 0) cpu_relax();
-        held_ = std::unique_lock<std::mutex>();
-    }
 
   private:
     static constexpr unsigned MAXP = 40;
@@ -845,7 +824,6 @@ class StagePool {
         src_ = src;
         n_ = n;
         chunk_ = chunk;
-        done_.store(0, std::memory_order_relaxed);
         left_.store((int)parts, std::memory_order_relaxed);
         job_ = (job_ + 1) & 0xFFFF;
         word_.store(((unsigned long long)job_ << 48) | ((unsigned long long)parts << 40), std::memory_order_release);
@@ -863,7 +841,6 @@ class StagePool {
                                             std::memory_order_acquire)) {
                 const size_t lo = std::min(n_, i * chunk_), hi = std::min(n_, lo + chunk_);
                 if (lo < hi) memcpy(dst_ + lo, src_ + lo, hi - lo);
-                done_.fetch_or(1ull << i, std::memory_order_acq_rel);
                 left_.fetch_sub(1, std::memory_order_acq_rel);
                 return true;
             }
@@ -892,12 +869,11 @@ class StagePool {
     std::mutex m_, call_;
     std::condition_variable cv_;
     std::atomic<int> active_{0}, left_{0};
-    std::atomic<unsigned long long> word_{0}, done_{0}, gen_{0};
+    std::atomic<unsigned long long> word_{0}, gen_{0};
     unsigned job_ = 0;
     uint8_t *dst_ = nullptr;
     const uint8_t *src_ = nullptr;
     size_t n_ = 0, chunk_ = 0;
-    std::unique_lock<std::mutex> held_;
 };
 }  // namespace
 

@@ -525,7 +525,7 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
 #pragma unroll 1
         for (uint32_t i = 0; i < nm;) {
             uint32_t k = 1, tot = S.u.a.miss[i] >> 16;
-            if (!strict)
+            if (!strict || GPUBPE_SEQ_ENGINE)  // (the sequential engine is exact for any table)
                 while (i + k < nm && tot + (S.u.a.miss[i + k] >> 16) <= 32) tot += S.u.a.miss[i + k++] >> 16;
 #ifdef GPUBPE_DEBUG_STAMPS
             long long eng_acc[6] = {0, 0, 0, 0, 0, 0};
@@ -537,7 +537,8 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
             }
             c_pass += np_;
 #else
-            c_pass += warp_pack_bpe(T, C.base, sb, S.sid, S.u.a.miss + i, k, strict);
+            if (GPUBPE_SEQ_ENGINE) c_pass += warp_seq_bpe(T, C.base, sb, S.sid, S.u.a.miss + i, k);
+            else c_pass += warp_pack_bpe(T, C.base, sb, S.sid, S.u.a.miss + i, k, strict);
 #endif
             i += k;
         }

@@ -32,6 +32,9 @@
 #include "engine.cuh"
 #include "warp_engine.cuh"
 
+#ifndef GPUBPE_SEQ_ENGINE
+#define GPUBPE_SEQ_ENGINE 1  // memo misses: 1 = warp_seq_bpe, 0 = warp_pack_bpe (multi-merge)
+#endif
 constexpr int WT = 512;         // bytes per warp tile (16 per lane)
 constexpr int HALO = 32;        // bytes staged past the tile: any short segment ends inside
 constexpr int LD = WT + HALO;   // staged bytes

@@ -230,3 +230,106 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
     __syncwarp();
     return np;
 }
+
+// ------------------------------------------------------------------ sequential
+//
+// warp_seq_bpe: the same packs (list[0..k): start | len << 16, sum len <= 32,
+// lane j = token j) merged the reference's own way -- every step merges, in
+// every packed segment, the leftmost pair of minimum rank (engines.py:269-335)
+// -- so it is exact for ANY table, well-formed or not.  Nothing moves between
+// lanes: a merged pair's right token just dies (alive mask L), a token's right
+// neighbour is the next live lane, and only the winner and the live token
+// before it re-probe (two probes in flight per step).  A step is a segmented
+// min, two ballots and one probe round, against the multi-merge pass's walks,
+// compaction shuffles and rl/rr loads; its latency (one dependent probe) is
+// what the tail of a latency-bound call waits for.  Returns the steps run.
+static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base, const uint32_t *sbw,
+                                        uint32_t *sid, const uint32_t *list, uint32_t k) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t ent_l = lane < k ? list[lane] : 0u;
+    const uint32_t len_l = ent_l >> 16;
+    uint32_t off = len_l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL_MASK, off, o);
+        if (lane >= (uint32_t)o) off += y;
+    }
+    const uint32_t total = __shfl_sync(FULL_MASK, off, 31);
+    off -= len_l;  // first lane of segment `lane`
+    const uint32_t heads = __reduce_or_sync(FULL_MASK, lane < k ? (1u << off) : 0u);
+    const bool valid = lane < total;
+    const uint32_t le = (lane >= 31) ? 0xFFFFFFFFu : ((2u << lane) - 1);
+    const uint32_t seg = (uint32_t)__popc(heads & le) - 1;
+    const uint32_t f = 31 - __clz(heads & le);               // first lane of my segment
+    const uint32_t ha = heads & ~le;
+    const uint32_t send = ha ? (uint32_t)(__ffs(ha) - 1) : total;  // one past my segment's last lane
+    const uint32_t ent = __shfl_sync(FULL_MASK, ent_l, seg & 31);
+    const uint32_t p0 = ent & 0xFFFFu;
+    uint32_t tok = valid ? base[sb_byte(sbw, p0 + lane - f)] : 0u;
+    uint32_t L = __ballot_sync(FULL_MASK, valid);  // live tokens
+    uint32_t rk = GPUBPE_INF, nw = 0;
+    {
+        const uint32_t t1 = __shfl_down_sync(FULL_MASK, tok, 1);
+        if (valid && lane + 1 < send) {
+            const PairHit h = probe_pair(T, tok, t1);
+            rk = h.rank;
+            nw = h.nw;
+        }
+    }
+    const uint32_t fmask = ~((1u << f) - 1);  // lanes >= f
+    const bool head = (heads >> lane) & 1u;
+    uint32_t steps = 0;
+    for (;;) {
+        const bool alive = (L >> lane) & 1u;
+        const bool live = alive && rk != GPUBPE_INF;
+        if (!__any_sync(FULL_MASK, live)) break;
+        ++steps;
+        uint32_t m;
+        if (k == 1) {
+            m = __reduce_min_sync(FULL_MASK, live ? rk : GPUBPE_INF);
+        } else {  // forward segmented min (head flag in bit 31), read at the segment's last lane
+            uint32_t x = (live ? min(rk, 0x7FFFFFFFu) : 0x7FFFFFFFu) | ((head || !valid) ? 0x80000000u : 0u);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL_MASK, x, o);
+                if (lane >= (uint32_t)o && !(x >> 31)) x = min(x, y & 0x7FFFFFFFu) | (y & 0x80000000u);
+            }
+            const uint32_t sm = __shfl_sync(FULL_MASK, x, valid ? send - 1 : lane) & 0x7FFFFFFFu;
+            m = sm == 0x7FFFFFFFu ? GPUBPE_INF : sm;
+        }
+        // the leftmost candidate of each segment merges with the next live token
+        const unsigned cand = __ballot_sync(FULL_MASK, live && rk == m);
+        const unsigned mine = cand & fmask;
+        const bool win = live && rk == m && (uint32_t)(__ffs(mine) - 1) == lane;
+        const unsigned W = __ballot_sync(FULL_MASK, win);
+        const unsigned before = L & ((1u << lane) - 1);  // live lanes before me
+        const int pl = before ? 31 - __clz(before) : -1;
+        const bool dies = alive && pl >= 0 && ((W >> pl) & 1u);  // my left neighbour merged me in
+        if (win) tok = nw;
+        L &= ~__ballot_sync(FULL_MASK, dies);
+        // new right neighbours: the winners' and the tokens just before the winners
+        const unsigned after = L & ~le;
+        const uint32_t rn = after ? (uint32_t)(__ffs(after) - 1) : 32u;
+        const uint32_t rt = __shfl_sync(FULL_MASK, tok, rn & 31);
+        const bool still = (L >> lane) & 1u;
+        if (still && (win || (rn < 32 && ((W >> rn) & 1u)))) {
+            if (rn < send) {
+                const PairHit h = probe_pair(T, tok, rt);
+                rk = h.rank;
+                nw = h.nw;
+            } else {
+                rk = GPUBPE_INF;
+            }
+        }
+        if (!still) rk = GPUBPE_INF;
+    }
+    // write back: each segment's live tokens in order, the first tagged with the count
+    if ((L >> lane) & 1u) sid[SI(p0 + __popc(L & fmask & ((1u << lane) - 1)))] = tok;
+    __syncwarp();
+    if (valid && head) {
+        const uint32_t smask = (send >= 32 ? 0xFFFFFFFFu : ((1u << send) - 1)) & fmask;
+        sid[SI(p0)] |= (uint32_t)__popc(L & smask) << 24;
+    }
+    __syncwarp();
+    return steps;
+}
