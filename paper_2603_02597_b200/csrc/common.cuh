@@ -2,9 +2,9 @@
 //
 // Layout in HBM (built once per context by ctx.cu, L2-resident afterwards):
 //   pair table   uint4 slots {left, right, rank, new}, power-of-two capacity at
-//                <= 50% load, fmix64 hash of (left<<32)|right, linear probing.
-//                Same hash family as the reference (merge_table.py:49-57) but a
-//                single 16-byte slot per probe instead of two 8-byte arrays.
+//                <= 50% load, two-choice cuckoo: the two halves of fmix64 of
+//                (left<<32)|right (the reference's hash, merge_table.py:49-57)
+//                pick the two slots a rule may sit in (pair_slots).
 //   rl / rr      per internal id: min rank of any rule with the id as LEFT /
 //                RIGHT operand (INF if none) -- the blocking test of the exact
 //                multi-merge pass.
@@ -47,8 +47,16 @@ __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t x) {
     return x;
 }
 
-__host__ __device__ __forceinline__ uint32_t pair_home(uint32_t l, uint32_t r, uint32_t mask) {
-    return (uint32_t)(fmix64(((uint64_t)l << 32) | r) & mask);
+// Two-choice cuckoo slots of a pair: the low and high halves of one fmix64 of
+// (left << 32) | right (the reference's key and hash, merge_table.py:49-57).
+// Every rule sits in one of its two slots, so a probe is two independent
+// 16-byte loads -- one round trip for hits and misses alike, no chains.
+struct PairSlots {
+    uint32_t a, b;
+};
+__host__ __device__ __forceinline__ PairSlots pair_slots(uint32_t l, uint32_t r, uint32_t mask) {
+    const uint64_t h = fmix64(((uint64_t)l << 32) | r);
+    return PairSlots{(uint32_t)h & mask, (uint32_t)(h >> 32) & mask};
 }
 
 // Memo hash over a byte string given as 8-byte little-endian chunks.
@@ -77,13 +85,12 @@ struct PairHit {
 };
 
 __device__ __forceinline__ PairHit probe_pair(const DevTables &T, uint32_t l, uint32_t r) {
-    uint32_t i = pair_home(l, r, T.pair_mask);
-    for (;;) {
-        uint4 s = __ldg(&T.pairs[i]);
-        if (s.x == l && s.y == r) return PairHit{s.z, s.w};
-        if (s.x == GPUBPE_INF && s.y == GPUBPE_INF) return PairHit{GPUBPE_INF, 0};
-        i = (i + 1) & T.pair_mask;
-    }
+    const PairSlots ps = pair_slots(l, r, T.pair_mask);
+    const uint4 a = __ldg(&T.pairs[ps.a]);
+    const uint4 b = __ldg(&T.pairs[ps.b]);
+    if (a.x == l && a.y == r) return PairHit{a.z, a.w};
+    if (b.x == l && b.y == r) return PairHit{b.z, b.w};
+    return PairHit{GPUBPE_INF, 0};
 }
 
 __device__ __forceinline__ bool is_junction(const uint32_t *jb, uint32_t x, uint32_t y) {

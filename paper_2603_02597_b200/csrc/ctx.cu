@@ -269,23 +269,40 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
         return bail(fail(ctx, GPUBPE_EINVAL, "more than 2^24 distinct token ids (%llu)", (unsigned long long)n_ids));
 
     BUILD_STAMP(1);
-    // ---- pair table
+    // ---- pair table: two-choice cuckoo (common.cuh pair_slots) at <= 50% load;
+    //      an insertion that cannot settle doubles the capacity and starts over
     uint64_t cap = 2;
     while (cap < 2 * n_rules) cap <<= 1;
-    std::vector<uint4> slots(cap, make_uint4(GPUBPE_INF, GPUBPE_INF, 0, 0));
-    for (uint64_t i = 0; i < n_rules; ++i) {
-        uint32_t h = pair_home(L[i], R[i], (uint32_t)(cap - 1));
-        for (;;) {
-            uint4 &sl = slots[h];
-            if (sl.x == GPUBPE_INF && sl.y == GPUBPE_INF) {
-                sl = make_uint4(L[i], R[i], rank[i], NW[i]);
-                break;
+    std::vector<uint4> slots;
+    for (;;) {
+        slots.assign(cap, make_uint4(GPUBPE_INF, GPUBPE_INF, 0, 0));
+        const uint32_t mask = (uint32_t)(cap - 1);
+        auto empty = [](const uint4 &v) { return v.x == GPUBPE_INF && v.y == GPUBPE_INF; };
+        bool settled = true;
+        for (uint64_t i = 0; i < n_rules && settled; ++i) {
+            const PairSlots ps = pair_slots(L[i], R[i], mask);
+            for (uint32_t h : {ps.a, ps.b})
+                if (slots[h].x == L[i] && slots[h].y == R[i])
+                    return bail(fail(ctx, GPUBPE_ETABLE, "pair (%u, %u) duplicated at rank %u",
+                                     left[i], right[i], rank[i]));
+            uint4 cur = make_uint4(L[i], R[i], rank[i], NW[i]);
+            uint32_t pos = empty(slots[ps.a]) || !empty(slots[ps.b]) ? ps.a : ps.b;
+            for (int kick = 0;; ++kick) {
+                if (empty(slots[pos])) {
+                    slots[pos] = cur;
+                    break;
+                }
+                if (kick == 512) {
+                    settled = false;
+                    break;
+                }
+                std::swap(cur, slots[pos]);  // the evicted rule moves to its other slot
+                const PairSlots q = pair_slots(cur.x, cur.y, mask);
+                pos = pos == q.a ? q.b : q.a;
             }
-            if (sl.x == L[i] && sl.y == R[i])
-                return bail(fail(ctx, GPUBPE_ETABLE, "pair (%u, %u) duplicated at rank %u",
-                                 left[i], right[i], rank[i]));
-            h = (h + 1) & (uint32_t)(cap - 1);
         }
+        if (settled) break;
+        cap <<= 1;
     }
     BUILD_STAMP(2);
     // ---- rl / rr and well-formedness
@@ -600,6 +617,8 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.arrive = ctx->cur_arrive;
         P.piece = ctx->cur_piece ? ctx->cur_piece : 1;
         P.arrive_tag = ctx->arrive_tag;
+        static const int pf_env = getenv("GPUBPE_PREFETCH") ? atoi(getenv("GPUBPE_PREFETCH")) : 1;
+        P.prefetch_tables = pf_env;
         P.gscr = static_cast<unsigned long long *>(ctx->ws_gscr.p);
         P.glist = static_cast<uint32_t *>(ctx->ws_glist.p);
         ctx->last_n_tiles = n_tiles;

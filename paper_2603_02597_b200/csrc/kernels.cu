@@ -529,7 +529,8 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
                 while (i + k < nm && tot + (S.u.a.miss[i + k] >> 16) <= 32) tot += S.u.a.miss[i + k++] >> 16;
 #ifdef GPUBPE_DEBUG_STAMPS
             long long eng_acc[6] = {0, 0, 0, 0, 0, 0};
-            const uint32_t np_ = warp_pack_bpe(T, C.base, sb, S.sid, S.u.a.miss + i, k, strict, eng_acc);
+            const uint32_t np_ = GPUBPE_SEQ_ENGINE ? warp_seq_bpe(T, C.base, sb, S.sid, S.u.a.miss + i, k, eng_acc)
+                                                   : warp_pack_bpe(T, C.base, sb, S.sid, S.u.a.miss + i, k, strict, eng_acc);
             if (P.dbg && lane == 0) {
                 for (int q = 0; q < 6; ++q) atomicAdd(&P.dbg[32768 + q], (unsigned long long)eng_acc[q]);
                 atomicAdd(&P.dbg[32768 + 6], (unsigned long long)np_);
@@ -1317,6 +1318,20 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
         if (t < P.n_tiles && lane_ * 128 < P.tile_bytes + HALO) {
             const unsigned long long at = t * (unsigned long long)P.tile_bytes + (unsigned long long)lane_ * 128;
             if (at < P.n_bytes) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.bytes + at));
+        }
+    }
+    if (kOneEach && P.prefetch_tables) {
+        // latency calls: every CTA pulls its slice of the pair table and the memo
+        // into L2 (a few hundred 128-B lines each), so the probes on the tail's
+        // critical path (the memo misses' merge steps) hit L2, not DRAM
+        const unsigned long long np = ((unsigned long long)P.T.pair_mask + 1) * 16 / 128;
+        const unsigned long long nm = P.T.memo ? ((unsigned long long)P.T.memo_mask + 1) * 16 / 128 : 0;
+        const unsigned long long per = (np + nm + gridDim.x - 1) / gridDim.x;
+        const unsigned long long l = (unsigned long long)blockIdx.x * per + tid;
+        if (tid < per) {
+            if (l < np) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(reinterpret_cast<const char *>(P.T.pairs) + 128 * l));
+            else if (l < np + nm)
+                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(reinterpret_cast<const char *>(P.T.memo) + 128 * (l - np)));
         }
     }
     for (int k = tid; k < 2048; k += NT) C.jb[k] = __ldg(&P.T.jbits[k]);

@@ -244,8 +244,13 @@ static __device__ uint32_t warp_pack_bpe(const DevTables &T, const uint32_t *bas
 // compaction shuffles and rl/rr loads; its latency (one dependent probe) is
 // what the tail of a latency-bound call waits for.  Returns the steps run.
 static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base, const uint32_t *sbw,
-                                        uint32_t *sid, const uint32_t *list, uint32_t k) {
+                                        uint32_t *sid, const uint32_t *list, uint32_t k,
+                                        long long *eng_acc = nullptr) {
     const uint32_t lane = threadIdx.x & 31;
+#ifdef GPUBPE_DEBUG_STAMPS
+    long long eng_prev;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(eng_prev));
+#endif
     const uint32_t ent_l = lane < k ? list[lane] : 0u;
     const uint32_t len_l = ent_l >> 16;
     uint32_t off = len_l;
@@ -279,6 +284,8 @@ static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base
     const uint32_t fmask = ~((1u << f) - 1);  // lanes >= f
     const bool head = (heads >> lane) & 1u;
     uint32_t steps = 0;
+    (void)__any_sync(FULL_MASK, rk == 0);  // (stamps: wait for the probes)
+    ENG_MARK(0);
     for (;;) {
         const bool alive = (L >> lane) & 1u;
         const bool live = alive && rk != GPUBPE_INF;
@@ -297,6 +304,7 @@ static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base
             const uint32_t sm = __shfl_sync(FULL_MASK, x, valid ? send - 1 : lane) & 0x7FFFFFFFu;
             m = sm == 0x7FFFFFFFu ? GPUBPE_INF : sm;
         }
+        ENG_MARK(1);
         // the leftmost candidate of each segment merges with the next live token
         const unsigned cand = __ballot_sync(FULL_MASK, live && rk == m);
         const unsigned mine = cand & fmask;
@@ -307,11 +315,14 @@ static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base
         const bool dies = alive && pl >= 0 && ((W >> pl) & 1u);  // my left neighbour merged me in
         if (win) tok = nw;
         L &= ~__ballot_sync(FULL_MASK, dies);
+        ENG_MARK(2);
         // new right neighbours: the winners' and the tokens just before the winners
         const unsigned after = L & ~le;
         const uint32_t rn = after ? (uint32_t)(__ffs(after) - 1) : 32u;
         const uint32_t rt = __shfl_sync(FULL_MASK, tok, rn & 31);
         const bool still = (L >> lane) & 1u;
+        (void)__any_sync(FULL_MASK, rt == 0);
+        ENG_MARK(3);
         if (still && (win || (rn < 32 && ((W >> rn) & 1u)))) {
             if (rn < send) {
                 const PairHit h = probe_pair(T, tok, rt);
@@ -322,6 +333,8 @@ static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base
             }
         }
         if (!still) rk = GPUBPE_INF;
+        (void)__any_sync(FULL_MASK, rk == 0);
+        ENG_MARK(4);
     }
     // write back: each segment's live tokens in order, the first tagged with the count
     if ((L >> lane) & 1u) sid[SI(p0 + __popc(L & fmask & ((1u << lane) - 1)))] = tok;

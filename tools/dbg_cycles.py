@@ -43,7 +43,9 @@ p1 = st[:, 7] - st[:, 1]; p2 = st[:, 2] - st[:, 7]
 print("segments pass1 p50 %7.0f p90 %7.0f | pass2 p50 %7.0f p90 %7.0f" % (*np.percentile(p1, [50, 90]), *np.percentile(p2, [50, 90])))
 eng = h[32768:32776]
 if eng[7]:
-    names = ["setup+probe0", "seg scan", "segmin+runs", "walks", "compaction", "re-probe"]
+    names = (["setup+probe0", "segmented min", "winners+deaths", "neighbour shfl", "probes", "-"]
+             if os.environ.get("SEQ", "1") == "1" else
+             ["setup+probe0", "seg scan", "segmin+runs", "walks", "compaction", "re-probe"])
     print("warp engine: %d packs, %d passes (%.1f per pack)" % (eng[7], eng[6], eng[6] / eng[7]))
     for q, n in enumerate(names):
         print("  %-14s %8.0f cycles per pack  %6.0f per pass" % (n, eng[q] / eng[7], eng[q] / max(eng[6], 1)))
