@@ -617,8 +617,6 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.arrive = ctx->cur_arrive;
         P.piece = ctx->cur_piece ? ctx->cur_piece : 1;
         P.arrive_tag = ctx->arrive_tag;
-        static const int pf_env = getenv("GPUBPE_PREFETCH") ? atoi(getenv("GPUBPE_PREFETCH")) : 1;
-        P.prefetch_tables = pf_env;
         P.gscr = static_cast<unsigned long long *>(ctx->ws_gscr.p);
         P.glist = static_cast<uint32_t *>(ctx->ws_glist.p);
         ctx->last_n_tiles = n_tiles;

@@ -1320,20 +1320,6 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
             if (at < P.n_bytes) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.bytes + at));
         }
     }
-    if (kOneEach && P.prefetch_tables) {
-        // latency calls: every CTA pulls its slice of the pair table and the memo
-        // into L2 (a few hundred 128-B lines each), so the probes on the tail's
-        // critical path (the memo misses' merge steps) hit L2, not DRAM
-        const unsigned long long np = ((unsigned long long)P.T.pair_mask + 1) * 16 / 128;
-        const unsigned long long nm = P.T.memo ? ((unsigned long long)P.T.memo_mask + 1) * 16 / 128 : 0;
-        const unsigned long long per = (np + nm + gridDim.x - 1) / gridDim.x;
-        const unsigned long long l = (unsigned long long)blockIdx.x * per + tid;
-        if (tid < per) {
-            if (l < np) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(reinterpret_cast<const char *>(P.T.pairs) + 128 * l));
-            else if (l < np + nm)
-                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(reinterpret_cast<const char *>(P.T.memo) + 128 * (l - np)));
-        }
-    }
     for (int k = tid; k < 2048; k += NT) C.jb[k] = __ldg(&P.T.jbits[k]);
     for (int k = tid; k < 256; k += NT) C.base[k] = __ldg(&P.T.base[k]);
     if (tid < (int)(sizeof(PassCounters) / 8)) (&C.pc.n_segments)[tid] = 0;

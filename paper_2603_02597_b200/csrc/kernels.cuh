@@ -130,7 +130,6 @@ struct EncodeParams {
     const unsigned int *arrive;  // overlapped host calls: per-piece arrival words (DMA'd after each
                                  // piece of the input), else null -- a tile waits for its pieces
     unsigned long long piece;    // bytes per piece
-    int prefetch_tables;         // one-round calls: L2 prefetch of the pair table and memo
     unsigned int arrive_tag;     // value of an arrived piece's word in this call
     unsigned long long *dbg;     // debug timestamps (GPUBPE_DEBUG & 8), else null
     int dbg_phase_a_only;        // GPUBPE_DEBUG & 16: profile phase A alone (output invalid)

@@ -310,20 +310,20 @@ static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base
         const unsigned mine = cand & fmask;
         const bool win = live && rk == m && (uint32_t)(__ffs(mine) - 1) == lane;
         const unsigned W = __ballot_sync(FULL_MASK, win);
-        const unsigned before = L & ((1u << lane) - 1);  // live lanes before me
-        const int pl = before ? 31 - __clz(before) : -1;
-        const bool dies = alive && pl >= 0 && ((W >> pl) & 1u);  // my left neighbour merged me in
+        // each winner's right neighbour dies: the next live lane above it, found
+        // for every winner at once by a carry through the dead lanes of ~L
+        L &= ~((~L + (W << 1)) & L);
         if (win) tok = nw;
-        L &= ~__ballot_sync(FULL_MASK, dies);
         ENG_MARK(2);
         // new right neighbours: the winners' and the tokens just before the winners
         const unsigned after = L & ~le;
         const uint32_t rn = after ? (uint32_t)(__ffs(after) - 1) : 32u;
-        const uint32_t rt = __shfl_sync(FULL_MASK, tok, rn & 31);
         const bool still = (L >> lane) & 1u;
+        const bool before_win = rn < 32 && ((W >> rn) & 1u);
+        const uint32_t rt = __shfl_sync(FULL_MASK, tok, rn & 31);
         (void)__any_sync(FULL_MASK, rt == 0);
         ENG_MARK(3);
-        if (still && (win || (rn < 32 && ((W >> rn) & 1u)))) {
+        if (still && (win || before_win)) {
             if (rn < send) {
                 const PairHit h = probe_pair(T, tok, rt);
                 rk = h.rank;
