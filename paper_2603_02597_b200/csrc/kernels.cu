@@ -169,20 +169,19 @@ __device__ long long cta_first_nonjunction(const EncodeParams &P, const uint32_t
     return hi;
 }
 
-// Cut bits of the 16 positions of group g (position k: cut before byte k).
-__device__ __forceinline__ uint32_t group_cuts(const uint32_t *jb, const uint32_t *sbw, int g,
-                                               uint32_t prevb) {
-    uint32_t x = g ? sb_byte(sbw, 16 * g - 1) : prevb;
-    const uint32_t w[4] = {sbw[SW(4 * g)], sbw[SW(4 * g + 1)], sbw[SW(4 * g + 2)], sbw[SW(4 * g + 3)]};
+// Cut bits of the 8 positions of group g (position k: cut before byte 8g + k).
+__device__ __forceinline__ uint32_t group8_cuts(const uint32_t *jb, const uint32_t *sbw, int g, uint32_t prevb) {
+    uint32_t x = g ? sb_byte(sbw, 8 * g - 1) : prevb;
+    const uint32_t w[2] = {sbw[SW(2 * g)], sbw[SW(2 * g + 1)]};
     uint32_t m = 0;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < 8; ++k) {
         const uint32_t y = (w[k >> 2] >> (8 * (k & 3))) & 0xFFu;
         const uint32_t idx = (x << 8) | y;
         m |= ((jb[idx >> 5] >> (idx & 31)) & 1u) << k;
         x = y;
     }
-    return ~m & 0xFFFFu;
+    return ~m & 0xFFu;
 }
 
 // First cut in [q, lim], lim - q < 32; -1 if none.
@@ -381,25 +380,26 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
     TSTAMP(0, sb[SW(4 * lane)] + prevb);
 
     // ---- 2. cut bits: junction misses, start and end of input
+    //         (8 positions per lane, so small tiles use 20 lanes, not 10; four
+    //         lanes' bytes make one word; one zero word past the staged bytes)
     {
-        const int ng = ld / 16;
-        uint32_t m[2] = {0u, 0u};
+        const int ng = ld / 8;
 #pragma unroll 1
-        for (int g = lane, i = 0; g < ng; g += 32, ++i) {
-            uint32_t mg = group_cuts(C.jb, sb, g, prevb);
-            const int p0 = 16 * g;
-            if (p0 >= nst) mg = 0;
-            else if (p0 + 16 > nst) mg &= (1u << (nst - p0)) - 1;
-            if (a + nst == N && nst >= p0 && nst < p0 + 16) mg |= 1u << (nst - p0);
-            if (g == 0 && a == 0) mg |= 1u;
-            if (i == 0) m[0] = mg; else m[1] = mg;
-        }
-        const uint32_t n0 = __shfl_down_sync(FULL_MASK, m[0], 1);
-        const uint32_t nh = __shfl_down_sync(FULL_MASK, m[1], 1);
-        if (!(lane & 1)) S.cm[lane >> 1] = (m[0] & 0xFFFFu) | (n0 << 16);
-        if (lane == 0) {
-            S.cm[16] = (m[1] & 0xFFFFu) | (nh << 16);
-            S.cm[17] = 0;
+        for (int i = 0; 32 * i < ng + 4; ++i) {
+            const int g = lane + 32 * i;
+            uint32_t mg = 0;
+            if (g < ng) {
+                mg = group8_cuts(C.jb, sb, g, prevb);
+                const int p0 = 8 * g;
+                if (p0 >= nst) mg = 0;
+                else if (p0 + 8 > nst) mg &= (1u << (nst - p0)) - 1;
+                if (a + nst == N && nst >= p0 && nst < p0 + 8) mg |= 1u << (nst - p0);
+                if (g == 0 && a == 0) mg |= 1u;
+            }
+            uint32_t v = mg << (8 * (lane & 3));
+            v |= __shfl_xor_sync(FULL_MASK, v, 1);
+            v |= __shfl_xor_sync(FULL_MASK, v, 2);
+            if (!(lane & 3) && (g >> 2) < NGRP / 2 + 1) S.cm[g >> 2] = v;
         }
     }
     __syncwarp();

@@ -284,7 +284,9 @@ static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base
     const uint32_t fmask = ~((1u << f) - 1);  // lanes >= f
     const bool head = (heads >> lane) & 1u;
     uint32_t steps = 0;
+#ifdef GPUBPE_DEBUG_STAMPS
     (void)__any_sync(FULL_MASK, rk == 0);  // (stamps: wait for the probes)
+#endif
     ENG_MARK(0);
     for (;;) {
         const bool alive = (L >> lane) & 1u;
@@ -294,6 +296,12 @@ static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base
         uint32_t m;
         if (k == 1) {
             m = __reduce_min_sync(FULL_MASK, live ? rk : GPUBPE_INF);
+        } else if (k <= 4) {  // one reduction per segment
+            m = GPUBPE_INF;
+            for (uint32_t q = 0; q < k; ++q) {
+                const uint32_t v = __reduce_min_sync(FULL_MASK, (live && seg == q) ? rk : GPUBPE_INF);
+                if (seg == q) m = v;
+            }
         } else {  // forward segmented min (head flag in bit 31), read at the segment's last lane
             uint32_t x = (live ? min(rk, 0x7FFFFFFFu) : 0x7FFFFFFFu) | ((head || !valid) ? 0x80000000u : 0u);
 #pragma unroll
@@ -321,7 +329,9 @@ static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base
         const bool still = (L >> lane) & 1u;
         const bool before_win = rn < 32 && ((W >> rn) & 1u);
         const uint32_t rt = __shfl_sync(FULL_MASK, tok, rn & 31);
+#ifdef GPUBPE_DEBUG_STAMPS
         (void)__any_sync(FULL_MASK, rt == 0);
+#endif
         ENG_MARK(3);
         if (still && (win || before_win)) {
             if (rn < send) {
@@ -333,7 +343,9 @@ static __device__ uint32_t warp_seq_bpe(const DevTables &T, const uint32_t *base
             }
         }
         if (!still) rk = GPUBPE_INF;
+#ifdef GPUBPE_DEBUG_STAMPS
         (void)__any_sync(FULL_MASK, rk == 0);
+#endif
         ENG_MARK(4);
     }
     // write back: each segment's live tokens in order, the first tagged with the count
