@@ -105,6 +105,8 @@ struct gpubpe_ctx {
     const unsigned int *cur_arrive = nullptr;  // for the encode being launched
     uint64_t cur_piece = 0;
     unsigned long long *dbg_buf = nullptr;  // GPUBPE_DEBUG & 8 timestamps
+    StateMirror *h_mirror = nullptr, *d_mirror = nullptr;  // host calls: the kernel's results (mapped)
+    StateMirror *cur_mirror = nullptr;                     // for the encode being launched
     std::chrono::steady_clock::time_point t_call;  // GPUBPE_HOSTTIME: gpubpe_encode entry
     int tl_n = 0;                                  // GPUBPE_HOSTTIME=2: piece events of this call
     cudaEvent_t *tl_ev = nullptr;
@@ -617,6 +619,7 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.arrive = ctx->cur_arrive;
         P.piece = ctx->cur_piece ? ctx->cur_piece : 1;
         P.arrive_tag = ctx->arrive_tag;
+        P.mirror = ctx->cur_mirror;
         P.gscr = static_cast<unsigned long long *>(ctx->ws_gscr.p);
         P.glist = static_cast<uint32_t *>(ctx->ws_glist.p);
         ctx->last_n_tiles = n_tiles;
@@ -804,12 +807,15 @@ class StagePool {
         return *p;
     }
     void begin() {
-        if (active_.fetch_add(1) == 0) {
+        if (active_.fetch_add(1) == 0 && sleeping_.load(std::memory_order_acquire) > 0) {
             std::lock_guard<std::mutex> g(m_);
             cv_.notify_all();
         }
     }
-    void end() { active_.fetch_sub(1); }
+    void end() {
+        last_end_.store(now_ns(), std::memory_order_relaxed);
+        active_.fetch_sub(1, std::memory_order_release);
+    }
     // memcpy split in (workers + 1) parts, the caller working too
     void copy(uint8_t *dst, const uint8_t *src, size_t n) {
         const unsigned parts = (unsigned)th_.size() + 1;
@@ -832,7 +838,7 @@ class StagePool {
     static constexpr unsigned long long BITS = (1ull << MAXP) - 1;
     StagePool() {
         const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-        const unsigned nw = std::min(3u, hw / 4);
+        const unsigned nw = std::min(7u, hw / 2 > 0 ? hw / 2 - 1 : 0u);  // host copies scale to ~8 threads
         for (unsigned i = 0; i < nw; ++i) th_.emplace_back([this] { loop(); });
         for (auto &t : th_) t.detach();
     }
@@ -863,14 +869,28 @@ class StagePool {
             }
         }
     }
+    static unsigned long long now_ns() {
+        return (unsigned long long)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                   std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
+    // Workers spin inside host calls and for a grace period after the last one
+    // (GPUBPE_SPIN_US, default 200 us), so back-to-back calls find them awake
+    // (a condition-variable wake-up costs several microseconds); then they sleep.
     void loop() {
+        static const unsigned long long grace =
+            1000ull * (unsigned long long)(getenv("GPUBPE_SPIN_US") ? atoll(getenv("GPUBPE_SPIN_US")) : 200);
         unsigned long long seen = 0;
         for (;;) {
             {
                 std::unique_lock<std::mutex> g(m_);
+                sleeping_.fetch_add(1);
                 cv_.wait(g, [&] { return active_.load() > 0; });
+                sleeping_.fetch_sub(1);
             }
-            while (active_.load(std::memory_order_acquire) > 0) {  // spin only inside a host call
+            for (unsigned spins = 0;; ++spins) {
+                if (active_.load(std::memory_order_acquire) == 0 && (spins & 1023) == 0 &&
+                    now_ns() - last_end_.load(std::memory_order_relaxed) > grace)
+                    break;
                 const unsigned long long gen = gen_.load(std::memory_order_acquire);
                 if (gen == seen) {
                     cpu_relax();
@@ -885,8 +905,8 @@ class StagePool {
     std::vector<std::thread> th_;
     std::mutex m_, call_;
     std::condition_variable cv_;
-    std::atomic<int> active_{0}, left_{0};
-    std::atomic<unsigned long long> word_{0}, gen_{0};
+    std::atomic<int> active_{0}, left_{0}, sleeping_{0};
+    std::atomic<unsigned long long> word_{0}, gen_{0}, last_end_{0};
     unsigned job_ = 0;
     uint8_t *dst_ = nullptr;
     const uint8_t *src_ = nullptr;
@@ -1242,6 +1262,19 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
     if ((rc = ensure_pinned(ctx, need))) return rc;
     if (!ctx->io_ev[0])
         for (auto &e : ctx->io_ev) CK(cudaEventCreate(&e));
+    if (!ctx->h_mirror) {
+        CK(cudaHostAlloc(reinterpret_cast<void **>(&ctx->h_mirror), sizeof(StateMirror), cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ctx->d_mirror), ctx->h_mirror, 0));
+        ++ctx->n_allocs;
+    }
+    // the kernel's last CTA writes the results here (kernels.cu kernel_exit): no D2H copy
+    volatile StateMirror *mir = ctx->h_mirror;
+    mir->n_ids = ~0ull;  // (sentinel: a kernel that did not write falls back to a copy)
+    ctx->cur_mirror = ctx->d_mirror;
+    struct MirrorOff {
+        gpubpe_ctx *c;
+        ~MirrorOff() { c->cur_mirror = nullptr; }
+    } mirror_off{ctx};
     uint8_t *pin = ctx->pin;
     uint8_t *dv = nullptr;  // device copy of the same layout (modes 0 and 2)
     if (mode != 1) {
@@ -1288,13 +1321,23 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         memcpy(pin + o_doffs, h_doc_offs, offs_b);
         CK(cudaMemcpyAsync(dv + o_doffs, pin + o_doffs, offs_b, cudaMemcpyHostToDevice, ctx->s_copy));
         const unsigned n_pieces = (unsigned)((n_bytes + ov_piece - 1) / ov_piece);
+        static const bool ovt = getenv("GPUBPE_HOSTTIME") && atoi(getenv("GPUBPE_HOSTTIME")) == 3;
+        static cudaEvent_t oev[3];
+        if (ovt && !oev[0])
+            for (auto &e : oev) cudaEventCreate(&e);
+        auto th0 = now();
+        if (ovt) cudaEventRecord(oev[0], ctx->s_copy);
+        decltype(th0) th1 = th0;
         for (unsigned k = 0; k < n_pieces; ++k) {
             const size_t lo = (size_t)k * ov_piece, len = std::min<size_t>(ov_piece, n_bytes - lo);
             StagePool::get().copy(pin + o_in + lo, h_bytes + lo, len);
+            if (k == 0) th1 = now();
             CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, len, cudaMemcpyHostToDevice, ctx->s_copy));
             CK(cudaMemcpyAsync(ctx->d_arrive + ARRIVE_STRIDE * k, ctx->h_tag, sizeof(unsigned int),
                                cudaMemcpyHostToDevice, ctx->s_copy));
         }
+        if (ovt) cudaEventRecord(oev[1], ctx->s_copy);
+        auto th2 = now();
         CK(cudaEventRecord(ctx->io_ev[0], s));
         ctx->cur_arrive = ctx->d_arrive;
         ctx->cur_piece = ov_piece;
@@ -1308,6 +1351,19 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         ctx->cur_arrive = nullptr;
         ctx->cur_piece = 0;
         if (rc) return rc;
+        if (ovt) {  // GPUBPE_HOSTTIME=3: host and device timeline of the overlapped call
+            cudaEventRecord(oev[2], s);
+            auto th3 = now();
+            cudaStreamSynchronize(s);
+            auto th4 = now();
+            float dma, ker;
+            cudaEventElapsedTime(&dma, oev[0], oev[1]);
+            cudaEventElapsedTime(&ker, oev[0], oev[2]);
+            auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
+            fprintf(stderr, "overlap: host entry->stage start %.1f | staged %.1f | DMAs enqueued %.1f | launched %.1f | "
+                            "synced %.1f us; GPU from the first DMA: data in %.1f | kernel end %.1f us\n",
+                    us(t_a, th0), us(t_a, th1), us(t_a, th2), us(t_a, th3), us(t_a, th4), dma * 1e3, ker * 1e3);
+        }
     } else if (n_bytes && !stage && mapped_alias(h_bytes)) {  // caller bytes already pinned: no staging copy
         memcpy(pin + o_doffs, h_doc_offs, offs_b);
         CK(cudaMemcpyAsync(dv + o_in, h_bytes, n_bytes, cudaMemcpyHostToDevice, s));
@@ -1359,13 +1415,20 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
     }
     CK(cudaEventRecord(ctx->io_ev[1], s));
     if (mode != 1 && mode != 3) CK(cudaMemcpyAsync(pin + o_ooffs, dv + o_ooffs, offs_b, cudaMemcpyDeviceToHost, s));
-    if (n_bytes) {  // the counters come back in the same sync (none needed by gpubpe_query)
-        const EncodeState *last = static_cast<const EncodeState *>(ctx->ws_state.p) + ((ctx->calls - 1) & 1);
-        CK(cudaMemcpyAsync(ctx->h_state, last, sizeof(EncodeState), cudaMemcpyDeviceToHost, s));
-    }
     auto t_c = now();
     CK(cudaStreamSynchronize(s));
     auto t_d = now();
+    ctx->cur_mirror = nullptr;
+    if (n_bytes) {  // the counters, from the mirror (or, if the kernel did not fill it, a copy)
+        if (mir->n_ids != ~0ull) {
+            ctx->h_state->n_ids = mir->n_ids;
+            ctx->h_state->overflow = mir->overflow;
+            ctx->h_state->c = *const_cast<const PassCounters *>(&mir->c);
+        } else {
+            const EncodeState *last = static_cast<const EncodeState *>(ctx->ws_state.p) + ((ctx->calls - 1) & 1);
+            CK(cudaMemcpy(ctx->h_state, last, sizeof(EncodeState), cudaMemcpyDeviceToHost));
+        }
+    }
     if (ctx->tl_n) {
         float ms;
         fprintf(stderr, "timeline (us from the first piece's enqueue):");
@@ -1850,6 +1913,9 @@ extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe
     for (auto &e : ctx->io_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);
+    if (ctx->h_mirror) cudaFreeHost(ctx->h_mirror);
+    if (ctx->h_tag) cudaFreeHost(ctx->h_tag);
+    if (ctx->d_arrive) cudaFree(ctx->d_arrive);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;

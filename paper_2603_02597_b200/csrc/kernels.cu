@@ -1298,6 +1298,26 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
 
 // ------------------------------------------------------------------ kernel
 
+// Every exit of k_encode: the last CTA to leave copies the call's results
+// (id count, overflow flag, counters) to P.mirror, pinned host memory mapped
+// into the device, so a host call reads them after its synchronisation with
+// no device-to-host copy (one DMA costs ~9 us of setup on this link).
+__device__ __forceinline__ void kernel_exit(const EncodeParams &P) {
+    if (!P.mirror) return;
+    __syncthreads();  // this CTA's counter atomics are issued
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&P.st->exit_ctr, 1ull) == gridDim.x - 1) {
+            __threadfence();
+            P.mirror->n_ids = __ldcg(&P.st->n_ids);
+            P.mirror->overflow = __ldcg(&P.st->overflow);
+            const unsigned long long *c = &P.st->c.n_segments;
+            unsigned long long *d = &P.mirror->c.n_segments;
+            for (int i = 0; i < (int)(sizeof(PassCounters) / 8); ++i) d[i] = __ldcg(&c[i]);
+        }
+    }
+}
+
 // kOneEach: the batch has at most one tile per warp (one round; tiles assigned
 // statically).  A separate instantiation keeps the general kernel's code (and
 // register allocation) exactly as tuned for many tiles per warp.
@@ -1371,6 +1391,7 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
                     if (P.dbg && tid == 0) P.dbg[36864 + 4 * blockIdx.x + 1] = gtimer();
                     if (hi > lo) place_range_one(P, C, lo, hi, C.bcast[0]);
                     if (P.dbg && tid == 0) P.dbg[4 * blockIdx.x + 3] = gtimer();
+                    kernel_exit(P);
                     return;
                 }
                 // deferred segments: the general path below (every CTA read the same count)
@@ -1411,6 +1432,7 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
         if (D > d_done) {
             if (D > P.rec_cap) {
                 if (blockIdx.x == 0 && tid == 0) atomicExch(&st->overflow, 1ull);
+                kernel_exit(P);
                 return;
             }
             encode_deferred(P, C, d_done, D, t0, par, nbar);
@@ -1420,7 +1442,10 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
                 st->rec_ctr = 0;
                 st->rec_ctr2 = 0;
             }
-            if (__ldcg(&st->overflow)) return;
+            if (__ldcg(&st->overflow)) {
+                kernel_exit(P);
+                return;
+            }
             d_done = D;
         }
         // ---- phase B: place this CTA's contiguous range of the round's tiles
@@ -1449,6 +1474,7 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
     }
     if constexpr (!kOneEach) publish_counters(C, X, &st->c);
     if (P.dbg && tid == 0) P.dbg[4 * blockIdx.x + 3] = gtimer();
+    kernel_exit(P);
 }
 
 // ------------------------------------------------------------------ lookup

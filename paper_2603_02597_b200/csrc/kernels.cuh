@@ -88,9 +88,17 @@ struct EncodeState {
     unsigned long long arena_used;   // u32 words requested from the arena
     unsigned long long overflow;     // arena or record list overflowed: host re-runs
     unsigned long long n_ids;
-    unsigned long long pad2[2];
+    unsigned long long exit_ctr;     // CTAs that left the kernel (the last one fills EncodeParams.mirror)
+    unsigned long long pad2[1];
     PassCounters c;
     unsigned long long rng[RNG_MAX];  // one-round calls: per placement range, tiles done << 40 | entries
+};
+
+// The results a host call needs, written by the last CTA into mapped pinned memory.
+struct StateMirror {
+    unsigned long long n_ids;
+    unsigned long long overflow;
+    PassCounters c;
 };
 
 struct DefRec {
@@ -131,6 +139,7 @@ struct EncodeParams {
                                  // piece of the input), else null -- a tile waits for its pieces
     unsigned long long piece;    // bytes per piece
     unsigned int arrive_tag;     // value of an arrived piece's word in this call
+    StateMirror *mirror;         // host calls: results for the host (mapped pinned), else null
     unsigned long long *dbg;     // debug timestamps (GPUBPE_DEBUG & 8), else null
     int dbg_phase_a_only;        // GPUBPE_DEBUG & 16: profile phase A alone (output invalid)
 };

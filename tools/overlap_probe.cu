@@ -98,6 +98,44 @@ int main() {
         for (int k = 0; k < np && k < 7; ++k) printf(" %.1f", (last[1 + k] - last[0]) / 1e3);
         printf(" us after the first CTA\n");
     }
+    {  // the input split over 1..4 copy streams (one piece + arrival word each), kernel waiting
+        cudaStream_t cs[4];
+        for (auto &c : cs) cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking);
+        for (int ns = 1; ns <= 4; ns *= 2) {
+            const size_t pc = pieces * piece / ns;
+            double best = 1e9;
+            unsigned long long last[8] = {};
+            for (int it = 0; it < 20; ++it) {
+                cudaMemsetAsync(d_st, 0, 64, 0);
+                unsigned long long init = ~0ull;
+                cudaMemcpyAsync(d_st, &init, 8, cudaMemcpyHostToDevice, 0);
+                cudaStreamSynchronize(0);
+                *h_tag = ++tag;
+                auto t0 = std::chrono::steady_clock::now();
+                for (int k = 0; k < ns; ++k) {
+                    cudaMemcpyAsync(d_buf + k * pc, h_pin + k * pc, pc, cudaMemcpyHostToDevice, cs[k]);
+                    cudaMemcpyAsync(d_arrive + 32 * k, h_tag, 4, cudaMemcpyHostToDevice, cs[k]);
+                }
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(148);
+                cfg.blockDim = dim3(1024);
+                cfg.dynamicSmemBytes = 200 << 10;
+                cfg.stream = 0;
+                cudaLaunchKernelEx(&cfg, k_wait, (const unsigned *)d_arrive, tag, ns, d_st);
+                cudaStreamSynchronize(0);
+                auto t1 = std::chrono::steady_clock::now();
+                const double us = std::chrono::duration<double, std::micro>(t1 - t0).count();
+                cudaMemcpy(h_st, d_st, 64, cudaMemcpyDeviceToHost);
+                if (us < best) {
+                    best = us;
+                    for (int k = 0; k < 8; ++k) last[k] = h_st[k];
+                }
+            }
+            printf("%d copy streams x %zu KB (DMA first, then the kernel): host %.1f us; seen at", ns, pc >> 10, best);
+            for (int k = 0; k < ns; ++k) printf(" %.1f", (last[1 + k] - last[0]) / 1e3);
+            printf(" us after the first CTA\n");
+        }
+    }
     {  // plain H2D of the whole buffer, timed alone
         double best = 1e9;
         for (int it = 0; it < 20; ++it) {
