@@ -59,12 +59,18 @@ __host__ __device__ __forceinline__ PairSlots pair_slots(uint32_t l, uint32_t r,
     return PairSlots{(uint32_t)h & mask, (uint32_t)(h >> 32) & mask};
 }
 
-// Memo hash over a byte string given as 8-byte little-endian chunks.
+// Memo hash over a byte string given as 8-byte little-endian chunks:
+// multiplicative (one 64-bit multiply per chunk, most strings are one chunk);
+// the slot is taken from the top bits (memo_slot_of), which every input bit
+// reaches.
 __host__ __device__ __forceinline__ uint64_t memo_hash_step(uint64_t h, uint64_t chunk) {
-    return fmix64(h ^ chunk);
+    return (h ^ chunk) * 0x9E3779B97F4A7C15ull;
 }
 __host__ __device__ __forceinline__ uint64_t memo_hash_init(uint32_t len) {
-    return 0x9E3779B97F4A7C15ull * (uint64_t)(len + 1);
+    return (uint64_t)(len + 1) * 0xC2B2AE3D27D4EB4Full;
+}
+__host__ __device__ __forceinline__ uint32_t memo_slot_of(uint64_t h, uint32_t mask) {
+    return (uint32_t)(h >> 40) & mask;
 }
 
 #ifdef __CUDACC__

@@ -490,7 +490,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
                         blob.push_back(ch);
                     }
                 }
-                uint32_t h = (uint32_t)memo_hash_bytes(sv, len) & (uint32_t)(mcap - 1);
+                uint32_t h = memo_slot_of(memo_hash_bytes(sv, len), (uint32_t)(mcap - 1));
                 while (memo[h].w != 0) h = (h + 1) & (uint32_t)(mcap - 1);
                 memo[h] = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), cand_int[k],
                                      len | (len > 8 ? boff << 8 : 0u));

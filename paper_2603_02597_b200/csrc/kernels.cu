@@ -208,15 +208,16 @@ __device__ __forceinline__ unsigned long long sb_load8(const uint32_t *sbw, uint
     return ((unsigned long long)hi << 32) | lo;
 }
 
+// The low n bytes of v (n >= 1; all of v from 8 on).
 __device__ __forceinline__ unsigned long long low_bytes(unsigned long long v, uint32_t n) {
-    return n >= 8 ? v : (v & ((1ull << (8 * n)) - 1));
+    return v & (~0ull >> (64 - 8 * min(n, 8u)));
 }
 
 // Memo home slot for staged bytes [p, p + len), 2 <= len <= SHORT_MAX.
 __device__ __forceinline__ uint32_t memo_slot(const uint32_t *sb, uint32_t p, uint32_t len, uint32_t mask) {
     unsigned long long h = memo_hash_step(memo_hash_init(len), low_bytes(sb_load8(sb, p), len));
     for (uint32_t c = 8; c < len; c += 8) h = memo_hash_step(h, low_bytes(sb_load8(sb, p + c), len - c));
-    return (uint32_t)h & mask;
+    return memo_slot_of(h, mask);
 }
 
 // Memo lookup continuing from slot `slot` whose entry `e` is already loaded.
