@@ -213,19 +213,16 @@ __device__ __forceinline__ unsigned long long low_bytes(unsigned long long v, ui
     return v & (~0ull >> (64 - 8 * min(n, 8u)));
 }
 
-// Memo home slot for staged bytes [p, p + len), 2 <= len <= SHORT_MAX.
-__device__ __forceinline__ uint32_t memo_slot(const uint32_t *sb, uint32_t p, uint32_t len, uint32_t mask) {
-    unsigned long long h = memo_hash_step(memo_hash_init(len), low_bytes(sb_load8(sb, p), len));
-    for (uint32_t c = 8; c < len; c += 8) h = memo_hash_step(h, low_bytes(sb_load8(sb, p + c), len - c));
-    return memo_slot_of(h, mask);
-}
-
-// Memo lookup continuing from slot `slot` whose entry `e` is already loaded.
-// The id, or INF when the string is not a memoised vocab token.
-__device__ uint32_t memo_resolve(const DevTables &T, const uint32_t *sb, uint32_t p, uint32_t len,
-                                 uint32_t slot, uint4 e) {
+// Memo lookup of staged bytes [p, p + len), 2 <= len <= SHORT_MAX: the id, or
+// INF when the string is not a memoised vocab token (a vocab string whose BPE
+// is itself).  Linear probing from the hash's slot to an empty one.
+__device__ uint32_t memo_lookup(const DevTables &T, const uint32_t *sb, uint32_t p, uint32_t len) {
     const unsigned long long c0 = low_bytes(sb_load8(sb, p), len);
+    unsigned long long h = memo_hash_step(memo_hash_init(len), c0);
+    for (uint32_t c = 8; c < len; c += 8) h = memo_hash_step(h, low_bytes(sb_load8(sb, p + c), len - c));
+    uint32_t slot = memo_slot_of(h, T.memo_mask);
     for (;;) {
+        const uint4 e = __ldg(&T.memo[slot]);
         if (e.w == 0) return GPUBPE_INF;
         if ((e.w & 0xFFu) == len && e.x == (uint32_t)c0 && e.y == (uint32_t)(c0 >> 32)) {
             bool eq = true;
@@ -235,7 +232,6 @@ __device__ uint32_t memo_resolve(const DevTables &T, const uint32_t *sb, uint32_
             if (eq) return e.z;
         }
         slot = (slot + 1) & T.memo_mask;
-        e = __ldg(&T.memo[slot]);
     }
 }
 
@@ -468,8 +464,9 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
     }
     __syncwarp();
 
-    // ---- 5. classify; memo candidates park their slot in sid and prefetch
-    //         its line into L1 (pass 1), then resolve (pass 2)
+    // ---- 5. classify and look up: length 1 -> base id, 2..SHORT_MAX -> memo
+    //         (hash, probe and compare in one pass: the other warps of the SM
+    //         cover the probe's latency), longer -> deferred
     const bool use_memo = T.memo_mask != 0;
 #pragma unroll 1
     for (uint32_t i = lane; i < nseg; i += 32) {
@@ -488,34 +485,18 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
         const uint32_t len = (uint32_t)(e - p);
         if (len == 1) {
             S.sid[SI(p)] = (1u << 24) | C.base[sb_byte(sb, p)];
-        } else if (use_memo) {
-            const uint32_t ms = memo_slot(sb, (uint32_t)p, len, T.memo_mask);
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(T.memo + ms));
-            S.sid[SI(p)] = ms;  // tag 0: memo pending (slots < 2^24)
-            S.sid[SI(p + 1)] = len;
-        } else {
+            continue;
+        }
+        const uint32_t id = use_memo ? memo_lookup(T, sb, (uint32_t)p, len) : GPUBPE_INF;
+        if (id == GPUBPE_INF) {  // not a memoised vocab string: the warp engine below
             S.u.a.miss[atomicAdd(&S.n_miss, 1u)] = (uint32_t)p | (len << 16);
             ++c_miss;
+            continue;
         }
+        ++c_memo;
+        S.sid[SI(p)] = (1u << 24) | id;
     }
     TSTAMP(7, c_seg);
-    if (use_memo) {
-#pragma unroll 1
-        for (uint32_t i = lane; i < nseg; i += 32) {
-            const int p = S.seg[i];
-            const uint32_t ms = S.sid[SI(p)];
-            if (ms >> 24) continue;
-            const uint32_t len = S.sid[SI(p + 1)];
-            const uint32_t id = memo_resolve(T, sb, (uint32_t)p, len, ms, __ldg(&T.memo[ms]));
-            if (id == GPUBPE_INF) {  // not a vocab string: the warp engine below
-                S.u.a.miss[atomicAdd(&S.n_miss, 1u)] = (uint32_t)p | (len << 16);
-                ++c_miss;
-                continue;
-            }
-            ++c_memo;
-            S.sid[SI(p)] = (1u << 24) | id;
-        }
-    }
     __syncwarp();
     TSTAMP(2, c_memo);
 
