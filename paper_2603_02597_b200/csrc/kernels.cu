@@ -122,6 +122,7 @@ __device__ long long warp_doc_from(const long long *offs, long long lo, unsigned
                                    long long p) {
     const int lane = threadIdx.x & 31;
     long long hi = (long long)n_docs - 1;
+    if (lo < hi && __ldg(&offs[lo + 1]) > p) return lo;  // still inside the last tile's document
     {   // the next 31 documents first: tiles of one warp move forward slowly
         const long long idx = lo + lane;
         const bool ok = idx <= hi && __ldg(&offs[idx]) <= p;
@@ -410,7 +411,24 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
     // ---- 3. document starts and chunk cuts inside the staged bytes
     long long dc = 0;  // document holding byte a
     if (P.n_docs > 1) dc = X.dcur = warp_doc_from(P.doc_offs, X.dcur, P.n_docs, a);
+    // inner: the staged bytes lie strictly inside document dc, with no chunk cut
+    // among them -- no cut to add here and no document offset to record (step 8)
+    bool inner = false;
     if (P.n_docs > 1 || (unsigned long long)N > P.max_seq_len) {
+        const long long ds = __ldg(&P.doc_offs[dc]), de = __ldg(&P.doc_offs[dc + 1]);
+        if (ds < a && de >= a + nst) {
+            inner = true;
+            if ((unsigned long long)(de - ds) > P.max_seq_len) {  // fixed-offset chunks: the next cut
+                const unsigned long long cb = P.chunk_budget, num = (unsigned long long)(a - ds);
+                unsigned long long r;
+                if ((cb & (cb - 1)) == 0) r = num & (cb - 1);
+                else if ((num >> 32) == 0 && (cb >> 32) == 0) r = (uint32_t)num % (uint32_t)cb;
+                else r = num % cb;
+                if (r == 0 || cb - r < (unsigned long long)nst) inner = false;
+            }
+        }
+    }
+    if (!inner && (P.n_docs > 1 || (unsigned long long)N > P.max_seq_len)) {
 #pragma unroll 1
         for (long long d0 = dc;; d0 += 32) {
             const long long d = d0 + lane;
@@ -571,7 +589,7 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
     TSTAMP(4, total);
 
     // ---- 8. tile-local entry offsets of the documents starting in this tile
-    if (P.n_docs > 1 || a == 0 || last) {
+    if ((P.n_docs > 1 || a == 0 || last) && !(inner && !last)) {
         long long dlb;  // first document with offs >= a
         if (__ldg(&P.doc_offs[dc]) < a) {
             dlb = dc + 1;
