@@ -173,6 +173,10 @@ static int ensure(gpubpe_ctx *ctx, DevBuf &b, size_t bytes, bool zero) {
     return GPUBPE_OK;
 }
 
+#ifndef GPUBPE_MEMO_SPREAD
+#define GPUBPE_MEMO_SPREAD 8  // memo slots per string (power-of-two capacity): short probe chains
+#endif
+
 static uint64_t memo_hash_bytes(const uint8_t *s, uint32_t len) {
     uint64_t h = memo_hash_init(len);
     for (uint32_t c = 0; c < len || c == 0; c += 8) {
@@ -374,7 +378,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
             if (len > 8) blob_max += (len - 1) / 8 * 8;
         }
     uint64_t memo_cap_max = 2;
-    while (memo_cap_max < 2 * memo_cand) memo_cap_max <<= 1;
+    while (memo_cap_max < (uint64_t)GPUBPE_MEMO_SPREAD * memo_cand) memo_cap_max <<= 1;
     {
         size_t need = table_slot(slots.size() * sizeof(uint4)) + 2 * table_slot((n_ids + 1) * 4) +
                       table_slot(jbits.size() * 4) + table_slot(256 * 4) +
@@ -473,7 +477,7 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_ctx_create(int devi
             for (size_t k = 0; k < cand.size(); ++k)
                 if (oo[k + 1] - oo[k] == 1 && oids[oo[k]] == cand_int[k]) keep.push_back(k);
             uint64_t mcap = 2;
-            while (mcap < 2 * keep.size()) mcap <<= 1;
+            while (mcap < (size_t)GPUBPE_MEMO_SPREAD * keep.size()) mcap <<= 1;  // load <= 1 / spread
             std::vector<uint4> memo(mcap, make_uint4(0, 0, 0, 0));
             std::vector<unsigned long long> blob;  // bytes 8.. as zero-padded 8-byte chunks
             for (size_t k : keep) {
