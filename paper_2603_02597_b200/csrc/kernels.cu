@@ -1129,6 +1129,7 @@ __device__ void grid_giants(const EncodeParams &P, CtaSmem &C, unsigned long lon
     const unsigned long long ng = __ldcg(&g[4]);  // giants of this round (same in every CTA)
     for (unsigned long long gi = 0; gi < ng; ++gi) {
         const unsigned long long r = __ldcg(&P.glist[gi]);
+        if (__ldcg(&P.recs[r].count) != REC_GIANT) continue;  // encoded by one CTA (cta_giants)
         const long long s0 = (long long)__ldcg(&P.recs[r].start);
         // the segment's end: each CTA scans a slice of [s0 + GIANT_MIN, lim)
         long long d = 0;
@@ -1258,6 +1259,42 @@ __device__ void encode_record(const EncodeParams &P, CtaSmem &C, const G &g, uns
 }
 
 
+// Several giants in a round: each CTA takes giants from the round's list and
+// encodes those of at most CTA_GIANT_MAX bytes alone (the block engine over
+// the arena), concurrently; longer ones keep their REC_GIANT mark for the
+// whole grid (grid_giants).  One giant alone is faster on the grid.
+__device__ void cta_giants(const EncodeParams &P, CtaSmem &C, unsigned long long t0, unsigned long long par) {
+    const int tid = threadIdx.x;
+    EncodeState *st = P.st;
+    const long long N = (long long)P.n_bytes;
+    const unsigned long long ng = __ldcg(&P.gscr[4]);
+    for (;;) {
+        if (tid == 0) C.bcast[1] = atomicAdd(&st->rec_ctr2, 1ull);
+        __syncthreads();
+        const unsigned long long gi = C.bcast[1];
+        __syncthreads();
+        if (gi >= ng) break;
+        const unsigned long long r = __ldcg(&P.glist[gi]);
+        const long long s0 = (long long)__ldcg(&P.recs[r].start);
+        long long d = 0;
+        if (P.n_docs > 1) {
+            if ((tid >> 5) == 0) {
+                const long long dd = warp_doc_from(P.doc_offs, 0, P.n_docs, s0);
+                if ((tid & 31) == 0) C.bcast[1] = (unsigned long long)dd;
+            }
+            __syncthreads();
+            d = (long long)C.bcast[1];
+            __syncthreads();
+        }
+        long long lim = next_struct_cut(P, d, s0);
+        if (lim > N) lim = N;
+        const long long hi = min(lim, s0 + (long long)CTA_GIANT_MAX + 1);
+        const long long e = cta_first_nonjunction(P, C.jb, s0 + GIANT_MIN, hi, C.es);
+        if (e >= hi && hi < lim) continue;  // longer than CTA_GIANT_MAX: the grid's
+        encode_record(P, C, BlockGroup{C.es}, r, s0, (unsigned long long)(e - s0), t0, par, tid == 0, &C.bcast[2]);
+    }
+}
+
 // Deferred records [d0, d1) of round r.  Pass 1: every warp takes records,
 // finds each segment's end (first cut after its start, looked for within
 // GIANT_MIN bytes) and encodes the medium ones with the warp engine; longer
@@ -1292,7 +1329,12 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
                       &C.w[wid].dl_arena);
     }
     grid_sync(st, ++nbar);
-    // ---- pass 2: every CTA together on each giant, in record order
+    // ---- pass 2: several giants -> one CTA each (up to CTA_GIANT_MAX bytes), then
+    //      every CTA together on each remaining giant, in record order
+    if (__ldcg(&P.gscr[4]) > 1) {
+        cta_giants(P, C, t0, par);
+        grid_sync(st, ++nbar);
+    }
     grid_giants(P, C, t0, par, nbar);
 }
 

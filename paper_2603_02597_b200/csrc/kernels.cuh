@@ -45,7 +45,8 @@ constexpr int NGRP = LD / 16;   // 16-position groups whose cut bits are compute
 constexpr int NW = GPUBPE_NW;   // warps per CTA
 constexpr int NT = NW * 32;     // threads per CTA
 constexpr int SHORT_MAX = 32;   // longest segment encoded inside the tile loop
-constexpr int GIANT_MIN = 4097; // deferred segments this long are encoded by the whole grid (else a warp)
+constexpr int GIANT_MIN = 4097; // deferred segments this long are giants (else a warp encodes them)
+constexpr int CTA_GIANT_MAX = 64 << 10;  // with several giants in a round, one CTA each up to this length
 constexpr int SLOT = WT + SHORT_MAX;  // scratch entries per tile (ids of segments starting in it)
 #ifndef GPUBPE_UNIT_MAX
 #define GPUBPE_UNIT_MAX 512

@@ -129,6 +129,24 @@ def test_million_byte_adversarial(tokenizer, oracle):
     assert got.device_stats["giant_segments"] >= 3
 
 
+def test_many_giant_documents(tokenizer, oracle):
+    """Many giant segments (> 4 KiB without a junction cut) in one call: up to
+    64 KiB each is encoded by one CTA, concurrently (kernels.cu cta_giants);
+    longer ones by the whole grid.  Digits, hex, letters and newline runs of
+    4-90 KB, with prose between some, under both chunking configs."""
+    r = random.Random(17)
+    kinds = ["digits", "hex", "letters", "newlines", "aaaa"]
+    docs = []
+    for i in range(160):
+        n = r.choice([4100, 5000, 9000, 17000, 33000, 65536, 70000, 90000]) if i % 7 else r.randint(4097, 12000)
+        body = ADVERSARIAL[kinds[i % len(kinds)]](n, r)
+        docs.append(body if i % 3 else b"The table " + body + b" ends here.")
+    for msl, cb in ((1 << 40, 1 << 40), (8192, 8192)):
+        got = bpe.tokenize_batch(docs, with_config(tokenizer, msl, cb))
+        assert_same(got.token_ids, oracle.encode_docs(docs, msl, cb), f"giant docs {msl}")
+        assert got.device_stats["giant_segments"] >= 20
+
+
 def test_many_small_and_empty_docs(tokenizer, oracle):
     r = random.Random(5)
     docs = []

@@ -58,6 +58,11 @@ def workloads():
             d = np.full(n, {"newlines": 10, "aaaa": 97}[kind], np.uint8)
         return d, np.array([0, n], np.int64), None
 
+    def giant_docs(n_docs, doc_bytes):  # every document one digit giant
+        rng = np.random.default_rng(1)
+        d = rng.integers(48, 58, n_docs * doc_bytes, dtype=np.uint8)
+        return d, np.arange(0, n_docs * doc_bytes + 1, doc_bytes, dtype=np.int64), None
+
     return {
         "c1_8k": lambda: single("c1_8k"),
         "c1_32k": lambda: single("c1_32k"),
@@ -69,6 +74,7 @@ def workloads():
         "adv_letters_1m": lambda: adversarial("letters", 1 << 20),
         "adv_newlines_1m": lambda: adversarial("newlines", 1 << 20),
         "adv_aaaa_1m": lambda: adversarial("aaaa", 1 << 20),
+        "adv_digit_docs_1000x10k": lambda: giant_docs(1000, 10000),
     }
 
 
