@@ -1292,7 +1292,7 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
     uint32_t *d_ids_direct = (mode == 3 && n_bytes) ? static_cast<uint32_t *>(mapped_alias(h_out_ids)) : nullptr;
     // overlapped launch (one pageable buffer of 128 KiB .. 16 MiB, default mode):
     // ~4 pieces, the kernel enqueued before them
-    static const bool no_overlap = getenv("GPUBPE_NO_OVERLAP") != nullptr;
+    const bool no_overlap = getenv("GPUBPE_NO_OVERLAP") != nullptr;  // (per call: tests switch it)
     // (every H2D copy costs ~7 us of setup on this PCIe 5 link, measured by
     // tools/overlap_probe.cu: one piece unless GPUBPE_OV_PIECES says otherwise)
     static const int ov_pieces = getenv("GPUBPE_OV_PIECES") ? std::max(1, atoi(getenv("GPUBPE_OV_PIECES"))) : 1;

@@ -915,3 +915,30 @@ def test_encode_batch_tensors(tokenizer, prose_samples):
     h, ho = ids.cpu().numpy().view(np.uint32), oo.cpu().numpy()
     gold = fixtures.golden_prose()[:12]
     assert [h[ho[i]:ho[i + 1]].tolist() for i in range(12)] == [g.tolist() for g in gold]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("overlap", [True, False])
+def test_single_document_host_paths(tokenizer, oracle, monkeypatch, overlap):
+    """The single-document latency path (hostlist.c encode_one ->
+    gpubpe_encode_host): below, at and above the overlapped-launch window
+    (128 KiB .. 16 MiB: the kernel is launched while its input is in flight
+    and its tiles wait for the arrival word), with chunking on and off, and
+    the counters read from the kernel's mapped mirror (no state copy)."""
+    import synth_corpus
+
+    if not overlap:
+        monkeypatch.setenv("GPUBPE_NO_OVERLAP", "1")
+    for n in (100_000, 131_071, 131_072, 600_000, 3_000_000):
+        doc = synth_corpus.english_bytes(n, n)
+        for msl, cb in ((1 << 40, 1 << 40), (8192, 8192), (100_000, 65_536)):
+            res = bpe.tokenize_batch([doc], with_config(tokenizer, msl, cb))
+            want = oracle.encode_docs([doc], msl, cb)
+            assert_same(res.token_ids, want, f"{n}/{msl}")
+            st = res.device_stats
+            assert st["n_ids"] == len(want[0]) and st["n_bytes"] == n and st["overflow"] == 0
+            assert st["memo_hits"] > 0 and st["n_segments"] >= st["memo_hits"]
+    # repeated calls of one size: no allocation
+    doc = synth_corpus.english_bytes(600_000, 3)
+    bpe.tokenize_batch([doc], with_config(tokenizer, 1 << 40, 1 << 40))
+    assert bpe.tokenize_batch([doc], with_config(tokenizer, 1 << 40, 1 << 40)).device_stats["allocations"] == 0
