@@ -107,6 +107,7 @@ struct gpubpe_ctx {
     unsigned long long *dbg_buf = nullptr;  // GPUBPE_DEBUG & 8 timestamps
     StateMirror *h_mirror = nullptr, *d_mirror = nullptr;  // host calls: the kernel's results (mapped)
     StateMirror *cur_mirror = nullptr;                     // for the encode being launched
+    unsigned long long mirror_tag = 0;                     // per host call
     std::chrono::steady_clock::time_point t_call;  // GPUBPE_HOSTTIME: gpubpe_encode entry
     int tl_n = 0;                                  // GPUBPE_HOSTTIME=2: piece events of this call
     cudaEvent_t *tl_ev = nullptr;
@@ -624,6 +625,7 @@ static int encode_impl(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes
         P.piece = ctx->cur_piece ? ctx->cur_piece : 1;
         P.arrive_tag = ctx->arrive_tag;
         P.mirror = ctx->cur_mirror;
+        P.mirror_tag = ctx->mirror_tag;
         P.gscr = static_cast<unsigned long long *>(ctx->ws_gscr.p);
         P.glist = static_cast<uint32_t *>(ctx->ws_glist.p);
         ctx->last_n_tiles = n_tiles;
@@ -1274,6 +1276,7 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
     // the kernel's last CTA writes the results here (kernels.cu kernel_exit): no D2H copy
     volatile StateMirror *mir = ctx->h_mirror;
     mir->n_ids = ~0ull;  // (sentinel: a kernel that did not write falls back to a copy)
+    const unsigned long long mtag = ++ctx->mirror_tag;
     ctx->cur_mirror = ctx->d_mirror;
     struct MirrorOff {
         gpubpe_ctx *c;
@@ -1420,7 +1423,26 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
     CK(cudaEventRecord(ctx->io_ev[1], s));
     if (mode != 1 && mode != 3) CK(cudaMemcpyAsync(pin + o_ooffs, dv + o_ooffs, offs_b, cudaMemcpyDeviceToHost, s));
     auto t_c = now();
-    CK(cudaStreamSynchronize(s));
+    // Wait for the results: with mapped outputs (mode 3) the kernel's last CTA
+    // writes the mirror after every store is visible to the host (system-scope
+    // fences), ~10 us before a stream synchronisation would return; the stream
+    // is polled now and then so a failed or mirror-less launch still ends the wait.
+    bool synced = false;
+    if (mode == 3 && n_bytes) {
+        for (unsigned it = 1;; ++it) {
+            if (mir->done == mtag) break;
+            if ((it & 1023) == 0) {
+                const cudaError_t q = cudaStreamQuery(s);
+                if (q == cudaSuccess) break;
+                if (q != cudaErrorNotReady) CK(q);
+            }
+            cpu_relax();
+        }
+    }
+    if (!(mode == 3 && n_bytes && mir->done == mtag && !mir->overflow)) {
+        CK(cudaStreamSynchronize(s));
+        synced = true;
+    }
     auto t_d = now();
     ctx->cur_mirror = nullptr;
     if (n_bytes) {  // the counters, from the mirror (or, if the kernel did not fill it, a copy)
@@ -1479,7 +1501,13 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
             copy_par(h_out_ids, pin + o_ids, total * 4);
         }
     }
-    if (kernel_ms) CK(cudaEventElapsedTime(kernel_ms, ctx->io_ev[0], ctx->io_ev[1]));
+    if (kernel_ms) {  // from the events once complete; else the host's view (enqueue to results)
+        if (synced || cudaEventQuery(ctx->io_ev[1]) == cudaSuccess)
+            CK(cudaEventElapsedTime(kernel_ms, ctx->io_ev[0], ctx->io_ev[1]));
+        else
+            *kernel_ms = (float)(std::chrono::duration<double, std::milli>(t_d - t_b).count());
+        cudaGetLastError();
+    }
     *n_ids_out = total;
     if (htime) {
         auto t_e = now();

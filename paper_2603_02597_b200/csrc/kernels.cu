@@ -1344,18 +1344,25 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
 // (id count, overflow flag, counters) to P.mirror, pinned host memory mapped
 // into the device, so a host call reads them after its synchronisation with
 // no device-to-host copy (one DMA costs ~9 us of setup on this link).
+//
+// System-scope fences: every CTA's stores (ids and offsets in mapped host
+// memory) reach the host before its exit count, and the mirror after all of
+// them, so a host that sees the mirror may read the results without waiting
+// for the stream to drain.
 __device__ __forceinline__ void kernel_exit(const EncodeParams &P) {
     if (!P.mirror) return;
-    __syncthreads();  // this CTA's counter atomics are issued
+    __syncthreads();  // this CTA's stores and counter atomics are issued
     if (threadIdx.x == 0) {
-        __threadfence();
+        __threadfence_system();
         if (atomicAdd(&P.st->exit_ctr, 1ull) == gridDim.x - 1) {
-            __threadfence();
+            __threadfence_system();
             P.mirror->n_ids = __ldcg(&P.st->n_ids);
             P.mirror->overflow = __ldcg(&P.st->overflow);
             const unsigned long long *c = &P.st->c.n_segments;
             unsigned long long *d = &P.mirror->c.n_segments;
             for (int i = 0; i < (int)(sizeof(PassCounters) / 8); ++i) d[i] = __ldcg(&c[i]);
+            __threadfence_system();
+            *reinterpret_cast<volatile unsigned long long *>(&P.mirror->done) = P.mirror_tag;  // last
         }
     }
 }

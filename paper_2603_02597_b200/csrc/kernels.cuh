@@ -100,6 +100,7 @@ struct StateMirror {
     unsigned long long n_ids;
     unsigned long long overflow;
     PassCounters c;
+    unsigned long long done;  // the call's tag, written last
 };
 
 struct DefRec {
@@ -141,6 +142,7 @@ struct EncodeParams {
     unsigned long long piece;    // bytes per piece
     unsigned int arrive_tag;     // value of an arrived piece's word in this call
     StateMirror *mirror;         // host calls: results for the host (mapped pinned), else null
+    unsigned long long mirror_tag;  // value of mirror->done once the results are complete
     unsigned long long *dbg;     // debug timestamps (GPUBPE_DEBUG & 8), else null
     int dbg_phase_a_only;        // GPUBPE_DEBUG & 16: profile phase A alone (output invalid)
 };

@@ -7,4 +7,4 @@ spec = fixtures.synth_sizes()["c1_131k"]; doc = synth_corpus.english_bytes(spec[
 W = 1 << 40
 tok = bpe.Tokenizer.from_files(*fixtures.gpt2_paths(), bpe.BlockConfig(max_seq_len=W, chunk_budget=W))
 for _ in range(60): bpe.tokenize_batch([doc], tok)
-' 2>&1 | grep -E "encode_impl|encode_host|timeline|overlap" | tail -${TAILN:-12}
+' 2>&1 | grep -E "encode_impl|encode_host|timeline|overlap|sync:" | tail -${TAILN:-12}
