@@ -494,7 +494,10 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
         if (e < 0) {  // longer than SHORT_MAX: deferred to the CTA engine
             const unsigned long long r = atomicAdd(&P.st->bar, 1ull << 32) >> 32;
             atomicAdd(&P.st->ndef[slot >= P.round_tiles], 1ull);
-            if (r < P.rec_cap) P.recs[r].start = (unsigned long long)(a + p);
+            if (r < P.rec_cap) {
+                P.recs[r].start = (unsigned long long)(a + p);
+                P.recs[r].doc = (unsigned long long)dc;  // the document holding the tile's first byte
+            }
             S.sid[SI(p)] = 0xFF000000u;
             S.sid[SI(p + 1)] = (uint32_t)r;
             S.n_def = 1;
@@ -550,7 +553,8 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
 #endif
 
     // ---- 7. entries in output order (chunked scan over the list) -> outbuf;
-    //         each segment's sid slot then holds its entry offset
+    //         each segment's sid slot then holds its entry offset (when step 8 runs)
+    const bool need_offs = (P.n_docs > 1 || a == 0 || last) && !(inner && !last);
     uint32_t total = 0;
 #pragma unroll 1
     for (uint32_t i0 = 0; i0 < nseg; i0 += 32) {
@@ -559,11 +563,16 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
         const int p = valid ? S.seg[i] : 0;
         const uint32_t v = valid ? S.sid[SI(p)] : 0u;
         const uint32_t cc = valid ? seg_entries(v) : 0u;
-        uint32_t incl = cc;
+        uint32_t incl;
+        if (__all_sync(FULL_MASK, cc <= 1u)) {  // one entry per segment (nearly always): no scan
+            incl = min((uint32_t)lane + 1u, nseg - i0);  // (the valid lanes are a prefix)
+        } else {
+            incl = cc;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(FULL_MASK, incl, o);
-            if (lane >= o) incl += y;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL_MASK, incl, o);
+                if (lane >= o) incl += y;
+            }
         }
         const uint32_t o = total + incl - cc;
         if (valid) {
@@ -574,7 +583,7 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
 #pragma unroll 1
                 for (uint32_t j = 1; j < cc; ++j) S.u.outbuf[o + j] = S.sid[SI(p + j)];
             }
-            S.sid[SI(p)] = o;
+            if (need_offs) S.sid[SI(p)] = o;  // (read by step 8 only)
         }
         total += __shfl_sync(FULL_MASK, incl, 31);
     }
@@ -589,7 +598,7 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
     TSTAMP(4, total);
 
     // ---- 8. tile-local entry offsets of the documents starting in this tile
-    if ((P.n_docs > 1 || a == 0 || last) && !(inner && !last)) {
+    if (need_offs) {
         long long dlb;  // first document with offs >= a
         if (__ldg(&P.doc_offs[dc]) < a) {
             dlb = dc + 1;
@@ -1135,7 +1144,7 @@ __device__ void grid_giants(const EncodeParams &P, CtaSmem &C, unsigned long lon
         long long d = 0;
         if (P.n_docs > 1) {
             if ((threadIdx.x >> 5) == 0) {
-                const long long dd = warp_doc_from(P.doc_offs, 0, P.n_docs, s0);
+                const long long dd = warp_doc_from(P.doc_offs, (long long)__ldcg(&P.recs[r].doc), P.n_docs, s0);
                 if ((threadIdx.x & 31) == 0) C.bcast[1] = (unsigned long long)dd;
             }
             __syncthreads();
@@ -1279,7 +1288,7 @@ __device__ void cta_giants(const EncodeParams &P, CtaSmem &C, unsigned long long
         long long d = 0;
         if (P.n_docs > 1) {
             if ((tid >> 5) == 0) {
-                const long long dd = warp_doc_from(P.doc_offs, 0, P.n_docs, s0);
+                const long long dd = warp_doc_from(P.doc_offs, (long long)__ldcg(&P.recs[r].doc), P.n_docs, s0);
                 if ((tid & 31) == 0) C.bcast[1] = (unsigned long long)dd;
             }
             __syncthreads();
@@ -1313,7 +1322,7 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
         r = __shfl_sync(FULL_MASK, r, 0);
         if (r >= d1) break;
         const long long s0 = (long long)__ldcg(&P.recs[r].start);
-        const long long d = P.n_docs > 1 ? warp_doc_from(P.doc_offs, 0, P.n_docs, s0) : 0;
+        const long long d = P.n_docs > 1 ? warp_doc_from(P.doc_offs, (long long)__ldcg(&P.recs[r].doc), P.n_docs, s0) : 0;
         long long lim = next_struct_cut(P, d, s0);
         if (lim > N) lim = N;
         const long long scan_hi = min(lim, s0 + (long long)GIANT_MIN);

@@ -108,6 +108,7 @@ struct DefRec {
     unsigned int count;        // ids it encodes to
     unsigned int res;          // arena word offset of its ids
     unsigned long long dst;    // giants: output position, copied grid-wide after placement
+    unsigned long long doc;    // a document at or before the one holding `start` (search hint)
 };
 
 struct EncodeParams {
