@@ -223,16 +223,20 @@ __global__ void __launch_bounds__(PT, 4) k_pretok(const __grid_constant__ Pretok
     __shared__ uint8_t sasc[128];
     __shared__ long long sdoc[2];  // documents holding the CTA's first and last byte
     if (threadIdx.x < 128) sasc[threadIdx.x] = Q.ascii[threadIdx.x];
-    if (threadIdx.x < 2) {
+    if (threadIdx.x < 64) {  // warps 0 / 1: 32-ary searches for the CTA's first / last byte
+        const int wsel = threadIdx.x >> 5, ln = threadIdx.x & 31;
         const long long nb = (long long)Q.n_bytes;
-        const long long q = min(nb - 1, ((long long)blockIdx.x * PT + (threadIdx.x ? PT - 1 : 0)) * 32 +
-                                            (threadIdx.x ? 31 : 0));
-        long long lo = 0, hi = (long long)Q.n_docs - 1;
-        while (lo < hi) {  // last d with offs[d] <= q
-            const long long mid = (lo + hi + 1) >> 1;
-            if (__ldg(&Q.doc_offs[mid]) <= q) lo = mid; else hi = mid - 1;
+        const long long q = min(nb - 1, ((long long)blockIdx.x * PT + (wsel ? PT - 1 : 0)) * 32 + (wsel ? 31 : 0));
+        long long lo = 0, hi = (long long)Q.n_docs - 1;  // last d in [lo, hi] with offs[d] <= q
+        while (hi > lo) {
+            const long long step = (hi - lo + 32) / 32;
+            const long long idx = lo + (long long)ln * step;
+            const bool ok = idx <= hi && __ldg(&Q.doc_offs[idx]) <= q;
+            const unsigned m = __ballot_sync(FULL_MASK, ok);  // lane 0 always holds
+            lo = lo + (long long)(31 - __clz(m)) * step;
+            hi = min(hi, lo + step - 1);
         }
-        sdoc[threadIdx.x] = lo;
+        if (ln == 0) sdoc[wsel] = lo;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
