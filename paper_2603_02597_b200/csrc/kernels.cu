@@ -844,6 +844,9 @@ __device__ void grid_sync(EncodeState *st, unsigned int k, unsigned long long *d
     __syncthreads();
 }
 
+#ifndef GPUBPE_POLL_NS
+#define GPUBPE_POLL_NS 256
+#endif
 // One-round calls: wait until every tile of the call is done -- per placement
 // range one word (tiles done << 40 | entries), one release add per tile --
 // then C.bcast[0] = the entries of the ranges before this CTA's and
@@ -868,7 +871,7 @@ __device__ void complete_one_round(const EncodeParams &P, CtaSmem &C, unsigned l
                 }
             }
             if (__all_sync(FULL_MASK, ok)) break;
-            __nanosleep(32);
+            __nanosleep(GPUBPE_POLL_NS);  // (the poller shares its SM with the slowest tiles' warps)
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(FULL_MASK, before, o);
