@@ -43,11 +43,11 @@ typedef struct gpubpe_stats {
     uint64_t passes;           /* merges applied = n_bytes - n_ids */
     uint64_t n_segments;       /* junction segments (incl. chunk / doc cuts) */
     uint64_t memo_hits;        /* segments resolved by one memo probe */
-    uint64_t short_merges;     /* segments merged by the per-thread greedy loop */
+    uint64_t short_merges;     /* memo-miss segments (<= 32 B) merged by the sequential warp engine */
     uint64_t medium_segments;  /* segments merged by the CTA engine in smem */
     uint64_t giant_segments;   /* segments merged by the giant (multi-window) engine */
     uint64_t giant_bytes;      /* bytes inside giant segments */
-    uint64_t engine_passes;    /* multi-merge passes run by CTA/giant engines */
+    uint64_t engine_passes;    /* warp-engine steps + multi-merge passes of the medium/giant engines */
     uint64_t tiles;            /* encode tiles launched */
     uint64_t overflow;         /* 1 if the giant arena overflowed (call re-run) */
     uint64_t well_formed;      /* 1 if the table admits exact multi-merge passes */
@@ -107,15 +107,22 @@ int gpubpe_encode(gpubpe_ctx *ctx, const uint8_t *d_bytes, uint64_t n_bytes,
 
 /*
  * Encode from and to HOST memory -- the reference's own call shape (bytes in,
- * ids out; tokenize_batch, chunker.py:110-187, for a packed batch).  Copies
- * the batch into context-owned pinned, device-mapped memory; the same encode
- * as gpubpe_encode then reads the bytes and writes the ids through PCIe
- * itself (zero-copy: the transfers overlap the kernel); the offsets and
- * exactly n_ids ids are copied out after one stream synchronisation.
+ * ids out; tokenize_batch, chunker.py:110-187, for a packed batch).  Stages
+ * the batch into context-owned pinned memory (several threads), copies it to
+ * the device in one H2D copy and launches the same encode as gpubpe_encode
+ * behind it (128 KiB .. 16 MiB: on the caller's stream while the copy is in
+ * flight, the tiles waiting for an arrival word); the kernel writes the ids
+ * and offsets straight into pinned, device-mapped host memory (the caller's
+ * h_out_ids when it comes from gpubpe_host_alloc) and its last CTA publishes
+ * the id count and counters there too, so the call returns as soon as they
+ * are visible (no device-to-host copy).  Batches above 64 MiB stream through
+ * a two-slot H2D / encode / D2H pipeline.  Synchronous for the caller.
  *   h_out_ids      capacity >= n_bytes (ids <= bytes)
  *   h_out_offs     n_docs+1 int64 CSR offsets of the ids
  *   n_ids_out      ids written
- *   kernel_ms      nullable: device time of the encode (CUDA events)
+ *   kernel_ms      nullable: device time of the encode (CUDA events; the
+ *                  host's enqueue-to-results time when the events are not
+ *                  complete yet)
  */
 int gpubpe_encode_host(gpubpe_ctx *ctx, const uint8_t *h_bytes, uint64_t n_bytes,
                        const int64_t *h_doc_offs, uint64_t n_docs, uint64_t max_seq_len,
