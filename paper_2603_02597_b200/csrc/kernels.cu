@@ -892,6 +892,7 @@ __device__ __noinline__ void place_range_one(const EncodeParams &P, CtaSmem &C, 
                                              unsigned long long hi, unsigned long long base) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int nt = (int)(hi - lo);
+    if (P.dbg && tid == 0) P.dbg[38000 + 4 * blockIdx.x] = gtimer();
     const uint32_t *slots = P.scratch + lo * SLOT;  // round 0: parity 0, t0 = 0
     const uint32_t *src = slots + (size_t)wid * SLOT;
     constexpr int PRE = 5;  // entries per lane fetched before the count is known (wt 128: <= 160)
@@ -902,6 +903,7 @@ __device__ __noinline__ void place_range_one(const EncodeParams &P, CtaSmem &C, 
         for (int j = 0; j < PRE; ++j) pre[j] = __ldcg(&src[lane + 32 * j]);
     }
     const uint32_t e = TW_ENTRIES(w);
+    if (P.dbg && lane == 0) atomicMax(&P.dbg[38000 + 4 * blockIdx.x + 1], gtimer() + (e & 0));
     uint32_t incl = e;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -925,8 +927,8 @@ __device__ __noinline__ void place_range_one(const EncodeParams &P, CtaSmem &C, 
         }
         for (uint32_t k = lane + 32 * PRE; k < n; k += 32) dst[k] = out_id(P.T, __ldcg(&src[k]));
         if (P.dbg && lane == 0) atomicMax(&P.dbg[36864 + 4 * blockIdx.x + 0], gtimer());
-        __syncwarp();
-        for (uint32_t k = lane; k < (n * 4 + 127) / 128; k += 32) l2_discard(src + 32 * k);
+        // (no L2 discard of the slot here: one discard per line costs ~1 us at the
+        // tail of a latency-bound call; these few MB are written back later)
         if (P.dbg && lane == 0) atomicMax(&P.dbg[36864 + 4 * blockIdx.x + 2], gtimer());
     }
     __syncthreads();

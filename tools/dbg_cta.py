@@ -39,3 +39,10 @@ if len(te):
     print("%-24s min %6.1f p50 %6.1f max %6.1f us (%d tiles)" % ("tile end", v.min(), np.median(v), v.max(), len(te)))
     v = (te[:, 0] - t0) / 1e3
     print("%-24s min %6.1f p50 %6.1f max %6.1f us" % ("tile start", v.min(), np.median(v), v.max()))
+pp = h[38000:38000 + 4 * 148].reshape(148, 4)
+for k, n in enumerate(["place_range_one entry", "tile words loaded (last warp)"]):
+    v = pp[:, k]
+    v = v[v > 0]
+    if len(v):
+        v = (v - t0) / 1e3
+        print("%-24s min %6.1f p50 %6.1f max %6.1f us" % (n, v.min(), np.median(v), v.max()))
