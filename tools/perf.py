@@ -75,6 +75,8 @@ def workloads():
         "adv_newlines_1m": lambda: adversarial("newlines", 1 << 20),
         "adv_aaaa_1m": lambda: adversarial("aaaa", 1 << 20),
         "adv_digit_docs_1000x10k": lambda: giant_docs(1000, 10000),
+        "adv_digits_64k": lambda: adversarial("digits", 1 << 16),
+        "adv_digit_docs_64x10k": lambda: giant_docs(64, 10000),
     }
 
 
@@ -137,6 +139,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--only", default="")
     ap.add_argument("--memo", type=int, default=1)
+    ap.add_argument("--strict", type=int, default=0,
+                    help="1: the engines take one merge per pass (as for a table that is not well-formed)")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--json", default="")
     args = ap.parse_args()
@@ -150,7 +154,7 @@ def main():
     peaks_p = ROOT / "MEASURED_PEAKS.json"
     peak = json.loads(peaks_p.read_text())["hbm_gbs"] if peaks_p.exists() else 6650.0
     tok = bpe.Tokenizer.from_files(*fixtures.gpt2_paths(), bpe.BlockConfig(max_seq_len=WHOLE, chunk_budget=WHOLE))
-    enc = tok.device_encoder(0, memo=bool(args.memo))
+    enc = tok.device_encoder(0, memo=bool(args.memo), strict=bool(args.strict))
     dev = torch.device("cuda", 0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
