@@ -721,6 +721,15 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_encode(gpubpe_ctx *
                        d_out_ids, d_out_offs, s, &checked);
 }
 
+// Host cores this process may use for its copy threads: the machine's, divided
+// among the ranks of one node (LOCAL_WORLD_SIZE, set by torchrun), at least 2.
+static unsigned host_cores_per_process() {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    const char *lw = getenv("LOCAL_WORLD_SIZE");
+    const unsigned ranks = lw ? (unsigned)std::max(1, atoi(lw)) : 1u;
+    return std::max(2u, hw / ranks);
+}
+
 // Host copies through pinned memory (staging, copy-out) on a small persistent
 // worker pool: the caller copies one chunk itself, workers the others.
 namespace {
@@ -761,7 +770,7 @@ class CopyPool {
 
   private:
     CopyPool() {
-        const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+        const unsigned hw = host_cores_per_process();
         const unsigned nw = std::min(7u, hw - 1);
         for (unsigned i = 0; i < nw; ++i) th_.emplace_back([this] { loop(); });
         for (auto &t : th_) t.detach();
@@ -843,7 +852,7 @@ class StagePool {
     static constexpr unsigned MAXP = 40;
     static constexpr unsigned long long BITS = (1ull << MAXP) - 1;
     StagePool() {
-        const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+        const unsigned hw = host_cores_per_process();
         const unsigned nw = std::min(7u, hw / 2 > 0 ? hw / 2 - 1 : 0u);  // host copies scale to ~8 threads
         for (unsigned i = 0; i < nw; ++i) th_.emplace_back([this] { loop(); });
         for (auto &t : th_) t.detach();
