@@ -30,7 +30,9 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef ENGINE_WALK
 #define ENGINE_WALK 64
+#endif
 
 struct EngineMem {
     uint32_t *tok, *tok2;  // tokens, double buffered
@@ -124,24 +126,54 @@ __device__ __forceinline__ uint32_t block_incl_max(uint32_t v, EngineShared &sh,
     return max(before, x);
 }
 
+// The blocking walks read their tokens, pair ranks and rl/rr in batches of
+// WALK_BATCH steps (all loads of a batch in flight together: two dependent
+// round trips per batch instead of per step), then decide the steps in order.
+#ifndef WALK_BATCH
+#define WALK_BATCH 4
+#endif
 __device__ __forceinline__ bool walk_left(const DevTables &T, const uint32_t *tok, const uint2 *pr,
                                           uint32_t j, uint32_t r) {
-    for (int step = 0; step < ENGINE_WALK; ++step) {
-        if (j == 0) return true;
-        if (__ldg(&T.rr[tok[j]]) > r) return true;
-        if (pr[j - 1].x < r) return false;
-        --j;
+    for (int step = 0; step < ENGINE_WALK; step += WALK_BATCH) {
+        uint32_t t[WALK_BATCH], pk[WALK_BATCH], bl[WALK_BATCH];
+#pragma unroll
+        for (int k = 0; k < WALK_BATCH; ++k) {
+            const bool in = (uint32_t)k < j;  // position j - k >= 1
+            t[k] = (uint32_t)k <= j ? tok[j - k] : 0u;
+            pk[k] = in ? pr[j - k - 1].x : GPUBPE_INF;
+        }
+#pragma unroll
+        for (int k = 0; k < WALK_BATCH; ++k) bl[k] = (uint32_t)k <= j ? __ldg(&T.rr[t[k]]) : 0u;
+#pragma unroll
+        for (int k = 0; k < WALK_BATCH; ++k) {
+            if (j == (uint32_t)k) return true;  // reached position 0
+            if (bl[k] > r) return true;
+            if (pk[k] < r) return false;
+        }
+        j -= WALK_BATCH;
     }
     return false;
 }
 
 __device__ __forceinline__ bool walk_right(const DevTables &T, const uint32_t *tok, const uint2 *pr,
                                            uint32_t j, uint32_t n, uint32_t r) {
-    for (int step = 0; step < ENGINE_WALK; ++step) {
-        if (j + 1 >= n) return true;
-        if (__ldg(&T.rl[tok[j]]) > r) return true;
-        if (pr[j].x < r) return false;
-        ++j;
+    for (int step = 0; step < ENGINE_WALK; step += WALK_BATCH) {
+        uint32_t t[WALK_BATCH], pk[WALK_BATCH], bl[WALK_BATCH];
+#pragma unroll
+        for (int k = 0; k < WALK_BATCH; ++k) {
+            const bool pair = j + k + 1 < n;  // token j + k has a right neighbour
+            t[k] = pair ? tok[j + k] : 0u;
+            pk[k] = pair ? pr[j + k].x : GPUBPE_INF;
+        }
+#pragma unroll
+        for (int k = 0; k < WALK_BATCH; ++k) bl[k] = j + k + 1 < n ? __ldg(&T.rl[t[k]]) : 0u;
+#pragma unroll
+        for (int k = 0; k < WALK_BATCH; ++k) {
+            if (j + k + 1 >= n) return true;
+            if (bl[k] > r) return true;
+            if (pk[k] < r) return false;
+        }
+        j += WALK_BATCH;
     }
     return false;
 }
