@@ -323,8 +323,9 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
     //         other warps watch the CTA's arrived mask in shared memory.
     if (P.arrive) {
         if (lane == 0) {
-            const uint32_t k0 = (uint32_t)((unsigned long long)(a > 0 ? a - 1 : 0) / P.piece);
-            const uint32_t k1 = (uint32_t)((unsigned long long)(a + nst - 1) / P.piece);
+            const bool one = P.piece >= P.n_bytes;  // (one piece: no division)
+            const uint32_t k0 = one ? 0u : (uint32_t)((unsigned long long)(a > 0 ? a - 1 : 0) / P.piece);
+            const uint32_t k1 = one ? 0u : (uint32_t)((unsigned long long)(a + nst - 1) / P.piece);
             const uint32_t need = (k1 >= 31 ? 0xFFFFFFFFu : ((2u << k1) - 1)) & ~((1u << k0) - 1);
             volatile uint32_t *arrived = &C.arrived;
             while ((*arrived & need) != need) {
@@ -1427,7 +1428,8 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
         if constexpr (kOneEach) {
             // placement ranges of q tiles; a finished tile adds itself to its range's word
             const bool fast = G <= (unsigned long long)RNG_MAX;
-            const unsigned long long q = (P.n_tiles + G - 1) / G;
+            // (32-bit: one round holds at most G * NW tiles; a 64-bit division is ~60 instructions)
+            const unsigned long long q = ((uint32_t)P.n_tiles + (uint32_t)G - 1) / (uint32_t)G;
             const unsigned long long t = t0 + (unsigned long long)wid * G + blockIdx.x;
             if (t < t1) {
                 const unsigned long long g0 = P.dbg ? gtimer() : 0;
@@ -1436,7 +1438,7 @@ __global__ void __launch_bounds__(NT, 1) k_encode(const __grid_constant__ Encode
                     __syncwarp();
                     // release (orders the warp's slot, tile word, document offsets and
                     // records before the add; no L1 invalidation, unlike __threadfence)
-                    if (lane == 0) red_release_add(&st->rng[t / q], (1ull << 40) | TW_ENTRIES(tw));
+                    if (lane == 0) red_release_add(&st->rng[(uint32_t)t / (uint32_t)q], (1ull << 40) | TW_ENTRIES(tw));
                 }
                 if (P.dbg && lane == 0 && t < 4096) {
                     P.dbg[1024 + 2 * t] = g0;
