@@ -297,6 +297,7 @@ def corpus_leg(args, mb: int, rank, world, local, dist, steps: int, warmup: int)
     import fixtures
     import synth_corpus
     import paper_2603_02597_b200 as bpe
+    from paper_2603_02597_b200 import device as bpe_device
 
     data, offs, (d0, d1), n_docs_all = synth_corpus.corpus_shard(mb << 20, rank, world, seed=0)
     n = len(data)
@@ -379,7 +380,9 @@ def corpus_leg(args, mb: int, rank, world, local, dist, steps: int, warmup: int)
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs x {world} GPU(s)" if p else "fallback"},
         "e2e": {"value": total_ids / e2e_s, "unit": UNIT, "h2d_bytes_per_step": total_bytes + 8 * (n_docs_all + 1),
                 "d2h_bytes_per_step": 4 * total_ids + 8 * (n_docs_all + 1), "steps": e2e_steps,
-                "input": "pinned host bytes", "output": "host ids (pageable beyond 8 GiB, else pooled pinned)",
+                "input": "pinned host bytes",
+                "output": ("host ids, pooled pinned result buffer" if 4 * n <= bpe_device._POOLED_MAX
+                           else "host ids, pageable result buffer (staged through pinned slots)"),
                 "path": "encode_packed_host (gpubpe_encode_host), wall clock, max over ranks"},
         "cpu_baseline": cpu, "clocks": clocks.summary(), "gpu_launches": steps,
     }

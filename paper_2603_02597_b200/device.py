@@ -9,6 +9,7 @@ method raises DeviceError when CUDA or the extension is unavailable.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -63,46 +64,68 @@ class _PinnedBlock:
             pass
 
 
+def _size_class(nbytes: int) -> int:
+    """Power-of-two classes up to 1 GiB, then whole GiB (a 43 GB result of a
+    10 GiB corpus shard must not pin 64 GiB)."""
+    if nbytes <= 1 << 30:
+        return 1 << max(20, int(nbytes - 1).bit_length())
+    return -(-nbytes // (1 << 30)) << 30
+
+
+def _pinned_limit() -> int:
+    """Largest result buffer kept in pinned memory: a quarter of physical RAM
+    split over the processes of this node (LOCAL_WORLD_SIZE), at least 8 GiB.
+    Results beyond it are pageable, and the streamed native path stages
+    their ids through its pinned slots (one host copy more)."""
+    try:
+        ram = os.sysconf("SC_PHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError, AttributeError):  # pragma: no cover
+        ram = 0
+    lws = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1") or 1))
+    return max(8 << 30, ram // (4 * lws))
+
+
 class _HostPool:
     """Recycled result buffers: pinned and device-mapped (gpubpe_host_alloc),
-    so the kernel writes the ids straight into them and nothing is copied out
+    so the device writes the ids straight into them and nothing is copied out
     on the host; reused across calls, so neither pinning nor page faults are
     paid per call.  A buffer returns here when its last result array dies."""
 
     def __init__(self, keep: int = 4):
-        self._free: dict[int, list[np.ndarray]] = {}
+        self._free: dict[tuple[int, bool], list[np.ndarray]] = {}
         self._keep = keep
         self._lock = threading.Lock()
-        self.pinned_max = 8 << 30  # larger result buffers are plain (pageable) host arrays
+        self.pinned_max = _pinned_limit()
+
+    def _pop(self, key):
+        with self._lock:
+            lst = self._free.get(key)
+            return lst.pop() if lst else None
 
     def take(self, nbytes: int, lib, device: int) -> np.ndarray:
-        cls = 1 << max(20, int(nbytes - 1).bit_length())
-        with self._lock:
-            lst = self._free.get(cls)
-            if lst:
-                return lst.pop()
+        cls = _size_class(nbytes)
+        buf = self._pop((cls, True))
+        if buf is not None:
+            return buf
         p = ctypes.c_void_p()
         if lib.gpubpe_host_alloc(device, cls, ctypes.byref(p)) == _native.OK and p.value:
             raw = (ctypes.c_uint8 * cls).from_address(p.value)
             raw._owner = _PinnedBlock(p.value, lib)  # freed when the last view of raw dies
             return np.frombuffer(raw, dtype=np.uint8)
-        return np.zeros(cls, dtype=np.uint8)  # pinned memory exhausted: the encode copies out
+        return self.take_pageable(nbytes)  # pinned memory exhausted: the encode copies out
 
     def take_pageable(self, nbytes: int) -> np.ndarray:
         """A plain host buffer (for results too large to pin), recycled like the
         pinned ones so its pages are faulted in once, not on every call."""
-        cls = 1 << max(20, int(nbytes - 1).bit_length())
-        with self._lock:
-            lst = self._free.get(-cls)
-            if lst:
-                return lst.pop()
-        return np.empty(cls, dtype=np.uint8)
+        cls = _size_class(nbytes)
+        buf = self._pop((cls, False))
+        return buf if buf is not None else np.empty(cls, dtype=np.uint8)
 
     def put(self, buf: np.ndarray) -> None:
-        key = buf.size if buf.size <= self.pinned_max else -buf.size
+        key = (buf.size, isinstance(buf.base, ctypes.Array))  # pinned blocks are views of a ctypes array
         with self._lock:
             lst = self._free.setdefault(key, [])
-            if len(lst) < (self._keep if 0 < key <= (256 << 20) else 1):
+            if len(lst) < (self._keep if buf.size <= (256 << 20) else 1):
                 lst.append(buf)
 
     def array(self, buf: np.ndarray, dtype, count: int) -> np.ndarray:
@@ -111,6 +134,13 @@ class _HostPool:
 
 _RESULTS = _HostPool()
 _POOLED_MAX = _RESULTS.pinned_max
+
+
+def _result_buffer(nbytes: int, lib, device: int) -> np.ndarray:
+    """The result buffer of one host encode: pinned up to _POOLED_MAX bytes."""
+    nbytes = max(int(nbytes), 4)
+    return (_RESULTS.take(nbytes, lib, device) if nbytes <= _POOLED_MAX
+            else _RESULTS.take_pageable(nbytes))
 
 
 def _hostlist():
@@ -375,9 +405,7 @@ class DeviceEncoder:
         lens = np.ascontiguousarray(lens, dtype=np.uint64)
         n_docs = len(lens)
         n = int(lens.sum())
-        pinned = 4 * n <= _POOLED_MAX
-        buf = (_RESULTS.take(4 * max(n, 1), self._lib, self.device) if pinned
-               else _RESULTS.take_pageable(4 * max(n, 1)))
+        buf = _result_buffer(4 * n, self._lib, self.device)
         ids = buf.view(np.uint32)
         out_offs = np.zeros(n_docs + 1, dtype=np.int64)
         n_ids = ctypes.c_uint64(0)
@@ -405,8 +433,7 @@ class DeviceEncoder:
         released, gpubpe_query).  The current CUDA stream of this device."""
         n = len(doc)
         units = 1 if n <= max_seq_len else -(-n // int(chunk_budget))
-        buf = (_RESULTS.take(4 * max(n, 1), self._lib, self.device) if 4 * n <= _POOLED_MAX
-               else _RESULTS.take_pageable(4 * max(n, 1)))
+        buf = _result_buffer(4 * n, self._lib, self.device)
         out_offs = np.empty(units + 1, dtype=np.int64)
         hl = _hostlist()
         if not getattr(hl, "_bound", False):
@@ -429,11 +456,9 @@ class DeviceEncoder:
         offs = np.ascontiguousarray(offs, dtype=np.int64)
         n = int(data.size)
         n_docs = int(offs.size) - 1
-        # large batches stream through the native pipeline, which copies the ids
-        # out part by part: a plain (recycled) host array is enough there
-        pinned = 4 * n <= _POOLED_MAX
-        buf = (_RESULTS.take(4 * max(n, 1), self._lib, self.device) if pinned
-               else _RESULTS.take_pageable(4 * max(n, 1)))
+        # large batches stream through the native pipeline, part by part: into
+        # this buffer directly when pinned, else through its pinned slots
+        buf = _result_buffer(4 * n, self._lib, self.device)
         ids = buf.view(np.uint32)
         out_offs = np.zeros(max(n_docs + 1, 1), dtype=np.int64)
         n_ids = ctypes.c_uint64(0)
@@ -443,7 +468,7 @@ class DeviceEncoder:
                 self.set_mode(mode)
             s = torch.cuda.current_stream(self.device)
             try:
-                    rc = self._lib.gpubpe_encode_host(self._h, _ptr(data), n, _ptr(offs), n_docs,
+                rc = self._lib.gpubpe_encode_host(self._h, _ptr(data), n, _ptr(offs), n_docs,
                                                   int(max_seq_len), int(chunk_budget), _ptr(ids),
                                                   _ptr(out_offs), ctypes.byref(n_ids), ctypes.byref(ms),
                                                   s.cuda_stream)
