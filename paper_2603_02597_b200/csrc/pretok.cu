@@ -42,7 +42,10 @@ namespace {
 constexpr int PT = 256;      // threads per CTA
 constexpr int BACK = 24;     // bytes decoded before a word (>= 4 code points of context)
 constexpr int AHEAD = 12;    // bytes decoded after it (2 code points of lookahead)
-constexpr int WIN = 32 + BACK + AHEAD;
+#ifndef GPUBPE_PRETOK_PW
+#define GPUBPE_PRETOK_PW 2
+#endif
+constexpr int PW = GPUBPE_PRETOK_PW;  // words per thread
 
 enum : uint8_t { C_O = 0, C_L = 1, C_N = 2, C_S = 3 };
 
@@ -217,79 +220,11 @@ __device__ __forceinline__ uint32_t rules_swar(const uint32_t (&x)[10]) {
     return bits;
 }
 
-}  // namespace
-
-__global__ void __launch_bounds__(PT, 4) k_pretok(const __grid_constant__ PretokParams Q) {
-    __shared__ uint8_t sasc[128];
-    __shared__ long long sdoc[2];  // documents holding the CTA's first and last byte
-    if (threadIdx.x < 128) sasc[threadIdx.x] = Q.ascii[threadIdx.x];
-    if (threadIdx.x < 64) {  // warps 0 / 1: 32-ary searches for the CTA's first / last byte
-        const int wsel = threadIdx.x >> 5, ln = threadIdx.x & 31;
-        const long long nb = (long long)Q.n_bytes;
-        const long long q = min(nb - 1, ((long long)blockIdx.x * PT + (wsel ? PT - 1 : 0)) * 32 + (wsel ? 31 : 0));
-        long long lo = 0, hi = (long long)Q.n_docs - 1;  // last d in [lo, hi] with offs[d] <= q
-        while (hi > lo) {
-            const long long step = (hi - lo + 32) / 32;
-            const long long idx = lo + (long long)ln * step;
-            const bool ok = idx <= hi && __ldg(&Q.doc_offs[idx]) <= q;
-            const unsigned m = __ballot_sync(FULL_MASK, ok);  // lane 0 always holds
-            lo = lo + (long long)(31 - __clz(m)) * step;
-            hi = min(hi, lo + step - 1);
-        }
-        if (ln == 0) sdoc[wsel] = lo;
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const unsigned long long w = (unsigned long long)blockIdx.x * PT + threadIdx.x;
-    const long long n = (long long)Q.n_bytes;
-    const long long p0 = (long long)w * 32, p1 = min(p0 + 32, n);
-    const bool active = w < Q.n_words;
-    // ---- the 48-byte window [p0 - 8, p0 + 40), 0 outside [0, n)
-    unsigned long long win[6];
-    const bool aligned = ((reinterpret_cast<uintptr_t>(Q.bytes) & 15) == 0);
-    if (active && aligned && p0 + 32 <= n) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(Q.bytes + p0);
-        const uint4 u = __ldg(src), v = __ldg(src + 1);
-        win[1] = ((unsigned long long)u.y << 32) | u.x;
-        win[2] = ((unsigned long long)u.w << 32) | u.z;
-        win[3] = ((unsigned long long)v.y << 32) | v.x;
-        win[4] = ((unsigned long long)v.w << 32) | v.z;
-    } else {
-#pragma unroll
-        for (int k = 1; k < 5; ++k) {
-            unsigned long long x = 0;
-            for (int b = 7; b >= 0; --b) {
-                const long long p = p0 + 8 * (k - 1) + b;
-                x = (x << 8) | ((active && p < n) ? __ldg(&Q.bytes[p]) : 0u);
-            }
-            win[k] = x;
-        }
-    }
-    win[0] = __shfl_up_sync(FULL_MASK, win[4], 1);
-    win[5] = __shfl_down_sync(FULL_MASK, win[1], 1);
-    if (lane == 0 || lane == 31) {
-        const int k = lane == 0 ? 0 : 5;
-        const long long q = lane == 0 ? p0 - 8 : p0 + 32;
-        unsigned long long x = 0;
-        if (aligned && q >= 0 && q + 8 <= n) {
-            x = __ldg(reinterpret_cast<const unsigned long long *>(Q.bytes + q));
-        } else {
-            for (int b = 7; b >= 0; --b) {
-                const long long p = q + b;
-                x = (x << 8) | ((active && p >= 0 && p < n) ? __ldg(&Q.bytes[p]) : 0u);
-            }
-        }
-        win[k] = x;
-    }
-    if (!active) return;
-    // the document holding byte p0 (last d with offs[d] <= p0; empty documents skipped)
-    long long lo = sdoc[0], hi = sdoc[1];
-    while (lo < hi) {
-        const long long mid = (lo + hi + 1) >> 1;
-        if (__ldg(&Q.doc_offs[mid]) <= p0) lo = mid; else hi = mid - 1;
-    }
-    long long d = lo;
-    while (__ldg(&Q.doc_offs[d + 1]) <= p0) ++d;
+// Token-start bits of the word [p0, p1) of documents d.. from its 48-byte
+// window: the SWAR path, the bit-parallel mask paths, else the scalar code
+// point path.
+__device__ __forceinline__ uint32_t word_bits(const PretokParams &Q, const uint8_t *sasc, long long p0,
+                                              long long p1, const unsigned long long (&win)[6], long long d) {
     if (Q.ascii_std) {
         const long long ds = __ldg(&Q.doc_offs[d]), de = __ldg(&Q.doc_offs[d + 1]);
         if ((Q.paths & 1) && ds <= p0 - 4 && de >= p0 + 36) {
@@ -301,10 +236,7 @@ __global__ void __launch_bounds__(PT, 4) k_pretok(const __grid_constant__ Pretok
                 hb |= x[i];
                 ap |= rng4(x[i] & 0x7F7F7F7Fu, ~x[i] & 0x80808080u, '\'', '\'');
             }
-            if (((hb & 0x80808080u) | ap) == 0) {
-                Q.out[w] = rules_swar(x);
-                return;
-            }
+            if (((hb & 0x80808080u) | ap) == 0) return rules_swar(x);
         }
         // every document meeting [p0, p1) in turn, on the bit-parallel masks restricted to it
         const Masks M = build_masks(win);
@@ -335,24 +267,26 @@ __global__ void __launch_bounds__(PT, 4) k_pretok(const __grid_constant__ Pretok
             }
             if (s1 >= p1) break;
         }
-        if (ok) {
-            Q.out[w] = bits;
-            return;
-        }
+        if (ok) return bits;
     }
     uint32_t bits = 0;
-    uint8_t cl[WIN], ch[WIN];
-    int16_t at[WIN];
     for (long long pos = p0; pos < p1;) {
         while (__ldg(&Q.doc_offs[d + 1]) <= pos) ++d;  // skip empty documents
         const long long ds = __ldg(&Q.doc_offs[d]), de = __ldg(&Q.doc_offs[d + 1]);
         const long long seg_end = min(p1, de);
-        // decode the code points of [q, min(de, seg_end + AHEAD)) of this document
+        // the code points of [q, min(de, seg_end + AHEAD)) of this document, streamed
+        // through a register window: slot 4 = code point k (the one decided), slots
+        // 0-3 = k-4 .. k-1, slot 5 = k+1 (v5: it exists)
         long long q = max(ds, pos - BACK);
         while (q > ds && q < pos && (__ldg(&Q.bytes[q]) & 0xC0u) == 0x80u) ++q;
         const long long qe = min(de, seg_end + AHEAD);
-        int m = 0;
-        for (long long i = q; i < qe && m < WIN;) {
+        const bool text_start = q == ds;  // code point 0 is the document's first
+        uint8_t C[6] = {0, 0, 0, 0, 0, 0}, A[6] = {0, 0, 0, 0, 0, 0};
+        long long P4 = 0, P5 = 0, i = q;
+        bool v5 = false;
+        auto next_cp = [&]() {  // decode the code point at byte i into slot 5
+            v5 = i < qe;
+            if (!v5) return;
             const uint32_t b0 = __ldg(&Q.bytes[i]);
             long long j = i + 1;
             while (j < de && (__ldg(&Q.bytes[j]) & 0xC0u) == 0x80u) ++j;  // continuation bytes join
@@ -368,53 +302,158 @@ __global__ void __launch_bounds__(PT, 4) k_pretok(const __grid_constant__ Pretok
                     c = cp_class(Q, cp);
                 }
             }
-            cl[m] = c;
-            ch[m] = a;
-            at[m] = (int16_t)(i - p0);
-            ++m;
+            C[5] = c;
+            A[5] = a;
+            P5 = i;
             i = j;
-        }
-        const bool text_start = q == ds;  // cl[0] is the document's first code point
-        auto tstart = [&](int j) -> bool {  // token start before code point j (apostrophe test)
-            if (j == 0) return text_start;
-            return cl[j - 1] == C_L || cl[j - 1] == C_N || (cl[j - 1] == C_S && ch[j - 1] != ' ');
         };
-        auto clen = [&](int j) -> int {  // contraction starting at code point j: its length, else 0
-            if (j < 0 || j >= m || ch[j] != '\'' || !tstart(j)) return 0;
-            const uint8_t a = j + 1 < m ? ch[j + 1] : 0, b = j + 2 < m ? ch[j + 2] : 0;
-            if (a == 's' || a == 'd' || a == 'm' || a == 't') return 2;
-            if ((a == 'l' && b == 'l') || (a == 'v' && b == 'e') || (a == 'r' && b == 'e')) return 3;
-            return 0;
-        };
-        for (int k = 0; k < m; ++k) {
-            const long long p = p0 + at[k];
-            if (p < pos) continue;
-            if (p >= seg_end) break;
+        next_cp();
+        for (long long k = 0; v5; ++k) {
+#pragma unroll
+            for (int t = 0; t < 5; ++t) {
+                C[t] = C[t + 1];
+                A[t] = A[t + 1];
+            }
+            P4 = P5;
+            next_cp();
+            if (P4 >= seg_end) break;
+            if (P4 < pos) continue;
+            // token start before code point j (in slot s): the apostrophe test
+            auto tstart = [&](long long j, int s) -> bool {
+                if (j == 0) return text_start;
+                return C[s - 1] == C_L || C[s - 1] == C_N || (C[s - 1] == C_S && A[s - 1] != ' ');
+            };
+            auto clen = [&](long long j, int s) -> int {  // contraction at code point j: its length, else 0
+                if (j < 0 || A[s] != '\'' || !tstart(j, s)) return 0;
+                const uint8_t a = (s + 1 < 5 || v5) ? A[s + 1] : 0, b = (s + 2 < 5 || v5) ? A[s + 2] : 0;
+                if (a == 's' || a == 'd' || a == 'm' || a == 't') return 2;
+                if ((a == 'l' && b == 'l') || (a == 'v' && b == 'e') || (a == 'r' && b == 'e')) return 3;
+                return 0;
+            };
             bool b;
             if (k == 0) {
                 b = text_start;  // (a word never starts BACK bytes into a document's interior)
-            } else if (cl[k] == C_S) {
-                b = cl[k - 1] != C_S || (k + 1 < m && cl[k + 1] != C_S);
-            } else if (cl[k - 1] == C_S) {
-                b = ch[k - 1] != ' ';
-            } else if (clen(k - 1)) {
+            } else if (C[4] == C_S) {
+                b = C[3] != C_S || (v5 && C[5] != C_S);
+            } else if (C[3] == C_S) {
+                b = A[3] != ' ';
+            } else if (clen(k - 1, 3)) {
                 b = false;
-            } else if (clen(k - 2) == 3) {
+            } else if (clen(k - 2, 2) == 3) {
                 b = false;
-            } else if (clen(k - 2) == 2 || clen(k - 3) == 3) {
+            } else if (clen(k - 2, 2) == 2 || clen(k - 3, 1) == 3) {
                 b = true;
             } else {
-                b = cl[k] != cl[k - 1];
+                b = C[4] != C[3];
             }
-            if (b) bits |= 1u << at[k];
+            if (b) bits |= 1u << (uint32_t)(P4 - p0);
         }
         pos = seg_end;
     }
-    Q.out[w] = bits;
+    return bits;
+}
+
+// The 32 bytes [p0, p0 + 32) as four little-endian words (0 past n), and for
+// lanes 0 / 31 the 8 bytes before / after them (the warp's window edges).
+__device__ __forceinline__ void load_word(const PretokParams &Q, long long p0, bool active, int lane,
+                                          unsigned long long (&r)[4], unsigned long long &edge) {
+    const long long n = (long long)Q.n_bytes;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(Q.bytes) & 15) == 0);
+    if (active && aligned && p0 + 32 <= n) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(Q.bytes + p0);
+        const uint4 u = __ldg(src), v = __ldg(src + 1);
+        r[0] = ((unsigned long long)u.y << 32) | u.x;
+        r[1] = ((unsigned long long)u.w << 32) | u.z;
+        r[2] = ((unsigned long long)v.y << 32) | v.x;
+        r[3] = ((unsigned long long)v.w << 32) | v.z;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            unsigned long long x = 0;
+            for (int b = 7; b >= 0; --b) {
+                const long long p = p0 + 8 * k + b;
+                x = (x << 8) | ((active && p < n) ? __ldg(&Q.bytes[p]) : 0u);
+            }
+            r[k] = x;
+        }
+    }
+    edge = 0;
+    if (lane == 0 || lane == 31) {
+        const long long q = lane == 0 ? p0 - 8 : p0 + 32;
+        if (aligned && q >= 0 && q + 8 <= n) {
+            edge = __ldg(reinterpret_cast<const unsigned long long *>(Q.bytes + q));
+        } else {
+            for (int b = 7; b >= 0; --b) {
+                const long long p = q + b;
+                edge = (edge << 8) | ((active && p >= 0 && p < n) ? __ldg(&Q.bytes[p]) : 0u);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+#ifndef GPUBPE_PRETOK_MINB
+#define GPUBPE_PRETOK_MINB 4
+#endif
+// PW words per thread: word k of thread t is the CTA's word k * PT + t (coalesced
+// rows); every word's bytes are loaded before the document search and the barrier.
+__global__ void __launch_bounds__(PT, GPUBPE_PRETOK_MINB) k_pretok(const __grid_constant__ PretokParams Q) {
+    __shared__ uint8_t sasc[128];
+    __shared__ long long sdoc[2];  // documents holding the CTA's first and last byte
+    const int lane = threadIdx.x & 31;
+    const unsigned long long w0 = (unsigned long long)blockIdx.x * (PT * PW) + threadIdx.x;
+    unsigned long long r[PW][4], edge[PW];
+#pragma unroll
+    for (int k = 0; k < PW; ++k)
+        load_word(Q, (long long)(w0 + k * PT) * 32, w0 + k * PT < Q.n_words, lane, r[k], edge[k]);
+    if (threadIdx.x < 128) sasc[threadIdx.x] = Q.ascii[threadIdx.x];
+    if (threadIdx.x < 64) {  // warps 0 / 1: 32-ary searches for the CTA's first / last byte
+        const int wsel = threadIdx.x >> 5, ln = threadIdx.x & 31;
+        const long long nb = (long long)Q.n_bytes;
+        const long long q =
+            min(nb - 1, ((long long)blockIdx.x * PT * PW + (wsel ? PT * PW - 1 : 0)) * 32 + (wsel ? 31 : 0));
+        long long lo = 0, hi = (long long)Q.n_docs - 1;  // last d in [lo, hi] with offs[d] <= q
+        while (hi > lo) {
+            const long long step = (hi - lo + 32) / 32;
+            const long long idx = lo + (long long)ln * step;
+            const bool ok = idx <= hi && __ldg(&Q.doc_offs[idx]) <= q;
+            const unsigned m = __ballot_sync(FULL_MASK, ok);  // lane 0 always holds
+            lo = lo + (long long)(31 - __clz(m)) * step;
+            hi = min(hi, lo + step - 1);
+        }
+        if (ln == 0) sdoc[wsel] = lo;
+    }
+    __syncthreads();
+    const long long n = (long long)Q.n_bytes;
+    long long d = sdoc[0];
+    const long long dhi = sdoc[1];
+#pragma unroll
+    for (int k = 0; k < PW; ++k) {
+        const unsigned long long w = w0 + k * PT;
+        unsigned long long win[6];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) win[j + 1] = r[k][j];
+        win[0] = __shfl_up_sync(FULL_MASK, win[4], 1);
+        win[5] = __shfl_down_sync(FULL_MASK, win[1], 1);
+        if (lane == 0) win[0] = edge[k];
+        if (lane == 31) win[5] = edge[k];
+        if (w >= Q.n_words) break;
+        const long long p0 = (long long)w * 32, p1 = min(p0 + 32, n);
+        // the document holding byte p0 (last d with offs[d] <= p0; empty documents
+        // skipped): a thread's words ascend, so the search resumes from the last one
+        long long hi = dhi;
+        while (d < hi) {
+            const long long mid = (d + hi + 1) >> 1;
+            if (__ldg(&Q.doc_offs[mid]) <= p0) d = mid; else hi = mid - 1;
+        }
+        while (__ldg(&Q.doc_offs[d + 1]) <= p0) ++d;
+        Q.out[w] = word_bits(Q, sasc, p0, p1, win, d);
+    }
 }
 
 cudaError_t launch_pretok(const PretokParams &Q, cudaStream_t s) {
     if (Q.n_words == 0) return cudaSuccess;
-    k_pretok<<<(unsigned int)((Q.n_words + PT - 1) / PT), PT, 0, s>>>(Q);
+    k_pretok<<<(unsigned int)((Q.n_words + PT * PW - 1) / (PT * PW)), PT, 0, s>>>(Q);
     return cudaGetLastError();
 }
