@@ -325,7 +325,7 @@ __device__ __forceinline__ uint32_t comp(const uint4 &v, int j) {
 }
 
 // OR 16 bytes (v) into the stage at byte position p, touching only the words
-// that hold bytes [p, p + n)
+// that hold bytes [p, p + n) (32-bit ORs: shared-memory 64-bit ORs measured 1.4x slower)
 __device__ __forceinline__ void or16(uint32_t *sw, uint32_t p, const uint4 &v, uint32_t n) {
     const uint32_t sh = 8 * (p & 3), wi = p >> 2, nw = ((p & 3) + n + 3) >> 2;
     atomicOr(&sw[wi], v.x << sh);
@@ -352,6 +352,19 @@ __device__ __forceinline__ long long warp_lower_bound(const long long *a, long l
 }
 }  // namespace
 
+// the 16-B records of row r's ids (lane's ids [4 lane, 4 lane + 4)); unknown ids
+// and ids past the end: length 0 (the first pass reported unknown ones)
+__device__ __forceinline__ void load_recs(const DecodeParams &P, unsigned long long r, int lane, const uint4 &idv,
+                                          uint4 (&rec)[RDPT]) {
+    const unsigned long long i0 = r * RROW + (unsigned long long)lane * RDPT;
+#pragma unroll
+    for (int j = 0; j < RDPT; ++j) {
+        const uint32_t id = comp(idv, j);
+        rec[j] = make_uint4(0, 0, 0, 0);
+        if (i0 + j < P.n_ids && id < P.n_vocab) rec[j] = __ldg(&P.vrec[id]);
+    }
+}
+
 struct RowSmem {
     __align__(16) uint8_t stage[RW][SOFF + STW + 48];
 };
@@ -373,30 +386,25 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
     if (r0 >= r1) return;
     long long cur = P.n_seqs ? warp_lower_bound(P.id_offs, 0, (long long)P.n_seqs + 1, r0 * RROW, lane) : 0;
     uint4 idv = load_ids4(P, r0, lane);
+    unsigned long long next_start = P.n_seqs && cur <= (long long)P.n_seqs ? (unsigned long long)__ldg(&P.id_offs[cur]) : ~0ull;
+
     // carry_lo >= 0: stage chunk 0 holds the previous row's last, partial 16-B chunk,
     // whose bytes from carry_lo on are ours (the warp's rows are contiguous, so only
     // the range's first and last chunks are shared with other warps)
     int carry_lo = -1;
     __syncwarp();
     for (unsigned long long r = r0; r < r1; ++r) {
-        uint4 nidv = make_uint4(0, 0, 0, 0);
-        if (r + 1 < r1) nidv = load_ids4(P, r + 1, lane);
         const unsigned long long t = r / RPT;
         const uint32_t rr = (uint32_t)(r % RPT);
         uint32_t pb = lane < (int)rr ? __ldg(&P.row_bytes[t * RPT + lane]) : 0u;
         const unsigned long long tb = __ldg(&P.tile_base[t]);
-        const unsigned long long i0 = r * RROW + (unsigned long long)lane * RDPT;
         uint4 rec[RDPT];
+        uint4 nidv = make_uint4(0, 0, 0, 0);
+        if (r + 1 < r1) nidv = load_ids4(P, r + 1, lane);
+        load_recs(P, r, lane, idv, rec);
         uint32_t sum = 0;
 #pragma unroll
-        for (int j = 0; j < RDPT; ++j) {
-            const uint32_t id = comp(idv, j);
-            rec[j] = make_uint4(0, 0, 0, 0);  // unknown ids: length 0 (the first pass reported them)
-            if (i0 + j < P.n_ids) {
-                if (id < P.n_vocab) rec[j] = __ldg(&P.vrec[id]);
-            }
-            sum += rec[j].x & 0xFFu;
-        }
+        for (int j = 0; j < RDPT; ++j) sum += rec[j].x & 0xFFu;
         uint32_t x = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -474,7 +482,9 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
                 reinterpret_cast<uint4 *>(stage + SOFF)[q] = make_uint4(0, 0, 0, 0);
             }
         }
-        if (P.n_seqs) {  // byte offsets of the sequences that start in this row
+        // byte offsets of the sequences that start in this row (next_start: the
+        // first sequence start not yet written, the same in every lane)
+        if (P.n_seqs && (next_start < (r + 1) * RROW || r + 1 == n_rows)) {
             const unsigned long long rowlo = r * RROW, rowhi = rowlo + RROW;
             const bool last = r + 1 == n_rows;
             for (;;) {
@@ -499,6 +509,7 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
                 cur += __popc(m);
                 if (m != FULL_MASK) break;
             }
+            next_start = cur <= (long long)P.n_seqs ? (unsigned long long)__ldg(&P.id_offs[cur]) : ~0ull;
         }
         if (r + 1 == n_rows && lane == 0) P.st->n_bytes = base + total;
         __syncwarp();
@@ -578,12 +589,24 @@ __global__ void __launch_bounds__(256) k_dec_tile_bytes(const __grid_constant__ 
     }
 }
 
+// one CTA: exclusive scan of the tile byte totals.  Up to SCAN_SMEM tiles (117 M
+// ids) the totals are staged in shared memory by coalesced loads, each thread
+// scans a contiguous run there and the bases leave by coalesced stores; larger
+// batches scan in global memory directly.
+constexpr unsigned SCAN_SMEM = 28 << 10;  // tiles (224 KiB of u64)
 __global__ void __launch_bounds__(1024) k_dec_scan(const unsigned long long *tile_bytes, unsigned long long n,
                                                    unsigned long long *tile_base) {
+    extern __shared__ unsigned long long sscan[];
     __shared__ unsigned long long wsum[32];
+    const bool staged = n <= SCAN_SMEM;
+    if (staged)
+        for (unsigned long long i = threadIdx.x; i < n; i += 1024) sscan[i] = __ldg(&tile_bytes[i]);
+    __syncthreads();
+    const unsigned long long *src = staged ? sscan : tile_bytes;
+    unsigned long long *dst = staged ? sscan : tile_base;
     const unsigned long long per = (n + 1023) / 1024, lo = min(n, threadIdx.x * per), hi = min(n, lo + per);
     unsigned long long s = 0;
-    for (unsigned long long i = lo; i < hi; ++i) s += tile_bytes[i];
+    for (unsigned long long i = lo; i < hi; ++i) s += src[i];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned long long x = s;
 #pragma unroll
@@ -605,8 +628,13 @@ __global__ void __launch_bounds__(1024) k_dec_scan(const unsigned long long *til
     __syncthreads();
     unsigned long long run = wsum[wid] + x - s;
     for (unsigned long long i = lo; i < hi; ++i) {
-        tile_base[i] = run;
-        run += tile_bytes[i];
+        const unsigned long long t = src[i];
+        dst[i] = run;
+        run += t;
+    }
+    if (staged) {
+        __syncthreads();
+        for (unsigned long long i = threadIdx.x; i < n; i += 1024) tile_base[i] = sscan[i];
     }
 }
 
@@ -614,7 +642,8 @@ cudaError_t launch_decode_offsets(const DecodeParams &P, unsigned long long *til
                                   unsigned long long *tile_base, cudaStream_t s) {
     if (P.n_tiles == 0) return cudaSuccess;
     k_dec_tile_bytes<<<(unsigned int)P.n_tiles, 256, 0, s>>>(P, tile_bytes);
-    k_dec_scan<<<1, 1024, 0, s>>>(tile_bytes, P.n_tiles, tile_base);
+    const size_t sm = P.n_tiles <= SCAN_SMEM ? P.n_tiles * sizeof(unsigned long long) : 0;
+    k_dec_scan<<<1, 1024, sm, s>>>(tile_bytes, P.n_tiles, tile_base);
     return cudaGetLastError();
 }
 
@@ -623,6 +652,9 @@ int decode_tile_ids() { return TD; }
 
 cudaError_t setup_decode() {
     cudaError_t e = cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_dec_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(SCAN_SMEM * sizeof(unsigned long long)));
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_decode_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
 }
