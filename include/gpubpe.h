@@ -144,6 +144,8 @@ int gpubpe_query(gpubpe_ctx *ctx, void *stream, gpubpe_stats *out);
  * and Tokenizer.decode, chunker.py:100-101).
  * gpubpe_set_vocab: the byte string of every decodable id (n strings; ids
  *   absent here, or with symbols containing non-byte characters, are unknown).
+ *   Empty strings (an empty symbol decodes to no bytes) and strings of any
+ *   length below 2 GiB are decodable.
  * gpubpe_decode: d_ids[n_ids] as n_seqs sequences (d_id_offs[n_seqs+1] CSR;
  *   n_seqs == 0: one sequence, no offsets) -> their byte strings back to back
  *   in d_out (capacity out_cap) with d_out_offs[n_seqs+1].  Synchronises.

@@ -135,8 +135,9 @@ class Tokenizer:
 
     def _symbol_bytes(self):
         """(ids uint32[], blob uint8[], offs uint64[]) of every id whose symbol maps
-        to a nonempty byte string (symbol_bytes semantics), vectorised: all
-        symbols are translated at once through a code point -> byte table."""
+        to a byte string -- empty symbols included, as b"" (decode_tokens,
+        byte_codec.py:121-146) -- vectorised: all symbols are translated at
+        once through a code point -> byte table."""
         cached = getattr(self, "_sym_cache", None)
         if cached is not None:
             return cached
@@ -155,7 +156,7 @@ class Tokenizer:
         seg = np.repeat(np.arange(n), lens)  # symbol index of every character
         bad = np.zeros(n, dtype=bool)
         bad[seg[val < 0]] = True
-        keep = (lens > 0) & ~bad
+        keep = ~bad
         blob = val[keep[seg]].astype(np.uint8) if cps.size else np.empty(0, np.uint8)
         offs = np.zeros(int(keep.sum()) + 1, dtype=np.uint64)
         np.cumsum(lens[keep], out=offs[1:])

@@ -65,6 +65,8 @@ struct gpubpe_ctx {
     uint8_t *d_vblob = nullptr;
     uint4 *d_vrec = nullptr;
     uint8_t *d_vlen = nullptr;
+    uint32_t *d_vlong = nullptr;
+    bool vocab_ext = false;  // decode vocabulary with empty or >= 255-byte strings
     uint32_t n_vocab_dec = 0;
     DevBuf dec_state, dec_status, dec_tiles;  // dec_tiles: tile byte totals + offsets (two-pass)
     // GPT-2 regex pre-tokenization (optional mode)
@@ -1619,32 +1621,42 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_set_vocab(gpubpe_ct
     for (uint64_t i = 0; i < n; ++i) max_id = std::max<uint64_t>(max_id, ids[i]);
     if (n && max_id >= (1ull << 26)) return fail(ctx, GPUBPE_EINVAL, "decode: ids must be < 2^26");
     // strings 16-B aligned and zero-padded: the kernel fetches them with 16-B loads;
-    // vinfo = (offset / 16) << 8 | length
-    std::vector<uint32_t> vinfo(n ? max_id + 1 : 1, GPUBPE_INF);
+    // vinfo = (offset / 16) << 8 | min(length, LEN_EXT); every length (empty symbols
+    // and strings of any size included, decode_tokens semantics) in vlong
+    std::vector<uint32_t> vinfo(n ? max_id + 1 : 1, GPUBPE_INF), vlong(vinfo.size(), 0);
     std::vector<uint8_t> blob;
     for (uint64_t i = 0; i < n; ++i) {
         const uint64_t len = offs[i + 1] - offs[i];
-        if (len == 0 || len > 255) continue;  // not decodable as bytes
+        if (len >= (1ull << 31)) return fail(ctx, GPUBPE_EINVAL, "decode: a vocab string exceeds 2 GiB");
         const uint64_t at = blob.size();
         if ((at >> 4) >= (1ull << 24)) return fail(ctx, GPUBPE_EINVAL, "decode: vocab strings exceed 256 MiB");
         blob.insert(blob.end(), bytes + offs[i], bytes + offs[i + 1]);
         blob.resize((blob.size() + 15) & ~(size_t)15, 0);
-        vinfo[ids[i]] = (uint32_t)((at >> 4) << 8) | (uint32_t)len;
+        vinfo[ids[i]] = (uint32_t)((at >> 4) << 8) | (uint32_t)std::min<uint64_t>(len, LEN_EXT);
+        vlong[ids[i]] = (uint32_t)len;
     }
     blob.resize(blob.size() + 16, 0);
     const uint64_t blob_b = blob.size();
     // per id: a 16-B record (length byte, then the string if it fits, else its
-    // blob chunk) and a 1-byte length table (the two-pass decode's first pass)
+    // blob chunk and length) and a 1-byte length table (the two-pass decode's
+    // first pass; LEN_EXT for empty and >= 255-byte strings, 0 for unknown ids)
     std::vector<uint8_t> vrec(vinfo.size() * 16, 0), vlen(vinfo.size(), 0);
+    bool ext = false;
     for (size_t i = 0; i < vinfo.size(); ++i) {
         if (vinfo[i] == GPUBPE_INF) continue;
-        const uint32_t len = vinfo[i] & 0xFFu, chunk = vinfo[i] >> 8;
+        const uint32_t len = vlong[i], chunk = vinfo[i] >> 8;
         uint8_t *r = &vrec[16 * i];
-        r[0] = (uint8_t)len;
-        if (len <= 15) memcpy(r + 1, &blob[16ull * chunk], len);
-        else memcpy(r + 4, &chunk, 4);
-        vlen[i] = (uint8_t)len;
+        r[0] = (uint8_t)std::min<uint32_t>(len, LEN_EXT);
+        if (len <= 15) {
+            memcpy(r + 1, &blob[16ull * chunk], len);
+        } else {
+            memcpy(r + 4, &chunk, 4);
+            memcpy(r + 8, &len, 4);
+        }
+        vlen[i] = (uint8_t)(len == 0 || len >= LEN_EXT ? LEN_EXT : len);
+        ext = ext || vlen[i] == LEN_EXT;
     }
+    ctx->vocab_ext = ext;
     if (ctx->d_vrec) cudaFree(ctx->d_vrec);
     if (ctx->d_vlen) cudaFree(ctx->d_vlen);
     ctx->d_vrec = nullptr;
@@ -1653,6 +1665,10 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_set_vocab(gpubpe_ct
     CK(cudaMemcpy(ctx->d_vrec, vrec.data(), vrec.size(), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&ctx->d_vlen, vlen.size()));
     CK(cudaMemcpy(ctx->d_vlen, vlen.data(), vlen.size(), cudaMemcpyHostToDevice));
+    if (ctx->d_vlong) cudaFree(ctx->d_vlong);
+    ctx->d_vlong = nullptr;
+    CK(cudaMalloc(&ctx->d_vlong, vlong.size() * 4));
+    CK(cudaMemcpy(ctx->d_vlong, vlong.data(), vlong.size() * 4, cudaMemcpyHostToDevice));
     if (ctx->d_vinfo) cudaFree(ctx->d_vinfo);
     if (ctx->d_vblob) cudaFree(ctx->d_vblob);
     ctx->d_vinfo = nullptr;
@@ -1714,6 +1730,8 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_decode(gpubpe_ctx *
     P.blob = ctx->d_vblob;
     P.vrec = ctx->d_vrec;
     P.vlen = ctx->d_vlen;
+    P.vlong = ctx->d_vlong;
+    P.ext = ctx->vocab_ext ? 1u : 0u;
     P.n_vocab = ctx->n_vocab_dec;
     P.ids = d_ids;
     P.n_ids = n_ids;
@@ -1948,6 +1966,7 @@ extern "C" __attribute__((visibility("default"))) void gpubpe_ctx_destroy(gpubpe
     if (ctx->d_vblob) cudaFree(ctx->d_vblob);
     if (ctx->d_vrec) cudaFree(ctx->d_vrec);
     if (ctx->d_vlen) cudaFree(ctx->d_vlen);
+    if (ctx->d_vlong) cudaFree(ctx->d_vlong);
     for (DevBuf *b : {&ctx->dec_state, &ctx->dec_status, &ctx->dec_tiles, &ctx->pt_bits, &ctx->mt_offs, &ctx->mt_counts})
         if (b->p) cudaFree(b->p);
     if (ctx->d_pt_classes) cudaFree(ctx->d_pt_classes);

@@ -57,8 +57,17 @@ __device__ __forceinline__ uint32_t info_of(const DecodeParams &P, uint32_t id) 
     return id < P.n_vocab ? __ldg(&P.vinfo[id]) : GPUBPE_INF;
 }
 
+// the byte length of a known id from its info word
+// (EXT: the vocabulary has empty or >= 255-byte strings; GPT-2 has neither)
+template <bool EXT>
+__device__ __forceinline__ uint32_t info_len(const DecodeParams &P, uint32_t inf, uint32_t id) {
+    const uint32_t l = inf & 0xFFu;
+    return EXT && l == LEN_EXT ? __ldg(&P.vlong[id]) : l;
+}
+
 }  // namespace
 
+template <bool EXT>
 __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant__ DecodeParams P) {
     extern __shared__ __align__(16) unsigned char dsm_raw[];
     DecSmem &S = *reinterpret_cast<DecSmem *>(dsm_raw);
@@ -104,7 +113,7 @@ __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant_
                     }
                 }
                 len[4 * k + j] = inf;  // blob chunk << 8 | length
-                gs[k] += inf & 0xFFu;
+                gs[k] += inf ? info_len<EXT>(P, inf, id[4 * k + j]) : 0u;
             }
         }
         // ---- offsets: warp scans (k-major), block scan of warp totals
@@ -187,7 +196,7 @@ __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant_
             S.goff[(wid * KG + k) * 32 + lane] = o;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const uint32_t inf = len[4 * k + j], l = inf & 0xFFu;
+                const uint32_t inf = len[4 * k + j], l = inf ? info_len<EXT>(P, inf, id[4 * k + j]) : 0u;
                 if (l) {
                     const uint4 *src = reinterpret_cast<const uint4 *>(P.blob) + (inf >> 8);
                     if (staged) {  // shared memory (the common case): the zero-padded
@@ -274,8 +283,8 @@ __global__ void __launch_bounds__(DT, 1024 / DT) k_decode(const __grid_constant_
                             uint32_t o = S.goff[(w * KG + k) * 32 + l2];
                             for (uint32_t jj = 0; jj < j; ++jj) {
                                 const unsigned long long ii = s - j + jj;
-                                const uint32_t inf = info_of(P, __ldg(&P.ids[ii]));
-                                o += inf == GPUBPE_INF ? 0u : (inf & 0xFFu);
+                                const uint32_t iid = __ldg(&P.ids[ii]), inf = info_of(P, iid);
+                                o += inf == GPUBPE_INF ? 0u : info_len<EXT>(P, inf, iid);
                             }
                             v = base + o;
                         }
@@ -352,6 +361,13 @@ __device__ __forceinline__ long long warp_lower_bound(const long long *a, long l
 }
 }  // namespace
 
+// the byte length in a 16-B record
+template <bool EXT>
+__device__ __forceinline__ uint32_t rec_len(const uint4 &rec) {
+    const uint32_t l = rec.x & 0xFFu;
+    return EXT && l == LEN_EXT ? rec.z : l;
+}
+
 // the 16-B records of row r's ids (lane's ids [4 lane, 4 lane + 4)); unknown ids
 // and ids past the end: length 0 (the first pass reported unknown ones)
 __device__ __forceinline__ void load_recs(const DecodeParams &P, unsigned long long r, int lane, const uint4 &idv,
@@ -372,6 +388,7 @@ struct RowSmem {
 #ifndef GPUBPE_DEC_MINB
 #define GPUBPE_DEC_MINB 4
 #endif
+template <bool EXT>
 __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const __grid_constant__ DecodeParams P) {
     extern __shared__ __align__(16) unsigned char rsm_raw[];
     RowSmem &S = *reinterpret_cast<RowSmem *>(rsm_raw);
@@ -404,7 +421,7 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
         load_recs(P, r, lane, idv, rec);
         uint32_t sum = 0;
 #pragma unroll
-        for (int j = 0; j < RDPT; ++j) sum += rec[j].x & 0xFFu;
+        for (int j = 0; j < RDPT; ++j) sum += rec_len<EXT>(rec[j]);
         uint32_t x = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -432,7 +449,7 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
             uint32_t o = SOFF + shift + excl;
 #pragma unroll
             for (int j = 0; j < RDPT; ++j) {
-                const uint32_t l = rec[j].x & 0xFFu;
+                const uint32_t l = rec_len<EXT>(rec[j]);
                 if (l && l <= 15) {
                     uint4 v = rec[j];
                     v.x &= ~0xFFu;  // the length byte lands (as zero) just before the string
@@ -447,7 +464,7 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
             uint32_t o = excl;
 #pragma unroll
             for (int j = 0; j < RDPT; ++j) {
-                const uint32_t l = rec[j].x & 0xFFu;
+                const uint32_t l = rec_len<EXT>(rec[j]);
                 uint8_t *dst = P.out + base + o;
                 if (l <= 15) {
                     for (uint32_t b = 0; b < l; ++b) dst[b] = (uint8_t)(comp(rec[j], (b + 1) >> 2) >> (8 * ((b + 1) & 3)));
@@ -502,7 +519,7 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
                 for (int j = 0; j < RDPT; ++j) {
                     const uint32_t v = __shfl_sync(FULL_MASK, pre, src);
                     if (j == jj) pick = v;
-                    pre += rec[j].x & 0xFFu;
+                    pre += rec_len<EXT>(rec[j]);
                 }
                 if (in) P.out_offs[d] = (long long)(s >= P.n_ids ? base + total : base + pick);
                 const unsigned m = __ballot_sync(FULL_MASK, in);
@@ -532,16 +549,18 @@ __global__ void __launch_bounds__(RW * 32, GPUBPE_DEC_MINB) k_decode_rows(const 
 }
 
 cudaError_t decode_rows_occupancy(int *blocks) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_decode_rows, RW * 32, sizeof(RowSmem));
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_decode_rows<false>, RW * 32, sizeof(RowSmem));
 }
 
 cudaError_t launch_decode_rows(const DecodeParams &P, int grid, cudaStream_t s) {
-    k_decode_rows<<<grid, RW * 32, sizeof(RowSmem), s>>>(P);
+    if (P.ext) k_decode_rows<true><<<grid, RW * 32, sizeof(RowSmem), s>>>(P);
+    else k_decode_rows<false><<<grid, RW * 32, sizeof(RowSmem), s>>>(P);
     return cudaGetLastError();
 }
 
 // ---- two-pass mode: tile byte totals (one CTA per tile, every CTA at once),
 //      then one CTA scans them into tile offsets; k_decode then needs no look-back
+template <bool EXT>
 __global__ void __launch_bounds__(256) k_dec_tile_bytes(const __grid_constant__ DecodeParams P,
                                                         unsigned long long *tile_bytes) {
     constexpr int IT = TD / (256 * 4);  // 4-id groups per thread, all loads issued together
@@ -569,8 +588,9 @@ __global__ void __launch_bounds__(256) k_dec_tile_bytes(const __grid_constant__ 
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (i + j < P.n_ids) {
-                const uint32_t l = id[k][j] < P.n_vocab ? __ldg(&P.vlen[id[k][j]]) : 0u;
+                uint32_t l = id[k][j] < P.n_vocab ? __ldg(&P.vlen[id[k][j]]) : 0u;
                 if (l == 0) atomicMin(&P.st->bad, i + j);
+                if (EXT && l == LEN_EXT) l = __ldg(&P.vlong[id[k][j]]);
                 sk += l;
             }
         }
@@ -641,7 +661,8 @@ __global__ void __launch_bounds__(1024) k_dec_scan(const unsigned long long *til
 cudaError_t launch_decode_offsets(const DecodeParams &P, unsigned long long *tile_bytes,
                                   unsigned long long *tile_base, cudaStream_t s) {
     if (P.n_tiles == 0) return cudaSuccess;
-    k_dec_tile_bytes<<<(unsigned int)P.n_tiles, 256, 0, s>>>(P, tile_bytes);
+    if (P.ext) k_dec_tile_bytes<true><<<(unsigned int)P.n_tiles, 256, 0, s>>>(P, tile_bytes);
+    else k_dec_tile_bytes<false><<<(unsigned int)P.n_tiles, 256, 0, s>>>(P, tile_bytes);
     const size_t sm = P.n_tiles <= SCAN_SMEM ? P.n_tiles * sizeof(unsigned long long) : 0;
     k_dec_scan<<<1, 1024, sm, s>>>(tile_bytes, P.n_tiles, tile_base);
     return cudaGetLastError();
@@ -651,19 +672,24 @@ size_t decode_smem_bytes() { return sizeof(DecSmem); }
 int decode_tile_ids() { return TD; }
 
 cudaError_t setup_decode() {
-    cudaError_t e = cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem));
+    cudaError_t e = cudaFuncSetAttribute(k_decode<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_decode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DecSmem));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_dec_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(SCAN_SMEM * sizeof(unsigned long long)));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_decode_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
+    e = cudaFuncSetAttribute(k_decode_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_decode_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RowSmem));
 }
 
 cudaError_t decode_occupancy(int *blocks) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_decode, DT, sizeof(DecSmem));
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_decode<false>, DT, sizeof(DecSmem));
 }
 
 cudaError_t launch_decode(const DecodeParams &P, int grid, cudaStream_t s) {
-    k_decode<<<grid, DT, sizeof(DecSmem), s>>>(P);
+    if (P.ext) k_decode<true><<<grid, DT, sizeof(DecSmem), s>>>(P);
+    else k_decode<false><<<grid, DT, sizeof(DecSmem), s>>>(P);
     return cudaGetLastError();
 }

@@ -2,6 +2,8 @@
 #pragma once
 #include <cstdint>
 
+constexpr uint32_t LEN_EXT = 255;
+
 struct DecodeState {
     unsigned long long tile_ctr;
     unsigned long long need;     // output bytes needed when out_cap was too small
@@ -10,11 +12,16 @@ struct DecodeState {
 };
 
 struct DecodeParams {
-    const uint32_t *vinfo;  // per id: blob offset << 8 | length, INF if not decodable
+    // Lengths: 1..254 in place; LEN_EXT (255) marks an id whose length is 0 (an
+    // empty symbol) or >= 255 -- its exact length is in vlong (and vrec's .z).
+    const uint32_t *vinfo;  // per id: blob offset << 8 | min(length, LEN_EXT), INF if not decodable
     const uint8_t *blob;
-    const uint4 *vrec;      // per id: 16-B record, byte 0 = length; length <= 15: the string in
-                            // bytes 1..15, else .y = its blob chunk (offset / 16); zero if unknown
-    const uint8_t *vlen;    // per id: length, 0 if not decodable
+    const uint4 *vrec;      // per id: 16-B record, byte 0 = length (0 for empty symbols); length
+                            // <= 15: the string in bytes 1..15, else .y = its blob chunk (offset / 16)
+                            // and byte 0 = min(length, LEN_EXT), .z = the length; zero if unknown
+    const uint8_t *vlen;    // per id: length (LEN_EXT: see vlong), 0 if not decodable
+    const uint32_t *vlong;  // per id: exact length (read only behind LEN_EXT)
+    uint32_t ext;           // the vocabulary has LEN_EXT lengths (kernels instantiated for them)
     uint32_t n_vocab;       // ids >= n_vocab are unknown
     const uint32_t *ids;
     unsigned long long n_ids;

@@ -697,6 +697,58 @@ def test_decode_rows_edge_cases(tokenizer):
                         torch.empty_like(o))
 
 
+def test_decode_empty_and_long_symbols():
+    """decode_tokens semantics (byte_codec.py:121-146) for symbols the GPT-2
+    vocabulary does not have: an empty symbol decodes to no bytes, symbols of
+    254, 255, 300 and 5000 bytes decode in full, a non-byte symbol is unknown --
+    in the single-pass, CTA-tile and two-pass row kernels."""
+    import os
+
+    import torch
+
+    from paper_2603_02597_b200.byte_codec import decode_tokens
+
+    enc = bpe.build_byte_encoder()
+    b2s = {b: s for s, b in enc.symbol_to_byte.items()}
+    vocab = {b2s[b]: b for b in range(256)}
+    rng = np.random.default_rng(5)
+    long_ids = {}
+    for k, n in enumerate((254, 255, 256, 300, 5000)):
+        sym = "".join(b2s[int(b)] for b in rng.integers(0, 256, n))
+        vocab[sym] = 300 + k
+        long_ids[300 + k] = n
+    vocab[""] = 400
+    vocab["\u2603"] = 401  # not a byte character: unknown
+    tok = bpe.Tokenizer(bpe.Vocab(vocab), bpe.build_table([]))
+    pool = np.array(list(range(256)) + list(long_ids) + [400] * 20, np.uint32)
+    seqs = [pool[rng.integers(0, pool.size, int(rng.integers(0, 40)))] for _ in range(300)]
+    seqs += [np.array([400, 400], np.uint32), np.array([], np.uint32), np.array([304] * 3, np.uint32)]
+    want = [decode_tokens(s.tolist(), tok.encoder, tok.vocab) for s in seqs]
+    assert tok.decode_batch(seqs) == want
+    # every kernel on one large batch (the row kernel is the default above ~1.5 M ids)
+    big = pool[rng.integers(0, pool.size, 2_000_000)]
+    offs = np.concatenate([[0], np.sort(rng.integers(0, big.size, 999)), [big.size]]).astype(np.int64)
+    want_bytes = b"".join(decode_tokens(big[offs[i]:offs[i + 1]].tolist(), tok.encoder, tok.vocab)
+                          for i in range(offs.size - 1))
+    d = tok.device_encoder()
+    d_ids = torch.from_numpy(big.view(np.int32)).cuda()
+    o = torch.from_numpy(offs).cuda()
+    for knob in (None, "GPUBPE_DEC_TILES", "GPUBPE_DEC_LOOKBACK"):
+        if knob:
+            os.environ[knob] = "1"
+        try:
+            out = torch.empty(len(want_bytes) + 64, dtype=torch.uint8, device="cuda")
+            oo = torch.empty_like(o)
+            nb = d.decode_into(d_ids, o, out, oo)
+        finally:
+            if knob:
+                os.environ.pop(knob)
+        assert nb == len(want_bytes), knob
+        assert out[:nb].cpu().numpy().tobytes() == want_bytes, knob
+    with pytest.raises(bpe.errors.UnknownTokenId):
+        tok.decode_batch([np.array([1, 401], np.uint32)])
+
+
 def test_integration_stub_binding(tokenizer, prose_samples):
     """The ctypes binding INTEGRATION.md shows a lanebpe maintainer (host buffers,
     no torch, no memo strings) gives the same ids as tokenize_batch."""
