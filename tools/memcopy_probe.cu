@@ -57,4 +57,18 @@ int main() {
         s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         printf("pinned D2H %.1f GB/s\n", n / s / 1e9);
     }
+    // both directions at once (two streams, pinned buffers): the ceiling of a
+    // streamed encode that reads bytes in and writes ids out
+    char *p2; cudaHostAlloc((void**)&p2, n, cudaHostAllocMapped);
+    char *d2; cudaMalloc(&d2, n);
+    cudaStream_t s1, s2; cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking); cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaDeviceSynchronize();
+        t0 = std::chrono::steady_clock::now();
+        cudaMemcpyAsync(d, p, n, cudaMemcpyHostToDevice, s1);
+        cudaMemcpyAsync(p2, d2, n, cudaMemcpyDeviceToHost, s2);
+        cudaDeviceSynchronize();
+        s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        printf("pinned H2D + D2H concurrently: %.1f GB/s each way, %.1f GB/s total\n", n / s / 1e9, 2 * n / s / 1e9);
+    }
 }
