@@ -124,6 +124,11 @@ class _HostPool:
     def put(self, buf: np.ndarray) -> None:
         key = (buf.size, isinstance(buf.base, ctypes.Array))  # pinned blocks are views of a ctypes array
         with self._lock:
+            if buf.size > (256 << 20):
+                # one large buffer of each kind at most: a run of calls whose sizes
+                # land in different GiB classes must not pin several of them
+                for k in [k for k in self._free if k[0] > (256 << 20) and k[1] == key[1] and k != key]:
+                    del self._free[k]
             lst = self._free.setdefault(key, [])
             if len(lst) < (self._keep if buf.size <= (256 << 20) else 1):
                 lst.append(buf)
