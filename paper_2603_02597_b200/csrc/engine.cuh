@@ -7,8 +7,11 @@
 //   3. applies them with a double-buffered stream compaction and re-probes
 //      only the pairs next to a merge.
 // Selection rule:
-//   * strict mode (table not well-formed, or forced): the single leftmost
-//     global-min pair -- one merge per pass, exactly the reference's order;
+//   * strict mode (table not well-formed, or forced): the pairs of rank r_min
+//     (even offset in their runs) in position order, up to and including the
+//     first whose merge creates a pair of rank <= r_min -- exactly the
+//     reference's order (each is the leftmost global minimum when its turn
+//     comes); at worst one merge per pass;
 //   * well-formed tables (every rule using token T ranks above every rule
 //     producing T; GPT-2 is): all pairs p with even offset inside their run of
 //     equal-rank pairs and either rank == r_min, or a bounded "blocking walk"
@@ -178,6 +181,25 @@ __device__ __forceinline__ bool walk_right(const DevTables &T, const uint32_t *t
     return false;
 }
 
+// Strict passes merge every r_min candidate up to the first "violation": a
+// candidate (pair i of rank r_min, even offset in its run; M.sel marks them)
+// whose merge creates a pair of rank <= r_min.  Its new token c is the same for
+// all candidates (one rule); its left neighbour is c when pair i - 2 is a
+// candidate (merged just before it), else token i - 1; its right neighbour is
+// token i + 2 (nothing to its right has merged yet).  Up to that candidate each
+// one is the leftmost global minimum when its turn comes.
+#ifndef STRICT_MULTI
+#define STRICT_MULTI 1
+#endif
+__device__ __forceinline__ bool strict_violates(const DevTables &T, const EngineMem &M, uint32_t i, uint32_t n,
+                                                uint32_t rmin) {
+    const uint32_t c = M.pr[i].y;
+    bool v = false;
+    if (i > 0) v = probe_pair(T, i >= 2 && M.sel[i - 2] ? c : M.tok[i - 1], c).rank <= rmin;
+    if (!v && i + 2 < n) v = probe_pair(T, c, M.tok[i + 2]).rank <= rmin;
+    return v;
+}
+
 // Cooperating groups the engine runs on: the whole CTA (giant segments) or
 // one warp (medium segments, 32 encoded per CTA at a time).
 struct BlockGroup {
@@ -275,11 +297,39 @@ static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_
             corrupt = pmin + 1 < n - 1 || pmin > 0;
             fault = !corrupt;
         }
-        if (strict || corrupt) {
+        if (corrupt || (strict && !STRICT_MULTI)) {
             for (uint32_t b = 0; b < n; b += nt) {
                 uint32_t i = b + me;
                 if (i < n) M.sel[i] = (i == pmin);
             }
+        } else if (strict) {
+            // candidates: pairs of rank r_min at even offset inside their run, merged
+            // in position order up to and including the first whose merge creates a
+            // pair of rank <= r_min (the reference merges that pair next)
+            uint32_t carry = 0;
+            unsigned long long first = ~0ull;
+            for (uint32_t b = 0; b < n; b += nt) {
+                uint32_t i = b + me;
+                bool pair = i + 1 < n;
+                uint32_t r = pair ? M.pr[i].x : GPUBPE_INF;
+                bool start = pair && (i == 0 || M.pr[i - 1].x != r);
+                uint32_t chunk_max;
+                uint32_t s = g.incl_max(start ? i : 0u, &chunk_max);
+                s = max(s, carry);
+                carry = max(carry, chunk_max);
+                if (i < n) M.sel[i] = pair && r == rmin && ((i - s) & 1u) == 0;
+            }
+            g.sync();
+            for (uint32_t b = 0; b < n; b += nt) {
+                uint32_t i = b + me;
+                if (i < n && M.sel[i] && strict_violates(T, M, i, n, rmin)) first = min(first, (unsigned long long)i);
+            }
+            const unsigned long long v = g.min_u64(first);
+            if (v != ~0ull)
+                for (uint32_t b = 0; b < n; b += nt) {
+                    uint32_t i = b + me;
+                    if (i < n && i > v) M.sel[i] = 0;
+                }
         } else {
             uint32_t carry = 0;
             for (uint32_t b = 0; b < n; b += nt) {

@@ -1000,14 +1000,18 @@ __device__ void publish_counters(CtaSmem &C, WarpCtx &X, PassCounters *dst) {
 //      so keep counts need no extra barrier; counts -> gscr;
 //   C  compaction at the global prefix of the counts (neighbours' selections
 //      were written before barrier B).
+// Strict passes add two barriers (B0: candidates marked, then the first one
+// whose merge creates a pair of rank <= r_min, engine.cuh strict_violates).
 // gscr: [0], [1] alternating kmin slots, [2] giant end, [3] arena offset,
+// [5], [6] alternating strict first-violation slots,
 // [8 + c] last run start + 1 of range c, [8 + G + c] kept tokens of range c.
 
 __device__ __forceinline__ bool grid_select(const DevTables &T, const EngineMem &M, uint32_t i, uint32_t n,
-                                            uint32_t s, uint32_t rmin, uint32_t pmin, bool strict) {
+                                            uint32_t s, uint32_t rmin, uint32_t pmin, bool strict,
+                                            unsigned long long vfirst) {
     if (i + 1 >= n) return false;
     const uint32_t r = M.pr[i].x;
-    if (strict) return i == pmin;
+    if (strict) return STRICT_MULTI ? __ldcg(&M.sel[i]) && i <= vfirst : i == pmin;  // (marks of B0)
     bool ok = r != GPUBPE_INF && ((i - s) & 1u) == 0;
     if (ok && r != rmin) ok = walk_left(T, M.tok, M.pr, s, r) && walk_right(T, M.tok, M.pr, i + 1, n, r);
     return ok;
@@ -1023,7 +1027,7 @@ __device__ uint32_t grid_engine_run(const EncodeParams &P, CtaSmem &C, EngineMem
         const PairHit h = probe_pair(T, M.tok[i], M.tok[i + 1]);
         M.pr[i] = make_uint2(h.rank, h.nw);
     }
-    if (c == 0 && tid == 0) g[0] = g[1] = ~0ull;
+    if (c == 0 && tid == 0) g[0] = g[1] = g[5] = g[6] = ~0ull;
     grid_sync(st, ++nbar);
     uint32_t passes = 0;
     while (n >= 2) {
@@ -1058,8 +1062,35 @@ __device__ uint32_t grid_engine_run(const EncodeParams &P, CtaSmem &C, EngineMem
         __syncthreads();
         carry = (uint32_t)C.bcast[1];
         const uint32_t s_before = carry ? carry - 1 : 0u;  // run start covering lo - 1
+        // ---- B0 (strict): candidates marked in M.sel, then the first one whose merge
+        //      creates a pair of rank <= r_min (engine.cuh strict_violates), grid-wide;
+        //      two barriers more
+        unsigned long long vfirst = ~0ull;
+        if (strict && STRICT_MULTI) {
+            uint32_t runs = carry;
+            for (uint32_t b = lo; b < hi; b += NT) {
+                const uint32_t i = b + tid;
+                const bool pair = i < hi && i + 1 < n;
+                const uint32_t r = pair ? M.pr[i].x : GPUBPE_INF;
+                const bool start = pair && (i == 0 || M.pr[i - 1].x != r);
+                uint32_t chunk_max;
+                uint32_t sv = block_incl_max(start ? i + 1 : 0u, C.es, &chunk_max);
+                sv = max(sv, runs);
+                runs = max(runs, chunk_max);
+                if (i < hi) M.sel[i] = pair && r == rmin && ((i - (sv ? sv - 1 : 0u)) & 1u) == 0;
+            }
+            grid_sync(st, ++nbar);
+            unsigned long long first = ~0ull;
+            for (uint32_t i = lo + tid; i < hi; i += NT)
+                if (__ldcg(&M.sel[i]) && strict_violates(T, M, i, n, rmin)) first = min(first, (unsigned long long)i);
+            const unsigned long long bf = block_min_u64(first, C.es);
+            if (tid == 0 && bf != ~0ull) atomicMin(&g[5 + (passes & 1)], bf);
+            grid_sync(st, ++nbar);
+            if (c == 0 && tid == 0) g[5 + ((passes + 1) & 1)] = ~0ull;  // the next pass's slot
+            vfirst = __ldcg(&g[5 + (passes & 1)]);
+        }
         // ---- B: selection of [lo, hi), redundant selection of lo - 1, keep counts
-        const bool sel_prev = lo > 0 && grid_select(T, M, lo - 1, n, s_before, rmin, pmin, strict);
+        const bool sel_prev = lo > 0 && grid_select(T, M, lo - 1, n, s_before, rmin, pmin, strict, vfirst);
         uint32_t runs = carry;  // max start + 1 seen so far
         for (uint32_t b = lo; b < hi; b += NT) {
             const uint32_t i = b + tid;
@@ -1070,7 +1101,7 @@ __device__ uint32_t grid_engine_run(const EncodeParams &P, CtaSmem &C, EngineMem
             uint32_t sv = block_incl_max(start ? i + 1 : 0u, C.es, &chunk_max);
             sv = max(sv, runs);
             runs = max(runs, chunk_max);
-            if (i < hi) M.sel[i] = grid_select(T, M, i, n, sv ? sv - 1 : 0u, rmin, pmin, strict);
+            if (i < hi) M.sel[i] = grid_select(T, M, i, n, sv ? sv - 1 : 0u, rmin, pmin, strict, vfirst);
         }
         __syncthreads();
         uint32_t kept = 0;
