@@ -46,7 +46,10 @@ class _Lease:
         return memoryview(self.buf)
 
     def __release_buffer__(self, view):
-        self.pool.put(self.buf)
+        try:
+            self.pool.put(self.buf)
+        except Exception:  # interpreter shutdown: nothing left to recycle into
+            pass
 
 
 class _PinnedBlock:
@@ -121,8 +124,10 @@ class _HostPool:
         buf = self._pop((cls, False))
         return buf if buf is not None else np.empty(cls, dtype=np.uint8)
 
-    def put(self, buf: np.ndarray) -> None:
-        key = (buf.size, isinstance(buf.base, ctypes.Array))  # pinned blocks are views of a ctypes array
+    def put(self, buf: np.ndarray, _carray=ctypes.Array) -> None:
+        # (_carray: bound at definition, as module globals may be gone when the last
+        # result array dies at interpreter shutdown)
+        key = (buf.size, isinstance(buf.base, _carray))  # pinned blocks are views of a ctypes array
         with self._lock:
             if buf.size > (256 << 20):
                 # one large buffer of each kind at most: a run of calls whose sizes
