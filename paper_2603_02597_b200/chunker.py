@@ -287,6 +287,14 @@ class _LazyCounters(PassCounters):
         return object.__getattribute__(self, name)
 
 
+def _split_views(ids: np.ndarray, offs: np.ndarray) -> list:
+    """[ids[offs[i]:offs[i + 1]] for each document], built in C (csrc/hostlist.c)."""
+    from .device import _hostlist
+
+    o = np.ascontiguousarray(offs, dtype=np.int64)
+    return _hostlist().split_views(np.ascontiguousarray(ids), o.ctypes.data, max(len(o) - 1, 0))
+
+
 def _tri(x: np.ndarray) -> np.ndarray:
     return x * (x + 1) // 2
 
@@ -558,16 +566,14 @@ def tokenize_batch(texts, tokenizer: Tokenizer, variant: str = "optimized",
     if len(pieces) == 1 and len(src) == len(ulens):
         ids, uo = pieces[0]
         uout = np.diff(uo)
-        doc_o = (uo if cut is None else uo[first]).tolist()
-        token_ids = [ids[a:b] for a, b in zip(doc_o, doc_o[1:])]
+        token_ids = _split_views(ids, uo if cut is None else uo[first])
     else:
         pout = np.concatenate([np.diff(o) for _, o in pieces])
         uout = np.bincount(src, weights=pout, minlength=len(ulens)).astype(np.int64)
         flat = np.concatenate([i for i, _ in pieces]) if pieces else np.empty(0, np.uint32)
         uo = np.zeros(len(ulens) + 1, np.int64)
         np.cumsum(uout, out=uo[1:])
-        doc_o = (uo if cut is None else uo[first]).tolist()
-        token_ids = [flat[a:b] for a, b in zip(doc_o, doc_o[1:])]
+        token_ids = _split_views(flat, uo if cut is None else uo[first])
     cl = ulens.astype(np.int64)
     uo_all = np.zeros(len(cl) + 1, np.int64)
     np.cumsum(uout, out=uo_all[1:])

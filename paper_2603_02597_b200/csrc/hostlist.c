@@ -17,9 +17,15 @@
  *     ptrs_addr  address of uint64[len(list)]: data addresses (written)
  *     lens_addr  address of uint64[len(list)]: lengths (written)
  * The caller keeps the list alive while the addresses are used.
+ *
+ * 3. split_views: the per-document result arrays of a batch (BatchResult.
+ *    token_ids) as views of the one result array, built in C (a Python
+ *    slicing loop costs ~0.1 us per document; C2 has 4,096).
  */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#define NPY_NO_DEPRECATED_API NPY_1_7_API_VERSION
+#include <numpy/arrayobject.h>
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -117,13 +123,61 @@ static PyObject *encode_one(PyObject *self, PyObject *args) {
     return Py_BuildValue("iKdN", 0, (unsigned long long)n_ids, (double)ms, t);
 }
 
+/* split_views(arr, offs_addr, n) -> list of n views arr[offs[i]:offs[i+1]]
+ * arr: a 1-D C-contiguous numpy array (each view keeps it alive);
+ * offs_addr: address of int64[n + 1], ascending, within [0, len(arr)]. */
+static PyObject *split_views(PyObject *self, PyObject *args) {
+    PyArrayObject *arr;
+    unsigned long long oa;
+    Py_ssize_t n;
+    (void)self;
+    if (!PyArg_ParseTuple(args, "O!Kn", &PyArray_Type, &arr, &oa, &n)) return NULL;
+    if (PyArray_NDIM(arr) != 1 || !PyArray_IS_C_CONTIGUOUS(arr) || n < 0 || (n > 0 && !oa)) {
+        PyErr_SetString(PyExc_ValueError, "split_views: a 1-D contiguous array and n + 1 offsets");
+        return NULL;
+    }
+    const int64_t *o = (const int64_t *)(uintptr_t)oa;
+    const npy_intp len = PyArray_DIM(arr, 0), isz = PyArray_ITEMSIZE(arr);
+    for (Py_ssize_t i = 0; i < n; ++i)
+        if (o[i] < 0 || o[i] > o[i + 1] || o[i + 1] > len) {
+            PyErr_SetString(PyExc_ValueError, "split_views: offsets out of order or range");
+            return NULL;
+        }
+    PyObject *out = PyList_New(n);
+    if (!out) return NULL;
+    char *data = PyArray_BYTES(arr);
+    PyArray_Descr *descr = PyArray_DESCR(arr);
+    const int flags = PyArray_FLAGS(arr) & (NPY_ARRAY_C_CONTIGUOUS | NPY_ARRAY_ALIGNED | NPY_ARRAY_WRITEABLE);
+    for (Py_ssize_t i = 0; i < n; ++i) {
+        npy_intp dim = (npy_intp)(o[i + 1] - o[i]);
+        Py_INCREF(descr);  /* stolen */
+        PyObject *v = PyArray_NewFromDescr(&PyArray_Type, descr, 1, &dim, NULL, data + o[i] * isz, flags, NULL);
+        if (!v) {
+            Py_DECREF(out);
+            return NULL;
+        }
+        Py_INCREF(arr);
+        if (PyArray_SetBaseObject((PyArrayObject *)v, (PyObject *)arr) < 0) {  /* steals arr */
+            Py_DECREF(v);
+            Py_DECREF(out);
+            return NULL;
+        }
+        PyList_SET_ITEM(out, i, v);
+    }
+    return out;
+}
+
 static PyMethodDef methods[] = {
     {"ptrs_lens", ptrs_lens, METH_VARARGS, "data addresses and lengths of a list of bytes"},
     {"bind", bind, METH_VARARGS, "bind the libgpubpe.so entry points"},
     {"encode_one", encode_one, METH_VARARGS, "single-document host encode"},
+    {"split_views", split_views, METH_VARARGS, "per-document views of a result array"},
     {NULL, NULL, 0, NULL},
 };
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_hostlist", NULL, -1, methods};
 
-PyMODINIT_FUNC PyInit__hostlist(void) { return PyModule_Create(&module); }
+PyMODINIT_FUNC PyInit__hostlist(void) {
+    import_array();
+    return PyModule_Create(&module);
+}

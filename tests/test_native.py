@@ -5,6 +5,7 @@ import ctypes
 import re
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
@@ -84,3 +85,25 @@ def test_hostlist_reads_bytes_addresses_through_the_c_api():
     with pytest.raises(TypeError):
         bytes_ptrs_lens([bytearray(b"a")])
     assert [x.size for x in bytes_ptrs_lens([])] == [0, 0]
+
+
+def test_hostlist_split_views():
+    """chunker._split_views (csrc/hostlist.c split_views): per-document views of
+    one result array, equal to Python slicing, keeping the array alive; empty
+    documents, zero documents and bad offsets."""
+    from paper_2603_02597_b200.chunker import _split_views
+
+    ids = np.arange(1000, dtype=np.uint32)
+    offs = np.array([0, 0, 3, 3, 700, 1000, 1000], np.int64)
+    views = _split_views(ids, offs)
+    o = offs.tolist()
+    assert len(views) == 6
+    for v, a, b in zip(views, o, o[1:]):
+        assert v.dtype == np.uint32 and v.base is ids and v.tolist() == ids[a:b].tolist()
+    assert _split_views(ids, np.zeros(1, np.int64)) == []
+    with pytest.raises(ValueError):
+        _split_views(ids, np.array([0, 5, 3], np.int64))
+    with pytest.raises(ValueError):
+        _split_views(ids, np.array([0, 1001], np.int64))
+    del ids
+    assert views[4].tolist() == list(range(700, 1000))  # the views keep the array alive
