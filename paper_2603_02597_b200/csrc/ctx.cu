@@ -812,6 +812,10 @@ static inline void cpu_relax() {
 #endif
 }
 
+// Copies bytes [lo, hi) of the batch to dst (gather entry point: documents
+// in separate buffers); null for a contiguous h_bytes.
+using StageFn = std::function<void(uint8_t *dst, uint64_t lo, uint64_t hi)>;
+
 namespace {
 // Jobs: a buffer split in parts (at most 40).  One 64-bit word holds the job
 // id, its part count and the claimed parts, so a claim (CAS) can only succeed
@@ -849,6 +853,24 @@ class StagePool {
         }
         while (left_.load(std::memory_order_acquire) > 0) cpu_relax();
     }
+    // the same for a gather: bytes [lo, hi) of the batch staged by fn, split in parts
+    void gather(uint8_t *dst, const StageFn &fn, uint64_t lo, uint64_t hi) {
+        const size_t n = hi - lo;
+        const unsigned parts = (unsigned)th_.size() + 1;
+        const size_t chunk = ((n + parts - 1) / parts + 63) & ~(size_t)63;
+        std::unique_lock<std::mutex> call(call_, std::try_to_lock);
+        if (!call.owns_lock()) {
+            fn(dst, lo, hi);
+            return;
+        }
+        fn_ = &fn;
+        base_ = lo;
+        post(dst, nullptr, n, chunk, parts);
+        while (claim_and_run()) {
+        }
+        while (left_.load(std::memory_order_acquire) > 0) cpu_relax();
+        fn_ = nullptr;
+    }
 
   private:
     static constexpr unsigned MAXP = 40;
@@ -880,7 +902,10 @@ class StagePool {
             if (word_.compare_exchange_weak(w, w | (1ull << i), std::memory_order_acq_rel,
                                             std::memory_order_acquire)) {
                 const size_t lo = std::min(n_, i * chunk_), hi = std::min(n_, lo + chunk_);
-                if (lo < hi) memcpy(dst_ + lo, src_ + lo, hi - lo);
+                if (lo < hi) {
+                    if (fn_) (*fn_)(dst_ + lo, base_ + lo, base_ + hi);
+                    else memcpy(dst_ + lo, src_ + lo, hi - lo);
+                }
                 left_.fetch_sub(1, std::memory_order_acq_rel);
                 return true;
             }
@@ -927,6 +952,8 @@ class StagePool {
     unsigned job_ = 0;
     uint8_t *dst_ = nullptr;
     const uint8_t *src_ = nullptr;
+    const StageFn *fn_ = nullptr;  // gather jobs: the stage function (else a memcpy from src_)
+    uint64_t base_ = 0;            // gather jobs: batch offset of dst_
     size_t n_ = 0, chunk_ = 0;
 };
 }  // namespace
@@ -1197,9 +1224,6 @@ static int encode_host_streamed(gpubpe_ctx *ctx, const uint8_t *h_bytes, const i
     return GPUBPE_OK;
 }
 
-// Copies bytes [lo, hi) of the batch to dst (gather entry point: documents
-// in separate buffers); null for a contiguous h_bytes.
-using StageFn = std::function<void(uint8_t *dst, uint64_t lo, uint64_t hi)>;
 
 static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const StageFn *stage, uint64_t n_bytes,
                             const int64_t *h_doc_offs, uint64_t n_docs, uint64_t max_seq_len, uint64_t chunk_budget,
@@ -1244,7 +1268,7 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
             on = false;
         }
         ~StageCall() { done(); }
-    } stage_call(!stage && n_bytes >= (128u << 10) && n_bytes <= (16u << 20) && !getenv("GPUBPE_NO_STAGE_POOL"));
+    } stage_call(n_bytes >= (128u << 10) && n_bytes <= (16u << 20) && !getenv("GPUBPE_NO_STAGE_POOL"));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ctx->alloc_mark = ctx->n_allocs;
     struct HostCall {  // gpubpe_encode calls below keep this call's allocation mark
@@ -1394,7 +1418,7 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         const size_t piece = pe ? std::max<size_t>(4096, (size_t)atoll(pe) << 10)
                                 : std::min<size_t>(4u << 20, std::max<size_t>(64u << 10, ((n_bytes / 4) + 65535) & ~(size_t)65535));
         // pieces of 128 KiB .. 4 MiB: split across the staging helpers
-        const bool helpers = !stage && piece >= (128u << 10) && piece <= (4u << 20) && !getenv("GPUBPE_NO_STAGE_POOL");
+        const bool helpers = piece >= (128u << 10) && piece <= (4u << 20) && !getenv("GPUBPE_NO_STAGE_POOL");
         auto copy_piece = [&](uint8_t *dst, const uint8_t *src, size_t len) {
             if (helpers) StagePool::get().copy(dst, src, len);
             else copy_par(dst, src, len);
@@ -1406,13 +1430,17 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         if (tl && !tev[0])
             for (auto &e : tev) cudaEventCreate(&e);
         if (tl) cudaEventRecord(tev[ntev++], s);
+        auto stage_piece = [&](uint8_t *dst, uint64_t a, uint64_t b) {
+            if (helpers) StagePool::get().gather(dst, *stage, a, b);
+            else (*stage)(dst, a, b);
+        };
         for (; lo + piece < n_bytes; lo += piece) {
-            if (stage) (*stage)(pin + o_in + lo, lo, lo + piece);
+            if (stage) stage_piece(pin + o_in + lo, lo, lo + piece);
             else copy_piece(pin + o_in + lo, h_bytes + lo, piece);
             CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, piece, cudaMemcpyHostToDevice, s));
             if (tl && ntev < 8) cudaEventRecord(tev[ntev++], s);
         }
-        if (stage) (*stage)(pin + o_in + lo, lo, n_bytes);
+        if (stage) stage_piece(pin + o_in + lo, lo, n_bytes);
         else copy_piece(pin + o_in + lo, h_bytes + lo, n_bytes - lo);
         CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, o_doffs + offs_b - lo, cudaMemcpyHostToDevice, s));
         if (tl) {  // GPU timeline of the pieces (GPUBPE_HOSTTIME=2): printed after the kernel
