@@ -43,13 +43,14 @@ struct DecSmem {
     __align__(16) uint8_t stage[STAGE + 32];
 };
 
+// relaxed gpu-scope look-back words (plain PTX, see kernels.cu st_relaxed)
 __device__ __forceinline__ void st_rel(unsigned long long *w, unsigned long long v) {
-    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(*w);
-    r.store(v, cuda::memory_order_relaxed);
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(w), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_rel(unsigned long long *w) {
-    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(*w);
-    return r.load(cuda::memory_order_relaxed);
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
+    return v;
 }
 
 // id -> (blob offset, length); INF info = unknown id

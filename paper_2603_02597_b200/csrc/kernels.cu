@@ -54,19 +54,22 @@ struct WarpCtx {
 
 // ------------------------------------------------------------------ helpers
 
+// Relaxed gpu-scope accesses as plain PTX (libcu++'s atomic_ref adds a
+// "local memory?" test and a local-memory fallback path to every access).
 __device__ __forceinline__ void st_relaxed(unsigned long long *w, unsigned long long v) {
-    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(*w);
-    r.store(v, cuda::memory_order_relaxed);
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(w), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_relaxed(unsigned long long *w) {
-    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> r(*w);
-    return r.load(cuda::memory_order_relaxed);
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
+    return v;
 }
 // Relaxed polling: an acquire load would invalidate the SM's L1 (CCTL.IVALL)
 // on every iteration and stall the other warps' L1/shared-memory traffic.
 __device__ __forceinline__ unsigned int ld_relaxed_u32(unsigned int *w) {
-    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> r(*w);
-    return r.load(cuda::memory_order_relaxed);
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+    return v;
 }
 
 __device__ __forceinline__ void red_release_add(unsigned long long *w, unsigned long long v) {
