@@ -1668,7 +1668,8 @@ extern "C" __attribute__((visibility("default"))) int gpubpe_set_vocab(gpubpe_ct
     // per id: a 16-B record (length byte, then the string if it fits, else its
     // blob chunk and length) and a 1-byte length table (the two-pass decode's
     // first pass; LEN_EXT for empty and >= 255-byte strings, 0 for unknown ids)
-    std::vector<uint8_t> vrec(vinfo.size() * 16, 0), vlen(vinfo.size(), 0);
+    // (vrec has one zero record more, at index n_vocab: unknown ids clamp to it)
+    std::vector<uint8_t> vrec((vinfo.size() + 1) * 16, 0), vlen(vinfo.size(), 0);
     bool ext = false;
     for (size_t i = 0; i < vinfo.size(); ++i) {
         if (vinfo[i] == GPUBPE_INF) continue;

@@ -373,6 +373,11 @@ __device__ __forceinline__ uint32_t rec_len(const uint4 &rec) {
 // and ids past the end: length 0 (the first pass reported unknown ones)
 __device__ __forceinline__ void load_recs(const DecodeParams &P, unsigned long long r, int lane, const uint4 &idv,
                                           uint4 (&rec)[RDPT]) {
+    if ((r + 1) * RROW <= P.n_ids) {  // a full row (warp-uniform): no bounds tests; ids
+#pragma unroll                           // >= n_vocab read the zero record at n_vocab
+        for (int j = 0; j < RDPT; ++j) rec[j] = __ldg(&P.vrec[min(comp(idv, j), P.n_vocab)]);
+        return;
+    }
     const unsigned long long i0 = r * RROW + (unsigned long long)lane * RDPT;
 #pragma unroll
     for (int j = 0; j < RDPT; ++j) {

@@ -18,7 +18,8 @@ struct DecodeParams {
     const uint8_t *blob;
     const uint4 *vrec;      // per id: 16-B record, byte 0 = length (0 for empty symbols); length
                             // <= 15: the string in bytes 1..15, else .y = its blob chunk (offset / 16)
-                            // and byte 0 = min(length, LEN_EXT), .z = the length; zero if unknown
+                            // and byte 0 = min(length, LEN_EXT), .z = the length; zero if unknown;
+                            // n_vocab + 1 records (the last one zero)
     const uint8_t *vlen;    // per id: length (LEN_EXT: see vlong), 0 if not decodable
     const uint32_t *vlong;  // per id: exact length (read only behind LEN_EXT)
     uint32_t ext;           // the vocabulary has LEN_EXT lengths (kernels instantiated for them)
