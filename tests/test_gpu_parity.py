@@ -857,6 +857,25 @@ def test_token_engine_random_tables_match_greedy(well_formed):
             assert c.passes == len(ids) - len(out)
 
 
+def test_strict_pass_stops_at_first_violation():
+    """Strict passes (tables that are not well-formed) merge the minimum-rank
+    candidates only up to the first one whose merge creates a pair of rank <=
+    the minimum; a candidate's left neighbour is the previous candidate's new
+    token when they are adjacent, even across runs.  (a,b)->c r5, (c,c)->d r1,
+    (d,a)->e r2 on "ababab": the reference merges @0, @1, then (c,c), then
+    (d,a): [e, b]; merging all three (a,b) pairs in one pass would give [d, c]."""
+    from oracle.oracle import greedy_merge
+
+    a, b, c, d, e = 10, 11, 20, 21, 22
+    rules = [bpe.MergeRule(c, c, 1, d), bpe.MergeRule(d, a, 2, e), bpe.MergeRule(a, b, 5, c)]
+    table = bpe.build_table(rules)
+    pair_map = {(r.left, r.right): (r.rank, r.new_token) for r in rules}
+    for ids in ([a, b, a, b, a, b], [a, b, a, b, a, b, a, b], [b, a, b, a, b, a, b], [a, b] * 20):
+        out, _ = bpe.sequential_bpe(ids, table)
+        assert out.tolist() == greedy_merge(ids, pair_map), ids
+    assert bpe.sequential_bpe([a, b, a, b, a, b], table)[0].tolist() == [e, b]
+
+
 @pytest.mark.parametrize("well_formed", [True, False])
 def test_byte_level_random_tables_match_oracle(well_formed):
     """k_encode (junction cuts, memo verification, warp / CTA / grid engines) with
