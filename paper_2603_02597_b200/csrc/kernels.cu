@@ -223,16 +223,22 @@ __device__ __forceinline__ unsigned long long low_bytes(unsigned long long v, ui
 __device__ uint32_t memo_lookup(const DevTables &T, const uint32_t *sb, uint32_t p, uint32_t len) {
     const unsigned long long c0 = low_bytes(sb_load8(sb, p), len);
     unsigned long long h = memo_hash_step(memo_hash_init(len), c0);
-    for (uint32_t c = 8; c < len; c += 8) h = memo_hash_step(h, low_bytes(sb_load8(sb, p + c), len - c));
+    // bytes 8..15 are kept for the verification (strings of 9..16 bytes: no reload)
+    const unsigned long long c1 = len > 8 ? low_bytes(sb_load8(sb, p + 8), len - 8) : 0ull;
+    if (len > 8) h = memo_hash_step(h, c1);
+    for (uint32_t c = 16; c < len; c += 8) h = memo_hash_step(h, low_bytes(sb_load8(sb, p + c), len - c));
     uint32_t slot = memo_slot_of(h, T.memo_mask);
     for (;;) {
         const uint4 e = __ldg(&T.memo[slot]);
         if (e.w == 0) return GPUBPE_INF;
         if ((e.w & 0xFFu) == len && e.x == (uint32_t)c0 && e.y == (uint32_t)(c0 >> 32)) {
             bool eq = true;
-            const unsigned long long *tail = T.blob + (e.w >> 8);
-            for (uint32_t c = 8, k = 0; c < len; c += 8, ++k)
-                eq &= __ldg(&tail[k]) == low_bytes(sb_load8(sb, p + c), len - c);
+            if (len > 8) {
+                const unsigned long long *tail = T.blob + (e.w >> 8);
+                eq = __ldg(&tail[0]) == c1;
+                for (uint32_t c = 16, k = 1; c < len; c += 8, ++k)
+                    eq &= __ldg(&tail[k]) == low_bytes(sb_load8(sb, p + c), len - c);
+            }
             if (eq) return e.z;
         }
         slot = (slot + 1) & T.memo_mask;
