@@ -499,7 +499,15 @@ __device__ __noinline__ uint32_t encode_tile(const EncodeParams &P, CtaSmem &C, 
 #pragma unroll 1
     for (uint32_t i = lane; i < nseg; i += 32) {
         const int p = S.seg[i];
-        const int e = next_cut(S.cm, p + 1, p + SHORT_MAX);
+        // its end: the next segment's start (the list holds every cut in the tile),
+        // past the tile the cut bits; -1 beyond SHORT_MAX
+        int e;
+        if (i + 1 < nseg) {
+            e = S.seg[i + 1];
+            if (e - p > SHORT_MAX) e = -1;
+        } else {
+            e = next_cut(S.cm, p + 1, p + SHORT_MAX);
+        }
         ++c_seg;
         if (e < 0) {  // longer than SHORT_MAX: deferred to the CTA engine
             const unsigned long long r = atomicAdd(&P.st->bar, 1ull << 32) >> 32;
