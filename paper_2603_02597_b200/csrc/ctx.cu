@@ -1328,16 +1328,26 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
     // A caller buffer that is itself pinned and device-mapped (gpubpe_host_alloc)
     // receives the ids directly: no copy-out at all.
     uint32_t *d_ids_direct = (mode == 3 && n_bytes) ? static_cast<uint32_t *>(mapped_alias(h_out_ids)) : nullptr;
+    // Large batches: the ids go to device memory and come back by one DMA once the
+    // count is known (PCIe writes from the SMs drain at ~26 GB/s, the copy engine
+    // moves ~55 GB/s; GPUBPE_DMA_IDS_MB, default 2: the crossover measured on C2)
+    static const long long dma_mb = getenv("GPUBPE_DMA_IDS_MB") ? atoll(getenv("GPUBPE_DMA_IDS_MB")) : 2;
+    const bool dma_ids = mode == 3 && dma_mb >= 0 && n_bytes >= ((uint64_t)dma_mb << 20) && n_bytes;
+    uint32_t *k_ids = dma_ids ? reinterpret_cast<uint32_t *>(dv + o_ids)
+                              : d_ids_direct ? d_ids_direct : reinterpret_cast<uint32_t *>(dout + o_ids);
     // overlapped launch (one pageable buffer of 128 KiB .. 16 MiB, default mode):
     // ~4 pieces, the kernel enqueued before them
     const bool no_overlap = getenv("GPUBPE_NO_OVERLAP") != nullptr;  // (per call: tests switch it)
     // (every H2D copy costs ~7 us of setup on this PCIe 5 link, measured by
     // tools/overlap_probe.cu: one piece unless GPUBPE_OV_PIECES says otherwise)
+    // (gathered batches: GPUBPE_OV_GATHER pieces, default 4 -- their staging is the long part)
     static const int ov_pieces = getenv("GPUBPE_OV_PIECES") ? std::max(1, atoi(getenv("GPUBPE_OV_PIECES"))) : 1;
-    const size_t ov_piece = std::max<size_t>(32u << 10, ((n_bytes / ov_pieces) + 4095) & ~(size_t)4095);
-    const bool overlap = !no_overlap && mode == 3 && !stage && ctx->mode == GPUBPE_MODE_DEFAULT &&
+    static const int ov_gather = getenv("GPUBPE_OV_GATHER") ? atoi(getenv("GPUBPE_OV_GATHER")) : 4;
+    const int pieces = stage ? std::max(1, ov_gather) : ov_pieces;
+    const size_t ov_piece = std::max<size_t>(32u << 10, ((n_bytes / pieces) + 4095) & ~(size_t)4095);
+    const bool overlap = !no_overlap && mode == 3 && (!stage || ov_gather > 0) && ctx->mode == GPUBPE_MODE_DEFAULT &&
                          n_bytes >= (128u << 10) && n_bytes <= (16u << 20) &&
-                         (n_bytes + ov_piece - 1) / ov_piece <= (size_t)ARRIVE_MAX && !mapped_alias(h_bytes);
+                         (n_bytes + ov_piece - 1) / ov_piece <= (size_t)ARRIVE_MAX && (stage || !mapped_alias(h_bytes));
     if (mode == 1) {  // zero-copy: the kernel reads and writes mapped host memory
         copy_par(pin + o_in, h_bytes, n_bytes);
         memcpy(pin + o_doffs, h_doc_offs, offs_b);
@@ -1372,7 +1382,8 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         decltype(th0) th1 = th0;
         for (unsigned k = 0; k < n_pieces; ++k) {
             const size_t lo = (size_t)k * ov_piece, len = std::min<size_t>(ov_piece, n_bytes - lo);
-            StagePool::get().copy(pin + o_in + lo, h_bytes + lo, len);
+            if (stage) StagePool::get().gather(pin + o_in + lo, *stage, lo, lo + len);
+            else StagePool::get().copy(pin + o_in + lo, h_bytes + lo, len);
             if (k == 0) th1 = now();
             CK(cudaMemcpyAsync(dv + o_in + lo, pin + o_in + lo, len, cudaMemcpyHostToDevice, ctx->s_copy));
             CK(cudaMemcpyAsync(ctx->d_arrive + ARRIVE_STRIDE * k, ctx->h_tag, sizeof(unsigned int),
@@ -1387,7 +1398,7 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         ctx->defer_check = true;  // the overflow check waits for the final synchronisation
         rc = gpubpe_encode(ctx, dv + o_in, n_bytes, reinterpret_cast<const int64_t *>(dv + o_doffs), n_docs,
                            max_seq_len, chunk_budget,
-                           d_ids_direct ? d_ids_direct : reinterpret_cast<uint32_t *>(dout + o_ids),
+                           k_ids,
                            reinterpret_cast<int64_t *>(dout + o_ooffs), stream);
         ctx->defer_check = dc;
         ctx->cur_arrive = nullptr;
@@ -1455,7 +1466,7 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         CK(cudaEventRecord(ctx->io_ev[0], s));
         rc = gpubpe_encode(ctx, dv + o_in, n_bytes, reinterpret_cast<const int64_t *>(dv + o_doffs), n_docs,
                            max_seq_len, chunk_budget,
-                           d_ids_direct ? d_ids_direct : reinterpret_cast<uint32_t *>(dout + o_ids),
+                           k_ids,
                            reinterpret_cast<int64_t *>(dout + o_ooffs), stream);
         if (rc) return rc;
     }
@@ -1514,7 +1525,7 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
         // the input is on the device now; re-run the plain path, which grows them
         rc = gpubpe_encode(ctx, dv + o_in, n_bytes, reinterpret_cast<const int64_t *>(dv + o_doffs), n_docs,
                            max_seq_len, chunk_budget,
-                           d_ids_direct ? d_ids_direct : reinterpret_cast<uint32_t *>(dout + o_ids),
+                           k_ids,
                            reinterpret_cast<int64_t *>(dout + o_ooffs), stream);
         if (rc) return rc;
         const EncodeState *last = static_cast<const EncodeState *>(ctx->ws_state.p) + ((ctx->calls - 1) & 1);
@@ -1528,7 +1539,12 @@ static int encode_host_core(gpubpe_ctx *ctx, const uint8_t *h_bytes, const Stage
                     (unsigned long long)n_bytes);
     memcpy(h_out_offs, p_oo, offs_b);
     if (total) {
-        if (d_ids_direct) {
+        if (dma_ids) {  // one D2H copy of exactly the ids produced
+            CK(cudaMemcpyAsync(d_ids_direct ? static_cast<void *>(h_out_ids) : static_cast<void *>(pin + o_ids),
+                               dv + o_ids, total * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (!d_ids_direct) copy_par(h_out_ids, pin + o_ids, total * 4);
+        } else if (d_ids_direct) {
             // already in place
         } else if (mode == 1 || mode == 3) {
             copy_par(h_out_ids, pin + o_ids, total * 4);
