@@ -33,9 +33,14 @@
 #pragma once
 #include "common.cuh"
 
+#include <type_traits>
+
 #ifndef ENGINE_WALK
 #define ENGINE_WALK 64
 #endif
+
+// A pair slot to be re-probed ({GPUBPE_INF, REPROBE}; a probe miss is {GPUBPE_INF, 0}).
+#define REPROBE 0xFFFFFFFFu
 
 struct EngineMem {
     uint32_t *tok, *tok2;  // tokens, double buffered
@@ -262,28 +267,39 @@ template <class G, bool EXT = false>
 static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_t n, bool strict, const G &g,
                                         uint32_t *passes_out, const uint32_t **out,
                                         EngineExt ext = EngineExt{nullptr, false}) {
+    // kSplit (the CTA): the dependent chains of a pass -- blocking walks and the
+    // re-probes after a merge -- run in loops of their own with no barrier inside,
+    // so every thread's chains overlap the others' instead of each chunk of the
+    // sequence waiting for its slowest walk or probe; the pass minimum is taken
+    // while re-probing.  The warp keeps the fused loops (its lanes are in lock
+    // step either way).
+    constexpr bool kSplit = !std::is_same<G, WarpGroup>::value;
     const uint32_t nt = g.size(), me = g.rank();
     uint32_t passes = 0;
     const uint32_t n0 = n;
     bool fault = EXT && ext.fault;
+    unsigned long long mine = ~0ull;  // (kSplit) this thread's min (rank, position) of the pass
     for (uint32_t b = 0; b < n; b += nt) {
         uint32_t i = b + me;
         if (i + 1 < n) {
             PairHit h = probe_pair(T, M.tok[i], M.tok[i + 1]);
             M.pr[i] = make_uint2(h.rank, h.nw);
+            if (kSplit && h.rank != GPUBPE_INF) mine = min(mine, ((unsigned long long)h.rank << 32) | i);
         }
     }
     g.sync();
     while (n >= 2) {
         // 1. min (rank, position)
-        unsigned long long mine = ~0ull;
-        for (uint32_t b = 0; b < n - 1; b += nt) {
-            uint32_t i = b + me;
-            if (i < n - 1) {
-                uint32_t r = M.pr[i].x;
-                if (r != GPUBPE_INF) {
-                    unsigned long long k = ((unsigned long long)r << 32) | i;
-                    mine = k < mine ? k : mine;
+        if (!kSplit) {
+            mine = ~0ull;
+            for (uint32_t b = 0; b < n - 1; b += nt) {
+                uint32_t i = b + me;
+                if (i < n - 1) {
+                    uint32_t r = M.pr[i].x;
+                    if (r != GPUBPE_INF) {
+                        unsigned long long k = ((unsigned long long)r << 32) | i;
+                        mine = k < mine ? k : mine;
+                    }
                 }
             }
         }
@@ -342,10 +358,22 @@ static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_
                 s = max(s, carry);
                 carry = max(carry, chunk_max);
                 bool ok = pair && r != GPUBPE_INF && ((i - s) & 1u) == 0;
-                if (ok && r != rmin)
+                if (kSplit) {
+                    // walks deferred: run start kept in tok2 (free until the compaction)
+                    if (i < n) M.tok2[i] = ok && r != rmin ? s : GPUBPE_INF;
+                } else if (ok && r != rmin) {
                     ok = walk_left(T, M.tok, M.pr, s, r) && walk_right(T, M.tok, M.pr, i + 1, n, r);
+                }
                 if (i < n) M.sel[i] = ok;
             }
+            if (kSplit)  // the same positions per thread as above: no barrier needed
+                for (uint32_t i = me; i + 1 < n; i += nt) {
+                    const uint32_t s = M.tok2[i];
+                    if (s != GPUBPE_INF) {
+                        const uint32_t r = M.pr[i].x;
+                        M.sel[i] = walk_left(T, M.tok, M.pr, s, r) && walk_right(T, M.tok, M.pr, i + 1, n, r);
+                    }
+                }
         }
         g.sync();
         if (EXT && corrupt) {
@@ -380,8 +408,12 @@ static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_
                     bool sn = M.sel[jn];
                     uint32_t tn = sn ? M.pr[jn].y : M.tok[jn];
                     if (sj || sn) {
-                        PairHit h = probe_pair(T, t, tn);
-                        M.pr2[pos] = make_uint2(h.rank, h.nw);
+                        if (kSplit) {
+                            M.pr2[pos] = make_uint2(GPUBPE_INF, REPROBE);  // probed below
+                        } else {
+                            PairHit h = probe_pair(T, t, tn);
+                            M.pr2[pos] = make_uint2(h.rank, h.nw);
+                        }
                     } else {
                         M.pr2[pos] = pj;
                     }
@@ -389,6 +421,19 @@ static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_
             }
         }
         g.sync();
+        if (kSplit) {  // re-probe the pairs next to a merge; the next pass's minimum
+            mine = ~0ull;
+            for (uint32_t p = me; p + 1 < carry; p += nt) {
+                uint2 v = M.pr2[p];
+                if (v.x == GPUBPE_INF && v.y == REPROBE) {
+                    const PairHit h = probe_pair(T, M.tok2[p], M.tok2[p + 1]);
+                    v = make_uint2(h.rank, h.nw);
+                    M.pr2[p] = v;
+                }
+                if (v.x != GPUBPE_INF) mine = min(mine, ((unsigned long long)v.x << 32) | p);
+            }
+            g.sync();
+        }
         n = carry;
         uint32_t *tt = M.tok; M.tok = M.tok2; M.tok2 = tt;
         uint2 *pp = M.pr; M.pr = M.pr2; M.pr2 = pp;

@@ -1118,8 +1118,25 @@ __device__ uint32_t grid_engine_run(const EncodeParams &P, CtaSmem &C, EngineMem
             uint32_t sv = block_incl_max(start ? i + 1 : 0u, C.es, &chunk_max);
             sv = max(sv, runs);
             runs = max(runs, chunk_max);
-            if (i < hi) M.sel[i] = grid_select(T, M, i, n, sv ? sv - 1 : 0u, rmin, pmin, strict, vfirst);
+            if (i < hi) {
+                if (strict) {
+                    M.sel[i] = grid_select(T, M, i, n, sv ? sv - 1 : 0u, rmin, pmin, strict, vfirst);
+                } else {  // walks deferred to the loop below (no barrier between the walks)
+                    const uint32_t s = sv ? sv - 1 : 0u;
+                    const bool ok = pair && r != GPUBPE_INF && ((i - s) & 1u) == 0;
+                    M.sel[i] = ok;
+                    M.tok2[i] = ok && r != rmin ? s : GPUBPE_INF;  // (tok2 is free until phase C)
+                }
+            }
         }
+        if (!strict)  // the same positions per thread as above
+            for (uint32_t i = lo + tid; i < hi; i += NT) {
+                const uint32_t s = M.tok2[i];
+                if (s != GPUBPE_INF) {
+                    const uint32_t r = M.pr[i].x;
+                    M.sel[i] = walk_left(T, M.tok, M.pr, s, r) && walk_right(T, M.tok, M.pr, i + 1, n, r);
+                }
+            }
         __syncthreads();
         uint32_t kept = 0;
         for (uint32_t j = lo + tid; j < hi; j += NT) {
@@ -1160,14 +1177,27 @@ __device__ uint32_t grid_engine_run(const EncodeParams &P, CtaSmem &C, EngineMem
                 const uint32_t jn = sj ? j + 2 : j + 1;
                 if (jn < n) {
                     const bool sn = __ldcg(&M.sel[jn]) != 0;
-                    const uint32_t tn = sn ? M.pr[jn].y : M.tok[jn];
                     if (sj || sn) {
-                        const PairHit h = probe_pair(T, t, tn);
-                        M.pr2[pos] = make_uint2(h.rank, h.nw);
+                        if (pos + 1 == pre + ktot) {  // the range's last pair: its right token is the next range's
+                            const uint32_t tn = sn ? M.pr[jn].y : M.tok[jn];
+                            const PairHit h = probe_pair(T, t, tn);
+                            M.pr2[pos] = make_uint2(h.rank, h.nw);
+                        } else {
+                            M.pr2[pos] = make_uint2(GPUBPE_INF, REPROBE);  // probed below
+                        }
                     } else {
                         M.pr2[pos] = pj;
                     }
                 }
+            }
+        }
+        __syncthreads();
+        // re-probes inside the range's output (no barrier between the probes)
+        for (uint32_t p = pre + tid; p + 1 < pre + ktot; p += NT) {
+            const uint2 v = M.pr2[p];
+            if (v.x == GPUBPE_INF && v.y == REPROBE) {
+                const PairHit h = probe_pair(T, M.tok2[p], M.tok2[p + 1]);
+                M.pr2[p] = make_uint2(h.rank, h.nw);
             }
         }
         grid_sync(st, ++nbar);
@@ -1194,7 +1224,7 @@ __device__ void grid_giants(const EncodeParams &P, CtaSmem &C, unsigned long lon
         const unsigned long long r = __ldcg(&P.glist[gi]);
         if (__ldcg(&P.recs[r].count) != REC_GIANT) continue;  // encoded by one CTA (cta_giants)
         const long long s0 = (long long)__ldcg(&P.recs[r].start);
-        // the segment's end: each CTA scans a slice of [s0 + GIANT_MIN, lim)
+        // the segment's end: each CTA scans a slice of [s0 + MEDIUM_MAX + 1, lim)
         long long d = 0;
         if (P.n_docs > 1) {
             if ((threadIdx.x >> 5) == 0) {
@@ -1206,7 +1236,7 @@ __device__ void grid_giants(const EncodeParams &P, CtaSmem &C, unsigned long lon
         }
         long long lim = next_struct_cut(P, d, s0);
         if (lim > N) lim = N;
-        const long long from = s0 + GIANT_MIN, span = lim - from;
+        const long long from = s0 + MEDIUM_MAX + 1, span = lim - from;
         const long long lo = from + span * blockIdx.x / gridDim.x, hi = from + span * (blockIdx.x + 1) / gridDim.x;
         if (blockIdx.x == 0 && tid == 0) g[2] = (unsigned long long)lim;
         grid_sync(st, ++nbar);
@@ -1352,7 +1382,7 @@ __device__ void cta_giants(const EncodeParams &P, CtaSmem &C, unsigned long long
         long long lim = next_struct_cut(P, d, s0);
         if (lim > N) lim = N;
         const long long hi = min(lim, s0 + (long long)CTA_GIANT_MAX + 1);
-        const long long e = cta_first_nonjunction(P, C.jb, s0 + GIANT_MIN, hi, C.es);
+        const long long e = cta_first_nonjunction(P, C.jb, s0 + MEDIUM_MAX + 1, hi, C.es);
         if (e >= hi && hi < lim) continue;  // longer than CTA_GIANT_MAX: the grid's
         encode_record(P, C, BlockGroup{C.es}, r, s0, (unsigned long long)(e - s0), t0, par, tid == 0, &C.bcast[2]);
     }
@@ -1360,7 +1390,7 @@ __device__ void cta_giants(const EncodeParams &P, CtaSmem &C, unsigned long long
 
 // Deferred records [d0, d1) of round r.  Pass 1: every warp takes records,
 // finds each segment's end (first cut after its start, looked for within
-// GIANT_MIN bytes) and encodes the medium ones with the warp engine; longer
+// MEDIUM_MAX + 1 bytes) and encodes the medium ones with the warp engine; longer
 // ones are marked.  Pass 2 (after a grid barrier): whole CTAs take the marked
 // giants.  Both write results to the arena and extra ids to the tile words.
 __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, unsigned long long d0,
@@ -1379,9 +1409,9 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
         const long long d = P.n_docs > 1 ? warp_doc_from(P.doc_offs, (long long)__ldcg(&P.recs[r].doc), P.n_docs, s0) : 0;
         long long lim = next_struct_cut(P, d, s0);
         if (lim > N) lim = N;
-        const long long scan_hi = min(lim, s0 + (long long)GIANT_MIN);
+        const long long scan_hi = min(lim, s0 + (long long)MEDIUM_MAX + 1);
         const long long send = warp_first_nonjunction(P, C.jb, s0 + 1, scan_hi);
-        if (send >= scan_hi && scan_hi < lim) {  // no cut within GIANT_MIN bytes: a job for the grid
+        if (send >= scan_hi && scan_hi < lim) {  // no cut within MEDIUM_MAX + 1 bytes: a CTA or grid job
             if (lane == 0) {
                 P.recs[r].count = REC_GIANT;
                 P.glist[atomicAdd(&P.gscr[4], 1ull)] = (uint32_t)r;
