@@ -1306,13 +1306,21 @@ __device__ long long warp_first_nonjunction(const EncodeParams &P, const uint32_
 
 // Group-engine encode of one deferred segment [s0, s0 + len) into the arena;
 // the record gets its count and result offset, its tile word the extra ids.
+// When the engine's buffers fit `smem` (the group's dead tile staging: the
+// round's tiles are done when deferred segments run), the passes run in shared
+// memory and only the result goes to the arena (every pass reads and writes
+// its whole sequence a few times, each access an L2 round trip in the arena).
+#ifndef GPUBPE_SMEM_ENGINE
+#define GPUBPE_SMEM_ENGINE 1
+#endif
 template <class G>
 __device__ void encode_record(const EncodeParams &P, CtaSmem &C, const G &g, unsigned long long r, long long s0,
                               unsigned long long len, unsigned long long t0, unsigned long long par, bool lead,
-                              unsigned long long *arena_off_bcast) {
+                              unsigned long long *arena_off_bcast, uint32_t *smem, size_t smem_bytes) {
     EncodeState *st = P.st;
+    const bool in_smem = GPUBPE_SMEM_ENGINE && ENGINE_BYTES(len) <= smem_bytes;
     if (lead) {
-        const unsigned long long words = (ENGINE_BYTES(len) + 15) / 16 * 4;
+        const unsigned long long words = in_smem ? (len + 3) / 4 * 4 : (ENGINE_BYTES(len) + 15) / 16 * 4;
         unsigned long long off = atomicAdd(&st->arena_used, words);
         if (off + words > P.arena_words) {
             atomicExch(&st->overflow, 1ull);
@@ -1324,7 +1332,7 @@ __device__ void encode_record(const EncodeParams &P, CtaSmem &C, const G &g, uns
     const unsigned long long off = *arena_off_bcast;
     if (off == ~0ull) return;  // the host re-runs with a larger arena
     EngineMem M;
-    M.tok = P.arena + off;
+    M.tok = in_smem ? smem : P.arena + off;
     M.tok2 = M.tok + len;
     M.pr = reinterpret_cast<uint2 *>(M.tok2 + len);
     M.pr2 = M.pr + len;
@@ -1335,6 +1343,10 @@ __device__ void encode_record(const EncodeParams &P, CtaSmem &C, const G &g, uns
     const uint32_t *res;
     const bool strict = P.strict || !P.T.well_formed;
     const uint32_t cnt = engine_run_g(P.T, M, (uint32_t)len, strict, g, &passes, &res);
+    if (in_smem) {
+        for (uint32_t j = g.rank(); j < cnt; j += g.size()) P.arena[off + j] = res[j];
+        res = P.arena + off;
+    }
     if (lead) {
         P.recs[r].count = cnt;
         P.recs[r].res = (uint32_t)(res - P.arena);
@@ -1384,7 +1396,8 @@ __device__ void cta_giants(const EncodeParams &P, CtaSmem &C, unsigned long long
         const long long hi = min(lim, s0 + (long long)CTA_GIANT_MAX + 1);
         const long long e = cta_first_nonjunction(P, C.jb, s0 + MEDIUM_MAX + 1, hi, C.es);
         if (e >= hi && hi < lim) continue;  // longer than CTA_GIANT_MAX: the grid's
-        encode_record(P, C, BlockGroup{C.es}, r, s0, (unsigned long long)(e - s0), t0, par, tid == 0, &C.bcast[2]);
+        encode_record(P, C, BlockGroup{C.es}, r, s0, (unsigned long long)(e - s0), t0, par, tid == 0, &C.bcast[2],
+                      reinterpret_cast<uint32_t *>(C.w), sizeof(C.w));
     }
 }
 
@@ -1419,7 +1432,7 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
             continue;
         }
         encode_record(P, C, WarpGroup{}, r, s0, (unsigned long long)(send - s0), t0, par, lane == 0,
-                      &C.w[wid].dl_arena);
+                      &C.w[wid].dl_arena, reinterpret_cast<uint32_t *>(&C.w[wid]), offsetof(WarpSmem, n_miss));
     }
     grid_sync(st, ++nbar);
     // ---- pass 2: several giants -> one CTA each (up to CTA_GIANT_MAX bytes), then

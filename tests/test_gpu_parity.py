@@ -147,6 +147,29 @@ def test_many_giant_documents(tokenizer, oracle):
         assert got.device_stats["giant_segments"] >= 20
 
 
+def test_deferred_segment_routes(tokenizer, oracle):
+    """Deferred segments of every route (kernels.cu encode_deferred / cta_giants):
+    <= 221 B on a warp in its shared tile staging, 222-512 B on a warp in the
+    arena, 513 B - 7 KB on one CTA in shared memory, longer on one CTA in the
+    arena, and a lone routed segment on the whole grid.  Many per call and one
+    per call, under both chunking configs."""
+    r = random.Random(23)
+    kinds = ["digits", "hex", "letters", "newlines", "aaaa", "spaces"]
+    sizes = [33, 100, 221, 222, 223, 400, 512, 513, 514, 900, 2000, 4096, 4097, 7100, 7185, 7186, 7300, 8192]
+    docs = []
+    for i in range(300):
+        n = sizes[i % len(sizes)] if i < 2 * len(sizes) else r.randint(33, 9000)
+        body = ADVERSARIAL[kinds[i % len(kinds)]](n, r)
+        docs.append(body if i % 4 else b"Value: " + body + b".")
+    for msl, cb in ((1 << 40, 1 << 40), (8192, 8192), (3000, 3000)):
+        got = bpe.tokenize_batch(docs, with_config(tokenizer, msl, cb))
+        assert_same(got.token_ids, oracle.encode_docs(docs, msl, cb), f"routes {msl}")
+    for n in (600, 5000):  # one routed segment alone in the call: the grid engine
+        doc = ADVERSARIAL["digits"](n, r)
+        got = bpe.tokenize_batch([doc], with_config(tokenizer, 1 << 40, 1 << 40)).token_ids
+        assert_same(got, oracle.encode_docs([doc], 1 << 40, 1 << 40), f"lone {n}")
+
+
 def test_many_small_and_empty_docs(tokenizer, oracle):
     r = random.Random(5)
     docs = []

@@ -77,6 +77,8 @@ def workloads():
         "adv_digit_docs_1000x10k": lambda: giant_docs(1000, 10000),
         "adv_digits_64k": lambda: adversarial("digits", 1 << 16),
         "adv_digit_docs_64x10k": lambda: giant_docs(64, 10000),
+        "adv_digit_docs_1000x6k": lambda: giant_docs(1000, 6000),
+        "adv_digit_docs_16384x200": lambda: giant_docs(16384, 200),
     }
 
 
