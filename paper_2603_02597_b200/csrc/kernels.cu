@@ -1389,10 +1389,12 @@ __device__ void encode_record(const EncodeParams &P, CtaSmem &C, const G &g, uns
 
 
 // Several giants in a round: each CTA takes giants from the round's list and
-// encodes those of at most CTA_GIANT_MAX bytes alone (the block engine over
-// the arena), concurrently; longer ones keep their REC_GIANT mark for the
-// whole grid (grid_giants).  One giant alone is faster on the grid.
-__device__ void cta_giants(const EncodeParams &P, CtaSmem &C, unsigned long long t0, unsigned long long par) {
+// encodes those of at most max_len bytes alone (the block engine, in shared
+// memory when it fits), concurrently; longer ones keep their REC_GIANT mark
+// for the whole grid (grid_giants).  A lone giant longer than
+// GPUBPE_LONE_CTA_MAX is faster on the grid.
+__device__ void cta_giants(const EncodeParams &P, CtaSmem &C, unsigned long long t0, unsigned long long par,
+                           long long max_len) {
     const int tid = threadIdx.x;
     EncodeState *st = P.st;
     const long long N = (long long)P.n_bytes;
@@ -1417,14 +1419,17 @@ __device__ void cta_giants(const EncodeParams &P, CtaSmem &C, unsigned long long
         }
         long long lim = next_struct_cut(P, d, s0);
         if (lim > N) lim = N;
-        const long long hi = min(lim, s0 + (long long)CTA_GIANT_MAX + 1);
+        const long long hi = min(lim, s0 + max_len + 1);
         const long long e = cta_first_nonjunction(P, C.jb, s0 + MEDIUM_MAX + 1, hi, C.es);
-        if (e >= hi && hi < lim) continue;  // longer than CTA_GIANT_MAX: the grid's
+        if (e >= hi && hi < lim) continue;  // longer than max_len: the grid's
         encode_record(P, C, BlockGroup{C.es}, r, s0, (unsigned long long)(e - s0), t0, par, tid == 0, &C.bcast[2],
                       reinterpret_cast<uint32_t *>(C.w), sizeof(C.w));
     }
 }
 
+#ifndef GPUBPE_LONE_CTA_MAX
+#define GPUBPE_LONE_CTA_MAX 4096
+#endif
 // Deferred records [d0, d1) of round r.  Pass 1: every warp takes records,
 // finds each segment's end (first cut after its start, looked for within
 // MEDIUM_MAX + 1 bytes) and encodes the medium ones with the warp engine; longer
@@ -1461,8 +1466,12 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
     grid_sync(st, ++nbar);
     // ---- pass 2: several giants -> one CTA each (up to CTA_GIANT_MAX bytes), then
     //      every CTA together on each remaining giant, in record order
-    if (__ldcg(&P.gscr[4]) > 1) {
-        cta_giants(P, C, t0, par);
+    //      (a lone one too when it is short: a pass of the grid engine costs three grid
+    //      barriers, so 600 B of digits take 314 us on the grid and 130 us on one CTA
+    //      in shared memory; the grid wins from ~6 KB)
+    const unsigned long long n_giants = __ldcg(&P.gscr[4]);
+    if (n_giants > 1 || (n_giants == 1 && GPUBPE_LONE_CTA_MAX > MEDIUM_MAX)) {
+        cta_giants(P, C, t0, par, n_giants > 1 ? CTA_GIANT_MAX : GPUBPE_LONE_CTA_MAX);
         grid_sync(st, ++nbar);
     }
     grid_giants(P, C, t0, par, nbar);

@@ -78,6 +78,10 @@ def workloads():
         "adv_digits_64k": lambda: adversarial("digits", 1 << 16),
         "adv_digit_docs_64x10k": lambda: giant_docs(64, 10000),
         "adv_digit_docs_1000x6k": lambda: giant_docs(1000, 6000),
+        "adv_digits_6k": lambda: giant_docs(1, 6000),
+        "adv_digits_600": lambda: giant_docs(1, 600),
+        "adv_digits_2k": lambda: giant_docs(1, 2000),
+        "adv_digits_4k": lambda: giant_docs(1, 4000),
         "adv_digit_docs_16384x200": lambda: giant_docs(16384, 200),
     }
 
