@@ -1232,7 +1232,7 @@ __device__ __forceinline__ void giant_masks(const EncodeParams &P, CtaSmem &C, u
 
 // All CTAs: encode the giant records of [d0, d1) one after another.
 __device__ void grid_giants(const EncodeParams &P, CtaSmem &C, unsigned long long t0, unsigned long long par,
-                            unsigned int &nbar) {
+                            unsigned int &nbar, long long mmax) {
     const int tid = threadIdx.x;
     EncodeState *st = P.st;
     unsigned long long *g = P.gscr;
@@ -1247,7 +1247,7 @@ __device__ void grid_giants(const EncodeParams &P, CtaSmem &C, unsigned long lon
         const unsigned long long gi = gi0 + 32 * w + (__ffs(m) - 1);
         const unsigned long long r = __ldcg(&P.glist[gi]);
         const long long s0 = (long long)__ldcg(&P.recs[r].start);
-        // the segment's end: each CTA scans a slice of [s0 + MEDIUM_MAX + 1, lim)
+        // the segment's end: each CTA scans a slice of [s0 + mmax + 1, lim)
         long long d = 0;
         if (P.n_docs > 1) {
             if ((threadIdx.x >> 5) == 0) {
@@ -1259,7 +1259,7 @@ __device__ void grid_giants(const EncodeParams &P, CtaSmem &C, unsigned long lon
         }
         long long lim = next_struct_cut(P, d, s0);
         if (lim > N) lim = N;
-        const long long from = s0 + MEDIUM_MAX + 1, span = lim - from;
+        const long long from = s0 + mmax + 1, span = lim - from;
         const long long lo = from + span * blockIdx.x / gridDim.x, hi = from + span * (blockIdx.x + 1) / gridDim.x;
         if (blockIdx.x == 0 && tid == 0) g[2] = (unsigned long long)lim;
         grid_sync(st, ++nbar);
@@ -1394,7 +1394,7 @@ __device__ void encode_record(const EncodeParams &P, CtaSmem &C, const G &g, uns
 // for the whole grid (grid_giants).  A lone giant longer than
 // GPUBPE_LONE_CTA_MAX is faster on the grid.
 __device__ void cta_giants(const EncodeParams &P, CtaSmem &C, unsigned long long t0, unsigned long long par,
-                           long long max_len) {
+                           long long max_len, long long mmax) {
     const int tid = threadIdx.x;
     EncodeState *st = P.st;
     const long long N = (long long)P.n_bytes;
@@ -1420,7 +1420,7 @@ __device__ void cta_giants(const EncodeParams &P, CtaSmem &C, unsigned long long
         long long lim = next_struct_cut(P, d, s0);
         if (lim > N) lim = N;
         const long long hi = min(lim, s0 + max_len + 1);
-        const long long e = cta_first_nonjunction(P, C.jb, s0 + MEDIUM_MAX + 1, hi, C.es);
+        const long long e = cta_first_nonjunction(P, C.jb, s0 + mmax + 1, hi, C.es);
         if (e >= hi && hi < lim) continue;  // longer than max_len: the grid's
         encode_record(P, C, BlockGroup{C.es}, r, s0, (unsigned long long)(e - s0), t0, par, tid == 0, &C.bcast[2],
                       reinterpret_cast<uint32_t *>(C.w), sizeof(C.w));
@@ -1441,6 +1441,10 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     EncodeState *st = P.st;
     const long long N = (long long)P.n_bytes;
+    // longest segment a warp encodes: MEDIUM_MAX, or FEW_MEDIUM_MAX when the round has
+    // no more records than CTAs (a warp walks a segment 32 positions at a time; with
+    // CTAs to spare, a whole CTA takes each longer one)
+    const long long mmax = d1 - d0 <= (unsigned long long)gridDim.x ? FEW_MEDIUM_MAX : MEDIUM_MAX;
     // ---- pass 1: warps
     for (;;) {
         unsigned long long r = 0;
@@ -1451,9 +1455,9 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
         const long long d = P.n_docs > 1 ? warp_doc_from(P.doc_offs, (long long)__ldcg(&P.recs[r].doc), P.n_docs, s0) : 0;
         long long lim = next_struct_cut(P, d, s0);
         if (lim > N) lim = N;
-        const long long scan_hi = min(lim, s0 + (long long)MEDIUM_MAX + 1);
+        const long long scan_hi = min(lim, s0 + mmax + 1);
         const long long send = warp_first_nonjunction(P, C.jb, s0 + 1, scan_hi);
-        if (send >= scan_hi && scan_hi < lim) {  // no cut within MEDIUM_MAX + 1 bytes: a CTA or grid job
+        if (send >= scan_hi && scan_hi < lim) {  // no cut within mmax + 1 bytes: a CTA or grid job
             if (lane == 0) {
                 P.recs[r].count = REC_GIANT;
                 P.glist[atomicAdd(&P.gscr[4], 1ull)] = (uint32_t)r;
@@ -1470,11 +1474,11 @@ __device__ __noinline__ void encode_deferred(const EncodeParams &P, CtaSmem &C, 
     //      barriers, so 600 B of digits take 314 us on the grid and 130 us on one CTA
     //      in shared memory; the grid wins from ~6 KB)
     const unsigned long long n_giants = __ldcg(&P.gscr[4]);
-    if (n_giants > 1 || (n_giants == 1 && GPUBPE_LONE_CTA_MAX > MEDIUM_MAX)) {
-        cta_giants(P, C, t0, par, n_giants > 1 ? CTA_GIANT_MAX : GPUBPE_LONE_CTA_MAX);
+    if (n_giants > 1 || (n_giants == 1 && GPUBPE_LONE_CTA_MAX > mmax)) {
+        cta_giants(P, C, t0, par, n_giants > 1 ? CTA_GIANT_MAX : GPUBPE_LONE_CTA_MAX, mmax);
         grid_sync(st, ++nbar);
     }
-    grid_giants(P, C, t0, par, nbar);
+    grid_giants(P, C, t0, par, nbar, mmax);
 }
 
 // ------------------------------------------------------------------ kernel

@@ -53,6 +53,10 @@ constexpr int GIANT_MIN = 4097; // deferred segments this long are giants (else 
 // a warp's pass walks the segment 32 positions at a time, each step a few dependent
 // L2 round trips, so a 2 KB digit run on a warp outlasts the whole giant pass
 constexpr int MEDIUM_MAX = GPUBPE_MEDIUM_MAX < GIANT_MIN - 1 ? GPUBPE_MEDIUM_MAX : GIANT_MIN - 1;
+#ifndef GPUBPE_FEW_MEDIUM_MAX
+#define GPUBPE_FEW_MEDIUM_MAX 128
+#endif
+constexpr int FEW_MEDIUM_MAX = GPUBPE_FEW_MEDIUM_MAX < MEDIUM_MAX ? GPUBPE_FEW_MEDIUM_MAX : MEDIUM_MAX;
 constexpr int CTA_GIANT_MAX = 64 << 10;  // with several giants in a round, one CTA each up to this length
 constexpr int SLOT = WT + SHORT_MAX;  // scratch entries per tile (ids of segments starting in it)
 #ifndef GPUBPE_UNIT_MAX
