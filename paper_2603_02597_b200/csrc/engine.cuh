@@ -44,6 +44,9 @@
 #ifndef GROUP_WALK
 #define GROUP_WALK 32
 #endif
+#ifndef WARP_WALK
+#define WARP_WALK 16  // the warp engine's (its lanes walk in lock step: the longest walk sets the pace)
+#endif
 
 // A pair slot to be re-probed ({GPUBPE_INF, REPROBE}; a probe miss is {GPUBPE_INF, 0}).
 #define REPROBE 0xFFFFFFFFu
@@ -280,6 +283,7 @@ static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_
     // while re-probing.  The warp keeps the fused loops (its lanes are in lock
     // step either way).
     constexpr bool kSplit = !std::is_same<G, WarpGroup>::value;
+    constexpr int kWalk = std::is_same<G, WarpGroup>::value ? WARP_WALK : GROUP_WALK;
     const uint32_t nt = g.size(), me = g.rank();
     uint32_t passes = 0;
     const uint32_t n0 = n;
@@ -368,7 +372,7 @@ static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_
                     // walks deferred: run start kept in tok2 (free until the compaction)
                     if (i < n) M.tok2[i] = ok && r != rmin ? s : GPUBPE_INF;
                 } else if (ok && r != rmin) {
-                    ok = walk_left(T, M.tok, M.pr, s, r, GROUP_WALK) && walk_right(T, M.tok, M.pr, i + 1, n, r, GROUP_WALK);
+                    ok = walk_left(T, M.tok, M.pr, s, r, kWalk) && walk_right(T, M.tok, M.pr, i + 1, n, r, kWalk);
                 }
                 if (i < n) M.sel[i] = ok;
             }
@@ -377,8 +381,8 @@ static __device__ uint32_t engine_run_g(const DevTables &T, EngineMem M, uint32_
                     const uint32_t s = M.tok2[i];
                     if (s != GPUBPE_INF) {
                         const uint32_t r = M.pr[i].x;
-                        M.sel[i] = walk_left(T, M.tok, M.pr, s, r, GROUP_WALK) &&
-                                   walk_right(T, M.tok, M.pr, i + 1, n, r, GROUP_WALK);
+                        M.sel[i] = walk_left(T, M.tok, M.pr, s, r, kWalk) &&
+                                   walk_right(T, M.tok, M.pr, i + 1, n, r, kWalk);
                     }
                 }
         }

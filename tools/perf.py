@@ -79,6 +79,7 @@ def workloads():
         "adv_digit_docs_64x10k": lambda: giant_docs(64, 10000),
         "adv_digit_docs_1000x6k": lambda: giant_docs(1000, 6000),
         "adv_digits_6k": lambda: giant_docs(1, 6000),
+        "adv_digits_7k": lambda: giant_docs(1, 7000),
         "adv_digits_600": lambda: giant_docs(1, 600),
         "adv_digits_200": lambda: giant_docs(1, 200),
         "adv_digits_400": lambda: giant_docs(1, 400),
