@@ -20,6 +20,7 @@ The oracle is oracle/ (the C restatement pinned to the reference's goldens).
 from __future__ import annotations
 
 import hashlib
+import os
 import random
 
 import numpy as np
@@ -158,11 +159,13 @@ def test_byte_level_fuzz(well_formed):
     """100 random byte-level tables x 60 documents per mode through
     tokenize_batch (k_encode), P-whole, including 4-20 KB runs (deferred
     and giant segments)."""
-    rng = random.Random(2000 + well_formed)
+    # GPUBPE_FUZZ_TABLES / GPUBPE_FUZZ_SEED widen the run by hand (longer GPU soaks)
+    n_tables = int(os.environ.get("GPUBPE_FUZZ_TABLES", "100"))
+    rng = random.Random(2000 + well_formed + 7919 * int(os.environ.get("GPUBPE_FUZZ_SEED", "0")))
     enc = bpe.build_byte_encoder()
     b2s = {b: s for s, b in enc.symbol_to_byte.items()}
     total, giants = 0, 0
-    for t in range(100):
+    for t in range(n_tables):
         symbols = {b2s[b]: b for b in range(256)}
         sym_of = {b: b2s[b] for b in range(256)}
         alphabet = bytes(rng.sample(range(256), rng.randrange(2, 7)))
@@ -199,4 +202,4 @@ def test_byte_level_fuzz(well_formed):
         total += len(docs)
         for d in tok._devices.values():
             d.close()
-    assert total == 6000 and giants > 100
+    assert total == 60 * n_tables and giants > n_tables
