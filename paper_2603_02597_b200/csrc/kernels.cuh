@@ -47,7 +47,7 @@ constexpr int NT = NW * 32;     // threads per CTA
 constexpr int SHORT_MAX = 32;   // longest segment encoded inside the tile loop
 constexpr int GIANT_MIN = 4097; // deferred segments this long are giants (else a warp encodes them)
 #ifndef GPUBPE_MEDIUM_MAX
-#define GPUBPE_MEDIUM_MAX 512
+#define GPUBPE_MEDIUM_MAX 1024
 #endif
 // deferred segments longer than this go to the CTA (or grid) engine with the giants:
 // a warp's pass walks the segment 32 positions at a time, each step a few dependent

@@ -149,13 +149,15 @@ def test_many_giant_documents(tokenizer, oracle):
 
 def test_deferred_segment_routes(tokenizer, oracle):
     """Deferred segments of every route (kernels.cu encode_deferred / cta_giants):
-    <= 221 B on a warp in its shared tile staging, 222-512 B on a warp in the
-    arena, 513 B - 7 KB on one CTA in shared memory, longer on one CTA in the
-    arena, and a lone routed segment on the whole grid.  Many per call and one
-    per call, under both chunking configs."""
+    <= 221 B on a warp in its shared tile staging, 222-1024 B on a warp in the
+    arena (129 B and up on one CTA when a call has few records), 1025 B - 7 KB
+    on one CTA in shared memory, longer on one CTA in the arena, and a lone
+    routed segment on one CTA (<= 4 KiB) or the whole grid.  Many per call and
+    one per call, under both chunking configs."""
     r = random.Random(23)
     kinds = ["digits", "hex", "letters", "newlines", "aaaa", "spaces"]
-    sizes = [33, 100, 221, 222, 223, 400, 512, 513, 514, 900, 2000, 4096, 4097, 7100, 7185, 7186, 7300, 8192]
+    sizes = [33, 100, 128, 129, 221, 222, 223, 400, 512, 513, 900, 1024, 1025, 1026, 2000, 4096, 4097, 7100,
+             7185, 7186, 7300, 8192]
     docs = []
     for i in range(300):
         n = sizes[i % len(sizes)] if i < 2 * len(sizes) else r.randint(33, 9000)
@@ -164,7 +166,7 @@ def test_deferred_segment_routes(tokenizer, oracle):
     for msl, cb in ((1 << 40, 1 << 40), (8192, 8192), (3000, 3000)):
         got = bpe.tokenize_batch(docs, with_config(tokenizer, msl, cb))
         assert_same(got.token_ids, oracle.encode_docs(docs, msl, cb), f"routes {msl}")
-    for n in (600, 5000):  # one routed segment alone in the call: the grid engine
+    for n in (130, 600, 4096, 4097, 5000):  # one routed segment alone: one CTA up to 4 KiB, else the grid
         doc = ADVERSARIAL["digits"](n, r)
         got = bpe.tokenize_batch([doc], with_config(tokenizer, 1 << 40, 1 << 40)).token_ids
         assert_same(got, oracle.encode_docs([doc], 1 << 40, 1 << 40), f"lone {n}")

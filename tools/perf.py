@@ -85,6 +85,8 @@ def workloads():
         "adv_digits_400": lambda: giant_docs(1, 400),
         "adv_digit_docs_100x400": lambda: giant_docs(100, 400),
         "adv_digit_docs_4096x400": lambda: giant_docs(4096, 400),
+        "adv_digit_docs_4096x800": lambda: giant_docs(4096, 800),
+        "adv_digit_docs_2048x2000": lambda: giant_docs(2048, 2000),
         "adv_digits_2k": lambda: giant_docs(1, 2000),
         "adv_digits_4k": lambda: giant_docs(1, 4000),
         "adv_digit_docs_16384x200": lambda: giant_docs(16384, 200),
